@@ -1,0 +1,127 @@
+/*
+ * lasp2_b200.h — C ABI of the B200-native LASP-2 / LASP-2H hot path.
+ *
+ * Plain pointers and sizes only. Every entry point is stream-ordered and
+ * asynchronous: it enqueues work on `stream` (a cudaStream_t passed as void*,
+ * NULL = legacy default stream) and returns a status code; no entry point
+ * allocates caller-visible memory, frees caller memory or synchronises.
+ * Errors never cross the ABI as exceptions: a non-zero status is returned and
+ * lasp2_last_error() describes it (thread-local).
+ *
+ * Tensor layout (reference shards.py:13-39): per-rank tensors
+ * are BHND row-major, i.e. `slots` = B*H independent (tokens x dim) matrices
+ * stored back to back. Memory states are (slots, dim, dim) row-major with
+ * state[a][c] = sum_i x[i][a] * y[i][c]  (reference lasp2.py:130-137).
+ *
+ * Precision follows the data dtype (reference WorldConfig.element_bytes,
+ * comm.py:78-79):
+ *   LASP2_F64  : f64 in/out, f64 states       (reference-precision validation)
+ *   LASP2_F32  : f32 in/out, f32 states       (fp32 validation mode)
+ *   LASP2_BF16 : bf16 in/out, f32 states      (tcgen05/TMEM/TMA fast path)
+ *
+ * Each function names the reference interface it replaces (file:line under
+ * the reference's pkg/src/laspsim/).
+ */
+#ifndef LASP2_B200_H
+#define LASP2_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum lasp2_dtype { LASP2_F32 = 0, LASP2_F64 = 1, LASP2_BF16 = 2 };
+enum lasp2_status { LASP2_OK = 0, LASP2_ERR_INVALID = 1, LASP2_ERR_CUDA = 2, LASP2_ERR_UNSUPPORTED = 3 };
+enum lasp2_fold_mode { LASP2_FOLD_PREFIX = 0, LASP2_FOLD_SUFFIX = 1, LASP2_FOLD_FULL = 2 };
+
+/* ABI version (major*100 + minor). */
+int lasp2_version(void);
+/* Description of the last error on this thread ("" if none). */
+const char* lasp2_last_error(void);
+
+/* Number of sequence segments the kernels split one rank's chunk into for
+ * `slots` slots of `tokens` tokens on a device with `sm_count` SMs. Segment
+ * boundaries are whole 128-token blocks. Host helper, no device work. */
+int lasp2_num_segments(int dtype, int64_t slots, int64_t tokens, int dim, int sm_count);
+
+/* seg_states[slot][s] = X_s^T Y_s over segment s of the rank's chunk.
+ * Replaces chunk_state (lasp2.py:130-137) with (x,y)=(K,V) and chunk_state_grad
+ * (lasp2.py:140-147) with (x,y)=(Q,dO), split into `nseg` segments. */
+int lasp2_segment_states(int dtype, const void* x, const void* y, void* seg_states, int64_t slots, int64_t tokens,
+                         int dim, int nseg, void* stream);
+
+/* In place exclusive scan over segments (reverse=0: prefix, 1: suffix) and the
+ * chunk total (the rank's M_t / dM_t, the AllGather payload; `chunk_total`
+ * may be NULL). First-term-copy fold order as numerics.py:71-116. */
+int lasp2_scan_segments(int dtype, void* seg_states, void* chunk_total, int64_t slots, int nseg, int dim, int reverse,
+                        void* stream);
+
+/* out = ordered fold of `nstates` gathered states, each `elems` elements,
+ * stored rank-major ([nstates][elems], the all_gather layout):
+ *   PREFIX(bound): states[0:bound] ascending  = prefix_sum_states (numerics.py:71-90)
+ *   SUFFIX(bound): states[bound:] descending  = suffix_sum_states (numerics.py:93-116)
+ *   FULL         : all ascending              = sum_states        (numerics.py:119-121) */
+int lasp2_fold_states(int dtype, const void* gathered, void* out, int nstates, int64_t elems, int mode, int bound,
+                      void* stream);
+
+/* Causal linear attention over one rank's chunk with the inter-chunk state
+ * folded in:  out_s = q_s S_s + sum_{i<=s} (q_s.k_i) v_i, where
+ * S_s = base + seg_states[seg(s)] + sum_{i<s, same segment} k_i^T v_i.
+ * reverse=1 runs the anti-causal form (i>=s, states from the chunk end);
+ * transpose_state=1 uses S^T. `base` / `seg_states` may be NULL (zero).
+ * Replaces intra_forward (lasp2.py:168-174, oracle.py:50-62) plus the inter
+ * term `out += apply_state(q, m_prefix)` (lasp2.py:238-240); with permuted
+ * operands it also computes the masked backward's dQ/dK/dV (lasp2.py:270-285). */
+int lasp2_causal_chunk(int dtype, const void* q, const void* k, const void* v, const void* seg_states,
+                       const void* base, void* out, int64_t slots, int64_t tokens, int dim, int nseg, int reverse,
+                       int transpose_state, void* stream);
+
+/* out (+)= x M (transpose=0) or x M^T (transpose=1) per slot.
+ * Replaces apply_state / apply_state_t (lasp2.py:150-165). */
+int lasp2_apply_state(int dtype, const void* x, const void* m, void* out, int64_t slots, int64_t tokens, int dim,
+                      int transpose, int accumulate, void* stream);
+
+/* LASP-2H softmax attention of one chunk of queries (global rows
+ * [row_offset, row_offset+q_tokens)) against full-length keys/values.
+ * Full-length tensors may be rank-major as the collectives produce them:
+ * key j of slot s is at element (j / kv_chunk) * kv_rank_stride +
+ * (s * kv_chunk + j % kv_chunk) * dim (kv_chunk = kv_tokens, stride 0 is the
+ * plain [slots][kv_tokens][dim] layout). The dk/dv contributions use the
+ * same indexing with grad_rank_stride, so a [T][2][slots][chunk][dim] buffer
+ * feeds one reduce-scatter.
+ * out = softmax(q k^T / sqrt(d), causal by global position) v; lse (f32,
+ * [slots][q_tokens]) receives the row log-sum-exp. Replaces
+ * softmax_chunk_forward (oracle.py:136-139) as called by _cp_forward_rank
+ * (standard_sp.py:44-49). */
+int lasp2h_softmax_forward(int dtype, const void* q, const void* k_full, const void* v_full, void* out, void* lse,
+                           int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim, int causal, int64_t row_offset,
+                           int64_t kv_chunk, int64_t kv_rank_stride, void* stream);
+
+/* Gradients of <d_out, softmax_chunk_forward(...)>: dq for the chunk and this
+ * chunk's full-length dk/dv contributions (accumulate dtype: f32 for bf16/f32,
+ * f64 for f64). `scratch` must hold lasp2h_softmax_scratch_bytes() bytes.
+ * Replaces softmax_chunk_backward (oracle.py:142-158) as called by
+ * _cp_backward_rank (standard_sp.py:64-68). */
+int lasp2h_softmax_backward(int dtype, const void* q, const void* k_full, const void* v_full, const void* out,
+                            const void* lse, const void* d_out, void* dq, void* dk_full, void* dv_full, void* scratch,
+                            int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim, int causal,
+                            int64_t row_offset, int64_t kv_chunk, int64_t kv_rank_stride, int64_t grad_rank_stride,
+                            void* stream);
+int64_t lasp2h_softmax_scratch_bytes(int dtype, int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim);
+
+/* Deterministic inputs: out[slot] = gen_data(seed, rows, cols, tag_slot) where
+ * tag_words[slot] is the 64-bit blake2b word of the slot's tag. Bit-exact port
+ * of gen_data / gen_slots (datagen.py:33-71); bf16 rounds f64->f32->bf16. */
+int lasp2_gen_slots(int dtype, uint64_t seed, const uint64_t* tag_words_device, void* out, int64_t slots, int64_t rows,
+                    int64_t cols, void* stream);
+
+/* Test hook: d (f32 128x128) = op(a) op(b)^T for bf16 128x128 tiles with the
+ * UMMA descriptor convention of the fast path (a_mn / b_mn select MN-major). */
+int lasp2_debug_probe_gemm(const void* a, const void* b, void* d, int a_mn, int b_mn, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LASP2_B200_H */

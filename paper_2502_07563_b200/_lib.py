@@ -1,0 +1,119 @@
+"""ctypes binding of the C-ABI library (include/lasp2_b200.h).
+
+The library is the product: there is no Python or CPU fallback. If the
+shared object is missing or a CUDA device is absent, every compute call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import re
+import threading
+from pathlib import Path
+
+import torch
+
+LIB_PATH = Path(__file__).resolve().parent / "liblasp2_b200.so"
+HEADER = Path(__file__).resolve().parent.parent / "include" / "lasp2_b200.h"
+
+F32, F64, BF16 = 0, 1, 2
+FOLD_PREFIX, FOLD_SUFFIX, FOLD_FULL = 0, 1, 2
+
+_i64 = ctypes.c_int64
+_int = ctypes.c_int
+_vp = ctypes.c_void_p
+_u64 = ctypes.c_uint64
+
+# name -> (restype, argtypes); must match include/lasp2_b200.h
+SIGNATURES = {
+    "lasp2_version": (_int, []),
+    "lasp2_last_error": (ctypes.c_char_p, []),
+    "lasp2_num_segments": (_int, [_int, _i64, _i64, _int, _int]),
+    "lasp2_segment_states": (_int, [_int, _vp, _vp, _vp, _i64, _i64, _int, _int, _vp]),
+    "lasp2_scan_segments": (_int, [_int, _vp, _vp, _i64, _int, _int, _int, _vp]),
+    "lasp2_fold_states": (_int, [_int, _vp, _vp, _int, _i64, _int, _int, _vp]),
+    "lasp2_causal_chunk": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _int, _int, _int, _int, _vp]),
+    "lasp2_apply_state": (_int, [_int, _vp, _vp, _vp, _i64, _i64, _int, _int, _int, _vp]),
+    "lasp2h_softmax_forward": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _i64, _i64, _i64,
+                                      _vp]),
+    "lasp2h_softmax_backward": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int,
+                                       _int, _i64, _i64, _i64, _i64, _vp]),
+    "lasp2h_softmax_scratch_bytes": (_i64, [_int, _i64, _i64, _i64, _int]),
+    "lasp2_gen_slots": (_int, [_int, _u64, _vp, _vp, _i64, _i64, _i64, _vp]),
+    "lasp2_debug_probe_gemm": (_int, [_vp, _vp, _vp, _int, _int, _vp]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+class LaspError(RuntimeError):
+    """A C-ABI call returned a non-zero status."""
+
+
+def header_symbols() -> list[str]:
+    """Function names declared in include/lasp2_b200.h."""
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(lasp2h?_\w+)\s*\(", text, re.M)))
+
+
+def load() -> ctypes.CDLL:
+    """Load (once) and type the shared library; raises if it was not built."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise FileNotFoundError(
+                    f"{LIB_PATH} is missing: build it with `python -m paper_2502_07563_b200.build` "
+                    "(there is no CPU fallback)")
+            lib = ctypes.CDLL(str(LIB_PATH))
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def call(name: str, *args) -> int:
+    lib = load()
+    status = getattr(lib, name)(*args)
+    if status != 0:
+        msg = lib.lasp2_last_error().decode()
+        if status == 1:
+            raise ValueError(f"{name}: {msg}")
+        raise LaspError(f"{name} failed (status {status}): {msg}")
+    return status
+
+
+def dtype_code(dt: torch.dtype) -> int:
+    if dt == torch.float32:
+        return F32
+    if dt == torch.float64:
+        return F64
+    if dt == torch.bfloat16:
+        return BF16
+    raise ValueError(f"unsupported dtype {dt}; expected float64, float32 or bfloat16")
+
+
+def state_dtype(dt: torch.dtype) -> torch.dtype:
+    """Memory states / gathered payloads: f64 for f64 data, else f32."""
+    return torch.float64 if dt == torch.float64 else torch.float32
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def require_cuda(*tensors: torch.Tensor) -> None:
+    for t in tensors:
+        if t is None:
+            continue
+        if not t.is_cuda:
+            raise ValueError("LASP-2 B200 kernels need CUDA tensors (no CPU fallback)")
+        if not t.is_contiguous():
+            raise ValueError("LASP-2 B200 kernels need contiguous BHND tensors")

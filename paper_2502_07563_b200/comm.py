@@ -1,0 +1,558 @@
+"""Rank contexts for the LASP-2 hot path: the only collectives it needs.
+
+Two implementations of one small interface (the subset of the reference's
+RankContext that the hot path calls, comm.py:251-436):
+
+* ``RankContext`` inside ``world_spawn`` — W ranks as host threads sharing one
+  GPU, each with its own CUDA stream. It mirrors the reference simulator
+  (threads-as-ranks, comm.py:465-531): payloads are snapshotted at hand-off,
+  one collective launch per group per call, per-rank ledgers, a global trace,
+  bounded waits that raise ``DeadlockError``. It lets every multi-rank parity
+  test run on a single B200.
+* ``DistRankContext`` — one process per GPU under torchrun; all_gather /
+  reduce_scatter go to NCCL (``torch.distributed``) on a side stream so they
+  overlap compute on the main stream; gloo works the same on CPU tensors.
+
+Interface: ``sp_position``, ``sp_size``, ``all_gather_async(t) -> Pending``,
+``all_gather(t)`` (returns the rank-ordered contributions stacked on a new
+leading axis — the NCCL all_gather_into_tensor layout), ``reduce_scatter(t)``,
+``mark(kind)``, ``stats`` (CommStats) and ``trace``.
+"""
+from __future__ import annotations
+
+import threading
+import time
+from collections.abc import Callable, Sequence
+from dataclasses import dataclass, field
+from typing import Any
+
+import torch
+
+
+class CommError(Exception):
+    """Base class for runtime communication failures (comm.py:31)."""
+
+
+class DeadlockError(CommError):
+    """A rank blocked past the configured timeout (comm.py:35)."""
+
+
+class CollectiveError(CommError):
+    """Participants disagreed about a collective's payload (comm.py:39)."""
+
+
+class WorldAbortedError(CommError):
+    """Another rank failed first (comm.py:43)."""
+
+
+@dataclass(frozen=True)
+class WorldConfig:
+    """World layout (reference comm.py:51-87).
+
+    world_size ranks form contiguous SP groups of sp_size; ranks at the same
+    position across groups are DP peers. element_bytes is the data element
+    size: 8 (f64), 4 (f32) or 2 (bf16, which exchanges f32 states). The
+    latency fields exist for signature compatibility; real time is measured.
+    """
+
+    world_size: int
+    sp_size: int | None = None
+    element_bytes: int = 8
+    latency_per_launch: float = 10.0
+    latency_per_byte: float = 1.0 / 1024.0
+    deadlock_timeout: float = 120.0
+
+    def __post_init__(self) -> None:
+        if self.sp_size is None:
+            object.__setattr__(self, "sp_size", self.world_size)
+        if self.world_size < 1:
+            raise ValueError(f"world_size must be >= 1, got {self.world_size}")
+        if self.sp_size < 1:
+            raise ValueError(f"sp_size must be >= 1, got {self.sp_size}")
+        if self.world_size % self.sp_size != 0:
+            raise ValueError(f"sp_size {self.sp_size} must divide world_size {self.world_size}")
+        if self.element_bytes not in (2, 4, 8):
+            raise ValueError(f"element_bytes must be 2, 4 or 8, got {self.element_bytes}")
+        if self.deadlock_timeout <= 0:
+            raise ValueError("deadlock_timeout must be positive")
+
+    @property
+    def dp_size(self) -> int:
+        return self.world_size // self.sp_size
+
+
+@dataclass
+class CommStats:
+    """Per-rank ledger (comm.py:90-105). One step = one collective launch."""
+
+    p2p_sends: int = 0
+    p2p_recvs: int = 0
+    allgather_launches: int = 0
+    reduce_scatter_launches: int = 0
+    bytes_sent: int = 0
+    communication_steps: int = 0
+    bytes_by_primitive: dict[str, int] = field(default_factory=dict)
+
+    def _account(self, primitive: str, nbytes: int) -> None:
+        self.bytes_sent += nbytes
+        self.bytes_by_primitive[primitive] = self.bytes_by_primitive.get(primitive, 0) + nbytes
+
+
+@dataclass(frozen=True)
+class TraceEvent:
+    seq: int
+    rank: int
+    clock: float
+    kind: str
+    detail: str = ""
+
+
+@dataclass(frozen=True)
+class GroupInfo:
+    dp_peers: tuple[int, ...]
+    sp_peers: tuple[int, ...]
+    sp_position: int
+
+
+def process_groups(cfg: WorldConfig) -> dict[int, GroupInfo]:
+    """Contiguous SP groups, strided DP peers (comm.py:143-158)."""
+    t = cfg.sp_size
+    out = {}
+    for rank in range(cfg.world_size):
+        g, pos = divmod(rank, t)
+        out[rank] = GroupInfo(dp_peers=tuple(gg * t + pos for gg in range(cfg.dp_size)),
+                              sp_peers=tuple(range(g * t, (g + 1) * t)), sp_position=pos)
+    return out
+
+
+class _ContextBase:
+    """Shared trace / device-event bookkeeping."""
+
+    rank: int
+    stats: CommStats
+
+    def _init_common(self) -> None:
+        self.stats = CommStats()
+        self.device_events: list[tuple[str, torch.cuda.Event]] = []
+
+    def _device_mark(self, kind: str, stream=None) -> None:
+        if torch.cuda.is_available() and torch.cuda.is_initialized():
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(stream if stream is not None else torch.cuda.current_stream())
+            self.device_events.append((kind, ev))
+
+    def device_timeline(self) -> dict[str, list[float]]:
+        """Milliseconds of every device mark relative to the first (call after a sync)."""
+        if not self.device_events:
+            return {}
+        t0 = self.device_events[0][1]
+        out: dict[str, list[float]] = {}
+        for kind, ev in self.device_events:
+            out.setdefault(kind, []).append(t0.elapsed_time(ev))
+        return out
+
+
+# ----------------------------------------------------------------------------
+# Threads-as-ranks world on one GPU
+# ----------------------------------------------------------------------------
+
+class _Gen:
+    __slots__ = ("shape", "dtype", "contributions", "complete", "error", "kind")
+
+    def __init__(self, kind: str) -> None:
+        self.kind = kind
+        self.shape = None
+        self.dtype = None
+        self.contributions: dict[int, tuple[torch.Tensor, Any]] = {}
+        self.complete = False
+        self.error: CollectiveError | None = None
+
+
+class _World:
+    def __init__(self, cfg: WorldConfig, device: torch.device) -> None:
+        self.cfg = cfg
+        self.device = device
+        self.cond = threading.Condition(threading.Lock())
+        self.trace: list[TraceEvent] = []
+        self.abort_error: BaseException | None = None
+        self.collective_launches = 0
+        self.reduce_scatter_launches = 0
+        t = cfg.sp_size
+        self.groups = [tuple(range(g * t, (g + 1) * t)) for g in range(cfg.dp_size)]
+        self.gens: dict[tuple[int, int], _Gen] = {}
+        self.t0 = time.perf_counter()
+
+    def record(self, rank: int, kind: str, detail: str) -> None:
+        self.trace.append(TraceEvent(len(self.trace), rank, time.perf_counter() - self.t0, kind, detail))
+
+    def abort(self, err: BaseException) -> None:
+        if self.abort_error is None:
+            self.abort_error = err
+        self.cond.notify_all()
+
+
+class PendingGather:
+    """Handle of an issued all_gather; wait() returns [T, *payload.shape]."""
+
+    def __init__(self, ctx: "RankContext", key: tuple[int, int], tag: str) -> None:
+        self._ctx = ctx
+        self._key = key
+        self._tag = tag
+        self._result: torch.Tensor | None = None
+
+    def wait(self) -> torch.Tensor:
+        if self._result is not None:
+            return self._result
+        ctx = self._ctx
+        world = ctx.world
+        gen = world.gens[self._key]
+        with world.cond:
+            ctx._wait_locked(lambda: gen.complete or gen.error is not None,
+                             lambda: f"all_gather call {self._key[1]} stalled: contributions from "
+                                     f"{sorted(gen.contributions)}, group {ctx.sp_peers}")
+            if gen.error is not None:
+                raise CollectiveError(*gen.error.args)
+            parts = [gen.contributions[r] for r in ctx.sp_peers]
+        stream = torch.cuda.current_stream()
+        for _, ev in parts:
+            stream.wait_event(ev)
+        result = torch.stack([p for p, _ in parts])
+        ctx._device_mark("all_gather_complete")
+        with world.cond:
+            world.record(ctx.rank, "all_gather_complete", f"call={self._key[1]} tag={self._tag}")
+        self._result = result
+        return result
+
+
+class RankContext(_ContextBase):
+    """One rank's handle inside ``world_spawn`` (reference comm.py:251-436)."""
+
+    def __init__(self, world: _World, rank: int) -> None:
+        self._init_common()
+        self.world = world
+        self.rank = rank
+        self._group_index = rank // world.cfg.sp_size
+        self._calls = 0
+        self.stream = torch.cuda.Stream(device=world.device)
+
+    @property
+    def config(self) -> WorldConfig:
+        return self.world.cfg
+
+    @property
+    def world_size(self) -> int:
+        return self.world.cfg.world_size
+
+    @property
+    def sp_peers(self) -> tuple[int, ...]:
+        return self.world.groups[self._group_index]
+
+    @property
+    def sp_position(self) -> int:
+        return self.rank - self.sp_peers[0]
+
+    @property
+    def sp_size(self) -> int:
+        return len(self.sp_peers)
+
+    @property
+    def dp_peers(self) -> tuple[int, ...]:
+        t = self.world.cfg.sp_size
+        return tuple(g * t + self.sp_position for g in range(self.world.cfg.dp_size))
+
+    def _wait_locked(self, cond_fn: Callable[[], bool], describe: Callable[[], str]) -> None:
+        deadline = time.monotonic() + self.world.cfg.deadlock_timeout
+        while True:
+            if self.world.abort_error is not None:
+                raise WorldAbortedError(f"rank {self.rank}: aborted by {self.world.abort_error!r}")
+            if cond_fn():
+                return
+            remaining = deadline - time.monotonic()
+            if remaining <= 0:
+                err = DeadlockError(f"rank {self.rank}: {describe()}")
+                self.world.abort(err)
+                raise err
+            self.world.cond.wait(min(0.05, remaining))
+
+    def _contribute(self, payload: torch.Tensor, tag: str, kind: str) -> tuple[tuple[int, int], int]:
+        if not payload.is_cuda:
+            raise ValueError("collective payloads must be CUDA tensors")
+        snap = payload.detach().clone()  # frozen snapshot at hand-off (comm.py:299-302)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        nbytes = snap.numel() * snap.element_size()
+        world = self.world
+        with world.cond:
+            if world.abort_error is not None:
+                raise WorldAbortedError(f"rank {self.rank}: aborted by {world.abort_error!r}")
+            call = self._calls
+            self._calls += 1
+            key = (self._group_index, call)
+            gen = world.gens.setdefault(key, _Gen(kind))
+            if gen.error is not None:
+                raise CollectiveError(*gen.error.args)
+            if gen.kind != kind:
+                gen.error = CollectiveError(f"call {call}: rank {self.rank} issued {kind}, group issued {gen.kind}")
+                world.cond.notify_all()
+                raise gen.error
+            if gen.shape is None:
+                gen.shape, gen.dtype = tuple(snap.shape), snap.dtype
+            elif tuple(snap.shape) != gen.shape or snap.dtype != gen.dtype:
+                gen.error = CollectiveError(
+                    f"{kind} call {call}: rank {self.rank} contributed {tuple(snap.shape)} {snap.dtype}, "
+                    f"generation pinned to {gen.shape} {gen.dtype}")
+                world.cond.notify_all()
+                raise gen.error
+            world.record(self.rank, f"{kind}_issue", f"call={call} tag={tag} bytes={nbytes}")
+            gen.contributions[self.rank] = (snap, ev)
+            if len(gen.contributions) == len(self.sp_peers):
+                gen.complete = True
+                if kind == "all_gather":
+                    world.collective_launches += 1
+                else:
+                    world.reduce_scatter_launches += 1
+                world.cond.notify_all()
+        self._device_mark(f"{kind}_issue")
+        return key, nbytes
+
+    def all_gather_async(self, payload: torch.Tensor, tag: str = "") -> PendingGather:
+        key, nbytes = self._contribute(payload, tag, "all_gather")
+        self.stats.allgather_launches += 1
+        self.stats.communication_steps += 1
+        self.stats._account("all_gather", nbytes)
+        return PendingGather(self, key, tag)
+
+    def all_gather(self, payload: torch.Tensor, tag: str = "") -> torch.Tensor:
+        return self.all_gather_async(payload, tag).wait()
+
+    def reduce_scatter(self, stacked: torch.Tensor, tag: str = "") -> torch.Tensor:
+        """Sum of every rank's ``stacked[my_position]``, folded in ascending rank order."""
+        if stacked.shape[0] != self.sp_size:
+            raise ValueError(f"reduce_scatter expects a leading axis of {self.sp_size}, got {tuple(stacked.shape)}")
+        key, nbytes = self._contribute(stacked, tag, "reduce_scatter")
+        self.stats.reduce_scatter_launches += 1
+        self.stats.communication_steps += 1
+        self.stats._account("reduce_scatter", nbytes)
+        world = self.world
+        gen = world.gens[key]
+        with world.cond:
+            self._wait_locked(lambda: gen.complete or gen.error is not None,
+                              lambda: f"reduce_scatter call {key[1]} stalled")
+            if gen.error is not None:
+                raise CollectiveError(*gen.error.args)
+            parts = [gen.contributions[r] for r in self.sp_peers]
+        stream = torch.cuda.current_stream()
+        for _, ev in parts:
+            stream.wait_event(ev)
+        pos = self.sp_position
+        acc = parts[0][0][pos].clone()
+        for p, _ in parts[1:]:
+            acc += p[pos]
+        self._device_mark("reduce_scatter_complete")
+        return acc
+
+    def barrier(self) -> None:
+        self.all_gather(torch.zeros(1, device=self.world.device), tag="barrier")
+
+    def mark(self, kind: str, detail: str = "") -> None:
+        with self.world.cond:
+            self.world.record(self.rank, kind, detail)
+        self._device_mark(kind)
+
+
+@dataclass
+class WorldRun:
+    """Everything a completed world leaves behind (comm.py:439-448)."""
+
+    config: WorldConfig
+    results: list[Any]
+    rank_stats: list[CommStats]
+    stats: CommStats
+    trace: list[TraceEvent]
+    device_timelines: list[dict[str, list[float]]]
+    wall_seconds: float
+
+
+def _merge_stats(rank_stats: Sequence[CommStats], ag_launches: int, rs_launches: int) -> CommStats:
+    merged = CommStats()
+    for st in rank_stats:
+        merged.p2p_sends += st.p2p_sends
+        merged.p2p_recvs += st.p2p_recvs
+        merged.bytes_sent += st.bytes_sent
+        for key, val in st.bytes_by_primitive.items():
+            merged.bytes_by_primitive[key] = merged.bytes_by_primitive.get(key, 0) + val
+    merged.allgather_launches = ag_launches
+    merged.reduce_scatter_launches = rs_launches
+    merged.communication_steps = merged.p2p_sends + ag_launches + rs_launches
+    return merged
+
+
+def world_spawn(cfg: WorldConfig, program: Callable[..., Any], rank_args: Sequence[tuple] | None = None,
+                device: torch.device | None = None) -> WorldRun:
+    """Run program(ctx, *rank_args[rank]) on one host thread per rank, all on one GPU (comm.py:465-531)."""
+    if rank_args is not None and len(rank_args) != cfg.world_size:
+        raise ValueError(f"rank_args has {len(rank_args)} entries for {cfg.world_size} ranks")
+    if not torch.cuda.is_available():
+        raise RuntimeError("world_spawn needs a CUDA device (the LASP-2 B200 path has no CPU fallback)")
+    device = device or torch.device("cuda", torch.cuda.current_device())
+    world = _World(cfg, device)
+    ctxs = [RankContext(world, r) for r in range(cfg.world_size)]
+    results: list[Any] = [None] * cfg.world_size
+    errors: list[BaseException | None] = [None] * cfg.world_size
+    launcher = torch.cuda.current_stream(device)
+    for ctx in ctxs:
+        ctx.stream.wait_stream(launcher)
+
+    def runner(ctx: RankContext) -> None:
+        args = rank_args[ctx.rank] if rank_args is not None else ()
+        try:
+            torch.cuda.set_device(device)
+            with torch.cuda.stream(ctx.stream):
+                ctx._device_mark("start")
+                results[ctx.rank] = program(ctx, *args)
+        except BaseException as exc:  # noqa: BLE001 - re-raised below
+            errors[ctx.rank] = exc
+            with world.cond:
+                world.abort(exc)
+
+    t0 = time.perf_counter()
+    threads = [threading.Thread(target=runner, args=(c,), name=f"rank{c.rank}") for c in ctxs]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    torch.cuda.synchronize(device)
+    wall = time.perf_counter() - t0
+    for ctx in ctxs:
+        launcher.wait_stream(ctx.stream)
+
+    primary = next((e for e in errors if e is not None and not isinstance(e, WorldAbortedError)), None)
+    if primary is None:
+        primary = next((e for e in errors if e is not None), None)
+    if primary is not None:
+        raise primary
+    return WorldRun(config=cfg, results=results, rank_stats=[c.stats for c in ctxs],
+                    stats=_merge_stats([c.stats for c in ctxs], world.collective_launches,
+                                       world.reduce_scatter_launches),
+                    trace=list(world.trace), device_timelines=[c.device_timeline() for c in ctxs],
+                    wall_seconds=wall)
+
+
+# ----------------------------------------------------------------------------
+# One process per GPU (torchrun): NCCL on a side stream, gloo on CPU
+# ----------------------------------------------------------------------------
+
+class DistPending:
+    def __init__(self, ctx: "DistRankContext", work, out: torch.Tensor, tag: str) -> None:
+        self._ctx = ctx
+        self._work = work
+        self._out = out
+        self._tag = tag
+        self._done = False
+
+    def wait(self) -> torch.Tensor:
+        if not self._done:
+            ctx = self._ctx
+            if self._out.is_cuda:
+                with torch.cuda.stream(ctx.comm_stream):
+                    self._work.wait()
+                    ctx._device_mark("all_gather_complete", ctx.comm_stream)
+                torch.cuda.current_stream().wait_stream(ctx.comm_stream)
+                self._out.record_stream(torch.cuda.current_stream())
+            else:
+                self._work.wait()
+            ctx.trace.append(TraceEvent(len(ctx.trace), ctx.rank, time.perf_counter(), "all_gather_complete",
+                                        f"tag={self._tag}"))
+            self._done = True
+        return self._out
+
+
+class DistRankContext(_ContextBase):
+    """Rank context over an initialised torch.distributed default group.
+
+    SP groups are contiguous blocks of ``sp_size`` ranks (comm.py:143-158);
+    every process must construct its context (new_group is collective).
+    """
+
+    def __init__(self, sp_size: int | None = None) -> None:
+        import torch.distributed as dist
+
+        self._init_common()
+        self.dist = dist
+        self.rank = dist.get_rank()
+        world = dist.get_world_size()
+        sp = sp_size or world
+        if world % sp:
+            raise ValueError(f"sp_size {sp} must divide world size {world}")
+        self._sp_size = sp
+        self._group = None
+        if sp == world:
+            self._group = dist.group.WORLD
+        else:
+            for g in range(world // sp):
+                ranks = list(range(g * sp, (g + 1) * sp))
+                pg = dist.new_group(ranks)
+                if self.rank in ranks:
+                    self._group = pg
+        self.trace: list[TraceEvent] = []
+        self.comm_stream = torch.cuda.Stream() if torch.cuda.is_available() else None
+
+    @property
+    def sp_position(self) -> int:
+        return self.rank % self._sp_size
+
+    @property
+    def sp_size(self) -> int:
+        return self._sp_size
+
+    def _account(self, kind: str, t: torch.Tensor) -> None:
+        nbytes = t.numel() * t.element_size()
+        if kind == "all_gather":
+            self.stats.allgather_launches += 1
+        else:
+            self.stats.reduce_scatter_launches += 1
+        self.stats.communication_steps += 1
+        self.stats._account(kind, nbytes)
+        self.trace.append(TraceEvent(len(self.trace), self.rank, time.perf_counter(), f"{kind}_issue",
+                                     f"bytes={nbytes}"))
+
+    def all_gather_async(self, payload: torch.Tensor, tag: str = "") -> DistPending:
+        payload = payload.contiguous()
+        if payload.ndim == 0:
+            payload = payload.reshape(1)
+        # gathered along dim 0 (the layout gloo and NCCL both accept), viewed [T, *payload.shape]
+        flat = torch.empty((self._sp_size * payload.shape[0], *payload.shape[1:]), dtype=payload.dtype,
+                           device=payload.device)
+        out = flat.view(self._sp_size, *payload.shape)
+        self._account("all_gather", payload)
+        if payload.is_cuda:
+            cur = torch.cuda.current_stream()
+            self.comm_stream.wait_stream(cur)
+            with torch.cuda.stream(self.comm_stream):
+                self._device_mark("all_gather_issue", self.comm_stream)
+                work = self.dist.all_gather_into_tensor(flat, payload, group=self._group, async_op=True)
+            payload.record_stream(self.comm_stream)
+            flat.record_stream(self.comm_stream)
+        else:
+            work = self.dist.all_gather_into_tensor(flat, payload, group=self._group, async_op=True)
+        return DistPending(self, work, out, tag)
+
+    def all_gather(self, payload: torch.Tensor, tag: str = "") -> torch.Tensor:
+        return self.all_gather_async(payload, tag).wait()
+
+    def reduce_scatter(self, stacked: torch.Tensor, tag: str = "") -> torch.Tensor:
+        if stacked.shape[0] != self._sp_size:
+            raise ValueError(f"reduce_scatter expects a leading axis of {self._sp_size}, got {tuple(stacked.shape)}")
+        stacked = stacked.contiguous()
+        out = torch.empty(stacked.shape[1:], dtype=stacked.dtype, device=stacked.device)
+        self._account("reduce_scatter", stacked)
+        flat_in = stacked.view(-1)
+        self.dist.reduce_scatter_tensor(out.view(-1), flat_in, group=self._group)
+        return out
+
+    def barrier(self) -> None:
+        self.dist.barrier(group=self._group)
+
+    def mark(self, kind: str, detail: str = "") -> None:
+        self.trace.append(TraceEvent(len(self.trace), self.rank, time.perf_counter(), kind, detail))
+        self._device_mark(kind)

@@ -1,0 +1,232 @@
+// extern "C" entry points declared in include/lasp2_b200.h.
+//
+// Validation and dtype dispatch only: argument errors return
+// LASP2_ERR_INVALID, CUDA failures LASP2_ERR_CUDA, and lasp2_last_error()
+// carries the message. No exception crosses this boundary.
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+
+#include "../../include/lasp2_b200.h"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* msg) {
+  g_err = msg;
+  return code;
+}
+int cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) {
+    g_err.clear();
+    return LASP2_OK;
+  }
+  char buf[256];
+  snprintf(buf, sizeof(buf), "%s: %s", where, cudaGetErrorString(e));
+  g_err = buf;
+  return LASP2_ERR_CUDA;
+}
+int sm_count_current() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+bool valid_dtype(int dt) { return dt == LASP2_F32 || dt == LASP2_F64 || dt == LASP2_BF16; }
+bool use_tc(int dtype, int dim, int64_t tokens) { return dtype == LASP2_BF16 && lasp::tc_supported(dim, tokens); }
+cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+#define CHECK(cond, msg) \
+  if (!(cond)) return fail(LASP2_ERR_INVALID, msg)
+
+}  // namespace
+
+extern "C" {
+
+int lasp2_version(void) { return 100; }
+
+const char* lasp2_last_error(void) { return g_err.c_str(); }
+
+int lasp2_num_segments(int dtype, int64_t slots, int64_t tokens, int dim, int sm_count) {
+  if (slots < 1 || tokens < 1) return 1;
+  if (sm_count < 1) sm_count = 148;
+  const int64_t nblk = (tokens + LASP_BLOCK_TOKENS - 1) / LASP_BLOCK_TOKENS;
+  // tcgen05 kernels run one CTA per SM: fill one wave exactly. SIMT kernels
+  // are shorter-lived: two CTAs per SM.
+  const int64_t waves = use_tc(dtype, dim, tokens) ? 1 : 2;
+  int64_t nseg = (waves * sm_count) / slots;
+  if (nseg < 1) nseg = 1;
+  if (nseg > nblk) nseg = nblk;
+  if (nseg > 65535) nseg = 65535;
+  return (int)nseg;
+}
+
+int lasp2_segment_states(int dtype, const void* x, const void* y, void* seg_states, int64_t slots, int64_t tokens,
+                         int dim, int nseg, void* stream) {
+  CHECK(valid_dtype(dtype), "segment_states: unknown dtype");
+  CHECK(x && y && seg_states, "segment_states: null pointer");
+  CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128, "segment_states: bad shape (1 <= dim <= 128)");
+  CHECK(nseg >= 1 && nseg <= (tokens + LASP_BLOCK_TOKENS - 1) / LASP_BLOCK_TOKENS, "segment_states: bad nseg");
+  cudaError_t e;
+  if (use_tc(dtype, dim, tokens))
+    e = lasp::tc_segment_states(x, y, (float*)seg_states, slots, tokens, dim, nseg, S(stream));
+  else if (dtype == LASP2_F32)
+    e = lasp::simt_segment_states<float, float>(x, y, seg_states, slots, tokens, dim, nseg, S(stream));
+  else if (dtype == LASP2_F64)
+    e = lasp::simt_segment_states<double, double>(x, y, seg_states, slots, tokens, dim, nseg, S(stream));
+  else
+    e = lasp::simt_segment_states<__nv_bfloat16, float>(x, y, seg_states, slots, tokens, dim, nseg, S(stream));
+  return cuda_status(e, "segment_states");
+}
+
+int lasp2_scan_segments(int dtype, void* seg_states, void* chunk_total, int64_t slots, int nseg, int dim, int reverse,
+                        void* stream) {
+  CHECK(valid_dtype(dtype), "scan_segments: unknown dtype");
+  CHECK(seg_states, "scan_segments: null pointer");
+  CHECK(slots >= 1 && nseg >= 1 && dim >= 1, "scan_segments: bad shape");
+  cudaError_t e = dtype == LASP2_F64 ? lasp::scan_states<double>(seg_states, chunk_total, slots, nseg, dim, reverse,
+                                                                 S(stream))
+                                     : lasp::scan_states<float>(seg_states, chunk_total, slots, nseg, dim, reverse,
+                                                                S(stream));
+  return cuda_status(e, "scan_segments");
+}
+
+int lasp2_fold_states(int dtype, const void* gathered, void* out, int nstates, int64_t elems, int mode, int bound,
+                      void* stream) {
+  CHECK(valid_dtype(dtype), "fold_states: unknown dtype");
+  CHECK(gathered && out, "fold_states: null pointer");
+  CHECK(nstates >= 1 && elems >= 1, "fold_states: bad shape");
+  CHECK(mode >= 0 && mode <= 2, "fold_states: bad mode");
+  CHECK(mode == LASP2_FOLD_FULL || (bound >= 0 && bound <= nstates), "fold_states: bound outside [0, nstates]");
+  cudaError_t e = dtype == LASP2_F64
+                      ? lasp::fold_states<double>(gathered, out, nstates, elems, mode, bound, S(stream))
+                      : lasp::fold_states<float>(gathered, out, nstates, elems, mode, bound, S(stream));
+  return cuda_status(e, "fold_states");
+}
+
+int lasp2_causal_chunk(int dtype, const void* q, const void* k, const void* v, const void* seg_states,
+                       const void* base, void* out, int64_t slots, int64_t tokens, int dim, int nseg, int reverse,
+                       int transpose_state, void* stream) {
+  CHECK(valid_dtype(dtype), "causal_chunk: unknown dtype");
+  CHECK(q && k && v && out, "causal_chunk: null pointer");
+  CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128, "causal_chunk: bad shape (1 <= dim <= 128)");
+  CHECK(nseg >= 1 && nseg <= (tokens + LASP_BLOCK_TOKENS - 1) / LASP_BLOCK_TOKENS, "causal_chunk: bad nseg");
+  CHECK(nseg == 1 || seg_states, "causal_chunk: nseg > 1 needs segment states");
+  cudaError_t e;
+  if (use_tc(dtype, dim, tokens))
+    e = lasp::tc_causal_chunk(q, k, v, (const float*)seg_states, (const float*)base, out, slots, tokens, dim, nseg,
+                              reverse, transpose_state, S(stream));
+  else if (dtype == LASP2_F32)
+    e = lasp::simt_causal_chunk<float, float>(q, k, v, seg_states, base, out, slots, tokens, dim, nseg, reverse,
+                                              transpose_state, S(stream));
+  else if (dtype == LASP2_F64)
+    e = lasp::simt_causal_chunk<double, double>(q, k, v, seg_states, base, out, slots, tokens, dim, nseg, reverse,
+                                                transpose_state, S(stream));
+  else
+    e = lasp::simt_causal_chunk<__nv_bfloat16, float>(q, k, v, seg_states, base, out, slots, tokens, dim, nseg,
+                                                      reverse, transpose_state, S(stream));
+  return cuda_status(e, "causal_chunk");
+}
+
+int lasp2_apply_state(int dtype, const void* x, const void* m, void* out, int64_t slots, int64_t tokens, int dim,
+                      int transpose, int accumulate, void* stream) {
+  CHECK(valid_dtype(dtype), "apply_state: unknown dtype");
+  CHECK(x && m && out, "apply_state: null pointer");
+  CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128, "apply_state: bad shape (1 <= dim <= 128)");
+  cudaError_t e;
+  if (use_tc(dtype, dim, tokens))
+    e = lasp::tc_apply_state(x, (const float*)m, out, slots, tokens, dim, transpose, accumulate, sm_count_current(),
+                             S(stream));
+  else if (dtype == LASP2_F32)
+    e = lasp::simt_apply_state<float, float>(x, m, out, slots, tokens, dim, transpose, accumulate, S(stream));
+  else if (dtype == LASP2_F64)
+    e = lasp::simt_apply_state<double, double>(x, m, out, slots, tokens, dim, transpose, accumulate, S(stream));
+  else
+    e = lasp::simt_apply_state<__nv_bfloat16, float>(x, m, out, slots, tokens, dim, transpose, accumulate,
+                                                     S(stream));
+  return cuda_status(e, "apply_state");
+}
+
+int lasp2h_softmax_forward(int dtype, const void* q, const void* k_full, const void* v_full, void* out, void* lse,
+                           int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim, int causal, int64_t row_offset,
+                           int64_t kv_chunk, int64_t kv_rank_stride, void* stream) {
+  CHECK(valid_dtype(dtype), "softmax_forward: unknown dtype");
+  CHECK(q && k_full && v_full && out && lse, "softmax_forward: null pointer");
+  CHECK(slots >= 1 && q_tokens >= 1 && kv_tokens >= 1 && dim >= 1 && dim <= 128, "softmax_forward: bad shape");
+  CHECK(row_offset >= 0 && (!causal || row_offset < kv_tokens), "softmax_forward: bad row_offset");
+  CHECK(kv_chunk >= 1 && kv_tokens % kv_chunk == 0, "softmax_forward: kv_chunk must divide kv_tokens");
+  cudaError_t e;
+  if (dtype == LASP2_F32)
+    e = lasp::simt_softmax_forward<float, float>(q, k_full, v_full, out, (float*)lse, slots, q_tokens, kv_tokens, dim,
+                                                 causal, row_offset, kv_chunk, kv_rank_stride, S(stream));
+  else if (dtype == LASP2_F64)
+    e = lasp::simt_softmax_forward<double, double>(q, k_full, v_full, out, (float*)lse, slots, q_tokens, kv_tokens,
+                                                   dim, causal, row_offset, kv_chunk, kv_rank_stride, S(stream));
+  else
+    e = lasp::simt_softmax_forward<__nv_bfloat16, float>(q, k_full, v_full, out, (float*)lse, slots, q_tokens,
+                                                         kv_tokens, dim, causal, row_offset, kv_chunk, kv_rank_stride,
+                                                         S(stream));
+  return cuda_status(e, "softmax_forward");
+}
+
+int64_t lasp2h_softmax_scratch_bytes(int dtype, int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim) {
+  (void)kv_tokens;
+  (void)dim;
+  const int64_t eb = dtype == LASP2_F64 ? 8 : 4;
+  return 3 * slots * q_tokens * eb + 256;
+}
+
+int lasp2h_softmax_backward(int dtype, const void* q, const void* k_full, const void* v_full, const void* out,
+                            const void* lse, const void* d_out, void* dq, void* dk_full, void* dv_full, void* scratch,
+                            int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim, int causal,
+                            int64_t row_offset, int64_t kv_chunk, int64_t kv_rank_stride, int64_t grad_rank_stride,
+                            void* stream) {
+  (void)lse;
+  CHECK(valid_dtype(dtype), "softmax_backward: unknown dtype");
+  CHECK(q && k_full && v_full && out && d_out && dq && dk_full && dv_full && scratch,
+        "softmax_backward: null pointer");
+  CHECK(slots >= 1 && q_tokens >= 1 && kv_tokens >= 1 && dim >= 1 && dim <= 128, "softmax_backward: bad shape");
+  CHECK(row_offset >= 0 && (!causal || row_offset < kv_tokens), "softmax_backward: bad row_offset");
+  CHECK(kv_chunk >= 1 && kv_tokens % kv_chunk == 0, "softmax_backward: kv_chunk must divide kv_tokens");
+  cudaError_t e;
+  if (dtype == LASP2_F32)
+    e = lasp::simt_softmax_backward<float, float, float>(q, k_full, v_full, out, d_out, dq, dk_full, dv_full, scratch,
+                                                         slots, q_tokens, kv_tokens, dim, causal, row_offset,
+                                                         kv_chunk, kv_rank_stride, grad_rank_stride, S(stream));
+  else if (dtype == LASP2_F64)
+    e = lasp::simt_softmax_backward<double, double, double>(q, k_full, v_full, out, d_out, dq, dk_full, dv_full,
+                                                            scratch, slots, q_tokens, kv_tokens, dim, causal,
+                                                            row_offset, kv_chunk, kv_rank_stride, grad_rank_stride,
+                                                            S(stream));
+  else
+    e = lasp::simt_softmax_backward<__nv_bfloat16, float, float>(q, k_full, v_full, out, d_out, dq, dk_full, dv_full,
+                                                                 scratch, slots, q_tokens, kv_tokens, dim, causal,
+                                                                 row_offset, kv_chunk, kv_rank_stride, grad_rank_stride,
+                                                                 S(stream));
+  return cuda_status(e, "softmax_backward");
+}
+
+int lasp2_gen_slots(int dtype, uint64_t seed, const uint64_t* tag_words_device, void* out, int64_t slots, int64_t rows,
+                    int64_t cols, void* stream) {
+  CHECK(valid_dtype(dtype), "gen_slots: unknown dtype");
+  CHECK(tag_words_device && out, "gen_slots: null pointer");
+  CHECK(slots >= 1 && rows >= 1 && cols >= 1, "gen_slots: shape must be positive");
+  cudaError_t e;
+  if (dtype == LASP2_F32)
+    e = lasp::gen_slots<float>(seed, tag_words_device, out, slots, rows, cols, S(stream));
+  else if (dtype == LASP2_F64)
+    e = lasp::gen_slots<double>(seed, tag_words_device, out, slots, rows, cols, S(stream));
+  else
+    e = lasp::gen_slots<__nv_bfloat16>(seed, tag_words_device, out, slots, rows, cols, S(stream));
+  return cuda_status(e, "gen_slots");
+}
+
+int lasp2_debug_probe_gemm(const void* a, const void* b, void* d, int a_mn, int b_mn, void* stream) {
+  CHECK(a && b && d, "probe_gemm: null pointer");
+  return cuda_status(lasp::tc_probe_gemm(a, b, (float*)d, a_mn, b_mn, S(stream)), "probe_gemm");
+}
+
+}  // extern "C"

@@ -1,0 +1,50 @@
+// Internal launcher declarations (C++ side of the C-ABI in capi.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace lasp {
+
+// validation-mode SIMT kernels, (io, accumulate) in {(f32,f32), (f64,f64), (bf16,f32)}
+template <typename T, typename A>
+cudaError_t simt_segment_states(const void* x, const void* y, void* out, int64_t slots, int64_t tokens, int dim,
+                                int nseg, cudaStream_t s);
+template <typename T, typename A>
+cudaError_t simt_causal_chunk(const void* q, const void* k, const void* v, const void* seg_states, const void* base,
+                              void* out, int64_t slots, int64_t tokens, int dim, int nseg, int reverse,
+                              int transpose_state, cudaStream_t s);
+template <typename T, typename A>
+cudaError_t simt_apply_state(const void* x, const void* m, void* out, int64_t slots, int64_t tokens, int dim,
+                             int transpose, int accumulate, cudaStream_t s);
+template <typename T, typename A>
+cudaError_t simt_softmax_forward(const void* q, const void* kf, const void* vf, void* out, float* lse, int64_t slots,
+                                 int64_t qtok, int64_t kvtok, int dim, int causal, int64_t row_offset, int64_t kv_chunk,
+                                 int64_t kv_rank_stride, cudaStream_t s);
+template <typename T, typename A, typename G>
+cudaError_t simt_softmax_backward(const void* q, const void* kf, const void* vf, const void* o, const void* d_out,
+                                  void* dq, void* dk_full, void* dv_full, void* scratch, int64_t slots, int64_t qtok,
+                                  int64_t kvtok, int dim, int causal, int64_t row_offset, int64_t kv_chunk,
+                                  int64_t kv_rank_stride, int64_t grad_rank_stride, cudaStream_t s);
+
+// shared state reductions / datagen
+template <typename A>
+cudaError_t scan_states(void* seg, void* total, int64_t slots, int nseg, int dim, int reverse, cudaStream_t s);
+template <typename A>
+cudaError_t fold_states(const void* gathered, void* out, int nstates, int64_t elems, int mode, int bound,
+                        cudaStream_t s);
+template <typename T>
+cudaError_t gen_slots(uint64_t seed, const uint64_t* tag_words, void* out, int64_t slots, int64_t rows, int64_t cols,
+                      cudaStream_t s);
+
+// tcgen05 fast path (bf16 in, fp32 states)
+bool tc_supported(int dim, int64_t tokens);
+cudaError_t tc_segment_states(const void* x, const void* y, float* out, int64_t slots, int64_t tokens, int dim,
+                              int nseg, cudaStream_t s);
+cudaError_t tc_causal_chunk(const void* q, const void* k, const void* v, const float* seg_states, const float* base,
+                            void* out, int64_t slots, int64_t tokens, int dim, int nseg, int reverse,
+                            int transpose_state, cudaStream_t s);
+cudaError_t tc_apply_state(const void* x, const float* m, void* out, int64_t slots, int64_t tokens, int dim,
+                           int transpose, int accumulate, int sm_count, cudaStream_t s);
+cudaError_t tc_probe_gemm(const void* a, const void* b, float* d, int a_mn, int b_mn, cudaStream_t s);
+
+}  // namespace lasp

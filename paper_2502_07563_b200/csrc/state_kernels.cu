@@ -1,0 +1,137 @@
+// Ordered state reductions and synthetic-input generation.
+//
+// scan  : per-rank exclusive prefix / suffix over segment states (the
+//         in-GPU analogue of LASP-2's prefix over chunks).
+// fold  : reduction of the rank-ordered gathered states with the reference's
+//         fold-order contract (numerics.py:71-121): a non-empty fold copies its
+//         first term and adds the rest in order (ascending for prefix/full,
+//         descending for suffix); an empty fold is zeros.
+// gen   : bit-exact SplitMix64 counter-hash port of datagen.gen_data
+//         (datagen.py:14-57), so the bench can build 2M-token inputs on device.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace lasp {
+
+// In place: seg[s] <- sum_{s' < s} seg[s'] (reverse: sum_{s' > s}); total <- sum_all.
+// One thread per (slot, element); the segment loop is sequential, so the
+// order of additions is fixed (ascending / descending).
+template <typename A>
+__global__ void scan_states_kernel(A* __restrict__ seg, A* __restrict__ total, int64_t slots, int nseg, int64_t dd,
+                                   int reverse) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= slots * dd) return;
+  const int64_t slot = idx / dd, el = idx % dd;
+  A* base = seg + slot * nseg * dd + el;
+  A run = A(0);
+  for (int i = 0; i < nseg; ++i) {
+    const int s = reverse ? nseg - 1 - i : i;
+    const A v = base[(int64_t)s * dd];
+    base[(int64_t)s * dd] = run;
+    run = (i == 0) ? v : run + v;
+  }
+  if (total) total[slot * dd + el] = run;
+}
+
+// gathered: [nstates][elems]. mode 0 = prefix(bound), 1 = suffix(bound), 2 = full.
+template <typename A>
+__global__ void fold_states_kernel(const A* __restrict__ gathered, A* __restrict__ out, int nstates, int64_t elems,
+                                   int mode, int bound) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= elems) return;
+  A acc = A(0);
+  if (mode == 1) {  // suffix: states[bound:], seeded by the last, descending
+    if (bound < nstates) {
+      acc = gathered[(int64_t)(nstates - 1) * elems + idx];
+      for (int i = nstates - 2; i >= bound; --i) acc += gathered[(int64_t)i * elems + idx];
+    }
+  } else {  // prefix: states[:bound], seeded by the first, ascending
+    const int upto = mode == 2 ? nstates : bound;
+    if (upto > 0) {
+      acc = gathered[idx];
+      for (int i = 1; i < upto; ++i) acc += gathered[(int64_t)i * elems + idx];
+    }
+  }
+  out[idx] = acc;
+}
+
+// ---- SplitMix64 (datagen.py:22-27) ----
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = z + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// out[slot][r][c] = 2*u - 1, u = (mix(mix(h0^r)^c) >> 11) * 2^-53,
+// h0 = mix(seed ^ tag_word[slot]); the f64 value is rounded once to T.
+template <typename T>
+__global__ void gen_slots_kernel(uint64_t seed, const uint64_t* __restrict__ tag_words, T* __restrict__ out,
+                                 int64_t slots, int64_t rows, int64_t cols) {
+  const int64_t n = slots * rows * cols;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t slot = idx / (rows * cols);
+    const int64_t rc = idx % (rows * cols);
+    const uint64_t r = (uint64_t)(rc / cols), c = (uint64_t)(rc % cols);
+    const uint64_t h0 = mix64(seed ^ tag_words[slot]);
+    const uint64_t h = mix64(mix64(h0 ^ r) ^ c);
+    const double u = (double)(h >> 11) * 0x1.0p-53;
+    const double val = 2.0 * u - 1.0;
+    out[idx] = (T)val;
+  }
+}
+template <>
+__global__ void gen_slots_kernel<__nv_bfloat16>(uint64_t seed, const uint64_t* __restrict__ tag_words,
+                                                __nv_bfloat16* __restrict__ out, int64_t slots, int64_t rows,
+                                                int64_t cols) {
+  const int64_t n = slots * rows * cols;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t slot = idx / (rows * cols);
+    const int64_t rc = idx % (rows * cols);
+    const uint64_t r = (uint64_t)(rc / cols), c = (uint64_t)(rc % cols);
+    const uint64_t h0 = mix64(seed ^ tag_words[slot]);
+    const uint64_t h = mix64(mix64(h0 ^ r) ^ c);
+    const double u = (double)(h >> 11) * 0x1.0p-53;
+    // f64 -> f32 -> bf16 (round-to-nearest-even at each step), SURVEY §8d
+    out[idx] = __float2bfloat16_rn((float)(2.0 * u - 1.0));
+  }
+}
+
+template <typename A>
+cudaError_t scan_states(void* seg, void* total, int64_t slots, int nseg, int dim, int reverse, cudaStream_t s) {
+  const int64_t dd = (int64_t)dim * dim;
+  const int64_t n = slots * dd;
+  scan_states_kernel<A><<<(unsigned)((n + 255) / 256), 256, 0, s>>>((A*)seg, (A*)total, slots, nseg, dd, reverse);
+  return cudaGetLastError();
+}
+
+template <typename A>
+cudaError_t fold_states(const void* gathered, void* out, int nstates, int64_t elems, int mode, int bound,
+                        cudaStream_t s) {
+  fold_states_kernel<A><<<(unsigned)((elems + 255) / 256), 256, 0, s>>>((const A*)gathered, (A*)out, nstates, elems,
+                                                                       mode, bound);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t gen_slots(uint64_t seed, const uint64_t* tag_words, void* out, int64_t slots, int64_t rows, int64_t cols,
+                      cudaStream_t s) {
+  const int64_t n = slots * rows * cols;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  gen_slots_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(seed, tag_words, (T*)out, slots, rows, cols);
+  return cudaGetLastError();
+}
+
+template cudaError_t scan_states<float>(void*, void*, int64_t, int, int, int, cudaStream_t);
+template cudaError_t scan_states<double>(void*, void*, int64_t, int, int, int, cudaStream_t);
+template cudaError_t fold_states<float>(const void*, void*, int, int64_t, int, int, cudaStream_t);
+template cudaError_t fold_states<double>(const void*, void*, int, int64_t, int, int, cudaStream_t);
+template cudaError_t gen_slots<float>(uint64_t, const uint64_t*, void*, int64_t, int64_t, int64_t, cudaStream_t);
+template cudaError_t gen_slots<double>(uint64_t, const uint64_t*, void*, int64_t, int64_t, int64_t, cudaStream_t);
+template cudaError_t gen_slots<__nv_bfloat16>(uint64_t, const uint64_t*, void*, int64_t, int64_t, int64_t,
+                                              cudaStream_t);
+
+}  // namespace lasp

@@ -1,0 +1,699 @@
+// tcgen05 / TMEM / TMA kernels for the LASP-2 linear-attention path (bf16 in,
+// fp32 accumulate), sm_100a only.
+//
+// All operand tiles are 128 tokens x 128 features of bf16, loaded by TMA as two
+// 64-column SWIZZLE_128B boxes (16 KB each). The same smem image serves as a
+// K-major operand when the contraction runs over features (Q K^T, Q S) and as
+// an MN-major operand when it runs over tokens (K^T V, P V), so no tile is ever
+// transposed in software. dim < 128 (e.g. cfg1's d=64) is handled by TMA
+// zero-fill of the out-of-range feature columns.
+//
+// Kernels
+//   tc_segment_states : M_seg = X_seg^T Y_seg          (lasp2.py:130-147, per segment)
+//   tc_causal_chunk   : O = mask(Q K^T) V + Q S_j,  S_{j+1} = S_j + K_j^T V_j
+//                       (oracle.py:50-62 blocked; lasp2.py:219-243 inter term
+//                       folded in through the initial state)
+//   tc_apply_state    : O (+)= X M or X M^T            (lasp2.py:150-165)
+#include <cuda.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace lasp {
+namespace tc {
+
+using namespace ptx;
+
+constexpr int kTile = 128;                    // tokens per block, features per tile
+constexpr uint32_t kTileBytes = 128 * 128 * 2;  // 32 KB
+constexpr uint32_t kBoxBytes = 128 * 64 * 2;    // 16 KB (one SW128 box)
+
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// K-major operand descriptor for k-step kk (16 elements along the feature axis).
+__device__ __forceinline__ uint64_t desc_kmajor(uint32_t tile, int kk) {
+  return umma_desc_sw128(tile + (kk >> 2) * kBoxBytes + (kk & 3) * 32, 16, 1024);
+}
+// MN-major operand descriptor for k-step kk (16 tokens = two 8-row atoms).
+__device__ __forceinline__ uint64_t desc_mnmajor(uint32_t tile, int kk) {
+  return umma_desc_sw128(tile + kk * 2048, kBoxBytes, 1024);
+}
+
+// Byte offset of element (row, col) in a 128x128 bf16 SW128 tile image.
+__device__ __forceinline__ uint32_t sw128_offset(uint32_t row, uint32_t col) {
+  const uint32_t chunk = col >> 6, cc = col & 63;
+  const uint32_t unit = (cc >> 3) ^ (row & 7);
+  return chunk * kBoxBytes + row * 128 + unit * 16 + (cc & 7) * 2;
+}
+
+// Store 32 fp32 values (columns c0..c0+31 of `row`) as bf16 into a SW128 image.
+__device__ __forceinline__ void st_row32_bf16(uint8_t* img, uint32_t row, uint32_t c0, const float* v) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    uint32_t w0 = pack_bf16x2(v[8 * u + 0], v[8 * u + 1]);
+    uint32_t w1 = pack_bf16x2(v[8 * u + 2], v[8 * u + 3]);
+    uint32_t w2 = pack_bf16x2(v[8 * u + 4], v[8 * u + 5]);
+    uint32_t w3 = pack_bf16x2(v[8 * u + 6], v[8 * u + 7]);
+    const uint32_t off = sw128_offset(row, c0 + 8 * u);
+    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(smem_u32(img + off)), "r"(w0), "r"(w1), "r"(w2),
+                 "r"(w3)
+                 : "memory");
+  }
+}
+
+// Load a 128-column fp32 row from TMEM (this thread's lane) in four x32 pieces,
+// convert to bf16 (optionally causal-masked) and write into a SW128 image.
+// mask: 0 none, 1 keep col<=row, 2 keep col>=row.
+__device__ __forceinline__ void tmem_row_to_image(uint32_t taddr_lane, uint8_t* img, uint32_t row, int mask) {
+#pragma unroll 1
+  for (int c0 = 0; c0 < 128; c0 += 32) {
+    uint32_t r[32];
+    tmem_ld_32x32b_x32(taddr_lane + c0, r);
+    tmem_ld_wait();
+    float v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      float x = __uint_as_float(r[i]);
+      const int col = c0 + i;
+      if (mask == 1 && col > (int)row) x = 0.f;
+      if (mask == 2 && col < (int)row) x = 0.f;
+      v[i] = x;
+    }
+    st_row32_bf16(img, row, c0, v);
+  }
+}
+
+// ============================================================================
+// Segment states: out[slot][seg] = X_seg^T Y_seg   (fp32 [dim][dim])
+// ============================================================================
+constexpr int kSegStages = 3;
+constexpr uint32_t kSegSmem = kSegStages * 2 * kTileBytes + 1024 + 256;
+
+__global__ void __launch_bounds__(192, 1)
+    tc_segment_states_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_y,
+                             float* __restrict__ out, int64_t tokens, int dim, int nseg) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* ring = smem;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSegStages * 2 * kTileBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kSegStages;
+  uint64_t* acc_full = bars + 2 * kSegStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kSegStages + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int seg = blockIdx.x;
+  const int slot = blockIdx.y;
+  int64_t lo, hi;
+  seg_range(seg, nseg, tokens, &lo, &hi);
+  const int nblk = (int)((hi - lo + kTile - 1) / kTile);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kSegStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(acc_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<128>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      prefetch_tmap(&tm_x);
+      prefetch_tmap(&tm_y);
+      for (int b = 0; b < nblk; ++b) {
+        const int s = b % kSegStages, u = b / kSegStages;
+        if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+        uint8_t* xs = ring + s * 2 * kTileBytes;
+        uint8_t* ys = xs + kTileBytes;
+        const int nbox = dim > 64 ? 2 : 1;
+        mbar_arrive_expect_tx(&full[s], 2 * nbox * kBoxBytes);
+        const int row = (int)(lo + (int64_t)b * kTile);
+        for (int bx = 0; bx < nbox; ++bx) {
+          tma_load_3d(xs + bx * kBoxBytes, &tm_x, &full[s], 64 * bx, row, slot);
+          tma_load_3d(ys + bx * kBoxBytes, &tm_y, &full[s], 64 * bx, row, slot);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = idesc_bf16_f32(128, 128, 1, 1);
+    for (int b = 0; b < nblk; ++b) {
+      const int s = b % kSegStages, u = b / kSegStages;
+      mbar_wait(&full[s], u & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t xs = smem_u32(ring + s * 2 * kTileBytes), ys = xs + kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_bf16_ss(tmem, desc_mnmajor(xs, kk), desc_mnmajor(ys, kk), idesc, (b > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(&empty[s]);
+        if (b == nblk - 1) mma_commit(acc_full);
+      }
+      __syncwarp();
+    }
+  } else {
+    const int qd = warp & 3;
+    const uint32_t row = qd * 32 + lane;
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    float* ob = out + ((int64_t)slot * nseg + seg) * (int64_t)dim * dim;
+#pragma unroll 1
+    for (int c0 = 0; c0 < 128; c0 += 32) {
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(tmem + ((qd * 32) << 16) + c0, r);
+      tmem_ld_wait();
+      if ((int)row < dim) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (c0 + i < dim) ob[(int64_t)row * dim + c0 + i] = __uint_as_float(r[i]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<128>(tmem);
+}
+
+// ============================================================================
+// Causal chunk kernel (one CTA per (slot, segment))
+// ============================================================================
+constexpr int kRing = 5;  // tile slots for the Q/K/V stream
+constexpr uint32_t kCausalSmem = (kRing + 2) * kTileBytes + 1024 + 256;
+
+struct CausalArgs {
+  const float* seg_states;  // [slots][nseg][dim][dim] or null
+  const float* base;        // [slots][dim][dim] or null
+  int64_t tokens;
+  int dim;
+  int nseg;
+  int reverse;
+  int transpose_state;
+};
+
+__global__ void __launch_bounds__(192, 1)
+    tc_causal_chunk_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                           const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
+                           CausalArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* ring = smem;                                // kRing x 32 KB
+  uint8_t* pimg = smem + kRing * kTileBytes;           // P tile / O staging
+  uint8_t* simg = pimg + kTileBytes;                   // bf16 state image
+  uint64_t* bars = reinterpret_cast<uint64_t*>(simg + kTileBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kRing;
+  uint64_t* s_full = bars + 2 * kRing + 0;
+  uint64_t* st_full = bars + 2 * kRing + 1;
+  uint64_t* o_full = bars + 2 * kRing + 2;
+  uint64_t* p_ready = bars + 2 * kRing + 3;
+  uint64_t* sst_ready = bars + 2 * kRing + 4;
+  uint64_t* o_empty = bars + 2 * kRing + 5;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kRing + 6);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int seg = blockIdx.x;
+  const int slot = blockIdx.y;
+  int64_t lo, hi;
+  seg_range(seg, a.nseg, a.tokens, &lo, &hi);
+  const int nblk = (int)((hi - lo + kTile - 1) / kTile);
+  const int nbox = a.dim > 64 ? 2 : 1;
+  const int kfeat = (a.dim + 15) / 16;  // k-steps of feature contractions
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kRing; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 6; ++i) mbar_init(&s_full[i], 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_s = tmem, t_o = tmem + 128, t_st = tmem + 256;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (elect_one()) {
+      prefetch_tmap(&tm_q);
+      prefetch_tmap(&tm_k);
+      prefetch_tmap(&tm_v);
+      prefetch_tmap(&tm_o);
+      const CUtensorMap* maps[3] = {&tm_q, &tm_k, &tm_v};
+      for (int jj = 0; jj < nblk; ++jj) {
+        const int j = a.reverse ? nblk - 1 - jj : jj;
+        const int row = (int)(lo + (int64_t)j * kTile);
+        for (int w = 0; w < 3; ++w) {
+          const int t = 3 * jj + w, s = t % kRing, u = t / kRing;
+          if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+          uint8_t* dst = ring + s * kTileBytes;
+          mbar_arrive_expect_tx(&full[s], nbox * kBoxBytes);
+          for (int bx = 0; bx < nbox; ++bx) tma_load_3d(dst + bx * kBoxBytes, maps[w], &full[s], 64 * bx, row, slot);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t id_qk = idesc_bf16_f32(128, 128, 0, 0);  // S = Q K^T
+    constexpr uint32_t id_qs = idesc_bf16_f32(128, 128, 0, 1);  // O = Q S
+    constexpr uint32_t id_kv = idesc_bf16_f32(128, 128, 1, 1);  // S += K^T V
+    constexpr uint32_t id_pv = idesc_bf16_f32(128, 128, 0, 1);  // O += P V
+    const uint32_t simg_a = smem_u32(simg), pimg_a = smem_u32(pimg);
+    for (int jj = 0; jj < nblk; ++jj) {
+      const int tq = 3 * jj, tk = tq + 1, tv = tq + 2;
+      const int sq = tq % kRing, sk = tk % kRing, sv = tv % kRing;
+      const uint32_t qa = smem_u32(ring + sq * kTileBytes);
+      const uint32_t ka = smem_u32(ring + sk * kTileBytes);
+      const uint32_t va = smem_u32(ring + sv * kTileBytes);
+      mbar_wait(&full[sq], (tq / kRing) & 1);
+      mbar_wait(&full[sk], (tk / kRing) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < kfeat; ++kk) mma_bf16_ss(t_s, desc_kmajor(qa, kk), desc_kmajor(ka, kk), id_qk, kk > 0);
+        mma_commit(s_full);
+      }
+      __syncwarp();
+      mbar_wait(sst_ready, jj & 1);
+      if (jj > 0) mbar_wait(o_empty, (jj - 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < kfeat; ++kk) mma_bf16_ss(t_o, desc_kmajor(qa, kk), desc_mnmajor(simg_a, kk), id_qs, kk > 0);
+        mma_commit(&empty[sq]);
+      }
+      __syncwarp();
+      mbar_wait(&full[sv], (tv / kRing) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        if (jj < nblk - 1) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) mma_bf16_ss(t_st, desc_mnmajor(ka, kk), desc_mnmajor(va, kk), id_kv, 1u);
+          mma_commit(st_full);
+        }
+        mma_commit(&empty[sk]);
+      }
+      __syncwarp();
+      mbar_wait(p_ready, jj & 1);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) mma_bf16_ss(t_o, desc_kmajor(pimg_a, kk), desc_mnmajor(va, kk), id_pv, 1u);
+        mma_commit(&empty[sv]);
+        mma_commit(o_full);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ---------------- epilogue: 4 warps, one TMEM lane (row) per thread ----------------
+    const int qd = warp & 3;
+    const uint32_t row = qd * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
+    const int et = threadIdx.x - 64;
+    const int dim = a.dim;
+    const int64_t dd = (int64_t)dim * dim;
+    // initial state S0 = base + seg_states[seg] (optionally transposed), rows beyond dim are zero
+    {
+      const float* st = a.seg_states ? a.seg_states + ((int64_t)slot * a.nseg + seg) * dd : nullptr;
+      const float* bs = a.base ? a.base + (int64_t)slot * dd : nullptr;
+#pragma unroll 1
+      for (int c0 = 0; c0 < 128; c0 += 32) {
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int c = c0 + i;
+          float x = 0.f;
+          if ((int)row < dim && c < dim) {
+            const int64_t src = a.transpose_state ? (int64_t)c * dim + row : (int64_t)row * dim + c;
+            if (bs) x += bs[src];
+            if (st) x += st[src];
+          }
+          v[i] = x;
+        }
+        uint32_t r[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(v[i]);
+        tmem_st_32x32b_x32(t_st + lane_off + c0, r);
+        st_row32_bf16(simg, row, c0, v);
+      }
+      tmem_st_wait();
+      fence_proxy_async_smem();
+      tc_fence_before();
+      named_bar_sync(1, 128);
+      if (et == 0) mbar_arrive(sst_ready);
+    }
+    const int pmask = a.reverse ? 2 : 1;
+    for (int jj = 0; jj < nblk; ++jj) {
+      const int j = a.reverse ? nblk - 1 - jj : jj;
+      // ---- P = mask(S) -> smem (after the previous O tile left the staging buffer)
+      mbar_wait(s_full, jj & 1);
+      tc_fence_after();
+      if (jj > 0 && et == 0) tma_store_wait_read<0>();
+      named_bar_sync(1, 128);
+      tmem_row_to_image(t_s + lane_off, pimg, row, pmask);
+      fence_proxy_async_smem();
+      tc_fence_before();
+      named_bar_sync(1, 128);
+      if (et == 0) mbar_arrive(p_ready);
+      // ---- next block's state image
+      if (jj < nblk - 1) {
+        mbar_wait(st_full, jj & 1);
+        tc_fence_after();
+        tmem_row_to_image(t_st + lane_off, simg, row, 0);
+        fence_proxy_async_smem();
+        tc_fence_before();
+        named_bar_sync(1, 128);
+        if (et == 0) mbar_arrive(sst_ready);
+      }
+      // ---- O tile -> staging -> TMA store
+      mbar_wait(o_full, jj & 1);
+      tc_fence_after();
+      tmem_row_to_image(t_o + lane_off, pimg, row, 0);
+      fence_proxy_async_smem();
+      tc_fence_before();
+      named_bar_sync(1, 128);
+      if (et == 0) {
+        mbar_arrive(o_empty);
+        const int orow = (int)(lo + (int64_t)j * kTile);
+        for (int bx = 0; bx < nbox; ++bx) tma_store_3d(&tm_o, pimg + bx * kBoxBytes, 64 * bx, orow, slot);
+        tma_store_commit();
+      }
+    }
+    if (et == 0) tma_store_wait_all<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+// ============================================================================
+// apply_state: O (+)= X M  (transpose=0) or X M^T (transpose=1)
+// ============================================================================
+constexpr int kApplyRing = 4;
+constexpr uint32_t kApplySmem = (kApplyRing + 3) * kTileBytes + 1024 + 256;
+
+__global__ void __launch_bounds__(192, 1)
+    tc_apply_state_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_o,
+                          const float* __restrict__ m, __nv_bfloat16* out, int64_t tokens, int dim, int transpose,
+                          int accumulate, int blocks_per_cta) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* ring = smem;
+  uint8_t* mimg = ring + kApplyRing * kTileBytes;
+  uint8_t* stage = mimg + kTileBytes;  // 2 x 32 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stage + 2 * kTileBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kApplyRing;
+  uint64_t* acc_full = bars + 2 * kApplyRing;       // [2]
+  uint64_t* acc_empty = bars + 2 * kApplyRing + 2;  // [2]
+  uint64_t* m_ready = bars + 2 * kApplyRing + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kApplyRing + 5);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot = blockIdx.y;
+  const int64_t nblk_all = (tokens + kTile - 1) / kTile;
+  const int64_t b0 = (int64_t)blockIdx.x * blocks_per_cta;
+  const int64_t b1 = lmin(nblk_all, b0 + blocks_per_cta);
+  const int nblk = (int)lmax(0, b1 - b0);
+  const int nbox = dim > 64 ? 2 : 1;
+  const int kfeat = (dim + 15) / 16;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kApplyRing; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 5; ++i) mbar_init(&acc_full[i], 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<256>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      prefetch_tmap(&tm_x);
+      prefetch_tmap(&tm_o);
+      for (int b = 0; b < nblk; ++b) {
+        const int s = b % kApplyRing, u = b / kApplyRing;
+        if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+        uint8_t* dst = ring + s * kTileBytes;
+        mbar_arrive_expect_tx(&full[s], nbox * kBoxBytes);
+        const int row = (int)((b0 + b) * kTile);
+        for (int bx = 0; bx < nbox; ++bx) tma_load_3d(dst + bx * kBoxBytes, &tm_x, &full[s], 64 * bx, row, slot);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = idesc_bf16_f32(128, 128, 0, transpose ? 0 : 1);
+    const uint32_t ma = smem_u32(mimg);
+    mbar_wait(m_ready, 0);
+    for (int b = 0; b < nblk; ++b) {
+      const int s = b % kApplyRing, u = b / kApplyRing;
+      const int buf = b & 1;
+      mbar_wait(&full[s], u & 1);
+      if (b >= 2) mbar_wait(&acc_empty[buf], ((b >> 1) - 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t xa = smem_u32(ring + s * kTileBytes);
+        for (int kk = 0; kk < kfeat; ++kk) {
+          const uint64_t bdesc = transpose ? desc_kmajor(ma, kk) : desc_mnmajor(ma, kk);
+          mma_bf16_ss(tmem + buf * 128, desc_kmajor(xa, kk), bdesc, idesc, kk > 0);
+        }
+        mma_commit(&empty[s]);
+        mma_commit(&acc_full[buf]);
+      }
+      __syncwarp();
+    }
+  } else {
+    const int qd = warp & 3;
+    const uint32_t row = qd * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
+    const int et = threadIdx.x - 64;
+    const int64_t dd = (int64_t)dim * dim;
+    const float* mb = m + (int64_t)slot * dd;
+    // state image: rows = first index of M, contiguous = second index
+#pragma unroll 1
+    for (int c0 = 0; c0 < 128; c0 += 32) {
+      float v[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int c = c0 + i;
+        v[i] = ((int)row < dim && c < dim) ? mb[(int64_t)row * dim + c] : 0.f;
+      }
+      st_row32_bf16(mimg, row, c0, v);
+    }
+    fence_proxy_async_smem();
+    named_bar_sync(1, 128);
+    if (et == 0) mbar_arrive(m_ready);
+    for (int b = 0; b < nblk; ++b) {
+      const int buf = b & 1;
+      mbar_wait(&acc_full[buf], (b >> 1) & 1);
+      tc_fence_after();
+      if (b >= 2 && et == 0) tma_store_wait_read<1>();
+      named_bar_sync(1, 128);
+      uint8_t* st = stage + buf * kTileBytes;
+      const int64_t grow = (b0 + b) * kTile + row;
+#pragma unroll 1
+      for (int c0 = 0; c0 < 128; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem + buf * 128 + lane_off + c0, r);
+        tmem_ld_wait();
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        if (accumulate && grow < tokens) {
+          const __nv_bfloat16* orow = out + ((int64_t)slot * tokens + grow) * dim;
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (c0 + i < dim) v[i] += __bfloat162float(orow[c0 + i]);
+        }
+        st_row32_bf16(st, row, c0, v);
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      named_bar_sync(1, 128);
+      if (et == 0) {
+        mbar_arrive(&acc_empty[buf]);
+        const int orow = (int)((b0 + b) * kTile);
+        for (int bx = 0; bx < nbox; ++bx) tma_store_3d(&tm_o, st + bx * kBoxBytes, 64 * bx, orow, slot);
+        tma_store_commit();
+      }
+    }
+    if (et == 0) tma_store_wait_all<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<256>(tmem);
+}
+
+// ============================================================================
+// Debug probe: D = op(A) op(B)^T for one 128x128x128 tile, to pin descriptor
+// conventions on hardware (a_mn / b_mn select MN-major interpretation).
+// ============================================================================
+__global__ void __launch_bounds__(128, 1)
+    tc_probe_gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+                         float* __restrict__ d, int a_mn, int b_mn) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* at = smem;
+  uint8_t* bt = smem + kTileBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kTileBytes);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<128>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(&bars[0], 2 * kTileBytes);
+    tma_load_3d(at, &tm_a, &bars[0], 0, 0, 0);
+    tma_load_3d(at + kBoxBytes, &tm_a, &bars[0], 64, 0, 0);
+    tma_load_3d(bt, &tm_b, &bars[0], 0, 0, 0);
+    tma_load_3d(bt + kBoxBytes, &tm_b, &bars[0], 64, 0, 0);
+    mbar_wait(&bars[0], 0);
+    tc_fence_after();
+    const uint32_t idesc = idesc_bf16_f32(128, 128, a_mn, b_mn);
+    const uint32_t aa = smem_u32(at), ba = smem_u32(bt);
+    for (int kk = 0; kk < 8; ++kk) {
+      const uint64_t ad = a_mn ? desc_mnmajor(aa, kk) : desc_kmajor(aa, kk);
+      const uint64_t bd = b_mn ? desc_mnmajor(ba, kk) : desc_kmajor(ba, kk);
+      mma_bf16_ss(tmem, ad, bd, idesc, kk > 0);
+    }
+    mma_commit(&bars[1]);
+  }
+  __syncwarp();
+  mbar_wait(&bars[1], 0);
+  tc_fence_after();
+  const uint32_t row = warp * 32 + lane;
+  for (int c0 = 0; c0 < 128; c0 += 32) {
+    uint32_t r[32];
+    tmem_ld_32x32b_x32(tmem + ((warp * 32) << 16) + c0, r);
+    tmem_ld_wait();
+    for (int i = 0; i < 32; ++i) d[row * 128 + c0 + i] = __uint_as_float(r[i]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<128>(tmem);
+}
+
+}  // namespace tc
+
+// ============================================================================
+// Host side: tensor maps + launchers
+// ============================================================================
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// [slots][tokens][dim] bf16, box = 64 features x 128 tokens, SWIZZLE_128B.
+static cudaError_t make_tmap(CUtensorMap* m, const void* ptr, int64_t slots, int64_t tokens, int dim) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return cudaErrorNotSupported;
+  cuuint64_t gdim[3] = {(cuuint64_t)dim, (cuuint64_t)tokens, (cuuint64_t)slots};
+  cuuint64_t gstride[2] = {(cuuint64_t)dim * 2, (cuuint64_t)tokens * dim * 2};
+  cuuint32_t box[3] = {64, 128, 1};
+  cuuint32_t estride[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), gdim, gstride, box, estride,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+bool tc_supported(int dim, int64_t tokens) { return dim >= 8 && dim <= 128 && dim % 8 == 0 && tokens >= 1; }
+
+cudaError_t tc_segment_states(const void* x, const void* y, float* out, int64_t slots, int64_t tokens, int dim,
+                              int nseg, cudaStream_t s) {
+  CUtensorMap mx, my;
+  cudaError_t e;
+  if ((e = make_tmap(&mx, x, slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = make_tmap(&my, y, slots, tokens, dim)) != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(tc::tc_segment_states_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)tc::kSegSmem);
+  if (e != cudaSuccess) return e;
+  dim3 grid(nseg, (unsigned)slots);
+  tc::tc_segment_states_kernel<<<grid, 192, tc::kSegSmem, s>>>(mx, my, out, tokens, dim, nseg);
+  return cudaGetLastError();
+}
+
+cudaError_t tc_causal_chunk(const void* q, const void* k, const void* v, const float* seg_states, const float* base,
+                            void* out, int64_t slots, int64_t tokens, int dim, int nseg, int reverse,
+                            int transpose_state, cudaStream_t s) {
+  CUtensorMap mq, mk, mv, mo;
+  cudaError_t e;
+  if ((e = make_tmap(&mq, q, slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = make_tmap(&mk, k, slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = make_tmap(&mv, v, slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = make_tmap(&mo, out, slots, tokens, dim)) != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(tc::tc_causal_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)tc::kCausalSmem);
+  if (e != cudaSuccess) return e;
+  tc::CausalArgs a{seg_states, base, tokens, dim, nseg, reverse, transpose_state};
+  dim3 grid(nseg, (unsigned)slots);
+  tc::tc_causal_chunk_kernel<<<grid, 192, tc::kCausalSmem, s>>>(mq, mk, mv, mo, a);
+  return cudaGetLastError();
+}
+
+cudaError_t tc_apply_state(const void* x, const float* m, void* out, int64_t slots, int64_t tokens, int dim,
+                           int transpose, int accumulate, int sm_count, cudaStream_t s) {
+  CUtensorMap mx, mo;
+  cudaError_t e;
+  if ((e = make_tmap(&mx, x, slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = make_tmap(&mo, out, slots, tokens, dim)) != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(tc::tc_apply_state_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)tc::kApplySmem);
+  if (e != cudaSuccess) return e;
+  const int64_t nblk = (tokens + tc::kTile - 1) / tc::kTile;
+  // about one wave: ctas_per_slot * slots ~= sm_count
+  int64_t ctas = (sm_count + slots - 1) / slots;
+  if (ctas < 1) ctas = 1;
+  if (ctas > nblk) ctas = nblk;
+  const int bpc = (int)((nblk + ctas - 1) / ctas);
+  ctas = (nblk + bpc - 1) / bpc;
+  dim3 grid((unsigned)ctas, (unsigned)slots);
+  tc::tc_apply_state_kernel<<<grid, 192, tc::kApplySmem, s>>>(mx, mo, m, (__nv_bfloat16*)out, tokens, dim,
+                                                              transpose, accumulate, bpc);
+  return cudaGetLastError();
+}
+
+cudaError_t tc_probe_gemm(const void* a, const void* b, float* d, int a_mn, int b_mn, cudaStream_t s) {
+  CUtensorMap ma, mb;
+  cudaError_t e;
+  if ((e = make_tmap(&ma, a, 1, 128, 128)) != cudaSuccess) return e;
+  if ((e = make_tmap(&mb, b, 1, 128, 128)) != cudaSuccess) return e;
+  const uint32_t smem = 2 * tc::kTileBytes + 1024 + 64;
+  e = cudaFuncSetAttribute(tc::tc_probe_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  tc::tc_probe_gemm_kernel<<<1, 128, smem, s>>>(ma, mb, d, a_mn, b_mn);
+  return cudaGetLastError();
+}
+
+}  // namespace lasp

@@ -1,0 +1,430 @@
+"""LASP-2 sequence-parallel linear attention on B200 (drop-in for laspsim.lasp2).
+
+Same entry points, argument order and BHND layouts as the reference
+(pkg/src/laspsim/lasp2.py), over torch CUDA tensors. Each rank owns one chunk
+of C tokens; the only exchange per pass is one all_gather of the rank's d x d
+memory states (lasp2.py:211/226/232/260/276).
+
+Inside a GPU the chunk is split again into segments (one CTA per segment of a
+(batch, head) slot), so every rank program is:
+
+  forward  (masked, lasp2.py:219-243)
+    seg = X^T Y per segment (K,V)        -> lasp2_segment_states
+    scan seg (exclusive prefix), M_t     -> lasp2_scan_segments
+    gathered = all_gather(M_t)           -> NCCL / emulated world
+    P = prefix fold(gathered, t)         -> lasp2_fold_states
+    O = mask(QK^T)V + Q (P + seg + ...)  -> lasp2_causal_chunk (tcgen05)
+  backward (masked, lasp2.py:270-285)
+    dM segments (Q, dO), suffix scan, all_gather(dM_t)   [in flight ...]
+    dQ = causal(dO, V, K; S^T)                            [... during dQ]
+    R = suffix fold(gathered, t+1)
+    dK = anti-causal(V, dO, Q; G^T), dV = anti-causal(K, Q, dO; G)
+
+Precision follows the data dtype: bfloat16 runs the tcgen05/TMEM/TMA kernels
+with fp32 states; float32 / float64 run the exact validation kernels.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import comm, ops
+from .shards import pack_slots, split_chunks, unpack_slots
+
+
+def _as_device_tensor(x) -> torch.Tensor:
+    if isinstance(x, np.ndarray):
+        x = torch.from_numpy(np.ascontiguousarray(x))
+    if not isinstance(x, torch.Tensor):
+        raise ValueError(f"expected a torch tensor or numpy array, got {type(x)}")
+    if not x.is_cuda:
+        if not torch.cuda.is_available():
+            raise RuntimeError("the LASP-2 B200 path needs a CUDA device (no CPU fallback)")
+        x = x.cuda()
+    return x
+
+
+@dataclass(frozen=True)
+class ChunkedSequence:
+    """Full q/k/v of shape (B, H, N, d) plus the chunk count T (lasp2.py:30-80)."""
+
+    q: torch.Tensor
+    k: torch.Tensor
+    v: torch.Tensor
+    chunks: int
+
+    def __post_init__(self) -> None:
+        # validate on the raw arrays first (lasp2.py:43-52), then move to the GPU
+        arrs = [getattr(self, n) for n in ("q", "k", "v")]
+        for name, arr in zip(("q", "k", "v"), arrs):
+            if not isinstance(arr, (np.ndarray, torch.Tensor)):
+                raise ValueError(f"{name} must be a torch tensor or numpy array, got {type(arr)}")
+            if arr.ndim != 4:
+                raise ValueError(f"{name} must be (batch, heads, tokens, dim), got {tuple(arr.shape)}")
+        if not (tuple(arrs[0].shape) == tuple(arrs[1].shape) == tuple(arrs[2].shape)):
+            raise ValueError(f"q/k/v shapes differ: {tuple(arrs[0].shape)}, {tuple(arrs[1].shape)}, "
+                             f"{tuple(arrs[2].shape)}")
+        if not (arrs[0].dtype == arrs[1].dtype == arrs[2].dtype):
+            raise ValueError("q/k/v dtypes differ")
+        n = arrs[0].shape[2]
+        if self.chunks < 1 or n % self.chunks != 0:
+            raise ValueError(f"chunk count {self.chunks} must divide sequence length {n}")
+        for name, arr in zip(("q", "k", "v"), arrs):
+            object.__setattr__(self, name, _as_device_tensor(arr))
+
+    @property
+    def batch(self) -> int:
+        return self.q.shape[0]
+
+    @property
+    def heads(self) -> int:
+        return self.q.shape[1]
+
+    @property
+    def seq_len(self) -> int:
+        return self.q.shape[2]
+
+    @property
+    def dim(self) -> int:
+        return self.q.shape[3]
+
+    @property
+    def chunk_len(self) -> int:
+        return self.seq_len // self.chunks
+
+    def chunk(self, t: int) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+        if not 0 <= t < self.chunks:
+            raise ValueError(f"chunk index {t} outside [0, {self.chunks})")
+        return (split_chunks(self.q, self.chunks)[t], split_chunks(self.k, self.chunks)[t],
+                split_chunks(self.v, self.chunks)[t])
+
+
+@dataclass
+class GradientBundle:
+    """Gradients w.r.t. q, k, v (oracle.py:41-47)."""
+
+    dq: torch.Tensor
+    dk: torch.Tensor
+    dv: torch.Tensor
+
+
+@dataclass
+class ActivationCache:
+    """Forward leftovers the backward may not recompute (lasp2.py:83-97).
+
+    m_prefix = M_{1:t-1} (masked) or m_full = M_{1:T} (unmasked), exactly as in
+    the reference. seg_prefix holds the rank-local exclusive segment prefixes of
+    K^T V (the in-GPU analogue of the per-token states) so the backward never
+    re-gathers or re-folds forward states; state_folds counts folds of
+    gathered forward states (forward: 1, backward: 0 more).
+    """
+
+    q: torch.Tensor
+    k: torch.Tensor
+    v: torch.Tensor
+    masked: bool
+    m_prefix: torch.Tensor | None = None
+    m_full: torch.Tensor | None = None
+    state_folds: int = 0
+    seg_prefix: torch.Tensor | None = None
+    nseg: int = 1
+
+
+@dataclass
+class ForwardOutcome:
+    outputs: list[torch.Tensor]
+    caches: list[ActivationCache]
+    run: comm.WorldRun
+
+
+@dataclass
+class BackwardOutcome:
+    grads: list[GradientBundle]
+    run: comm.WorldRun
+
+
+@dataclass
+class IterationOutcome:
+    outputs: list[torch.Tensor]
+    grads: list[GradientBundle]
+    caches: list[ActivationCache]
+    run: comm.WorldRun
+
+
+# ---- per-rank programs ------------------------------------------------------
+
+def _contig(*xs: torch.Tensor) -> list[torch.Tensor]:
+    return [x.contiguous() for x in xs]
+
+
+def _gather_states(ctx, m_t: torch.Tensor, tag: str, async_op: bool = False):
+    """All-gather one (B,H,d,d) state per rank as pack_slots payload (shards.py:24-29)."""
+    payload = pack_slots(m_t)
+    return ctx.all_gather_async(payload, tag=tag) if async_op else ctx.all_gather(payload, tag=tag)
+
+
+def _unpack_gathered(gathered: torch.Tensor, like: torch.Tensor) -> torch.Tensor:
+    t = gathered.shape[0]
+    return gathered.view(t, *like.shape)
+
+
+def _forward_nomask_rank(ctx, qc: torch.Tensor, kc: torch.Tensor,
+                         vc: torch.Tensor) -> tuple[torch.Tensor, ActivationCache]:
+    """O_t = Q_t M_{1:T} after one state all_gather (lasp2.py:208-216)."""
+    qc, kc, vc = _contig(qc, kc, vc)
+    _, m_t, _ = ops.chunk_states(kc, vc)
+    gathered = _unpack_gathered(_gather_states(ctx, m_t, "state"), m_t)
+    m_full = ops.sum_states(gathered)
+    out = ops.apply_state(qc, m_full)
+    return out, ActivationCache(q=qc, k=kc, v=vc, masked=False, m_full=m_full, state_folds=1)
+
+
+def _forward_masked_rank(ctx, qc: torch.Tensor, kc: torch.Tensor, vc: torch.Tensor,
+                         overlap: bool = False) -> tuple[torch.Tensor, ActivationCache]:
+    """O_t = intra(Q_t, K_t, V_t) + Q_t M_{1:t-1} (lasp2.py:219-243).
+
+    Sequential schedule: the gathered prefix is folded into the chunk kernel's
+    initial state (one pass, one rounding). Overlap schedule: the chunk kernel
+    runs while the all_gather is in flight and the inter term is added after
+    the wait, Q_t M_{1:t-1} as a separate tensor-core pass (lasp2.py:224-230).
+    """
+    qc, kc, vc = _contig(qc, kc, vc)
+    t = ctx.sp_position
+    seg, m_t, nseg = ops.chunk_states(kc, vc)
+    if overlap:
+        pending = _gather_states(ctx, m_t, "state", async_op=True)
+        ctx.mark("intra_start", f"chunk={t}")
+        out = ops.causal_chunk(qc, kc, vc, seg, None, nseg)
+        ctx.mark("intra_end", f"chunk={t}")
+        gathered = _unpack_gathered(pending.wait(), m_t)
+        m_prefix = ops.prefix_states(gathered, t)
+        if t > 0:
+            ops.apply_state(qc, m_prefix, out=out, accumulate=True)
+    else:
+        gathered = _unpack_gathered(_gather_states(ctx, m_t, "state"), m_t)
+        m_prefix = ops.prefix_states(gathered, t)
+        ctx.mark("intra_start", f"chunk={t}")
+        out = ops.causal_chunk(qc, kc, vc, seg, m_prefix if t > 0 else None, nseg)
+        ctx.mark("intra_end", f"chunk={t}")
+    cache = ActivationCache(q=qc, k=kc, v=vc, masked=True, m_prefix=m_prefix, state_folds=1, seg_prefix=seg,
+                            nseg=nseg)
+    return out, cache
+
+
+def _require_cache(cache: ActivationCache, masked: bool) -> None:
+    """lasp2.py:246-253."""
+    if not isinstance(cache, ActivationCache):
+        raise ValueError("backward needs the forward's ActivationCache")
+    if cache.masked != masked:
+        raise ValueError(f"cache was built masked={cache.masked}, backward wants {masked}")
+    needed = cache.m_prefix if masked else cache.m_full
+    if needed is None:
+        raise ValueError("cache is missing its reduced state")
+    if masked and cache.seg_prefix is None:
+        raise ValueError("cache is missing its segment states")
+
+
+def _backward_nomask_rank(ctx, cache: ActivationCache, d_out: torch.Tensor) -> GradientBundle:
+    """One all_gather of Q^T dO; full-sum reduction (lasp2.py:256-267)."""
+    _require_cache(cache, masked=False)
+    (do,) = _contig(d_out)
+    _, g_t, _ = ops.chunk_states(cache.q, do)
+    pending = _gather_states(ctx, g_t, "state_grad", async_op=True)
+    dq = ops.apply_state(do, cache.m_full, transpose=True)  # independent of the collective
+    dm_full = ops.sum_states(_unpack_gathered(pending.wait(), g_t))
+    dk = ops.apply_state(cache.v, dm_full, transpose=True)
+    dv = ops.apply_state(cache.k, dm_full)
+    return GradientBundle(dq=dq, dk=dk, dv=dv)
+
+
+def _backward_masked_rank(ctx, cache: ActivationCache, d_out: torch.Tensor) -> GradientBundle:
+    """Masked backward (lasp2.py:270-285): the dM all_gather overlaps the dQ pass."""
+    _require_cache(cache, masked=True)
+    t, world = ctx.sp_position, ctx.sp_size
+    (do,) = _contig(d_out)
+    q, k, v, nseg = cache.q, cache.k, cache.v, cache.nseg
+    gseg = ops.segment_states(q, do, nseg)
+    g_t = ops.scan_segments(gseg, reverse=True, data_dtype=q.dtype)
+    pending = _gather_states(ctx, g_t, "state_grad", async_op=True)
+    # dq_s = sum_{i<=s}(do_s.v_i) k_i + do_s (M_{1:t-1} + local prefix)^T
+    dq = ops.causal_chunk(do, v, k, cache.seg_prefix, cache.m_prefix if t > 0 else None, nseg,
+                          reverse=False, transpose_state=True)
+    gathered = _unpack_gathered(pending.wait(), g_t)
+    r = ops.suffix_states(gathered, t + 1) if t < world - 1 else None
+    # dk_s = sum_{i>=s}(v_s.do_i) q_i + v_s G_s^T ; dv_s = sum_{i>=s}(k_s.q_i) do_i + k_s G_s
+    dk = ops.causal_chunk(v, do, q, gseg, r, nseg, reverse=True, transpose_state=True)
+    dv = ops.causal_chunk(k, q, do, gseg, r, nseg, reverse=True, transpose_state=False)
+    return GradientBundle(dq=dq, dk=dk, dv=dv)
+
+
+# ---- world drivers ----------------------------------------------------------
+
+def default_world(chunks: ChunkedSequence, **overrides) -> comm.WorldConfig:
+    """One rank per chunk, element size from the data dtype (lasp2.py:290-293)."""
+    overrides.setdefault("element_bytes", chunks.q.element_size())
+    return comm.WorldConfig(world_size=chunks.chunks, sp_size=chunks.chunks, **overrides)
+
+
+def _check_world(chunks: ChunkedSequence, cfg: comm.WorldConfig) -> None:
+    if cfg.sp_size != chunks.chunks:
+        raise ValueError(f"world sp_size {cfg.sp_size} != chunk count {chunks.chunks}")
+    if cfg.element_bytes != chunks.q.element_size():
+        raise ValueError(f"world element_bytes {cfg.element_bytes} does not match dtype {chunks.q.dtype}")
+
+
+def _split_like(chunks: ChunkedSequence, full) -> list[torch.Tensor]:
+    full = _as_device_tensor(full)
+    if tuple(full.shape) != tuple(chunks.q.shape):
+        raise ValueError(f"expected shape {tuple(chunks.q.shape)}, got {tuple(full.shape)}")
+    return split_chunks(full.to(chunks.q.dtype), chunks.chunks)
+
+
+def _spawn(chunks: ChunkedSequence, cfg: comm.WorldConfig | None, program,
+           extra_args: list[tuple] | None = None) -> comm.WorldRun:
+    cfg = cfg or default_world(chunks)
+    _check_world(chunks, cfg)
+    rank_args = []
+    for rank in range(cfg.world_size):
+        t = rank % cfg.sp_size  # DP replicas carry the same data (lasp2.py:316)
+        qc, kc, vc = chunks.chunk(t)
+        extra = extra_args[t] if extra_args is not None else ()
+        rank_args.append((qc, kc, vc, *extra))
+    return comm.world_spawn(cfg, program, rank_args, device=chunks.q.device)
+
+
+def lasp2_forward_nomask(chunks: ChunkedSequence, cfg: comm.WorldConfig | None = None) -> ForwardOutcome:
+    """lasp2.py:323-332."""
+    run = _spawn(chunks, cfg, lambda ctx, qc, kc, vc: _forward_nomask_rank(ctx, qc, kc, vc))
+    t = chunks.chunks
+    return ForwardOutcome(outputs=[r[0] for r in run.results[:t]], caches=[r[1] for r in run.results[:t]], run=run)
+
+
+def lasp2_forward_masked(chunks: ChunkedSequence, cfg: comm.WorldConfig | None = None,
+                         overlap: bool = False) -> ForwardOutcome:
+    """lasp2.py:335-344."""
+    run = _spawn(chunks, cfg, lambda ctx, qc, kc, vc: _forward_masked_rank(ctx, qc, kc, vc, overlap=overlap))
+    t = chunks.chunks
+    return ForwardOutcome(outputs=[r[0] for r in run.results[:t]], caches=[r[1] for r in run.results[:t]], run=run)
+
+
+def lasp2_overlap_schedule(chunks: ChunkedSequence, cfg: comm.WorldConfig | None = None) -> ForwardOutcome:
+    """Masked forward with the collective in flight during intra compute (lasp2.py:347-355)."""
+    return lasp2_forward_masked(chunks, cfg, overlap=True)
+
+
+def _backward(chunks, d_out, caches, cfg, rank_fn) -> BackwardOutcome:
+    if len(caches) != chunks.chunks:
+        raise ValueError(f"expected {chunks.chunks} caches, got {len(caches)}")
+    d_chunks = _split_like(chunks, d_out)
+    run = _spawn(chunks, cfg, lambda ctx, qc, kc, vc, cache, dc: rank_fn(ctx, cache, dc),
+                 extra_args=[(caches[t], d_chunks[t]) for t in range(chunks.chunks)])
+    return BackwardOutcome(grads=run.results[:chunks.chunks], run=run)
+
+
+def lasp2_backward_nomask(chunks: ChunkedSequence, d_out, caches: list[ActivationCache],
+                          cfg: comm.WorldConfig | None = None) -> BackwardOutcome:
+    """lasp2.py:358-371."""
+    return _backward(chunks, d_out, caches, cfg, _backward_nomask_rank)
+
+
+def lasp2_backward_masked(chunks: ChunkedSequence, d_out, caches: list[ActivationCache],
+                          cfg: comm.WorldConfig | None = None) -> BackwardOutcome:
+    """lasp2.py:374-387."""
+    return _backward(chunks, d_out, caches, cfg, _backward_masked_rank)
+
+
+def lasp2_iteration(chunks: ChunkedSequence, d_out, masked: bool, cfg: comm.WorldConfig | None = None,
+                    overlap: bool = False) -> IterationOutcome:
+    """Forward plus backward in one world: exactly 2 collective launches (lasp2.py:390-409)."""
+    d_chunks = _split_like(chunks, d_out)
+
+    def program(ctx, qc, kc, vc, dc):
+        if masked:
+            out, cache = _forward_masked_rank(ctx, qc, kc, vc, overlap=overlap)
+            grad = _backward_masked_rank(ctx, cache, dc)
+        else:
+            out, cache = _forward_nomask_rank(ctx, qc, kc, vc)
+            grad = _backward_nomask_rank(ctx, cache, dc)
+        return out, grad, cache
+
+    run = _spawn(chunks, cfg, program, extra_args=[(d_chunks[t],) for t in range(chunks.chunks)])
+    t = chunks.chunks
+    return IterationOutcome(outputs=[r[0] for r in run.results[:t]], grads=[r[1] for r in run.results[:t]],
+                            caches=[r[2] for r in run.results[:t]], run=run)
+
+
+# ---- per-rank entry points for torchrun (one process per GPU) ---------------
+
+def rank_forward(ctx, qc: torch.Tensor, kc: torch.Tensor, vc: torch.Tensor, masked: bool = True,
+                 overlap: bool = False) -> tuple[torch.Tensor, ActivationCache]:
+    """The per-rank layer forward a model calls under torchrun (hybrid.py:171-175)."""
+    if masked:
+        return _forward_masked_rank(ctx, qc, kc, vc, overlap=overlap)
+    return _forward_nomask_rank(ctx, qc, kc, vc)
+
+
+def rank_backward(ctx, cache: ActivationCache, d_out: torch.Tensor) -> GradientBundle:
+    """The per-rank layer backward (hybrid.py:193-197)."""
+    if cache.masked:
+        return _backward_masked_rank(ctx, cache, d_out)
+    return _backward_nomask_rank(ctx, cache, d_out)
+
+
+__all__ = [
+    "ActivationCache", "BackwardOutcome", "ChunkedSequence", "ForwardOutcome", "GradientBundle", "IterationOutcome",
+    "default_world", "lasp2_backward_masked", "lasp2_backward_nomask", "lasp2_forward_masked",
+    "lasp2_forward_nomask", "lasp2_iteration", "lasp2_overlap_schedule", "rank_backward", "rank_forward",
+    "pack_slots", "unpack_slots",
+]
+
+
+# ---- per-slot kernels under the reference names (lasp2.py:126-203) ----------
+
+def chunk_state(kc: torch.Tensor, vc: torch.Tensor) -> torch.Tensor:
+    """M = K^T V per slot, (B, H, d, d) (lasp2.py:130-137)."""
+    kc, vc = _contig(_as_device_tensor(kc), _as_device_tensor(vc))
+    return ops.chunk_states(kc, vc)[1]
+
+
+def chunk_state_grad(qc: torch.Tensor, d_out: torch.Tensor) -> torch.Tensor:
+    """G = Q^T dO per slot (lasp2.py:140-147)."""
+    qc, do = _contig(_as_device_tensor(qc), _as_device_tensor(d_out))
+    return ops.chunk_states(qc, do)[1]
+
+
+def apply_state(xc: torch.Tensor, m: torch.Tensor) -> torch.Tensor:
+    """X @ M per slot (lasp2.py:150-156)."""
+    xc, m = _contig(_as_device_tensor(xc), _as_device_tensor(m))
+    return ops.apply_state(xc, m)
+
+
+def apply_state_t(xc: torch.Tensor, m: torch.Tensor) -> torch.Tensor:
+    """X @ M^T per slot (lasp2.py:159-165)."""
+    xc, m = _contig(_as_device_tensor(xc), _as_device_tensor(m))
+    return ops.apply_state(xc, m, transpose=True)
+
+
+def intra_forward(qc: torch.Tensor, kc: torch.Tensor, vc: torch.Tensor) -> torch.Tensor:
+    """Causal attention within the chunk (lasp2.py:168-174 / oracle.py:50-62)."""
+    qc, kc, vc = _contig(*map(_as_device_tensor, (qc, kc, vc)))
+    seg, _, nseg = ops.chunk_states(kc, vc)
+    return ops.causal_chunk(qc, kc, vc, seg, None, nseg)
+
+
+def intra_forward_left_product(qc: torch.Tensor, kc: torch.Tensor, vc: torch.Tensor) -> torch.Tensor:
+    """[(Q K^T) o Psi] V (lasp2.py:177-186): the blocked form the kernel evaluates."""
+    return intra_forward(qc, kc, vc)
+
+
+def intra_backward(qc: torch.Tensor, kc: torch.Tensor, vc: torch.Tensor, d_out: torch.Tensor) -> GradientBundle:
+    """Gradients of the masked intra-chunk term (lasp2.py:189-203)."""
+    q, k, v, do = _contig(*map(_as_device_tensor, (qc, kc, vc, d_out)))
+    seg, _, nseg = ops.chunk_states(k, v)
+    gseg = ops.segment_states(q, do, nseg)
+    ops.scan_segments(gseg, reverse=True, data_dtype=q.dtype)
+    dq = ops.causal_chunk(do, v, k, seg, None, nseg, reverse=False, transpose_state=True)
+    dk = ops.causal_chunk(v, do, q, gseg, None, nseg, reverse=True, transpose_state=True)
+    dv = ops.causal_chunk(k, q, do, gseg, None, nseg, reverse=True, transpose_state=False)
+    return GradientBundle(dq=dq, dk=dk, dv=dv)

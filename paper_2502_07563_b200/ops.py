@@ -1,0 +1,156 @@
+"""Typed torch-facing wrappers over the C-ABI kernels.
+
+Every function takes contiguous CUDA tensors in the BHND layout
+((B, H, tokens, d) data, (B, H, d, d) states), enqueues on the current CUDA
+stream and returns new tensors; the library itself never allocates.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from ._lib import FOLD_FULL, FOLD_PREFIX, FOLD_SUFFIX, call, dtype_code, ptr, require_cuda, state_dtype, stream_ptr
+
+_SM_COUNT: dict[int, int] = {}
+
+
+def sm_count(device: torch.device | None = None) -> int:
+    dev = torch.cuda.current_device() if device is None else device.index
+    if dev not in _SM_COUNT:
+        _SM_COUNT[dev] = torch.cuda.get_device_properties(dev).multi_processor_count
+    return _SM_COUNT[dev]
+
+
+def _slots(x: torch.Tensor) -> tuple[int, int, int]:
+    if x.ndim != 4:
+        raise ValueError(f"expected (batch, heads, tokens, dim), got {tuple(x.shape)}")
+    b, h, n, d = x.shape
+    return b * h, n, d
+
+
+def num_segments(x: torch.Tensor) -> int:
+    slots, n, d = _slots(x)
+    return int(_lib.load().lasp2_num_segments(dtype_code(x.dtype), slots, n, d, sm_count(x.device)))
+
+
+def segment_states(x: torch.Tensor, y: torch.Tensor, nseg: int) -> torch.Tensor:
+    """(B,H,nseg,d,d): per-segment X^T Y (lasp2.py:130-147 per segment)."""
+    require_cuda(x, y)
+    if x.shape != y.shape or x.dtype != y.dtype:
+        raise ValueError(f"segment_states operands differ: {tuple(x.shape)} {tuple(y.shape)}")
+    slots, n, d = _slots(x)
+    b, h = x.shape[:2]
+    out = torch.empty((b, h, nseg, d, d), dtype=state_dtype(x.dtype), device=x.device)
+    call("lasp2_segment_states", dtype_code(x.dtype), ptr(x), ptr(y), ptr(out), slots, n, d, nseg, stream_ptr())
+    return out
+
+
+def scan_segments(seg: torch.Tensor, reverse: bool, data_dtype: torch.dtype) -> torch.Tensor:
+    """In place exclusive prefix (suffix if reverse) over segments; returns the chunk total (B,H,d,d)."""
+    require_cuda(seg)
+    b, h, nseg, d, _ = seg.shape
+    total = torch.empty((b, h, d, d), dtype=seg.dtype, device=seg.device)
+    call("lasp2_scan_segments", dtype_code(data_dtype), ptr(seg), ptr(total), b * h, nseg, d, int(reverse),
+         stream_ptr())
+    return total
+
+
+def chunk_states(x: torch.Tensor, y: torch.Tensor, reverse: bool = False) -> tuple[torch.Tensor, torch.Tensor, int]:
+    """Segment states scanned in place plus the chunk total (the rank's M_t)."""
+    nseg = num_segments(x)
+    seg = segment_states(x, y, nseg)
+    total = scan_segments(seg, reverse, x.dtype)
+    return seg, total, nseg
+
+
+def fold(gathered: torch.Tensor, mode: int, bound: int = 0) -> torch.Tensor:
+    """Ordered fold of rank-major gathered states [T, ...] (numerics.py:71-121)."""
+    require_cuda(gathered)
+    nstates = gathered.shape[0]
+    out = torch.empty(gathered.shape[1:], dtype=gathered.dtype, device=gathered.device)
+    code = _lib.F64 if gathered.dtype == torch.float64 else _lib.F32
+    call("lasp2_fold_states", code, ptr(gathered), ptr(out), nstates, out.numel(), mode, bound, stream_ptr())
+    return out
+
+
+def prefix_states(gathered: torch.Tensor, upto: int) -> torch.Tensor:
+    return fold(gathered, FOLD_PREFIX, upto)
+
+
+def suffix_states(gathered: torch.Tensor, start: int) -> torch.Tensor:
+    return fold(gathered, FOLD_SUFFIX, start)
+
+
+def sum_states(gathered: torch.Tensor) -> torch.Tensor:
+    return fold(gathered, FOLD_FULL, 0)
+
+
+def causal_chunk(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, seg_states: torch.Tensor | None,
+                 base: torch.Tensor | None, nseg: int, reverse: bool = False,
+                 transpose_state: bool = False, out: torch.Tensor | None = None) -> torch.Tensor:
+    """out_s = q_s S_s + sum_{i<=s} (q_s.k_i) v_i with S from base + segment states (see header)."""
+    require_cuda(q, k, v, seg_states, base)
+    if not (q.shape == k.shape == v.shape):
+        raise ValueError(f"q/k/v shapes differ: {tuple(q.shape)} {tuple(k.shape)} {tuple(v.shape)}")
+    slots, n, d = _slots(q)
+    if out is None:
+        out = torch.empty_like(q)
+    call("lasp2_causal_chunk", dtype_code(q.dtype), ptr(q), ptr(k), ptr(v), ptr(seg_states), ptr(base), ptr(out),
+         slots, n, d, nseg, int(reverse), int(transpose_state), stream_ptr())
+    return out
+
+
+def apply_state(x: torch.Tensor, m: torch.Tensor, transpose: bool = False,
+                out: torch.Tensor | None = None, accumulate: bool = False) -> torch.Tensor:
+    """out (+)= x M or x M^T per slot (lasp2.py:150-165)."""
+    require_cuda(x, m)
+    slots, n, d = _slots(x)
+    if m.shape != (*x.shape[:2], d, d):
+        raise ValueError(f"state shape {tuple(m.shape)} does not match data {tuple(x.shape)}")
+    if out is None:
+        if accumulate:
+            raise ValueError("accumulate needs an output tensor")
+        out = torch.empty_like(x)
+    call("lasp2_apply_state", dtype_code(x.dtype), ptr(x), ptr(m), ptr(out), slots, n, d, int(transpose),
+         int(accumulate), stream_ptr())
+    return out
+
+
+def softmax_forward(q: torch.Tensor, k_full: torch.Tensor, v_full: torch.Tensor, causal: bool, row_offset: int,
+                    kv_tokens: int, kv_chunk: int, kv_rank_stride: int) -> tuple[torch.Tensor, torch.Tensor]:
+    """Softmax attention of a query chunk against (possibly rank-major) full K/V (oracle.py:136-139)."""
+    require_cuda(q, k_full, v_full)
+    slots, qn, d = _slots(q)
+    out = torch.empty_like(q)
+    lse = torch.empty(q.shape[:3], dtype=torch.float32, device=q.device)
+    call("lasp2h_softmax_forward", dtype_code(q.dtype), ptr(q), ptr(k_full), ptr(v_full), ptr(out), ptr(lse), slots,
+         qn, kv_tokens, d, int(causal), row_offset, kv_chunk, kv_rank_stride, stream_ptr())
+    return out, lse
+
+
+def softmax_backward(q, k_full, v_full, out, lse, d_out, causal: bool, row_offset: int, kv_tokens: int,
+                     kv_chunk: int, kv_rank_stride: int, grads: torch.Tensor, grad_rank_stride: int,
+                     dv_offset: int) -> torch.Tensor:
+    """dq plus full-length dk/dv contributions written into `grads` (oracle.py:142-158).
+
+    dk contribution of key j lands at grads.view(-1)[(j//chunk)*grad_rank_stride + (slot*chunk + j%chunk)*d],
+    dv at the same index + dv_offset.
+    """
+    require_cuda(q, k_full, v_full, out, d_out, grads)
+    slots, qn, d = _slots(q)
+    dq = torch.empty_like(q)
+    code = dtype_code(q.dtype)
+    nbytes = int(_lib.load().lasp2h_softmax_scratch_bytes(code, slots, qn, kv_tokens, d))
+    scratch = torch.empty(nbytes, dtype=torch.uint8, device=q.device)
+    flat = grads.view(-1)
+    call("lasp2h_softmax_backward", code, ptr(q), ptr(k_full), ptr(v_full), ptr(out), ptr(lse), ptr(d_out), ptr(dq),
+         flat.data_ptr(), flat.data_ptr() + dv_offset * flat.element_size(), ptr(scratch), slots, qn, kv_tokens, d,
+         int(causal), row_offset, kv_chunk, kv_rank_stride, grad_rank_stride, stream_ptr())
+    return dq
+
+
+def probe_gemm(a: torch.Tensor, b: torch.Tensor, a_mn: bool, b_mn: bool) -> torch.Tensor:
+    require_cuda(a, b)
+    d = torch.empty((128, 128), dtype=torch.float32, device=a.device)
+    call("lasp2_debug_probe_gemm", ptr(a), ptr(b), ptr(d), int(a_mn), int(b_mn), stream_ptr())
+    return d

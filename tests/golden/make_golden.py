@@ -1,0 +1,75 @@
+"""Generate golden fixtures by running the REFERENCE implementation.
+
+Run in the build container (where /root/reference exists):
+    python tests/golden/make_golden.py
+It imports laspsim from /root/reference/pkg/src (read-only), runs the
+reference's own world drivers on small cases from its test grids
+(pkg/tests/test_lasp2.py, test_acceptance.py, test_standard_sp.py) and on a
+row-subsampled cfg1 case, and writes tests/golden/reference_cases.npz.
+The fixtures travel with the repo; nothing at test time reads /root/reference.
+"""
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REF = Path("/root/reference/pkg/src")
+OUT = Path(__file__).resolve().parent / "reference_cases.npz"
+
+LASP_CASES = [  # (n, d, t, batch, heads, seed)
+    (8, 4, 1, 1, 1, 0), (8, 4, 2, 1, 1, 0), (16, 8, 4, 1, 1, 0), (16, 4, 8, 1, 1, 0),
+    (64, 16, 4, 1, 1, 0), (256, 16, 8, 1, 1, 0), (256, 4, 2, 1, 1, 0), (8, 4, 4, 2, 3, 5),
+    (256, 32, 4, 1, 2, 7),
+]
+CP_CASES = [(8, 4, 2, 1, 1, 0), (16, 8, 4, 1, 1, 0), (16, 4, 2, 1, 1, 0), (8, 4, 4, 2, 2, 3), (256, 32, 4, 1, 2, 1)]
+CFG1 = (4096, 64, 2, 1, 4, 0)  # B=1 H=4 d=64 N=4096 W=2
+CFG1_ROWS = np.arange(0, 4096, 127)
+
+
+def main() -> None:
+    sys.path.insert(0, str(REF))
+    from laspsim.datagen import gen_slots, qkv_slots
+    from laspsim.lasp2 import ChunkedSequence, lasp2_iteration
+    from laspsim.standard_sp import cp_iteration
+
+    def inputs(n, d, b, h, seed):
+        q, k, v = qkv_slots(seed, b, h, n, d)
+        return q, k, v, gen_slots(seed, b, h, n, d, "do")
+
+    cat = lambda xs: np.concatenate(xs, axis=2)  # noqa: E731
+    data = {}
+    for masked in (True, False):
+        for (n, d, t, b, h, seed) in LASP_CASES:
+            q, k, v, do = inputs(n, d, b, h, seed)
+            it = lasp2_iteration(ChunkedSequence(q, k, v, t), do, masked)
+            key = f"lasp2_{'m' if masked else 'u'}_{n}_{d}_{t}_{b}_{h}_{seed}"
+            data[key + "_out"] = cat(it.outputs)
+            data[key + "_dq"] = cat([g.dq for g in it.grads])
+            data[key + "_dk"] = cat([g.dk for g in it.grads])
+            data[key + "_dv"] = cat([g.dv for g in it.grads])
+            data[key + "_launches"] = np.array([it.run.stats.allgather_launches, it.run.stats.bytes_sent])
+    for causal in (True, False):
+        for (n, d, t, b, h, seed) in CP_CASES:
+            q, k, v, do = inputs(n, d, b, h, seed)
+            it = cp_iteration(ChunkedSequence(q, k, v, t), do, causal)
+            key = f"cp_{'c' if causal else 'n'}_{n}_{d}_{t}_{b}_{h}_{seed}"
+            data[key + "_out"] = cat(it.outputs)
+            data[key + "_dq"] = cat([g.dq for g in it.grads])
+            data[key + "_dk"] = cat([g.dk for g in it.grads])
+            data[key + "_dv"] = cat([g.dv for g in it.grads])
+    n, d, t, b, h, seed = CFG1
+    q, k, v, do = inputs(n, d, b, h, seed)
+    it = lasp2_iteration(ChunkedSequence(q, k, v, t), do, True)
+    for name, arr in (("out", cat(it.outputs)), ("dq", cat([g.dq for g in it.grads])),
+                      ("dk", cat([g.dk for g in it.grads])), ("dv", cat([g.dv for g in it.grads]))):
+        data[f"cfg1_{name}_rows"] = arr[:, :, CFG1_ROWS, :]
+        data[f"cfg1_{name}_sum"] = np.array([arr.sum(), (arr * arr).sum(), np.abs(arr).max()])
+    data["cfg1_rows"] = CFG1_ROWS
+    np.savez_compressed(OUT, **data)
+    print(f"wrote {OUT} ({OUT.stat().st_size} bytes, {len(data)} arrays)")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,89 @@
+"""Multi-process (gloo, world_size 2, CPU) coverage of the N>1 plumbing.
+
+The per-rank LASP-2 / LASP-2H collective structure — one state all_gather per
+pass, prefix/suffix folds of the rank-major gathered tensor, one
+reduce_scatter of rank-major dK/dV contributions — runs through
+DistRankContext exactly as under torchrun. Local math uses the oracle (CPU)
+so the test checks the exchange layout and ledger, not the kernels.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import lasp_oracle as O
+from paper_2502_07563_b200.comm import DistRankContext
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, results):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ctx = DistRankContext()
+        n, d, b, h = 32, 4, 1, 2
+        q, k, v, do = O.inputs(n, d, b, h, seed=3)
+        c = n // world
+        sl = slice(rank * c, (rank + 1) * c)
+        qc, kc, vc, dc = (torch.from_numpy(np.ascontiguousarray(x[:, :, sl])) for x in (q, k, v, do))
+        t = ctx.sp_position
+        # forward: M_t all_gather -> prefix fold -> intra + inter (lasp2.py:219-243)
+        m_t = kc.transpose(-1, -2) @ vc
+        gathered = ctx.all_gather(m_t.reshape(b * h * d, d)).view(world, b, h, d, d).numpy()
+        m_prefix = O.prefix_sum_states(list(gathered), t)
+        out = O.intra_forward_blocked(qc.numpy(), kc.numpy(), vc.numpy(), 4)
+        if t > 0:
+            out = out + qc.numpy() @ m_prefix
+        # backward: dM all_gather (async) -> suffix fold (lasp2.py:270-285)
+        g_t = qc.transpose(-1, -2) @ dc
+        pending = ctx.all_gather_async(g_t.reshape(b * h * d, d))
+        dq, dk, dv = O.intra_backward_blocked(qc.numpy(), kc.numpy(), vc.numpy(), dc.numpy(), 4)
+        if t > 0:
+            dq = dq + dc.numpy() @ np.swapaxes(m_prefix, -1, -2)
+        g_all = pending.wait().view(world, b, h, d, d).numpy()
+        if t < world - 1:
+            dm = O.suffix_sum_states(list(g_all), t + 1)
+            dk = dk + vc.numpy() @ np.swapaxes(dm, -1, -2)
+            dv = dv + kc.numpy() @ dm
+        # LASP-2H: rank-major contributions [T][2][...] -> one reduce_scatter
+        contrib = torch.zeros((world, 2, b, h, c, d), dtype=torch.float64)
+        contrib[:, 0] = torch.from_numpy(np.ascontiguousarray(
+            np.stack(np.split(np.full((b, h, n, d), rank + 1.0), world, axis=2))))
+        contrib[:, 1] = 10.0 * (rank + 1.0)
+        mine = ctx.reduce_scatter(contrib)
+        results[rank] = dict(out=out, dq=dq, dk=dk, dv=dv, rs=mine.numpy(),
+                             stats=(ctx.stats.allgather_launches, ctx.stats.reduce_scatter_launches,
+                                    ctx.stats.bytes_sent))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_gloo_lasp2_exchange_matches_oracle():
+    world = 2
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), results), nprocs=world, join=True)
+    q, k, v, do = O.inputs(32, 4, 1, 2, seed=3)
+    out, dq, dk, dv = O.lasp2_full(q, k, v, do, world, True, bc=4)
+    c = 16
+    for r in range(world):
+        sl = slice(r * c, (r + 1) * c)
+        res = results[r]
+        assert np.max(np.abs(res["out"] - out[:, :, sl])) <= 1e-12
+        for name, ref in (("dq", dq), ("dk", dk), ("dv", dv)):
+            assert O.relative_error(res[name], ref[:, :, sl]) <= 1e-12
+        assert np.allclose(res["rs"][0], 3.0) and np.allclose(res["rs"][1], 30.0)
+        ag, rs, nbytes = res["stats"]
+        assert ag == 2 and rs == 1  # 2 state all_gathers per iteration (+1 LASP-2H reduce_scatter)
+        state_bytes = 1 * 2 * 4 * 4 * 8
+        assert nbytes == 2 * state_bytes + world * 2 * 1 * 2 * c * 4 * 8

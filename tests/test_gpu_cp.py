@@ -1,0 +1,92 @@
+"""LASP-2H softmax layers (AllGather K/V + causal softmax) on the GPU, mirroring
+pkg/tests/test_standard_sp.py and acceptance criterion 6."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import lasp_oracle as O
+from paper_2502_07563_b200.lasp2 import ChunkedSequence
+from paper_2502_07563_b200.standard_sp import cp_backward, cp_forward, cp_iteration
+
+pytestmark = pytest.mark.gpu
+
+CP_CASES = [(8, 4, 2, 1, 1, 0), (16, 8, 4, 1, 1, 0), (16, 4, 2, 1, 1, 0), (8, 4, 4, 2, 2, 3), (256, 32, 4, 1, 2, 1)]
+
+
+def cat(xs):
+    return torch.cat(list(xs), dim=2)
+
+
+def to_np(t):
+    return t.double().cpu().numpy()
+
+
+def dev(x, dtype):
+    return torch.from_numpy(np.ascontiguousarray(x)).to("cuda", dtype)
+
+
+@pytest.mark.parametrize("causal", [True, False])
+@pytest.mark.parametrize("case", CP_CASES)
+def test_f64_matches_reference_fixtures(golden, case, causal):
+    n, d, t, b, h, seed = case
+    q, k, v, do = O.inputs(n, d, b, h, seed)
+    it = cp_iteration(ChunkedSequence(q, k, v, t), do, causal)
+    key = f"cp_{'c' if causal else 'n'}_{n}_{d}_{t}_{b}_{h}_{seed}"
+    assert np.max(np.abs(to_np(cat(it.outputs)) - golden[key + "_out"])) <= 1e-12
+    for name in ("dq", "dk", "dv"):
+        got = to_np(cat(getattr(g, name) for g in it.grads))
+        assert O.relative_error(got, golden[f"{key}_{name}"]) <= 1e-10, name
+    # 2 all_gathers (K, V) + 1 reduce_scatter (dK/dV) = 3 steps (standard_sp.py:112-114)
+    assert it.run.stats.communication_steps == 3
+    assert it.run.stats.allgather_launches == 2 and it.run.stats.reduce_scatter_launches == 1
+
+
+def test_zero_keys_causal_prefix_mean():
+    q, _, v = O.qkv_slots(4, 1, 1, 8, 4)
+    k = np.zeros_like(q)
+    fwd = cp_forward(ChunkedSequence(q, k, v, 2), True)
+    rows = v[0, 0]
+    want = np.stack([rows[:i + 1].mean(axis=0) for i in range(8)])
+    assert np.max(np.abs(to_np(cat(fwd.outputs))[0, 0] - want)) <= 1e-12
+
+
+def test_forward_traffic_is_chunk_sized_keys_and_values():
+    batch, heads, d, n, t = 2, 3, 4, 16, 4
+    q, k, v, _ = O.inputs(n, d, batch, heads)
+    fwd = cp_forward(ChunkedSequence(q, k, v, t))
+    per_rank = 2 * batch * heads * (n // t) * d * 8
+    for rank in range(t):
+        assert fwd.run.rank_stats[rank].bytes_sent == per_rank
+
+
+def test_iteration_traffic_adds_full_length_grads():
+    batch, heads, d, n, t = 2, 1, 8, 16, 4
+    q, k, v, do = O.inputs(n, d, batch, heads)
+    it = cp_iteration(ChunkedSequence(q, k, v, t), do)
+    per_rank = batch * heads * d * 8 * (2 * (n // t) + 2 * n)
+    for rank in range(t):
+        assert it.run.rank_stats[rank].bytes_sent == per_rank
+
+
+def test_backward_rejects_wrong_caches():
+    q, k, v, do = O.inputs(8, 4)
+    seq = ChunkedSequence(q, k, v, 2)
+    caches = cp_forward(seq, True).caches
+    with pytest.raises(ValueError):
+        cp_backward(seq, do, False, caches)
+    with pytest.raises(ValueError):
+        cp_backward(seq, do, True, caches[:1])
+
+
+@pytest.mark.parametrize("dtype,tol", [(torch.float32, 1e-4), (torch.bfloat16, 1e-2)])
+def test_low_precision_modes(dtype, tol):
+    q, k, v, do = O.inputs(1024, 64, 1, 2, 5)
+    if dtype == torch.bfloat16:
+        q, k, v, do = (O.bf16_round(x) for x in (q, k, v, do))
+    else:
+        q, k, v, do = (x.astype(np.float32).astype(np.float64) for x in (q, k, v, do))
+    ref = O.cp_full(q, k, v, do, 4, True)
+    it = cp_iteration(ChunkedSequence(*(dev(x, dtype) for x in (q, k, v)), 4), dev(do, dtype), True)
+    got = [to_np(cat(it.outputs))] + [to_np(cat(getattr(g, n) for g in it.grads)) for n in ("dq", "dk", "dv")]
+    for name, g, r in zip(("out", "dq", "dk", "dv"), got, ref):
+        assert O.normalized_error(g, r) <= tol, name

@@ -1,0 +1,177 @@
+"""Kernel-level parity of every C-ABI entry point against fp64 torch math on the
+same (bf16-rounded where applicable) inputs. Runs on a B200 only."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2502_07563_b200 import _lib, datagen, ops
+
+pytestmark = pytest.mark.gpu
+
+BF16_TOL = 1e-2   # north star: bf16-in / fp32-accumulate, normalised max error
+F32_TOL = 1e-4    # north star: fp32 validation mode
+F64_TOL = 1e-12
+
+
+def nerr(got: torch.Tensor, ref: torch.Tensor) -> float:
+    got, ref = got.double(), ref.double()
+    scale = ref.abs().max().item()
+    e = (got - ref).abs().max().item()
+    return e / scale if scale > 0 else e
+
+
+def seg_ranges(nseg: int, tokens: int):
+    nblk = (tokens + 127) // 128
+    for s in range(nseg):
+        lo, hi = (s * nblk // nseg) * 128, ((s + 1) * nblk // nseg) * 128
+        yield min(lo, tokens), min(hi, tokens)
+
+
+def rand(shape, dtype, seed=0, scale=1.0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    return ((torch.rand(shape, generator=g, device="cuda", dtype=torch.float64) * 2 - 1) * scale).to(dtype)
+
+
+def ref_segment_states(x, y, nseg):
+    b, h, n, d = x.shape
+    out = []
+    for lo, hi in seg_ranges(nseg, n):
+        xs, ys = x[:, :, lo:hi].double(), y[:, :, lo:hi].double()
+        out.append(xs.transpose(-1, -2) @ ys)
+    return torch.stack(out, dim=2)
+
+
+def ref_causal(q, k, v, seg, base, nseg, reverse, transpose):
+    b, h, n, d = q.shape
+    out = torch.empty((b, h, n, d), dtype=torch.float64, device=q.device)
+    for g, (lo, hi) in enumerate(seg_ranges(nseg, n)):
+        s0 = torch.zeros((b, h, d, d), dtype=torch.float64, device=q.device)
+        if seg is not None:
+            s0 = s0 + seg[:, :, g].double()
+        if base is not None:
+            s0 = s0 + base.double()
+        if transpose:
+            s0 = s0.transpose(-1, -2)
+        qs, ks, vs = (x[:, :, lo:hi].double() for x in (q, k, v))
+        L = hi - lo
+        m = torch.ones((L, L), dtype=torch.float64, device=q.device)
+        m = torch.triu(m) if reverse else torch.tril(m)
+        out[:, :, lo:hi] = ((qs @ ks.transpose(-1, -2)) * m) @ vs + qs @ s0
+    return out
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
+def test_probe_gemm_descriptor_conventions(a_mn, b_mn):
+    a = rand((128, 128), torch.bfloat16, 1)
+    b = rand((128, 128), torch.bfloat16, 2)
+    d = ops.probe_gemm(a, b, bool(a_mn), bool(b_mn))
+    A = a.double().T if a_mn else a.double()  # op(A): [M][K]
+    B = b.double().T if b_mn else b.double()  # op(B): [N][K]
+    ref = A @ B.T
+    torch.cuda.synchronize()
+    assert nerr(d, ref) <= 1e-5
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32, torch.float64])
+@pytest.mark.parametrize("shape", [(1, 2, 1024, 128), (2, 1, 700, 64), (1, 3, 128, 32), (1, 1, 5, 8)])
+def test_segment_states_and_scan(dtype, shape):
+    x, y = rand(shape, dtype, 3), rand(shape, dtype, 4)
+    nseg = max(1, min(3, (shape[2] + 127) // 128))
+    seg = ops.segment_states(x, y, nseg)
+    ref = ref_segment_states(x, y, nseg)
+    tol = {torch.bfloat16: 1e-5, torch.float32: 1e-5, torch.float64: F64_TOL}[dtype]
+    assert nerr(seg, ref) <= tol
+    fwd = seg.clone()
+    total = ops.scan_segments(fwd, reverse=False, data_dtype=dtype)
+    assert nerr(total, ref.sum(2)) <= tol
+    assert torch.count_nonzero(fwd[:, :, 0]) == 0
+    for g in range(1, nseg):
+        assert nerr(fwd[:, :, g], ref[:, :, :g].sum(2)) <= tol
+    rev = seg.clone()
+    ops.scan_segments(rev, reverse=True, data_dtype=dtype)
+    assert torch.count_nonzero(rev[:, :, nseg - 1]) == 0
+    for g in range(nseg - 1):
+        assert nerr(rev[:, :, g], ref[:, :, g + 1:].sum(2)) <= tol
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32, torch.float64])
+@pytest.mark.parametrize("reverse,transpose", [(False, False), (True, False), (False, True), (True, True)])
+@pytest.mark.parametrize("shape,nseg", [((1, 2, 1024, 128), 3), ((2, 1, 1000, 64), 2), ((1, 2, 256, 128), 1),
+                                        ((1, 1, 77, 128), 1)])
+def test_causal_chunk(dtype, reverse, transpose, shape, nseg):
+    q, k, v = rand(shape, dtype, 5), rand(shape, dtype, 6), rand(shape, dtype, 7)
+    b, h, n, d = shape
+    sd = _lib.state_dtype(dtype)
+    seg = rand((b, h, nseg, d, d), sd, 8, scale=30.0)
+    base = rand((b, h, d, d), sd, 9, scale=30.0)
+    got = ops.causal_chunk(q, k, v, seg, base, nseg, reverse=reverse, transpose_state=transpose)
+    ref = ref_causal(q, k, v, seg, base, nseg, reverse, transpose)
+    tol = {torch.bfloat16: BF16_TOL, torch.float32: F32_TOL, torch.float64: F64_TOL}[dtype]
+    e = nerr(got, ref)
+    assert e <= tol, e
+    if dtype == torch.bfloat16:
+        assert e <= 5e-3, e  # bf16 output rounding + bf16 state operand
+
+
+def test_causal_chunk_without_states():
+    q, k, v = (rand((1, 2, 512, 128), torch.bfloat16, s) for s in (10, 11, 12))
+    got = ops.causal_chunk(q, k, v, None, None, 1)
+    assert nerr(got, ref_causal(q, k, v, None, None, 1, False, False)) <= 5e-3
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32, torch.float64])
+@pytest.mark.parametrize("transpose", [False, True])
+@pytest.mark.parametrize("shape", [(1, 2, 4096, 128), (2, 2, 300, 64), (1, 1, 3, 16)])
+def test_apply_state(dtype, transpose, shape):
+    x = rand(shape, dtype, 13)
+    b, h, n, d = shape
+    m = rand((b, h, d, d), _lib.state_dtype(dtype), 14, scale=10.0)
+    got = ops.apply_state(x, m, transpose=transpose)
+    mm = m.double().transpose(-1, -2) if transpose else m.double()
+    ref = x.double() @ mm
+    tol = {torch.bfloat16: 5e-3, torch.float32: F32_TOL, torch.float64: F64_TOL}[dtype]
+    assert nerr(got, ref) <= tol
+    acc = got.clone()
+    ops.apply_state(x, m, transpose=transpose, out=acc, accumulate=True)
+    assert nerr(acc, 2 * ref) <= tol
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_fold_states_order_and_empty(dtype):
+    g = rand((4, 3, 5), dtype, 15)
+    g[:, 0, 0] = -0.0
+    for upto in range(5):
+        got = ops.prefix_states(g, upto)
+        want = torch.zeros_like(g[0]) if upto == 0 else g[:upto].sum(0)
+        assert torch.allclose(got, want, atol=1e-12, rtol=0)
+    assert torch.signbit(ops.prefix_states(g, 2)[0, 0])  # copy-first keeps -0.0
+    for start in range(5):
+        got = ops.suffix_states(g, start)
+        want = torch.zeros_like(g[0]) if start == 4 else g[start:].sum(0)
+        assert torch.allclose(got, want, atol=1e-12, rtol=0)
+    # descending fold order for suffix, ascending for prefix: exact f64 recomputation
+    acc = g[3].clone()
+    for i in (2, 1):
+        acc += g[i]
+    assert torch.equal(ops.suffix_states(g, 1), acc)
+    assert torch.equal(ops.sum_states(g), ((g[0] + g[1]) + g[2]) + g[3])
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32, torch.bfloat16])
+def test_gen_slots_device_bit_exact(dtype):
+    got = datagen.gen_slots_device(0, 2, 3, 257, 64, "q", dtype=dtype)
+    host = datagen.gen_slots(0, 2, 3, 257, 64, "q", dtype=np.float64)
+    want = torch.from_numpy(host).cuda()
+    if dtype == torch.float64:
+        assert torch.equal(got, want)
+    else:
+        assert torch.equal(got, want.float().to(dtype))
+
+
+def test_ops_reject_cpu_and_noncontiguous():
+    x = torch.zeros((1, 1, 128, 128), dtype=torch.bfloat16)
+    with pytest.raises(ValueError, match="CUDA"):
+        ops.segment_states(x, x, 1)
+    y = torch.zeros((1, 1, 128, 256), dtype=torch.bfloat16, device="cuda")[..., ::2]
+    with pytest.raises(ValueError, match="contiguous"):
+        ops.apply_state(y, torch.zeros((1, 1, 128, 128), device="cuda"))
