@@ -1,0 +1,365 @@
+"""LASP-2 layer benchmark (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1)
+
+Headline workload (BASELINE.json configs[1], the first GPU config):
+cfg2 = LASP-2 unmasked (bidirectional) layer fwd+bwd, B=1 H=16 d=128,
+N=131072 tokens in total, C = N/W per GPU (strong scaling, as the config fixes N).
+The same line carries the masked cfg3 layer (N=524288, the Linear-Llama3-1B
+shape) under "secondary", measured the same way.
+
+One step = rank_forward + rank_backward of one layer on the rank's chunk
+(state all_gather over NCCL for N>1). Inputs (SplitMix64 counter-hash, the
+reference datagen, generated on device) are 2 GiB+ per step, far above the
+126 MB L2, so no flush is needed. Device time = CUDA events on the compute
+stream between barrier+synchronize brackets, max over ranks.
+
+--impl reference times the reference algorithm's CPU implementation (the
+numpy oracle port under oracle/, f32, all host cores) on a bounded sample of
+the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "LASP-2 fwd+bwd tokens/sec at 1/2/4/8 B200, % of bf16 tensor peak"
+UNIT = "tokens/s"
+H, D, B = 16, 128, 1
+WORKLOADS = {
+    "cfg2": dict(name="cfg2: LASP-2 unmasked (bidirectional) layer fwd+bwd, B=1 H=16 d=128, N=131072 total",
+                 n=131072, masked=False),
+    "cfg3": dict(name="cfg3: LASP-2 masked layer fwd+bwd at Linear-Llama3-1B shape, B=1 H=16 d=128, N=524288 total",
+                 n=524288, masked=True),
+}
+BC = 256  # block size pinned for the algorithmic FLOP count
+
+
+def flops_per_token(masked: bool) -> float:
+    """Causal-useful algorithmic FLOPs per token (all heads), BASELINE.md §3."""
+    per_head = 12 * D * D + (7 * D * (BC + 1) if masked else 0)
+    return float(per_head * H)
+
+
+def min_bytes_per_token() -> float:
+    """fwd reads q,k,v writes o; bwd reads q,k,v,dO writes dq,dk,dv: 22*d bytes/token/head (bf16)."""
+    return 22.0 * D * H
+
+
+def load_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        j = json.loads(p.read_text())
+        return dict(hbm=j["hbm_gbs"], tensor=j["bf16_tflops"], tensor_sustained=j.get("bf16_tflops_sustained"),
+                    source="measured (MEASURED_PEAKS.json)")
+    return dict(hbm=6650.0, tensor=1590.0, tensor_sustained=1400.0, source="fallback (B200_PROFILING.md)")
+
+
+def ncu_traffic(kernel_key: str):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu summary, if present."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None
+    try:
+        return json.loads(p.read_text()).get(kernel_key)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int) -> None:
+        self.index = index
+        self.samples: list[list[str]] = []
+        self._stop = threading.Event()
+        self._proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self._proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                           "--format=csv,noheader,nounits", "-lms", "100"],
+                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._thread = threading.Thread(target=self._read, daemon=True)
+            self._thread.start()
+        except FileNotFoundError:
+            self._proc = None
+        return self
+
+    def _read(self):
+        for line in self._proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self._proc is not None:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self._proc.kill()
+
+    def summary(self) -> dict:
+        rows = [r for r in self.samples if len(r) >= 7]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm / cpu_baseline: the oracle port on a bounded sample
+# ---------------------------------------------------------------------------
+
+def cpu_reference(workload: str, budget_s: float = 20.0) -> dict:
+    import numpy as np
+
+    from oracle import lasp_oracle as O
+
+    wl = WORKLOADS[workload]
+    cores = len(os.sched_getaffinity(0))
+    n = 2048 if wl["masked"] else 8192
+    q, k, v, do = (O.gen_slots(0, B, H, n, D, t, np.float32) for t in ("q", "k", "v", "do"))
+    # warm-up once, then as many full fwd+bwd iterations of the sample as fit the budget
+    O.lasp2_full(q, k, v, do, 1, wl["masked"], bc=BC)
+    times = []
+    t_end = time.perf_counter() + budget_s
+    while time.perf_counter() < t_end or len(times) < 2:
+        t0 = time.perf_counter()
+        O.lasp2_full(q, k, v, do, 1, wl["masked"], bc=BC)
+        times.append(time.perf_counter() - t0)
+        if len(times) >= 50:
+            break
+    med = statistics.median(times)
+    return {"value": n / med, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"numpy f32 oracle (oracle/lasp_oracle.py, restating lasp2.py:208-285 blocked at Bc={BC}) "
+                      f"on N={n} tokens of the same B=1 H=16 d=128 layer, T=1, median of {len(times)} "
+                      f"iterations, OpenBLAS threads={os.environ.get('OPENBLAS_NUM_THREADS', 'default')}"}
+
+
+def run_reference_arm(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = dict(workload=WORKLOADS[args.workload]["name"], global_batch=B, seq_len=WORKLOADS[args.workload]["n"],
+               heads=H, dim=D)
+    vals = []
+    for _ in range(args.warmup):
+        cpu_reference(args.workload, budget_s=0.5)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        vals.append(cpu_reference(args.workload, budget_s=max(0.5, min(5.0, 120.0 / max(1, args.steps)))))
+    wall = time.perf_counter() - t0
+    v = statistics.median(x["value"] for x in vals)
+    base = dict(vals[0])
+    base["value"] = v
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": WORKLOADS[args.workload]["n"] / v * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (reference datagen SplitMix64 counter-hash)", "config": cfg,
+            "cpu_baseline": base, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": wall}
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def measure_workload(workload: str, ctx, rank: int, world: int, steps: int, warmup: int, device) -> dict:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2502_07563_b200 import _lib
+    from paper_2502_07563_b200.datagen import gen_slots_device
+    from paper_2502_07563_b200.lasp2 import rank_backward, rank_forward
+
+    wl = WORKLOADS[workload]
+    n, masked = wl["n"], wl["masked"]
+    c = n // world
+    q, k, v, do = (gen_slots_device(0, B, H, c, D, t, torch.bfloat16, device=device, row_offset=rank * c)
+                   for t in ("q", "k", "v", "do"))
+
+    def step(q, k, v, do):
+        out, cache = rank_forward(ctx, q, k, v, masked=masked)
+        g = rank_backward(ctx, cache, do)
+        return out, g
+
+    for _ in range(warmup):
+        step(q, k, v, do)
+    stream = torch.cuda.current_stream()
+
+    def sync_all():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=device, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # --- device-timed region (inputs resident in HBM) ---
+    _lib.PROFILER.reset(enabled=True)
+    sync_all()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(device.index) as clocks:
+        t0.record(stream)
+        for _ in range(steps):
+            step(q, k, v, do)
+        t1.record(stream)
+        sync_all()
+    ms = max_over_ranks(t0.elapsed_time(t1) / steps)
+    durations = _lib.PROFILER.durations_ms()
+    launches = _lib.PROFILER.launches
+    _lib.PROFILER.reset(enabled=False)
+
+    # --- end-to-end through the public API with host buffers ---
+    pin = lambda t: t.cpu().pin_memory()  # noqa: E731
+    hq, hk, hv, hdo = pin(q), pin(k), pin(v), pin(do)
+    outs_host = [torch.empty(q.shape, dtype=q.dtype, pin_memory=True) for _ in range(4)]
+    h2d = 4 * q.numel() * q.element_size()
+    d2h = 4 * q.numel() * q.element_size()
+    e2e_steps = max(2, min(steps, 5))
+    sync_all()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        dq_, dk_, dv_, ddo = (x.to(device, non_blocking=True) for x in (hq, hk, hv, hdo))
+        out, g = step(dq_, dk_, dv_, ddo)
+        for dst, src in zip(outs_host, (out, g.dq, g.dk, g.dv)):
+            dst.copy_(src, non_blocking=True)
+    e1.record(stream)
+    sync_all()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e2e_steps)
+
+    # --- dominant kernel (most device time per step) and its roofline ---
+    per_kernel = {k2: sum(v2) / steps for k2, v2 in durations.items()}
+    dom = max(per_kernel, key=per_kernel.get)
+    dom_launch_ms = statistics.mean(durations[dom])
+    unit_bytes = B * H * c * D * 2  # one bf16 (B,H,C,d) tensor
+    algo_bytes = {"lasp2_causal_chunk": 4 * unit_bytes, "lasp2_apply_state": 2 * unit_bytes,
+                  "lasp2_segment_states": 2 * unit_bytes}.get(dom, 0)
+    return dict(n=n, c=c, masked=masked, ms=ms, e2e_ms=e2e_ms, per_kernel_ms=per_kernel, dominant=dom,
+                dom_launch_ms=dom_launch_ms, dom_algo_bytes=algo_bytes, launches_per_step=launches / steps,
+                h2d=h2d * world, d2h=d2h * world, clocks=clocks.summary(), e2e_steps=e2e_steps)
+
+
+def summarize(r: dict, world: int, peaks: dict) -> dict:
+    tok_s = r["n"] / (r["ms"] / 1e3)
+    flop_s = flops_per_token(r["masked"]) * tok_s
+    byte_s = min_bytes_per_token() * tok_s
+    achieved = r["dom_algo_bytes"] / (r["dom_launch_ms"] / 1e3) / 1e9
+    return dict(
+        value=tok_s, ms_per_step=r["ms"],
+        tensor_tflops_per_gpu=flop_s / world / 1e12,
+        tensor_frac_of_peak=flop_s / world / (peaks["tensor"] * 1e12),
+        min_bytes_gbs_per_gpu=byte_s / world / 1e9,
+        hbm_frac_of_peak=byte_s / world / (peaks["hbm"] * 1e9),
+        per_kernel_ms_per_step=r["per_kernel_ms"],
+        roofline={"kernel": r["dominant"], "bound": "hbm", "achieved": achieved, "peak": peaks["hbm"],
+                  "unit": "GB/s", "frac": achieved / peaks["hbm"], "traffic": ncu_traffic(r["dominant"]),
+                  "peak_source": peaks["source"],
+                  "algorithmic_bytes_per_launch": r["dom_algo_bytes"], "avg_launch_ms": r["dom_launch_ms"]},
+        e2e={"value": r["n"] / (r["e2e_ms"] / 1e3), "unit": UNIT, "h2d_bytes_per_step": r["h2d"],
+             "d2h_bytes_per_step": r["d2h"], "ms_per_step": r["e2e_ms"], "steps": r["e2e_steps"]},
+        gpu_launches_per_step=r["launches_per_step"], clocks=r["clocks"])
+
+
+def run_gpu_arm(args) -> None:
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}; launch N>1 with torchrun")
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    from paper_2502_07563_b200 import comm
+
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=device)
+        ctx = comm.DistRankContext()
+    else:
+        ctx = comm.LocalRankContext()
+    peaks = load_peaks()
+    main = measure_workload(args.workload, ctx, rank, world, args.steps, args.warmup, device)
+    sec_name = "cfg3" if args.workload == "cfg2" else "cfg2"
+    secondary = None if args.no_secondary else measure_workload(sec_name, ctx, rank, world, args.steps, args.warmup,
+                                                                device)
+    if rank == 0:
+        s = summarize(main, world, peaks)
+        line = {"metric": METRIC, "value": s["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": s["ms_per_step"], "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic: reference datagen (SplitMix64 counter-hash) generated on device, bf16",
+                "config": {"workload": WORKLOADS[args.workload]["name"], "global_batch": B,
+                           "seq_len": main["n"], "chunk_per_gpu": main["c"], "heads": H, "dim": D,
+                           "parallelism": f"sp{world}", "masked": main["masked"],
+                           "l2": "inputs >= 2 GiB per step >> 126 MB L2; no flush needed"},
+                "tensor_frac_of_peak": s["tensor_frac_of_peak"], "tensor_tflops_per_gpu": s["tensor_tflops_per_gpu"],
+                "hbm_frac_of_peak_min_bytes": s["hbm_frac_of_peak"], "roofline": s["roofline"],
+                "e2e": s["e2e"], "gpu_launches": int(round(s["gpu_launches_per_step"] * args.steps)),
+                "clocks": s["clocks"], "per_kernel_ms_per_step": s["per_kernel_ms_per_step"]}
+        if secondary is not None:
+            ss = summarize(secondary, world, peaks)
+            line["secondary"] = {"workload": WORKLOADS[sec_name]["name"], "value": ss["value"], "unit": UNIT,
+                                 "ms_per_step": ss["ms_per_step"], "chunk_per_gpu": secondary["c"],
+                                 "tensor_frac_of_peak": ss["tensor_frac_of_peak"],
+                                 "tensor_tflops_per_gpu": ss["tensor_tflops_per_gpu"],
+                                 "hbm_frac_of_peak_min_bytes": ss["hbm_frac_of_peak"], "roofline": ss["roofline"],
+                                 "e2e": ss["e2e"], "per_kernel_ms_per_step": ss["per_kernel_ms_per_step"]}
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_reference(args.workload, budget_s=args.cpu_budget)
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3 (timing rules)")
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()

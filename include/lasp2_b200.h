@@ -110,11 +110,13 @@ int lasp2h_softmax_backward(int dtype, const void* q, const void* k_full, const 
                             void* stream);
 int64_t lasp2h_softmax_scratch_bytes(int dtype, int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim);
 
-/* Deterministic inputs: out[slot] = gen_data(seed, rows, cols, tag_slot) where
- * tag_words[slot] is the 64-bit blake2b word of the slot's tag. Bit-exact port
- * of gen_data / gen_slots (datagen.py:33-71); bf16 rounds f64->f32->bf16. */
+/* Deterministic inputs: out[slot] = rows [row_offset, row_offset+rows) of
+ * gen_data(seed, *, cols, tag_slot) where tag_words[slot] is the 64-bit blake2b
+ * word of the slot's tag. Bit-exact port of gen_data / gen_slots
+ * (datagen.py:33-71); bf16 rounds f64->f32->bf16. row_offset lets each rank
+ * generate only its own chunk of the full sequence. */
 int lasp2_gen_slots(int dtype, uint64_t seed, const uint64_t* tag_words_device, void* out, int64_t slots, int64_t rows,
-                    int64_t cols, void* stream);
+                    int64_t cols, int64_t row_offset, void* stream);
 
 /* Test hook: d (f32 128x128) = op(a) op(b)^T for bf16 128x128 tiles with the
  * UMMA descriptor convention of the fast path (a_mn / b_mn select MN-major). */

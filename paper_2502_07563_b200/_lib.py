@@ -38,7 +38,7 @@ SIGNATURES = {
     "lasp2h_softmax_backward": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int,
                                        _int, _i64, _i64, _i64, _i64, _vp]),
     "lasp2h_softmax_scratch_bytes": (_i64, [_int, _i64, _i64, _i64, _int]),
-    "lasp2_gen_slots": (_int, [_int, _u64, _vp, _vp, _i64, _i64, _i64, _vp]),
+    "lasp2_gen_slots": (_int, [_int, _u64, _vp, _vp, _i64, _i64, _i64, _i64, _vp]),
     "lasp2_debug_probe_gemm": (_int, [_vp, _vp, _vp, _int, _int, _vp]),
 }
 
@@ -74,9 +74,47 @@ def load() -> ctypes.CDLL:
     return _lib
 
 
+class _Profiler:
+    """Optional per-entry-point device timing and launch counting (bench.py).
+
+    When enabled, every C-ABI compute call is bracketed by CUDA events on the
+    stream it is enqueued on, so per-kernel durations are measured live inside
+    a timed region without a profiler attached.
+    """
+
+    def __init__(self) -> None:
+        self.enabled = False
+        self.launches = 0
+        self.events: dict[str, list] = {}
+
+    def reset(self, enabled: bool) -> None:
+        self.enabled = enabled
+        self.launches = 0
+        self.events = {}
+
+    def durations_ms(self) -> dict[str, list[float]]:
+        return {k: [a.elapsed_time(b) for a, b in v] for k, v in self.events.items()}
+
+
+PROFILER = _Profiler()
+# kernels launched per call of each entry point (for gpu_launches accounting)
+KERNELS_PER_CALL = {"lasp2h_softmax_backward": 4}
+_NO_LAUNCH = {"lasp2_version", "lasp2_last_error", "lasp2_num_segments", "lasp2h_softmax_scratch_bytes"}
+
+
 def call(name: str, *args) -> int:
     lib = load()
-    status = getattr(lib, name)(*args)
+    prof = PROFILER
+    if prof.enabled and name not in _NO_LAUNCH:
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        status = getattr(lib, name)(*args)
+        b.record()
+        prof.events.setdefault(name, []).append((a, b))
+        prof.launches += KERNELS_PER_CALL.get(name, 1)
+    else:
+        status = getattr(lib, name)(*args)
     if status != 0:
         msg = lib.lasp2_last_error().decode()
         if status == 1:

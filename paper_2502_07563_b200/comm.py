@@ -556,3 +556,47 @@ class DistRankContext(_ContextBase):
     def mark(self, kind: str, detail: str = "") -> None:
         self.trace.append(TraceEvent(len(self.trace), self.rank, time.perf_counter(), kind, detail))
         self._device_mark(kind)
+
+
+class LocalRankContext(_ContextBase):
+    """World of one rank (T = 1) without torch.distributed: collectives are
+    local, still accounted as one launch each (the bench's N=1 path)."""
+
+    def __init__(self) -> None:
+        self._init_common()
+        self.rank = 0
+        self.trace: list[TraceEvent] = []
+
+    sp_position = 0
+    sp_size = 1
+
+    def _account(self, kind: str, t: torch.Tensor) -> None:
+        if kind == "all_gather":
+            self.stats.allgather_launches += 1
+        else:
+            self.stats.reduce_scatter_launches += 1
+        self.stats.communication_steps += 1
+        self.stats._account(kind, t.numel() * t.element_size())
+
+    def all_gather_async(self, payload: torch.Tensor, tag: str = ""):
+        self._account("all_gather", payload)
+        out = payload.unsqueeze(0)
+
+        class _Done:
+            def wait(self_inner):
+                return out
+
+        return _Done()
+
+    def all_gather(self, payload: torch.Tensor, tag: str = "") -> torch.Tensor:
+        return self.all_gather_async(payload, tag).wait()
+
+    def reduce_scatter(self, stacked: torch.Tensor, tag: str = "") -> torch.Tensor:
+        self._account("reduce_scatter", stacked)
+        return stacked[0]
+
+    def barrier(self) -> None:
+        pass
+
+    def mark(self, kind: str, detail: str = "") -> None:
+        pass

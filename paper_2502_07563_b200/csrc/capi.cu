@@ -210,17 +210,17 @@ int lasp2h_softmax_backward(int dtype, const void* q, const void* k_full, const 
 }
 
 int lasp2_gen_slots(int dtype, uint64_t seed, const uint64_t* tag_words_device, void* out, int64_t slots, int64_t rows,
-                    int64_t cols, void* stream) {
+                    int64_t cols, int64_t row_offset, void* stream) {
   CHECK(valid_dtype(dtype), "gen_slots: unknown dtype");
   CHECK(tag_words_device && out, "gen_slots: null pointer");
-  CHECK(slots >= 1 && rows >= 1 && cols >= 1, "gen_slots: shape must be positive");
+  CHECK(slots >= 1 && rows >= 1 && cols >= 1 && row_offset >= 0, "gen_slots: shape must be positive");
   cudaError_t e;
   if (dtype == LASP2_F32)
-    e = lasp::gen_slots<float>(seed, tag_words_device, out, slots, rows, cols, S(stream));
+    e = lasp::gen_slots<float>(seed, tag_words_device, out, slots, rows, cols, row_offset, S(stream));
   else if (dtype == LASP2_F64)
-    e = lasp::gen_slots<double>(seed, tag_words_device, out, slots, rows, cols, S(stream));
+    e = lasp::gen_slots<double>(seed, tag_words_device, out, slots, rows, cols, row_offset, S(stream));
   else
-    e = lasp::gen_slots<__nv_bfloat16>(seed, tag_words_device, out, slots, rows, cols, S(stream));
+    e = lasp::gen_slots<__nv_bfloat16>(seed, tag_words_device, out, slots, rows, cols, row_offset, S(stream));
   return cuda_status(e, "gen_slots");
 }
 

@@ -34,7 +34,7 @@ cudaError_t fold_states(const void* gathered, void* out, int nstates, int64_t el
                         cudaStream_t s);
 template <typename T>
 cudaError_t gen_slots(uint64_t seed, const uint64_t* tag_words, void* out, int64_t slots, int64_t rows, int64_t cols,
-                      cudaStream_t s);
+                      int64_t row0, cudaStream_t s);
 
 // tcgen05 fast path (bf16 in, fp32 states)
 bool tc_supported(int dim, int64_t tokens);

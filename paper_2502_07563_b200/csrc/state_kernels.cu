@@ -67,13 +67,13 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 // h0 = mix(seed ^ tag_word[slot]); the f64 value is rounded once to T.
 template <typename T>
 __global__ void gen_slots_kernel(uint64_t seed, const uint64_t* __restrict__ tag_words, T* __restrict__ out,
-                                 int64_t slots, int64_t rows, int64_t cols) {
+                                 int64_t slots, int64_t rows, int64_t cols, int64_t row0) {
   const int64_t n = slots * rows * cols;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t slot = idx / (rows * cols);
     const int64_t rc = idx % (rows * cols);
-    const uint64_t r = (uint64_t)(rc / cols), c = (uint64_t)(rc % cols);
+    const uint64_t r = (uint64_t)(rc / cols + row0), c = (uint64_t)(rc % cols);
     const uint64_t h0 = mix64(seed ^ tag_words[slot]);
     const uint64_t h = mix64(mix64(h0 ^ r) ^ c);
     const double u = (double)(h >> 11) * 0x1.0p-53;
@@ -84,13 +84,13 @@ __global__ void gen_slots_kernel(uint64_t seed, const uint64_t* __restrict__ tag
 template <>
 __global__ void gen_slots_kernel<__nv_bfloat16>(uint64_t seed, const uint64_t* __restrict__ tag_words,
                                                 __nv_bfloat16* __restrict__ out, int64_t slots, int64_t rows,
-                                                int64_t cols) {
+                                                int64_t cols, int64_t row0) {
   const int64_t n = slots * rows * cols;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t slot = idx / (rows * cols);
     const int64_t rc = idx % (rows * cols);
-    const uint64_t r = (uint64_t)(rc / cols), c = (uint64_t)(rc % cols);
+    const uint64_t r = (uint64_t)(rc / cols + row0), c = (uint64_t)(rc % cols);
     const uint64_t h0 = mix64(seed ^ tag_words[slot]);
     const uint64_t h = mix64(mix64(h0 ^ r) ^ c);
     const double u = (double)(h >> 11) * 0x1.0p-53;
@@ -117,11 +117,11 @@ cudaError_t fold_states(const void* gathered, void* out, int nstates, int64_t el
 
 template <typename T>
 cudaError_t gen_slots(uint64_t seed, const uint64_t* tag_words, void* out, int64_t slots, int64_t rows, int64_t cols,
-                      cudaStream_t s) {
+                      int64_t row0, cudaStream_t s) {
   const int64_t n = slots * rows * cols;
   int64_t blocks = (n + 255) / 256;
   if (blocks > 148 * 64) blocks = 148 * 64;
-  gen_slots_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(seed, tag_words, (T*)out, slots, rows, cols);
+  gen_slots_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(seed, tag_words, (T*)out, slots, rows, cols, row0);
   return cudaGetLastError();
 }
 
@@ -129,9 +129,9 @@ template cudaError_t scan_states<float>(void*, void*, int64_t, int, int, int, cu
 template cudaError_t scan_states<double>(void*, void*, int64_t, int, int, int, cudaStream_t);
 template cudaError_t fold_states<float>(const void*, void*, int, int64_t, int, int, cudaStream_t);
 template cudaError_t fold_states<double>(const void*, void*, int, int64_t, int, int, cudaStream_t);
-template cudaError_t gen_slots<float>(uint64_t, const uint64_t*, void*, int64_t, int64_t, int64_t, cudaStream_t);
-template cudaError_t gen_slots<double>(uint64_t, const uint64_t*, void*, int64_t, int64_t, int64_t, cudaStream_t);
+template cudaError_t gen_slots<float>(uint64_t, const uint64_t*, void*, int64_t, int64_t, int64_t, int64_t, cudaStream_t);
+template cudaError_t gen_slots<double>(uint64_t, const uint64_t*, void*, int64_t, int64_t, int64_t, int64_t, cudaStream_t);
 template cudaError_t gen_slots<__nv_bfloat16>(uint64_t, const uint64_t*, void*, int64_t, int64_t, int64_t,
-                                              cudaStream_t);
+                                              int64_t, cudaStream_t);
 
 }  // namespace lasp
