@@ -78,50 +78,60 @@ def ncu_traffic(kernel_key: str):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock / throttle reasons sampled in-process through NVML every ~5 ms.
 
-    def __init__(self, index: int) -> None:
+    Started before warm-up (so nothing spawns inside a timed region);
+    summary(t0, t1) keeps only samples taken inside [t0, t1] (host clock).
+    """
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, index: int, period: float = 0.005) -> None:
         self.index = index
-        self.samples: list[list[str]] = []
+        self.period = period
+        self.samples: list[tuple[float, float, int]] = []
+        self.max_mhz = None
         self._stop = threading.Event()
-        self._proc = None
+        self._thread = None
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
         try:
-            self._proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                           "--format=csv,noheader,nounits", "-lms", "100"],
-                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM))
+            self._thread = threading.Thread(target=self._run, daemon=True)
             self._thread.start()
-        except FileNotFoundError:
-            self._proc = None
+        except Exception:  # noqa: BLE001 - reported as unsampled
+            self._thread = None
         return self
 
-    def _read(self):
-        for line in self._proc.stdout:
-            self.samples.append([x.strip() for x in line.split(",")])
+    def _run(self):
+        nv, h = self._nv, self._h
+        while not self._stop.is_set():
+            try:
+                sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                rs = int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))
+                self.samples.append((time.time(), sm, rs))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(self.period)
 
     def __exit__(self, *exc):
-        if self._proc is not None:
-            self._proc.terminate()
-            try:
-                self._proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self._proc.kill()
+        self._stop.set()
+        if self._thread is not None:
+            self._thread.join(timeout=2)
 
-    def summary(self) -> dict:
-        rows = [r for r in self.samples if len(r) >= 7]
+    def summary(self, t0: float | None = None, t1: float | None = None) -> dict:
+        rows = [r for r in self.samples if (t0 is None or r[0] >= t0) and (t1 is None or r[0] <= t1)]
         if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(rows)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "samples": 0}
+        reasons = sorted({n for _, _, rs in rows for n, bit in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": statistics.median(r[1] for r in rows), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(rows)}
 
 
 # ---------------------------------------------------------------------------
@@ -183,7 +193,8 @@ def run_reference_arm(args) -> None:
 # GPU arm
 # ---------------------------------------------------------------------------
 
-def measure_workload(workload: str, ctx, rank: int, world: int, steps: int, warmup: int, device) -> dict:
+def measure_workload(workload: str, ctx, rank: int, world: int, steps: int, warmup: int, device,
+                     use_graph: bool = True) -> dict:
     import torch
     import torch.distributed as dist
 
@@ -197,14 +208,10 @@ def measure_workload(workload: str, ctx, rank: int, world: int, steps: int, warm
     q, k, v, do = (gen_slots_device(0, B, H, c, D, t, torch.bfloat16, device=device, row_offset=rank * c)
                    for t in ("q", "k", "v", "do"))
 
-    def step(q, k, v, do):
+    def step():
         out, cache = rank_forward(ctx, q, k, v, masked=masked)
         g = rank_backward(ctx, cache, do)
-        return out, g
-
-    for _ in range(warmup):
-        step(q, k, v, do)
-    stream = torch.cuda.current_stream()
+        return out, g.dq, g.dk, g.dv
 
     def sync_all():
         torch.cuda.synchronize()
@@ -219,50 +226,92 @@ def measure_workload(workload: str, ctx, rank: int, world: int, steps: int, warm
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # --- device-timed region (inputs resident in HBM) ---
-    _lib.PROFILER.reset(enabled=True)
-    sync_all()
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stream = torch.cuda.current_stream()
     with ClockSampler(device.index) as clocks:
+        for _ in range(warmup):
+            step()
+        sync_all()
+
+        # (1) per-kernel profile: launches queued behind a device sleep, so every
+        #     CUDA-event bracket measures the kernel alone (no host gaps)
+        prof_steps = max(1, min(steps, 10))
+        _lib.PROFILER.reset(enabled=True)
+        torch.cuda._sleep(int(6e8))
+        for _ in range(prof_steps):
+            step()
+        sync_all()
+        durations = _lib.PROFILER.durations_ms()
+        launches_per_step = _lib.PROFILER.launches / prof_steps
+        _lib.PROFILER.reset(enabled=False)
+
+        # (2) capture one step as a CUDA graph (host launch overhead removed)
+        graph = None
+        if use_graph:
+            try:
+                s2 = torch.cuda.Stream()
+                s2.wait_stream(stream)
+                with torch.cuda.stream(s2):
+                    step()
+                stream.wait_stream(s2)
+                sync_all()
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph):
+                    outs = step()
+                for _ in range(3):
+                    graph.replay()
+                sync_all()
+            except Exception as exc:  # noqa: BLE001 - fall back to eager, reported
+                print(f"[bench] graph capture failed ({exc!r}); timing eager launches", file=sys.stderr)
+                graph = None
+        run = graph.replay if graph is not None else step
+
+        # (3) timed region: K steps between barrier+synchronize brackets, max over ranks
+        sync_all()
+        h0 = time.time()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record(stream)
         for _ in range(steps):
-            step(q, k, v, do)
+            run()
         t1.record(stream)
         sync_all()
-    ms = max_over_ranks(t0.elapsed_time(t1) / steps)
-    durations = _lib.PROFILER.durations_ms()
-    launches = _lib.PROFILER.launches
-    _lib.PROFILER.reset(enabled=False)
+        h1 = time.time()
+        ms = max_over_ranks(t0.elapsed_time(t1) / steps)
+        clk = clocks.summary(h0, h1)
 
-    # --- end-to-end through the public API with host buffers ---
-    pin = lambda t: t.cpu().pin_memory()  # noqa: E731
-    hq, hk, hv, hdo = pin(q), pin(k), pin(v), pin(do)
-    outs_host = [torch.empty(q.shape, dtype=q.dtype, pin_memory=True) for _ in range(4)]
-    h2d = 4 * q.numel() * q.element_size()
-    d2h = 4 * q.numel() * q.element_size()
-    e2e_steps = max(2, min(steps, 5))
-    sync_all()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(e2e_steps):
-        dq_, dk_, dv_, ddo = (x.to(device, non_blocking=True) for x in (hq, hk, hv, hdo))
-        out, g = step(dq_, dk_, dv_, ddo)
-        for dst, src in zip(outs_host, (out, g.dq, g.dk, g.dv)):
-            dst.copy_(src, non_blocking=True)
-    e1.record(stream)
-    sync_all()
-    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e2e_steps)
+        # (4) end-to-end through the public API: H2D of the step's inputs from pinned
+        #     host memory, the layer fwd+bwd, D2H of its outputs and gradients
+        hq, hk, hv, hdo = (t.cpu().pin_memory() for t in (q, k, v, do))
+        outs_host = [torch.empty(q.shape, dtype=q.dtype, pin_memory=True) for _ in range(4)]
+        e2e_steps = max(2, min(steps, 5))
+        sync_all()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            for dst, src in zip((q, k, v, do), (hq, hk, hv, hdo)):
+                dst.copy_(src, non_blocking=True)
+            res = outs if graph is not None else None
+            if graph is not None:
+                graph.replay()
+            else:
+                res = step()
+            for dst, src in zip(outs_host, res):
+                dst.copy_(src, non_blocking=True)
+        e1.record(stream)
+        sync_all()
+        e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e2e_steps)
 
-    # --- dominant kernel (most device time per step) and its roofline ---
-    per_kernel = {k2: sum(v2) / steps for k2, v2 in durations.items()}
+    # dominant kernel (most device time per step) and its roofline
+    per_kernel = {k2: sum(v2) / prof_steps for k2, v2 in durations.items()}
     dom = max(per_kernel, key=per_kernel.get)
     dom_launch_ms = statistics.mean(durations[dom])
     unit_bytes = B * H * c * D * 2  # one bf16 (B,H,C,d) tensor
     algo_bytes = {"lasp2_causal_chunk": 4 * unit_bytes, "lasp2_apply_state": 2 * unit_bytes,
                   "lasp2_segment_states": 2 * unit_bytes}.get(dom, 0)
     return dict(n=n, c=c, masked=masked, ms=ms, e2e_ms=e2e_ms, per_kernel_ms=per_kernel, dominant=dom,
-                dom_launch_ms=dom_launch_ms, dom_algo_bytes=algo_bytes, launches_per_step=launches / steps,
-                h2d=h2d * world, d2h=d2h * world, clocks=clocks.summary(), e2e_steps=e2e_steps)
+                dom_launch_ms=dom_launch_ms, dom_algo_bytes=algo_bytes, launches_per_step=launches_per_step,
+                h2d=4 * q.numel() * q.element_size() * world, d2h=4 * q.numel() * q.element_size() * world,
+                clocks=clk, e2e_steps=e2e_steps, graph=graph is not None,
+                kernel_sum_ms=sum(per_kernel.values()))
 
 
 def summarize(r: dict, world: int, peaks: dict) -> dict:
@@ -283,7 +332,8 @@ def summarize(r: dict, world: int, peaks: dict) -> dict:
                   "algorithmic_bytes_per_launch": r["dom_algo_bytes"], "avg_launch_ms": r["dom_launch_ms"]},
         e2e={"value": r["n"] / (r["e2e_ms"] / 1e3), "unit": UNIT, "h2d_bytes_per_step": r["h2d"],
              "d2h_bytes_per_step": r["d2h"], "ms_per_step": r["e2e_ms"], "steps": r["e2e_steps"]},
-        gpu_launches_per_step=r["launches_per_step"], clocks=r["clocks"])
+        gpu_launches_per_step=r["launches_per_step"], clocks=r["clocks"], graph=r["graph"],
+        kernel_sum_ms=r["kernel_sum_ms"])
 
 
 def run_gpu_arm(args) -> None:
@@ -306,10 +356,10 @@ def run_gpu_arm(args) -> None:
     else:
         ctx = comm.LocalRankContext()
     peaks = load_peaks()
-    main = measure_workload(args.workload, ctx, rank, world, args.steps, args.warmup, device)
+    main = measure_workload(args.workload, ctx, rank, world, args.steps, args.warmup, device, not args.eager)
     sec_name = "cfg3" if args.workload == "cfg2" else "cfg2"
     secondary = None if args.no_secondary else measure_workload(sec_name, ctx, rank, world, args.steps, args.warmup,
-                                                                device)
+                                                                device, not args.eager)
     if rank == 0:
         s = summarize(main, world, peaks)
         line = {"metric": METRIC, "value": s["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -323,7 +373,8 @@ def run_gpu_arm(args) -> None:
                 "tensor_frac_of_peak": s["tensor_frac_of_peak"], "tensor_tflops_per_gpu": s["tensor_tflops_per_gpu"],
                 "hbm_frac_of_peak_min_bytes": s["hbm_frac_of_peak"], "roofline": s["roofline"],
                 "e2e": s["e2e"], "gpu_launches": int(round(s["gpu_launches_per_step"] * args.steps)),
-                "clocks": s["clocks"], "per_kernel_ms_per_step": s["per_kernel_ms_per_step"]}
+                "clocks": s["clocks"], "per_kernel_ms_per_step": s["per_kernel_ms_per_step"],
+                "kernel_sum_ms_per_step": s["kernel_sum_ms"], "cuda_graph": s["graph"]}
         if secondary is not None:
             ss = summarize(secondary, world, peaks)
             line["secondary"] = {"workload": WORKLOADS[sec_name]["name"], "value": ss["value"], "unit": UNIT,
@@ -331,7 +382,9 @@ def run_gpu_arm(args) -> None:
                                  "tensor_frac_of_peak": ss["tensor_frac_of_peak"],
                                  "tensor_tflops_per_gpu": ss["tensor_tflops_per_gpu"],
                                  "hbm_frac_of_peak_min_bytes": ss["hbm_frac_of_peak"], "roofline": ss["roofline"],
-                                 "e2e": ss["e2e"], "per_kernel_ms_per_step": ss["per_kernel_ms_per_step"]}
+                                 "e2e": ss["e2e"], "per_kernel_ms_per_step": ss["per_kernel_ms_per_step"],
+                                 "kernel_sum_ms_per_step": ss["kernel_sum_ms"], "clocks": ss["clocks"],
+                                 "gpu_launches_per_step": ss["gpu_launches_per_step"]}
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_reference(args.workload, budget_s=args.cpu_budget)
         print(json.dumps(line))
@@ -352,6 +405,7 @@ def main() -> None:
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--eager", action="store_true", help="time eager launches instead of CUDA-graph replay")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3 (timing rules)")

@@ -458,7 +458,8 @@ class DistPending:
                     self._work.wait()
                     ctx._device_mark("all_gather_complete", ctx.comm_stream)
                 torch.cuda.current_stream().wait_stream(ctx.comm_stream)
-                self._out.record_stream(torch.cuda.current_stream())
+                if not torch.cuda.is_current_stream_capturing():
+                    self._out.record_stream(torch.cuda.current_stream())
             else:
                 self._work.wait()
             ctx.trace.append(TraceEvent(len(ctx.trace), ctx.rank, time.perf_counter(), "all_gather_complete",
@@ -531,8 +532,9 @@ class DistRankContext(_ContextBase):
             with torch.cuda.stream(self.comm_stream):
                 self._device_mark("all_gather_issue", self.comm_stream)
                 work = self.dist.all_gather_into_tensor(flat, payload, group=self._group, async_op=True)
-            payload.record_stream(self.comm_stream)
-            flat.record_stream(self.comm_stream)
+            if not torch.cuda.is_current_stream_capturing():
+                payload.record_stream(self.comm_stream)
+                flat.record_stream(self.comm_stream)
         else:
             work = self.dist.all_gather_into_tensor(flat, payload, group=self._group, async_op=True)
         return DistPending(self, work, out, tag)

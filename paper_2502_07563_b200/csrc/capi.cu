@@ -159,7 +159,10 @@ int lasp2h_softmax_forward(int dtype, const void* q, const void* k_full, const v
   CHECK(row_offset >= 0 && (!causal || row_offset < kv_tokens), "softmax_forward: bad row_offset");
   CHECK(kv_chunk >= 1 && kv_tokens % kv_chunk == 0, "softmax_forward: kv_chunk must divide kv_tokens");
   cudaError_t e;
-  if (dtype == LASP2_F32)
+  if (dtype == LASP2_BF16 && lasp::tc_softmax_supported(dim, kv_chunk))
+    e = lasp::tc_softmax_forward(q, k_full, v_full, out, (float*)lse, slots, q_tokens, kv_tokens, dim, causal,
+                                 row_offset, kv_chunk, kv_rank_stride, S(stream));
+  else if (dtype == LASP2_F32)
     e = lasp::simt_softmax_forward<float, float>(q, k_full, v_full, out, (float*)lse, slots, q_tokens, kv_tokens, dim,
                                                  causal, row_offset, kv_chunk, kv_rank_stride, S(stream));
   else if (dtype == LASP2_F64)
@@ -174,9 +177,13 @@ int lasp2h_softmax_forward(int dtype, const void* q, const void* k_full, const v
 
 int64_t lasp2h_softmax_scratch_bytes(int dtype, int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim) {
   (void)kv_tokens;
-  (void)dim;
   const int64_t eb = dtype == LASP2_F64 ? 8 : 4;
-  return 3 * slots * q_tokens * eb + 256;
+  int64_t n = 3 * slots * q_tokens * eb + 256;
+  if (dtype == LASP2_BF16) {
+    const int64_t t = lasp::tc_softmax_bwd_scratch(slots, q_tokens, dim) + 256;
+    if (t > n) n = t;
+  }
+  return n;
 }
 
 int lasp2h_softmax_backward(int dtype, const void* q, const void* k_full, const void* v_full, const void* out,
@@ -184,7 +191,6 @@ int lasp2h_softmax_backward(int dtype, const void* q, const void* k_full, const 
                             int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim, int causal,
                             int64_t row_offset, int64_t kv_chunk, int64_t kv_rank_stride, int64_t grad_rank_stride,
                             void* stream) {
-  (void)lse;
   CHECK(valid_dtype(dtype), "softmax_backward: unknown dtype");
   CHECK(q && k_full && v_full && out && d_out && dq && dk_full && dv_full && scratch,
         "softmax_backward: null pointer");
@@ -192,7 +198,12 @@ int lasp2h_softmax_backward(int dtype, const void* q, const void* k_full, const 
   CHECK(row_offset >= 0 && (!causal || row_offset < kv_tokens), "softmax_backward: bad row_offset");
   CHECK(kv_chunk >= 1 && kv_tokens % kv_chunk == 0, "softmax_backward: kv_chunk must divide kv_tokens");
   cudaError_t e;
-  if (dtype == LASP2_F32)
+  if (dtype == LASP2_BF16 && lasp::tc_softmax_supported(dim, kv_chunk)) {
+    CHECK(lse, "softmax_backward: the bf16 path needs the forward's lse");
+    e = lasp::tc_softmax_backward(q, k_full, v_full, out, (const float*)lse, d_out, dq, (float*)dk_full,
+                                  (float*)dv_full, scratch, slots, q_tokens, kv_tokens, dim, causal, row_offset,
+                                  kv_chunk, kv_rank_stride, grad_rank_stride, S(stream));
+  } else if (dtype == LASP2_F32)
     e = lasp::simt_softmax_backward<float, float, float>(q, k_full, v_full, out, d_out, dq, dk_full, dv_full, scratch,
                                                          slots, q_tokens, kv_tokens, dim, causal, row_offset,
                                                          kv_chunk, kv_rank_stride, grad_rank_stride, S(stream));

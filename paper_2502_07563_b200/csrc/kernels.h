@@ -45,6 +45,17 @@ cudaError_t tc_causal_chunk(const void* q, const void* k, const void* v, const f
                             int transpose_state, cudaStream_t s);
 cudaError_t tc_apply_state(const void* x, const float* m, void* out, int64_t slots, int64_t tokens, int dim,
                            int transpose, int accumulate, int sm_count, cudaStream_t s);
+bool tc_softmax_supported(int dim, int64_t kv_chunk);
+cudaError_t tc_softmax_forward(const void* q, const void* kf, const void* vf, void* out, float* lse, int64_t slots,
+                               int64_t qtok, int64_t kvtok, int dim, int causal, int64_t row_offset, int64_t kv_chunk,
+                               int64_t kv_rank_stride, cudaStream_t s);
+int64_t tc_softmax_bwd_scratch(int64_t slots, int64_t qtok, int dim);
+cudaError_t tc_softmax_backward(const void* q, const void* kf, const void* vf, const void* o, const float* lse,
+                                const void* d_out, void* dq, float* dk_full, float* dv_full, void* scratch,
+                                int64_t slots, int64_t qtok, int64_t kvtok, int dim, int causal, int64_t row_offset,
+                                int64_t kv_chunk, int64_t kv_rank_stride, int64_t grad_rank_stride, cudaStream_t s);
+cudaError_t softmax_delta_bf16(const void* o, const void* d_out, float* delta, int64_t rows, int dim,
+                               cudaStream_t s);
 cudaError_t tc_probe_gemm(const void* a, const void* b, float* d, int a_mn, int b_mn, cudaStream_t s);
 
 }  // namespace lasp

@@ -534,6 +534,13 @@ cudaError_t simt_softmax_backward(const void* q, const void* kf, const void* vf,
   return cudaGetLastError();
 }
 
+cudaError_t softmax_delta_bf16(const void* o, const void* d_out, float* delta, int64_t rows, int dim,
+                               cudaStream_t s) {
+  simt_softmax_delta_kernel<__nv_bfloat16, float><<<(unsigned)((rows + 7) / 8), dim3(32, 8), 0, s>>>(
+      (const __nv_bfloat16*)o, (const __nv_bfloat16*)d_out, delta, rows, dim);
+  return cudaGetLastError();
+}
+
 // explicit instantiations: (io, accumulate) = (f32,f32), (f64,f64), (bf16,f32)
 #define LASP_INST(T, A)                                                                                         \
   template cudaError_t simt_segment_states<T, A>(const void*, const void*, void*, int64_t, int64_t, int, int,   \

@@ -16,74 +16,11 @@
 //   tc_apply_state    : O (+)= X M or X M^T            (lasp2.py:150-165)
 #include <cuda.h>
 
-#include "common.cuh"
 #include "kernels.h"
+#include "tc_common.cuh"
 
 namespace lasp {
 namespace tc {
-
-using namespace ptx;
-
-constexpr int kTile = 128;                    // tokens per block, features per tile
-constexpr uint32_t kTileBytes = 128 * 128 * 2;  // 32 KB
-constexpr uint32_t kBoxBytes = 128 * 64 * 2;    // 16 KB (one SW128 box)
-
-__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-// K-major operand descriptor for k-step kk (16 elements along the feature axis).
-__device__ __forceinline__ uint64_t desc_kmajor(uint32_t tile, int kk) {
-  return umma_desc_sw128(tile + (kk >> 2) * kBoxBytes + (kk & 3) * 32, 16, 1024);
-}
-// MN-major operand descriptor for k-step kk (16 tokens = two 8-row atoms).
-__device__ __forceinline__ uint64_t desc_mnmajor(uint32_t tile, int kk) {
-  return umma_desc_sw128(tile + kk * 2048, kBoxBytes, 1024);
-}
-
-// Byte offset of element (row, col) in a 128x128 bf16 SW128 tile image.
-__device__ __forceinline__ uint32_t sw128_offset(uint32_t row, uint32_t col) {
-  const uint32_t chunk = col >> 6, cc = col & 63;
-  const uint32_t unit = (cc >> 3) ^ (row & 7);
-  return chunk * kBoxBytes + row * 128 + unit * 16 + (cc & 7) * 2;
-}
-
-// Store 32 fp32 values (columns c0..c0+31 of `row`) as bf16 into a SW128 image.
-__device__ __forceinline__ void st_row32_bf16(uint8_t* img, uint32_t row, uint32_t c0, const float* v) {
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    uint32_t w0 = pack_bf16x2(v[8 * u + 0], v[8 * u + 1]);
-    uint32_t w1 = pack_bf16x2(v[8 * u + 2], v[8 * u + 3]);
-    uint32_t w2 = pack_bf16x2(v[8 * u + 4], v[8 * u + 5]);
-    uint32_t w3 = pack_bf16x2(v[8 * u + 6], v[8 * u + 7]);
-    const uint32_t off = sw128_offset(row, c0 + 8 * u);
-    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(smem_u32(img + off)), "r"(w0), "r"(w1), "r"(w2),
-                 "r"(w3)
-                 : "memory");
-  }
-}
-
-// Load a 128-column fp32 row from TMEM (this thread's lane) in four x32 pieces,
-// convert to bf16 (optionally causal-masked) and write into a SW128 image.
-// mask: 0 none, 1 keep col<=row, 2 keep col>=row.
-__device__ __forceinline__ void tmem_row_to_image(uint32_t taddr_lane, uint8_t* img, uint32_t row, int mask) {
-#pragma unroll 1
-  for (int c0 = 0; c0 < 128; c0 += 32) {
-    uint32_t r[32];
-    tmem_ld_32x32b_x32(taddr_lane + c0, r);
-    tmem_ld_wait();
-    float v[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      float x = __uint_as_float(r[i]);
-      const int col = c0 + i;
-      if (mask == 1 && col > (int)row) x = 0.f;
-      if (mask == 2 && col < (int)row) x = 0.f;
-      v[i] = x;
-    }
-    st_row32_bf16(img, row, c0, v);
-  }
-}
 
 // ============================================================================
 // Segment states: out[slot][seg] = X_seg^T Y_seg   (fp32 [dim][dim])
@@ -598,47 +535,15 @@ __global__ void __launch_bounds__(128, 1)
 // ============================================================================
 // Host side: tensor maps + launchers
 // ============================================================================
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static EncodeTiledFn get_encode() {
-  static EncodeTiledFn fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  }
-  return fn;
-}
-
-// [slots][tokens][dim] bf16, box = 64 features x 128 tokens, SWIZZLE_128B.
-static cudaError_t make_tmap(CUtensorMap* m, const void* ptr, int64_t slots, int64_t tokens, int dim) {
-  EncodeTiledFn enc = get_encode();
-  if (!enc) return cudaErrorNotSupported;
-  cuuint64_t gdim[3] = {(cuuint64_t)dim, (cuuint64_t)tokens, (cuuint64_t)slots};
-  cuuint64_t gstride[2] = {(cuuint64_t)dim * 2, (cuuint64_t)tokens * dim * 2};
-  cuuint32_t box[3] = {64, 128, 1};
-  cuuint32_t estride[3] = {1, 1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), gdim, gstride, box, estride,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
-}
-
 bool tc_supported(int dim, int64_t tokens) { return dim >= 8 && dim <= 128 && dim % 8 == 0 && tokens >= 1; }
 
 cudaError_t tc_segment_states(const void* x, const void* y, float* out, int64_t slots, int64_t tokens, int dim,
                               int nseg, cudaStream_t s) {
   CUtensorMap mx, my;
   cudaError_t e;
-  if ((e = make_tmap(&mx, x, slots, tokens, dim)) != cudaSuccess) return e;
-  if ((e = make_tmap(&my, y, slots, tokens, dim)) != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(tc::tc_segment_states_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)tc::kSegSmem);
-  if (e != cudaSuccess) return e;
+  if ((e = make_tmap_3d(&mx, x, slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = make_tmap_3d(&my, y, slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = set_smem_once((const void*)tc::tc_segment_states_kernel, tc::kSegSmem)) != cudaSuccess) return e;
   dim3 grid(nseg, (unsigned)slots);
   tc::tc_segment_states_kernel<<<grid, 192, tc::kSegSmem, s>>>(mx, my, out, tokens, dim, nseg);
   return cudaGetLastError();
@@ -649,13 +554,11 @@ cudaError_t tc_causal_chunk(const void* q, const void* k, const void* v, const f
                             int transpose_state, cudaStream_t s) {
   CUtensorMap mq, mk, mv, mo;
   cudaError_t e;
-  if ((e = make_tmap(&mq, q, slots, tokens, dim)) != cudaSuccess) return e;
-  if ((e = make_tmap(&mk, k, slots, tokens, dim)) != cudaSuccess) return e;
-  if ((e = make_tmap(&mv, v, slots, tokens, dim)) != cudaSuccess) return e;
-  if ((e = make_tmap(&mo, out, slots, tokens, dim)) != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(tc::tc_causal_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)tc::kCausalSmem);
-  if (e != cudaSuccess) return e;
+  if ((e = make_tmap_3d(&mq, q, slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = make_tmap_3d(&mk, k, slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = make_tmap_3d(&mv, v, slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = make_tmap_3d(&mo, out, slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = set_smem_once((const void*)tc::tc_causal_chunk_kernel, tc::kCausalSmem)) != cudaSuccess) return e;
   tc::CausalArgs a{seg_states, base, tokens, dim, nseg, reverse, transpose_state};
   dim3 grid(nseg, (unsigned)slots);
   tc::tc_causal_chunk_kernel<<<grid, 192, tc::kCausalSmem, s>>>(mq, mk, mv, mo, a);
@@ -666,14 +569,12 @@ cudaError_t tc_apply_state(const void* x, const float* m, void* out, int64_t slo
                            int transpose, int accumulate, int sm_count, cudaStream_t s) {
   CUtensorMap mx, mo;
   cudaError_t e;
-  if ((e = make_tmap(&mx, x, slots, tokens, dim)) != cudaSuccess) return e;
-  if ((e = make_tmap(&mo, out, slots, tokens, dim)) != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(tc::tc_apply_state_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)tc::kApplySmem);
-  if (e != cudaSuccess) return e;
+  if ((e = make_tmap_3d(&mx, x, slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = make_tmap_3d(&mo, out, slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = set_smem_once((const void*)tc::tc_apply_state_kernel, tc::kApplySmem)) != cudaSuccess) return e;
   const int64_t nblk = (tokens + tc::kTile - 1) / tc::kTile;
-  // about one wave: ctas_per_slot * slots ~= sm_count
-  int64_t ctas = (sm_count + slots - 1) / slots;
+  // exactly one wave (one CTA per SM): ctas_per_slot * slots <= sm_count
+  int64_t ctas = sm_count / slots;
   if (ctas < 1) ctas = 1;
   if (ctas > nblk) ctas = nblk;
   const int bpc = (int)((nblk + ctas - 1) / ctas);
@@ -687,8 +588,8 @@ cudaError_t tc_apply_state(const void* x, const float* m, void* out, int64_t slo
 cudaError_t tc_probe_gemm(const void* a, const void* b, float* d, int a_mn, int b_mn, cudaStream_t s) {
   CUtensorMap ma, mb;
   cudaError_t e;
-  if ((e = make_tmap(&ma, a, 1, 128, 128)) != cudaSuccess) return e;
-  if ((e = make_tmap(&mb, b, 1, 128, 128)) != cudaSuccess) return e;
+  if ((e = make_tmap_3d(&ma, a, 1, 128, 128)) != cudaSuccess) return e;
+  if ((e = make_tmap_3d(&mb, b, 1, 128, 128)) != cudaSuccess) return e;
   const uint32_t smem = 2 * tc::kTileBytes + 1024 + 64;
   e = cudaFuncSetAttribute(tc::tc_probe_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -1,0 +1,545 @@
+// tcgen05 flash-style causal softmax attention for LASP-2H (bf16 in, fp32
+// accumulate), sm_100a only.
+//
+// Forward, one CTA per (128-query tile, slot): queries are the rank's chunk at
+// global rows row_offset + [q0, q0+128); keys/values are the full gathered
+// sequence, read straight from the rank-major all_gather layout through a 4-D
+// TMA map {d, row-in-chunk, slot, rank}. Per 128-key block j:
+//   S_j = Q K_j^T           (tcgen05, TMEM, double-buffered)
+//   P_j = exp2(S_j*scale*log2e - m_j), online max/sum per row (softmax warps,
+//         one row per thread), bf16 -> SW128 smem (double-buffered)
+//   O_j = P_j V_j           (tcgen05, fresh TMEM accumulator, double-buffered)
+//   O  <- O * exp2(m_{j-1} - m_j) + O_j   (registers)
+// Only key blocks at or below the diagonal are visited (causal), the diagonal
+// block is masked by global position exactly as softmax_probs
+// (oracle.py:111-133). Output O / l in bf16, LSE (natural log) in fp32.
+#include "kernels.h"
+#include "tc_common.cuh"
+
+namespace lasp {
+namespace tc {
+
+constexpr int kKvRing = 4;  // K/V tile slots
+constexpr uint32_t kSmFwdSmem = (1 + kKvRing + 2) * kTileBytes + 1024 + 256;
+
+struct SmFwdArgs {
+  float* lse;
+  int64_t qtok;
+  int64_t kvtok;
+  int64_t chunk;
+  int64_t row_offset;
+  int dim;
+  int causal;
+  float scale_log2;  // log2(e) / sqrt(d)
+};
+
+__device__ __forceinline__ void kv_coords(int64_t key0, int64_t chunk, int* row, int* rank) {
+  *rank = (int)(key0 / chunk);
+  *row = (int)(key0 % chunk);
+}
+
+__global__ void __launch_bounds__(192, 1)
+    tc_softmax_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                          const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
+                          SmFwdArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* qimg = smem;
+  uint8_t* ring = qimg + kTileBytes;
+  uint8_t* pimg = ring + kKvRing * kTileBytes;  // [2] P tiles; pimg[0] is the O staging at the end
+  uint64_t* bars = reinterpret_cast<uint64_t*>(pimg + 2 * kTileBytes);
+  uint64_t* full = bars;                 // [kKvRing]
+  uint64_t* empty = bars + kKvRing;      // [kKvRing]
+  uint64_t* q_full = bars + 2 * kKvRing;
+  uint64_t* s_full = q_full + 1;   // [2]
+  uint64_t* p_ready = q_full + 3;  // [2]
+  uint64_t* o_full = q_full + 5;   // [2]
+  uint64_t* o_empty = q_full + 7;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + 9);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qt = blockIdx.x, slot = blockIdx.y;
+  const int64_t q0 = (int64_t)qt * kTile;
+  const int64_t kv_end = a.causal ? lmin(a.kvtok, a.row_offset + q0 + kTile) : a.kvtok;
+  const int nkb = (int)((kv_end + kTile - 1) / kTile);
+  const int nbox = a.dim > 64 ? 2 : 1;
+  const int kfeat = (a.dim + 15) / 16;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kKvRing; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 9; ++i) mbar_init(&q_full[i], 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;  // S[2] at cols 0/128, O[2] at 256/384
+
+  if (warp == 0) {
+    if (elect_one()) {
+      prefetch_tmap(&tm_q);
+      prefetch_tmap(&tm_k);
+      prefetch_tmap(&tm_v);
+      mbar_arrive_expect_tx(q_full, nbox * kBoxBytes);
+      for (int bx = 0; bx < nbox; ++bx) tma_load_3d(qimg + bx * kBoxBytes, &tm_q, q_full, 64 * bx, (int)q0, slot);
+      for (int j = 0; j < nkb; ++j) {
+        int row, rank;
+        kv_coords((int64_t)j * kTile, a.chunk, &row, &rank);
+        for (int w = 0; w < 2; ++w) {
+          const int t = 2 * j + w, s = t % kKvRing, u = t / kKvRing;
+          if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+          uint8_t* dst = ring + s * kTileBytes;
+          mbar_arrive_expect_tx(&full[s], nbox * kBoxBytes);
+          const CUtensorMap* m = w == 0 ? &tm_k : &tm_v;
+          for (int bx = 0; bx < nbox; ++bx) tma_load_4d(dst + bx * kBoxBytes, m, &full[s], 64 * bx, row, slot, rank);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t id_qk = idesc_bf16_f32(128, 128, 0, 0);
+    constexpr uint32_t id_pv = idesc_bf16_f32(128, 128, 0, 1);
+    const uint32_t qa = smem_u32(qimg);
+    mbar_wait(q_full, 0);
+    for (int j = 0; j <= nkb; ++j) {
+      if (j < nkb) {  // S_j = Q K_j^T into S[j&1]
+        const int t = 2 * j, s = t % kKvRing;
+        mbar_wait(&full[s], (t / kKvRing) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t ka = smem_u32(ring + s * kTileBytes);
+          for (int kk = 0; kk < kfeat; ++kk)
+            mma_bf16_ss(tmem + (j & 1) * 128, desc_kmajor(qa, kk), desc_kmajor(ka, kk), id_qk, kk > 0);
+          mma_commit(&s_full[j & 1]);
+          mma_commit(&empty[s]);
+        }
+        __syncwarp();
+      }
+      if (j >= 1) {  // O_{j-1} = P_{j-1} V_{j-1} into O[(j-1)&1]
+        const int jb = j - 1, b = jb & 1;
+        const int t = 2 * jb + 1, s = t % kKvRing;
+        mbar_wait(&p_ready[b], (jb >> 1) & 1);
+        if (jb >= 2) mbar_wait(&o_empty[b], ((jb >> 1) - 1) & 1);
+        mbar_wait(&full[s], (t / kKvRing) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t pa = smem_u32(pimg + b * kTileBytes), va = smem_u32(ring + s * kTileBytes);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            mma_bf16_ss(tmem + 256 + b * 128, desc_kmajor(pa, kk), desc_mnmajor(va, kk), id_pv, kk > 0);
+          mma_commit(&o_full[b]);
+          mma_commit(&empty[s]);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------- softmax / epilogue warps ----------------
+    const int qd = warp & 3;
+    const uint32_t row = qd * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
+    const int et = threadIdx.x - 64;
+    const int64_t gq = a.row_offset + q0 + row;  // global query position
+    float o_acc[128];
+#pragma unroll
+    for (int i = 0; i < 128; ++i) o_acc[i] = 0.f;
+    float m_run = -INFINITY, l_run = 0.f, corr_pending = 1.f;
+    for (int j = 0; j <= nkb; ++j) {
+      float corr_this = 1.f;
+      if (j < nkb) {
+        const int b = j & 1;
+        mbar_wait(&s_full[b], (j >> 1) & 1);
+        tc_fence_after();
+        const int64_t k0 = (int64_t)j * kTile;
+        const uint32_t ts = tmem + b * 128 + lane_off;
+        // pass 1: masked row max of this block
+        float bmax = -INFINITY;
+#pragma unroll 1
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(ts + c0, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int64_t kg = k0 + c0 + i;
+            const bool ok = kg < a.kvtok && (!a.causal || kg <= gq);
+            if (ok) bmax = fmaxf(bmax, __uint_as_float(r[i]));
+          }
+        }
+        const float m_new = fmaxf(m_run, bmax * a.scale_log2);
+        corr_this = (m_run == -INFINITY) ? 0.f : exp2f(m_run - m_new);
+        // pass 2: p = exp2(s*scale - m_new), row sum, bf16 -> P image
+        uint8_t* pb = pimg + b * kTileBytes;
+        float psum = 0.f;
+#pragma unroll 1
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(ts + c0, r);
+          tmem_ld_wait();
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int64_t kg = k0 + c0 + i;
+            const bool ok = kg < a.kvtok && (!a.causal || kg <= gq);
+            const float p = ok ? exp2f(fmaf(__uint_as_float(r[i]), a.scale_log2, -m_new)) : 0.f;
+            psum += p;
+            v[i] = p;
+          }
+          st_row32_bf16(pb, row, c0, v);
+        }
+        l_run = l_run * corr_this + psum;
+        m_run = m_new;
+        fence_proxy_async_smem();
+        tc_fence_before();
+        named_bar_sync(1, 128);
+        if (et == 0) mbar_arrive(&p_ready[b]);
+      }
+      if (j >= 1) {  // fold O_{j-1} into the register accumulator
+        const int jb = j - 1, b = jb & 1;
+        mbar_wait(&o_full[b], (jb >> 1) & 1);
+        tc_fence_after();
+        const uint32_t to = tmem + 256 + b * 128 + lane_off;
+#pragma unroll
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(to + c0, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o_acc[c0 + i] = fmaf(o_acc[c0 + i], corr_pending, __uint_as_float(r[i]));
+        }
+        tc_fence_before();
+        named_bar_sync(1, 128);
+        if (et == 0) mbar_arrive(&o_empty[b]);
+      }
+      corr_pending = corr_this;
+    }
+    // epilogue: O / l -> bf16 -> staging (P[0] is free: every PV has completed) -> TMA store
+    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+#pragma unroll
+    for (int c0 = 0; c0 < 128; c0 += 32) {
+      float v[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = o_acc[c0 + i] * inv;
+      st_row32_bf16(pimg, row, c0, v);
+    }
+    if (q0 + row < a.qtok)
+      a.lse[(int64_t)slot * a.qtok + q0 + row] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
+    fence_proxy_async_smem();
+    named_bar_sync(1, 128);
+    if (et == 0) {
+      for (int bx = 0; bx < nbox; ++bx) tma_store_3d(&tm_o, pimg + bx * kBoxBytes, 64 * bx, (int)q0, slot);
+      tma_store_commit();
+      tma_store_wait_all<0>();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+// ============================================================================
+// Backward, one CTA per (128-key block of the full sequence, slot). For every
+// query block i of this rank's chunk that sees the keys (causal by global
+// position):
+//   S = Q_i K^T, dP = dO_i V^T                         (tcgen05 -> TMEM)
+//   P = exp2(S*scale*log2e - lse_i*log2e), dS = P o (dP - D_i)   (one query row per thread)
+//   dV += P^T dO_i, dK += dS^T Q_i                      (TMEM accumulators; P / dS
+//                                                        images read MN-major)
+//   dQ_i += dS K * scale                               (TMEM -> red.global.add.v4.f32)
+// D_i = rowsum(dO_i o O_i) (oracle.py:155). dK*scale and dV are written in
+// fp32 to the rank-major contribution buffer for the reduce-scatter.
+// ============================================================================
+constexpr int kQRing = 3;
+constexpr uint32_t kSmBwdSmem = (2 + kQRing + 2) * kTileBytes + 1024 + 256;
+
+struct SmBwdArgs {
+  const float* lse;    // [slots][qtok] natural log
+  const float* delta;  // [slots][qtok]
+  float* dq_acc;       // [slots][qtok][dim] fp32, zeroed
+  float* dk_full;      // rank-major contributions
+  float* dv_full;
+  int64_t qtok;
+  int64_t kvtok;
+  int64_t chunk;
+  int64_t grad_rank_stride;
+  int64_t row_offset;
+  int dim;
+  int causal;
+  float scale;       // 1/sqrt(d)
+  float scale_log2;  // log2(e)/sqrt(d)
+};
+
+__global__ void __launch_bounds__(192, 1)
+    tc_softmax_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
+                          const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                          SmBwdArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* kimg = smem;
+  uint8_t* vimg = kimg + kTileBytes;
+  uint8_t* ring = vimg + kTileBytes;
+  uint8_t* pimg = ring + kQRing * kTileBytes;
+  uint8_t* dsimg = pimg + kTileBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(dsimg + kTileBytes);
+  uint64_t* full = bars;              // [kQRing]
+  uint64_t* empty = bars + kQRing;    // [kQRing]
+  uint64_t* kv_full = bars + 2 * kQRing;
+  uint64_t* sdp_full = kv_full + 1;
+  uint64_t* ds_ready = kv_full + 2;
+  uint64_t* dq_full = kv_full + 3;
+  uint64_t* dq_empty = kv_full + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_full + 5);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kb = blockIdx.x, slot = blockIdx.y;
+  const int64_t k0 = (int64_t)kb * kTile;
+  const int nqb_all = (int)((a.qtok + kTile - 1) / kTile);
+  int qb0 = 0;
+  if (a.causal) {
+    const int64_t first = k0 - a.row_offset;  // first local query row that can see key k0
+    qb0 = first <= 0 ? 0 : (int)(first / kTile);
+    if (first >= a.qtok) qb0 = nqb_all;
+  }
+  const int nq = nqb_all - qb0;  // visible query blocks
+  const int nbox = a.dim > 64 ? 2 : 1;
+  const int kfeat = (a.dim + 15) / 16;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kQRing; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 5; ++i) mbar_init(&kv_full[i], 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;  // S/dQ 0, dP 128, dV 256, dK 384
+  const uint32_t t_s = tmem, t_dp = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 384;
+
+  if (warp == 0) {
+    if (elect_one() && nq > 0) {
+      prefetch_tmap(&tm_q);
+      prefetch_tmap(&tm_do);
+      int row, rank;
+      kv_coords(k0, a.chunk, &row, &rank);
+      mbar_arrive_expect_tx(kv_full, 2 * nbox * kBoxBytes);
+      for (int bx = 0; bx < nbox; ++bx) {
+        tma_load_4d(kimg + bx * kBoxBytes, &tm_k, kv_full, 64 * bx, row, slot, rank);
+        tma_load_4d(vimg + bx * kBoxBytes, &tm_v, kv_full, 64 * bx, row, slot, rank);
+      }
+      for (int i = 0; i < nq; ++i) {
+        const int qrow = (qb0 + i) * kTile;
+        for (int w = 0; w < 2; ++w) {
+          const int t = 2 * i + w, s = t % kQRing, u = t / kQRing;
+          if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+          uint8_t* dst = ring + s * kTileBytes;
+          mbar_arrive_expect_tx(&full[s], nbox * kBoxBytes);
+          const CUtensorMap* m = w == 0 ? &tm_q : &tm_do;
+          for (int bx = 0; bx < nbox; ++bx) tma_load_3d(dst + bx * kBoxBytes, m, &full[s], 64 * bx, qrow, slot);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (nq > 0) {
+      constexpr uint32_t id_kk = idesc_bf16_f32(128, 128, 0, 0);  // S, dP
+      constexpr uint32_t id_mm = idesc_bf16_f32(128, 128, 1, 1);  // dV, dK (A = P^T / dS^T, B = dO / Q)
+      constexpr uint32_t id_km = idesc_bf16_f32(128, 128, 0, 1);  // dQ (A = dS, B = K)
+      const uint32_t ka = smem_u32(kimg), va = smem_u32(vimg), pa = smem_u32(pimg), dsa = smem_u32(dsimg);
+      mbar_wait(kv_full, 0);
+      for (int i = 0; i < nq; ++i) {
+        const int tq = 2 * i, tdo = tq + 1;
+        const int sq = tq % kQRing, sdo = tdo % kQRing;
+        const uint32_t qa = smem_u32(ring + sq * kTileBytes), doa = smem_u32(ring + sdo * kTileBytes);
+        mbar_wait(&full[sq], (tq / kQRing) & 1);
+        mbar_wait(&full[sdo], (tdo / kQRing) & 1);
+        if (i > 0) mbar_wait(dq_empty, (i - 1) & 1);  // S/dQ columns drained
+        tc_fence_after();
+        if (elect_one()) {
+          for (int kk = 0; kk < kfeat; ++kk) mma_bf16_ss(t_s, desc_kmajor(qa, kk), desc_kmajor(ka, kk), id_kk, kk > 0);
+          for (int kk = 0; kk < kfeat; ++kk)
+            mma_bf16_ss(t_dp, desc_kmajor(doa, kk), desc_kmajor(va, kk), id_kk, kk > 0);
+          mma_commit(sdp_full);
+        }
+        __syncwarp();
+        mbar_wait(ds_ready, i & 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            mma_bf16_ss(t_dv, desc_mnmajor(pa, kk), desc_mnmajor(doa, kk), id_mm, (i > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            mma_bf16_ss(t_dk, desc_mnmajor(dsa, kk), desc_mnmajor(qa, kk), id_mm, (i > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) mma_bf16_ss(t_s, desc_kmajor(dsa, kk), desc_mnmajor(ka, kk), id_km, kk > 0);
+          mma_commit(&empty[sq]);
+          mma_commit(&empty[sdo]);
+          mma_commit(dq_full);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    const int qd = warp & 3;
+    const uint32_t row = qd * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
+    const int et = threadIdx.x - 64;
+    for (int i = 0; i < nq; ++i) {
+      const int64_t qloc = (int64_t)(qb0 + i) * kTile + row;  // local query row of this thread
+      const bool qok = qloc < a.qtok;
+      const int64_t gq = a.row_offset + qloc;
+      const float lse2 = qok ? a.lse[(int64_t)slot * a.qtok + qloc] * 1.4426950408889634f : 0.f;
+      const float dl = qok ? a.delta[(int64_t)slot * a.qtok + qloc] : 0.f;
+      mbar_wait(sdp_full, i & 1);
+      tc_fence_after();
+      // P/dS images are free: the previous block's dq_full (all its MMAs) was waited below
+#pragma unroll 1
+      for (int c0 = 0; c0 < 128; c0 += 32) {
+        uint32_t rs[32], rp[32];
+        tmem_ld_32x32b_x32(t_s + lane_off + c0, rs);
+        tmem_ld_32x32b_x32(t_dp + lane_off + c0, rp);
+        tmem_ld_wait();
+        float pv[32], dsv[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const int64_t kg = k0 + c0 + e;
+          const bool ok = qok && kg < a.kvtok && (!a.causal || kg <= gq);
+          const float p = ok ? exp2f(fmaf(__uint_as_float(rs[e]), a.scale_log2, -lse2)) : 0.f;
+          pv[e] = p;
+          dsv[e] = p * (__uint_as_float(rp[e]) - dl);
+        }
+        st_row32_bf16(pimg, row, c0, pv);
+        st_row32_bf16(dsimg, row, c0, dsv);
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      named_bar_sync(1, 128);
+      if (et == 0) mbar_arrive(ds_ready);
+      // dQ partial -> fp32 global accumulator
+      mbar_wait(dq_full, i & 1);
+      tc_fence_after();
+      float* dqr = a.dq_acc + ((int64_t)slot * a.qtok + qloc) * a.dim;
+#pragma unroll 1
+      for (int c0 = 0; c0 < 128; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(t_s + lane_off + c0, r);
+        tmem_ld_wait();
+        if (qok && c0 < a.dim) {
+#pragma unroll
+          for (int e = 0; e < 32; e += 4) {
+            if (c0 + e < a.dim)
+              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dqr + c0 + e),
+                           "f"(__uint_as_float(r[e]) * a.scale), "f"(__uint_as_float(r[e + 1]) * a.scale),
+                           "f"(__uint_as_float(r[e + 2]) * a.scale), "f"(__uint_as_float(r[e + 3]) * a.scale)
+                           : "memory");
+          }
+        }
+      }
+      tc_fence_before();
+      named_bar_sync(1, 128);
+      if (et == 0) mbar_arrive(dq_empty);
+    }
+    // dK / dV rows of this key block (one key per thread) -> fp32 contributions
+    const int64_t key = k0 + row;
+    if (key < a.kvtok) {
+      const int64_t off = (key / a.chunk) * a.grad_rank_stride + ((int64_t)slot * a.chunk + key % a.chunk) * a.dim;
+      float* dkr = a.dk_full + off;
+      float* dvr = a.dv_full + off;
+      if (nq == 0) {
+        for (int c = 0; c < a.dim; c += 4) {
+          *reinterpret_cast<float4*>(dkr + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+          *reinterpret_cast<float4*>(dvr + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      } else {
+#pragma unroll 1
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+          uint32_t rk[32], rv[32];
+          tmem_ld_32x32b_x32(t_dk + lane_off + c0, rk);
+          tmem_ld_32x32b_x32(t_dv + lane_off + c0, rv);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; e += 4) {
+            if (c0 + e < a.dim) {
+              *reinterpret_cast<float4*>(dkr + c0 + e) =
+                  make_float4(__uint_as_float(rk[e]) * a.scale, __uint_as_float(rk[e + 1]) * a.scale,
+                              __uint_as_float(rk[e + 2]) * a.scale, __uint_as_float(rk[e + 3]) * a.scale);
+              *reinterpret_cast<float4*>(dvr + c0 + e) =
+                  make_float4(__uint_as_float(rv[e]), __uint_as_float(rv[e + 1]), __uint_as_float(rv[e + 2]),
+                              __uint_as_float(rv[e + 3]));
+            }
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+__global__ void dq_finalize_kernel(const float* __restrict__ acc, __nv_bfloat16* __restrict__ dq, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dq[i] = __float2bfloat16_rn(acc[i]);
+}
+
+}  // namespace tc
+
+bool tc_softmax_supported(int dim, int64_t kv_chunk) {
+  return dim >= 8 && dim <= 128 && dim % 8 == 0 && kv_chunk % 128 == 0;
+}
+
+cudaError_t tc_softmax_forward(const void* q, const void* kf, const void* vf, void* out, float* lse, int64_t slots,
+                               int64_t qtok, int64_t kvtok, int dim, int causal, int64_t row_offset, int64_t kv_chunk,
+                               int64_t kv_rank_stride, cudaStream_t s) {
+  CUtensorMap mq, mk, mv, mo;
+  cudaError_t e;
+  const int64_t ranks = kvtok / kv_chunk;
+  if ((e = make_tmap_3d(&mq, q, slots, qtok, dim)) != cudaSuccess) return e;
+  if ((e = make_tmap_4d(&mk, kf, ranks, slots, kv_chunk, dim, kv_rank_stride)) != cudaSuccess) return e;
+  if ((e = make_tmap_4d(&mv, vf, ranks, slots, kv_chunk, dim, kv_rank_stride)) != cudaSuccess) return e;
+  if ((e = make_tmap_3d(&mo, out, slots, qtok, dim)) != cudaSuccess) return e;
+  if ((e = set_smem_once((const void*)tc::tc_softmax_fwd_kernel, tc::kSmFwdSmem)) != cudaSuccess) return e;
+  tc::SmFwdArgs a{lse, qtok, kvtok, kv_chunk, row_offset, dim, causal, 1.4426950408889634f / sqrtf((float)dim)};
+  dim3 grid((unsigned)((qtok + 127) / 128), (unsigned)slots);
+  tc::tc_softmax_fwd_kernel<<<grid, 192, tc::kSmFwdSmem, s>>>(mq, mk, mv, mo, a);
+  return cudaGetLastError();
+}
+
+int64_t tc_softmax_bwd_scratch(int64_t slots, int64_t qtok, int dim) {
+  return slots * qtok * (dim + 1) * 4 + 256;
+}
+
+// scratch: delta [slots][qtok] fp32, dq_acc [slots][qtok][dim] fp32
+cudaError_t tc_softmax_backward(const void* q, const void* kf, const void* vf, const void* o, const float* lse,
+                                const void* d_out, void* dq, float* dk_full, float* dv_full, void* scratch,
+                                int64_t slots, int64_t qtok, int64_t kvtok, int dim, int causal, int64_t row_offset,
+                                int64_t kv_chunk, int64_t kv_rank_stride, int64_t grad_rank_stride, cudaStream_t s) {
+  float* delta = reinterpret_cast<float*>(scratch);
+  float* dq_acc = delta + ((slots * qtok + 63) / 64) * 64;
+  cudaError_t e = softmax_delta_bf16(o, d_out, delta, slots * qtok, dim, s);
+  if (e != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(dq_acc, 0, (size_t)slots * qtok * dim * 4, s)) != cudaSuccess) return e;
+  CUtensorMap mq, mdo, mk, mv;
+  const int64_t ranks = kvtok / kv_chunk;
+  if ((e = make_tmap_3d(&mq, q, slots, qtok, dim)) != cudaSuccess) return e;
+  if ((e = make_tmap_3d(&mdo, d_out, slots, qtok, dim)) != cudaSuccess) return e;
+  if ((e = make_tmap_4d(&mk, kf, ranks, slots, kv_chunk, dim, kv_rank_stride)) != cudaSuccess) return e;
+  if ((e = make_tmap_4d(&mv, vf, ranks, slots, kv_chunk, dim, kv_rank_stride)) != cudaSuccess) return e;
+  if ((e = set_smem_once((const void*)tc::tc_softmax_bwd_kernel, tc::kSmBwdSmem)) != cudaSuccess) return e;
+  tc::SmBwdArgs a{lse, delta, dq_acc, dk_full, dv_full, qtok, kvtok, kv_chunk, grad_rank_stride, row_offset, dim,
+                  causal, 1.f / sqrtf((float)dim), 1.4426950408889634f / sqrtf((float)dim)};
+  dim3 grid((unsigned)((kvtok + 127) / 128), (unsigned)slots);
+  tc::tc_softmax_bwd_kernel<<<grid, 192, tc::kSmBwdSmem, s>>>(mq, mdo, mk, mv, a);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const int64_t n = slots * qtok * dim;
+  tc::dq_finalize_kernel<<<(unsigned)lmin(148 * 16, (n + 255) / 256), 256, 0, s>>>(dq_acc, (__nv_bfloat16*)dq, n);
+  return cudaGetLastError();
+}
+
+}  // namespace lasp

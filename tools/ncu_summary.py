@@ -1,0 +1,68 @@
+"""Summarise ncu --set full captures (.ncu-rep) into profiles/ (text + json).
+
+usage: python tools/ncu_summary.py OUT_PREFIX rep1.ncu-rep [rep2 ...]
+Writes OUT_PREFIX.txt (key metrics + top stall reasons per kernel) and merges
+per-launch DRAM traffic into profiles/ncu_traffic.json keyed by C-ABI entry.
+"""
+import csv
+import io
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+KEYS = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__cycles_elapsed.avg.per_second",
+    "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "launch__grid_size", "launch__block_size",
+    "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "lts__t_bytes.sum", "l1tex__throughput.avg.pct_of_peak_sustained_active",
+]
+ENTRY = {"tc_causal_chunk": "lasp2_causal_chunk", "tc_apply_state": "lasp2_apply_state",
+         "tc_segment_states": "lasp2_segment_states", "tc_softmax_fwd": "lasp2h_softmax_forward",
+         "tc_softmax_bwd": "lasp2h_softmax_backward"}
+
+
+def raw(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    return [dict(zip(rows[0], r)) for r in rows[2:]], dict(zip(rows[0], rows[1]))
+
+
+def main():
+    prefix = Path(sys.argv[1])
+    lines = []
+    traffic_path = Path(__file__).resolve().parent.parent / "profiles" / "ncu_traffic.json"
+    traffic = json.loads(traffic_path.read_text()) if traffic_path.exists() else {}
+    for rep in sys.argv[2:]:
+        launches, units = raw(rep)
+        for rec in launches:
+            name = rec.get("Kernel Name", "?")
+            lines.append(f"== {Path(rep).name}: {name[:100]}")
+            for k in KEYS:
+                if k in rec:
+                    lines.append(f"  {k:90s} {rec[k]:>16s} {units.get(k, '')}")
+            stalls = sorted(((float(v), k) for k, v in rec.items()
+                             if k.startswith("smsp__average_warp_latency_issue_stalled_") and k.endswith(".ratio")
+                             and v.replace('.', '', 1).isdigit()), reverse=True)[:8]
+            if stalls:
+                lines.append("  top stall reasons (warp cycles per issued instruction):")
+                for v, k in stalls:
+                    lines.append(f"    {k.replace('smsp__average_warp_latency_issue_stalled_', ''):60s} {v:8.2f}")
+            try:
+                rd = float(rec["dram__bytes_read.sum"]) * (1e9 if units["dram__bytes_read.sum"] == "Gbyte" else 1e6 if units["dram__bytes_read.sum"] == "Mbyte" else 1)
+                wr = float(rec["dram__bytes_write.sum"]) * (1e9 if units["dram__bytes_write.sum"] == "Gbyte" else 1e6 if units["dram__bytes_write.sum"] == "Mbyte" else 1)
+                for key, entry in ENTRY.items():
+                    if key in name:
+                        traffic[entry] = {"bytes_per_launch": rd + wr, "read": rd, "write": wr,
+                                          "source": str(prefix.name), "kernel": name[:80]}
+            except (KeyError, ValueError):
+                pass
+    prefix.with_suffix(".txt").write_text("\n".join(lines) + "\n")
+    traffic_path.write_text(json.dumps(traffic, indent=1) + "\n")
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    main()
