@@ -66,13 +66,15 @@ def load_peaks() -> dict:
     return dict(hbm=6650.0, tensor=1590.0, tensor_sustained=1400.0, source="fallback (B200_PROFILING.md)")
 
 
-def ncu_traffic(kernel_key: str):
-    """Per-launch DRAM bytes of the dominant kernel from the committed ncu summary, if present."""
+def ncu_traffic(workload: str, kernel_key: str):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu capture
+    of this same bench command (profiles/ncu_traffic.json[workload][entry]), if present."""
     p = ROOT / "profiles" / "ncu_traffic.json"
     if not p.exists():
         return None
     try:
-        return json.loads(p.read_text()).get(kernel_key)
+        rec = json.loads(p.read_text()).get(workload, {}).get(kernel_key)
+        return None if rec is None else rec["bytes_per_launch"]
     except Exception:
         return None
 
@@ -307,7 +309,7 @@ def measure_workload(workload: str, ctx, rank: int, world: int, steps: int, warm
     unit_bytes = B * H * c * D * 2  # one bf16 (B,H,C,d) tensor
     algo_bytes = {"lasp2_causal_chunk": 4 * unit_bytes, "lasp2_apply_state": 2 * unit_bytes,
                   "lasp2_segment_states": 2 * unit_bytes}.get(dom, 0)
-    return dict(n=n, c=c, masked=masked, ms=ms, e2e_ms=e2e_ms, per_kernel_ms=per_kernel, dominant=dom,
+    return dict(workload=workload, n=n, c=c, masked=masked, ms=ms, e2e_ms=e2e_ms, per_kernel_ms=per_kernel, dominant=dom,
                 dom_launch_ms=dom_launch_ms, dom_algo_bytes=algo_bytes, launches_per_step=launches_per_step,
                 h2d=4 * q.numel() * q.element_size() * world, d2h=4 * q.numel() * q.element_size() * world,
                 clocks=clk, e2e_steps=e2e_steps, graph=graph is not None,
@@ -327,7 +329,7 @@ def summarize(r: dict, world: int, peaks: dict) -> dict:
         hbm_frac_of_peak=byte_s / world / (peaks["hbm"] * 1e9),
         per_kernel_ms_per_step=r["per_kernel_ms"],
         roofline={"kernel": r["dominant"], "bound": "hbm", "achieved": achieved, "peak": peaks["hbm"],
-                  "unit": "GB/s", "frac": achieved / peaks["hbm"], "traffic": ncu_traffic(r["dominant"]),
+                  "unit": "GB/s", "frac": achieved / peaks["hbm"], "traffic": ncu_traffic(r["workload"], r["dominant"]),
                   "peak_source": peaks["source"],
                   "algorithmic_bytes_per_launch": r["dom_algo_bytes"], "avg_launch_ms": r["dom_launch_ms"]},
         e2e={"value": r["n"] / (r["e2e_ms"] / 1e3), "unit": UNIT, "h2d_bytes_per_step": r["h2d"],

@@ -75,6 +75,28 @@ __device__ __forceinline__ void tmem_row_to_image(uint32_t taddr_lane, uint8_t* 
   }
 }
 
+// Columns [c_begin, c_begin + ncols) (multiple of 32) of this thread's TMEM lane
+// -> bf16 (optionally causal-masked: 1 keep col<=row, 2 keep col>=row) -> SW128 image.
+__device__ __forceinline__ void tmem_cols_to_image(uint32_t taddr_lane, uint8_t* img, uint32_t row, int c_begin,
+                                                   int ncols, int mask) {
+#pragma unroll 1
+  for (int c0 = c_begin; c0 < c_begin + ncols; c0 += 32) {
+    uint32_t r[32];
+    tmem_ld_32x32b_x32(taddr_lane + c0, r);
+    tmem_ld_wait();
+    float v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      float x = __uint_as_float(r[i]);
+      const int col = c0 + i;
+      if (mask == 1 && col > (int)row) x = 0.f;
+      if (mask == 2 && col < (int)row) x = 0.f;
+      v[i] = x;
+    }
+    st_row32_bf16(img, row, c0, v);
+  }
+}
+
 }  // namespace tc
 
 // host: opt a kernel into >48 KB dynamic smem once per (kernel, device).

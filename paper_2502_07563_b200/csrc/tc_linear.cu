@@ -134,7 +134,9 @@ struct CausalArgs {
   int transpose_state;
 };
 
-__global__ void __launch_bounds__(192, 1)
+constexpr int kCausalThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
+
+__global__ void __launch_bounds__(kCausalThreads, 1)
     tc_causal_chunk_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                            const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
                            CausalArgs a) {
@@ -148,11 +150,11 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* empty = bars + kRing;
   uint64_t* s_full = bars + 2 * kRing + 0;
   uint64_t* st_full = bars + 2 * kRing + 1;
-  uint64_t* o_full = bars + 2 * kRing + 2;
-  uint64_t* p_ready = bars + 2 * kRing + 3;
-  uint64_t* sst_ready = bars + 2 * kRing + 4;
-  uint64_t* o_empty = bars + 2 * kRing + 5;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kRing + 6);
+  uint64_t* p_ready = bars + 2 * kRing + 2;
+  uint64_t* sst_ready = bars + 2 * kRing + 3;
+  uint64_t* o_full = bars + 2 * kRing + 4;   // [2]
+  uint64_t* o_empty = bars + 2 * kRing + 6;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kRing + 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int seg = blockIdx.x;
@@ -168,7 +170,7 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    for (int i = 0; i < 6; ++i) mbar_init(&s_full[i], 1);
+    for (int i = 0; i < 8; ++i) mbar_init(&s_full[i], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -176,7 +178,9 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t t_s = tmem, t_o = tmem + 128, t_st = tmem + 256;
+  // TMEM: S [0,128), O[0] [128,256), running state [256,384), O[1] [384,512)
+  const uint32_t t_s = tmem, t_st = tmem + 256;
+  auto t_o = [&](int b) { return tmem + (b ? 384u : 128u); };
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
@@ -208,11 +212,13 @@ __global__ void __launch_bounds__(192, 1)
     for (int jj = 0; jj < nblk; ++jj) {
       const int tq = 3 * jj, tk = tq + 1, tv = tq + 2;
       const int sq = tq % kRing, sk = tk % kRing, sv = tv % kRing;
+      const int ob = jj & 1;
       const uint32_t qa = smem_u32(ring + sq * kTileBytes);
       const uint32_t ka = smem_u32(ring + sk * kTileBytes);
       const uint32_t va = smem_u32(ring + sv * kTileBytes);
       mbar_wait(&full[sq], (tq / kRing) & 1);
       mbar_wait(&full[sk], (tk / kRing) & 1);
+      if (jj > 0) mbar_wait(p_ready, (jj - 1) & 1);  // S tile drained by the epilogue
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
@@ -221,11 +227,12 @@ __global__ void __launch_bounds__(192, 1)
       }
       __syncwarp();
       mbar_wait(sst_ready, jj & 1);
-      if (jj > 0) mbar_wait(o_empty, (jj - 1) & 1);
+      if (jj >= 2) mbar_wait(&o_empty[ob], ((jj >> 1) - 1) & 1);
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < kfeat; ++kk) mma_bf16_ss(t_o, desc_kmajor(qa, kk), desc_mnmajor(simg_a, kk), id_qs, kk > 0);
+        for (int kk = 0; kk < kfeat; ++kk)
+          mma_bf16_ss(t_o(ob), desc_kmajor(qa, kk), desc_mnmajor(simg_a, kk), id_qs, kk > 0);
         mma_commit(&empty[sq]);
       }
       __syncwarp();
@@ -244,18 +251,21 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) mma_bf16_ss(t_o, desc_kmajor(pimg_a, kk), desc_mnmajor(va, kk), id_pv, 1u);
+        for (int kk = 0; kk < 8; ++kk) mma_bf16_ss(t_o(ob), desc_kmajor(pimg_a, kk), desc_mnmajor(va, kk), id_pv, 1u);
         mma_commit(&empty[sv]);
-        mma_commit(o_full);
+        mma_commit(&o_full[ob]);
       }
       __syncwarp();
     }
   } else {
-    // ---------------- epilogue: 4 warps, one TMEM lane (row) per thread ----------------
+    // -------- epilogue: 8 warps; warp w owns TMEM lanes 32*(w%4).. and columns [64*half, +64) --------
     const int qd = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int cb = 64 * half;
     const uint32_t row = qd * 32 + lane;
     const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
     const int et = threadIdx.x - 64;
+    constexpr uint32_t kEpi = kCausalThreads - 64;
     const int dim = a.dim;
     const int64_t dd = (int64_t)dim * dim;
     // initial state S0 = base + seg_states[seg] (optionally transposed), rows beyond dim are zero
@@ -263,7 +273,7 @@ __global__ void __launch_bounds__(192, 1)
       const float* st = a.seg_states ? a.seg_states + ((int64_t)slot * a.nseg + seg) * dd : nullptr;
       const float* bs = a.base ? a.base + (int64_t)slot * dd : nullptr;
 #pragma unroll 1
-      for (int c0 = 0; c0 < 128; c0 += 32) {
+      for (int c0 = cb; c0 < cb + 64; c0 += 32) {
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
@@ -285,41 +295,42 @@ __global__ void __launch_bounds__(192, 1)
       tmem_st_wait();
       fence_proxy_async_smem();
       tc_fence_before();
-      named_bar_sync(1, 128);
+      named_bar_sync(1, kEpi);
       if (et == 0) mbar_arrive(sst_ready);
     }
     const int pmask = a.reverse ? 2 : 1;
     for (int jj = 0; jj < nblk; ++jj) {
       const int j = a.reverse ? nblk - 1 - jj : jj;
+      const int ob = jj & 1;
       // ---- P = mask(S) -> smem (after the previous O tile left the staging buffer)
       mbar_wait(s_full, jj & 1);
       tc_fence_after();
       if (jj > 0 && et == 0) tma_store_wait_read<0>();
-      named_bar_sync(1, 128);
-      tmem_row_to_image(t_s + lane_off, pimg, row, pmask);
+      named_bar_sync(1, kEpi);
+      tmem_cols_to_image(t_s + lane_off, pimg, row, cb, 64, pmask);
       fence_proxy_async_smem();
       tc_fence_before();
-      named_bar_sync(1, 128);
+      named_bar_sync(1, kEpi);
       if (et == 0) mbar_arrive(p_ready);
       // ---- next block's state image
       if (jj < nblk - 1) {
         mbar_wait(st_full, jj & 1);
         tc_fence_after();
-        tmem_row_to_image(t_st + lane_off, simg, row, 0);
+        tmem_cols_to_image(t_st + lane_off, simg, row, cb, 64, 0);
         fence_proxy_async_smem();
         tc_fence_before();
-        named_bar_sync(1, 128);
+        named_bar_sync(1, kEpi);
         if (et == 0) mbar_arrive(sst_ready);
       }
       // ---- O tile -> staging -> TMA store
-      mbar_wait(o_full, jj & 1);
+      mbar_wait(&o_full[ob], (jj >> 1) & 1);
       tc_fence_after();
-      tmem_row_to_image(t_o + lane_off, pimg, row, 0);
+      tmem_cols_to_image(t_o(ob) + lane_off, pimg, row, cb, 64, 0);
       fence_proxy_async_smem();
       tc_fence_before();
-      named_bar_sync(1, 128);
+      named_bar_sync(1, kEpi);
       if (et == 0) {
-        mbar_arrive(o_empty);
+        mbar_arrive(&o_empty[ob]);
         const int orow = (int)(lo + (int64_t)j * kTile);
         for (int bx = 0; bx < nbox; ++bx) tma_store_3d(&tm_o, pimg + bx * kBoxBytes, 64 * bx, orow, slot);
         tma_store_commit();
@@ -561,7 +572,7 @@ cudaError_t tc_causal_chunk(const void* q, const void* k, const void* v, const f
   if ((e = set_smem_once((const void*)tc::tc_causal_chunk_kernel, tc::kCausalSmem)) != cudaSuccess) return e;
   tc::CausalArgs a{seg_states, base, tokens, dim, nseg, reverse, transpose_state};
   dim3 grid(nseg, (unsigned)slots);
-  tc::tc_causal_chunk_kernel<<<grid, 192, tc::kCausalSmem, s>>>(mq, mk, mv, mo, a);
+  tc::tc_causal_chunk_kernel<<<grid, tc::kCausalThreads, tc::kCausalSmem, s>>>(mq, mk, mv, mo, a);
   return cudaGetLastError();
 }
 

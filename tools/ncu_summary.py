@@ -1,6 +1,6 @@
 """Summarise ncu --set full captures (.ncu-rep) into profiles/ (text + json).
 
-usage: python tools/ncu_summary.py OUT_PREFIX rep1.ncu-rep [rep2 ...]
+usage: python tools/ncu_summary.py OUT_PREFIX WORKLOAD rep1.ncu-rep [rep2 ...]
 Writes OUT_PREFIX.txt (key metrics + top stall reasons per kernel) and merges
 per-launch DRAM traffic into profiles/ncu_traffic.json keyed by C-ABI entry.
 """
@@ -35,7 +35,9 @@ def main():
     lines = []
     traffic_path = Path(__file__).resolve().parent.parent / "profiles" / "ncu_traffic.json"
     traffic = json.loads(traffic_path.read_text()) if traffic_path.exists() else {}
-    for rep in sys.argv[2:]:
+    workload = sys.argv[2]
+    traffic.setdefault(workload, {})
+    for rep in sys.argv[3:]:
         launches, units = raw(rep)
         for rec in launches:
             name = rec.get("Kernel Name", "?")
@@ -43,19 +45,20 @@ def main():
             for k in KEYS:
                 if k in rec:
                     lines.append(f"  {k:90s} {rec[k]:>16s} {units.get(k, '')}")
+            pre = "smsp__average_warps_issue_stalled_"
             stalls = sorted(((float(v), k) for k, v in rec.items()
-                             if k.startswith("smsp__average_warp_latency_issue_stalled_") and k.endswith(".ratio")
+                             if k.startswith(pre) and k.endswith("_per_issue_active.ratio")
                              and v.replace('.', '', 1).isdigit()), reverse=True)[:8]
             if stalls:
                 lines.append("  top stall reasons (warp cycles per issued instruction):")
                 for v, k in stalls:
-                    lines.append(f"    {k.replace('smsp__average_warp_latency_issue_stalled_', ''):60s} {v:8.2f}")
+                    lines.append(f"    {k.replace(pre, '').replace('_per_issue_active.ratio', ''):40s} {v:8.2f}")
             try:
                 rd = float(rec["dram__bytes_read.sum"]) * (1e9 if units["dram__bytes_read.sum"] == "Gbyte" else 1e6 if units["dram__bytes_read.sum"] == "Mbyte" else 1)
                 wr = float(rec["dram__bytes_write.sum"]) * (1e9 if units["dram__bytes_write.sum"] == "Gbyte" else 1e6 if units["dram__bytes_write.sum"] == "Mbyte" else 1)
                 for key, entry in ENTRY.items():
                     if key in name:
-                        traffic[entry] = {"bytes_per_launch": rd + wr, "read": rd, "write": wr,
+                        traffic[workload][entry] = {"bytes_per_launch": rd + wr, "read": rd, "write": wr,
                                           "source": str(prefix.name), "kernel": name[:80]}
             except (KeyError, ValueError):
                 pass

@@ -74,5 +74,23 @@ def main():
     print(f"unmasked fwd+bwd {t:.3f} ms  {n / t * 1e3:.0f} tok/s {22 * d * h * n / t / 1e6:.0f} GB/s(min-bytes)")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and not (len(sys.argv) > 2 and sys.argv[2] == "softmax"):
     main()
+
+
+def softmax_probe(n=32768, h=16, d=128):
+    """Causal softmax attention (one rank, W=1) fwd and bwd throughput."""
+    q, k, v, do = (gen_slots_device(0, 1, h, n, d, t) for t in ("q", "k", "v", "do"))
+    per = h * n * d
+    out, lse = ops.softmax_forward(q, k, v, True, 0, n, n, 0)
+    t = timeit(lambda: ops.softmax_forward(q, k, v, True, 0, n, n, 0), 3)
+    fl_fwd = 4 * d * n * (n + 1) / 2 * h  # causal-useful: 2 GEMMs x 2 flop
+    print(f"softmax fwd N={n} H={h}: {t:.3f} ms  {fl_fwd / t / 1e9:.1f} TFLOP/s")
+    grads = torch.empty((1, 2, 1, h, n, d), dtype=torch.float32, device="cuda")
+    t = timeit(lambda: ops.softmax_backward(q, k, v, out, lse, do, True, 0, n, n, 0, grads, 0, per), 3)
+    fl_bwd = 10 * d * n * (n + 1) / 2 * h  # 5 GEMMs (S recompute, dP, dV, dK, dQ)
+    print(f"softmax bwd N={n} H={h}: {t:.3f} ms  {fl_bwd / t / 1e9:.1f} TFLOP/s (5-GEMM count)")
+
+
+if __name__ == "__main__" and len(sys.argv) > 2 and sys.argv[2] == "softmax":
+    softmax_probe(int(sys.argv[3]) if len(sys.argv) > 3 else 32768)
