@@ -280,24 +280,63 @@ def measure_workload(workload: str, ctx, rank: int, world: int, steps: int, warm
         ms = max_over_ranks(t0.elapsed_time(t1) / steps)
         clk = clocks.summary(h0, h1)
 
-        # (4) end-to-end through the public API: H2D of the step's inputs from pinned
-        #     host memory, the layer fwd+bwd, D2H of its outputs and gradients
-        hq, hk, hv, hdo = (t.cpu().pin_memory() for t in (q, k, v, do))
-        outs_host = [torch.empty(q.shape, dtype=q.dtype, pin_memory=True) for _ in range(4)]
-        e2e_steps = max(2, min(steps, 5))
+        # (4) end-to-end through the public API, pipelined over three streams with two
+        #     buffer sets: H2D of step i+1 (pinned host -> HBM) || fwd+bwd of step i ||
+        #     D2H of step i-1 (outputs and all three gradients -> pinned host).
+        bufs = [(q, k, v, do), tuple(t.clone() for t in (q, k, v, do))]
+        runners = []
+        for bi, (bq, bk, bv, bdo) in enumerate(bufs):
+            def make(bq=bq, bk=bk, bv=bv, bdo=bdo):
+                out, cache = rank_forward(ctx, bq, bk, bv, masked=masked)
+                g = rank_backward(ctx, cache, bdo)
+                return out, g.dq, g.dk, g.dv
+            if graph is not None:
+                if bi == 0:
+                    runners.append((graph.replay, outs))
+                else:
+                    g2 = torch.cuda.CUDAGraph()
+                    s3 = torch.cuda.Stream()
+                    s3.wait_stream(stream)
+                    with torch.cuda.stream(s3):
+                        make()
+                    stream.wait_stream(s3)
+                    sync_all()
+                    with torch.cuda.graph(g2):
+                        outs2 = make()
+                    runners.append((g2.replay, outs2))
+            else:
+                runners.append((make, None))
+        host_in = [t.cpu().pin_memory() for t in (q, k, v, do)]
+        host_out = [[torch.empty(q.shape, dtype=q.dtype, pin_memory=True) for _ in range(4)] for _ in range(2)]
+        h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
+        ev = lambda: torch.cuda.Event()  # noqa: E731
+        h2d_done, comp_done, d2h_done = [ev(), ev()], [ev(), ev()], [ev(), ev()]
+        e2e_steps = max(4, min(steps, 8))
         sync_all()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(e2e_steps):
-            for dst, src in zip((q, k, v, do), (hq, hk, hv, hdo)):
-                dst.copy_(src, non_blocking=True)
-            res = outs if graph is not None else None
-            if graph is not None:
-                graph.replay()
-            else:
-                res = step()
-            for dst, src in zip(outs_host, res):
-                dst.copy_(src, non_blocking=True)
+        e0.record(h2d_s)
+        for i in range(e2e_steps):
+            bi = i & 1
+            if i >= 2:
+                h2d_s.wait_event(comp_done[bi])  # inputs of set bi no longer read
+            with torch.cuda.stream(h2d_s):
+                for dst, src in zip(bufs[bi], host_in):
+                    dst.copy_(src, non_blocking=True)
+                h2d_done[bi].record(h2d_s)
+            stream.wait_event(h2d_done[bi])
+            if i >= 2:
+                stream.wait_event(d2h_done[bi])  # outputs of set bi already copied out
+            fn, static_outs = runners[bi]
+            res = fn()
+            res = static_outs if static_outs is not None else res
+            comp_done[bi].record(stream)
+            d2h_s.wait_event(comp_done[bi])
+            with torch.cuda.stream(d2h_s):
+                for dst, src in zip(host_out[bi], res):
+                    dst.copy_(src, non_blocking=True)
+                d2h_done[bi].record(d2h_s)
+        stream.wait_stream(h2d_s)
+        stream.wait_stream(d2h_s)
         e1.record(stream)
         sync_all()
         e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e2e_steps)

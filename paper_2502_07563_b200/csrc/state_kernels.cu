@@ -24,11 +24,22 @@ __global__ void scan_states_kernel(A* __restrict__ seg, A* __restrict__ total, i
   const int64_t slot = idx / dd, el = idx % dd;
   A* base = seg + slot * nseg * dd + el;
   A run = A(0);
-  for (int i = 0; i < nseg; ++i) {
-    const int s = reverse ? nseg - 1 - i : i;
-    const A v = base[(int64_t)s * dd];
-    base[(int64_t)s * dd] = run;
-    run = (i == 0) ? v : run + v;
+  // batches of 8 independent loads keep the (latency-bound) column walk in flight
+  for (int i0 = 0; i0 < nseg; i0 += 8) {
+    A vals[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u;
+      if (i < nseg) vals[u] = base[(int64_t)(reverse ? nseg - 1 - i : i) * dd];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u;
+      if (i < nseg) {
+        base[(int64_t)(reverse ? nseg - 1 - i : i) * dd] = run;
+        run = (i == 0) ? vals[u] : run + vals[u];
+      }
+    }
   }
   if (total) total[slot * dd + el] = run;
 }
