@@ -42,12 +42,18 @@ WORKLOADS = {
                  n=131072, masked=False),
     "cfg3": dict(name="cfg3: LASP-2 masked layer fwd+bwd at Linear-Llama3-1B shape, B=1 H=16 d=128, N=524288 total",
                  n=524288, masked=True),
+    # LASP-2H N layer (K/V all_gather + causal softmax); opt-in (compute-bound, seconds per step at full N)
+    "cfg4": dict(name="cfg4: LASP-2H causal softmax layer fwd+bwd (K/V AllGather), B=1 H=16 d=128, N=262144 total",
+                 n=262144, masked=True, softmax=True),
 }
 BC = 256  # block size pinned for the algorithmic FLOP count
 
 
-def flops_per_token(masked: bool) -> float:
-    """Causal-useful algorithmic FLOPs per token (all heads), BASELINE.md §3."""
+def flops_per_token(masked: bool, softmax: bool = False, n: int = 0) -> float:
+    """Causal-useful algorithmic FLOPs per token (all heads), BASELINE.md §3.
+    LASP-2H softmax: 7*d*N(N+1) per head for the whole layer -> 7*d*(N+1) per token."""
+    if softmax:
+        return float(7 * D * (n + 1) * H)
     per_head = 12 * D * D + (7 * D * (BC + 1) if masked else 0)
     return float(per_head * H)
 
@@ -147,21 +153,30 @@ def cpu_reference(workload: str, budget_s: float = 20.0) -> dict:
 
     wl = WORKLOADS[workload]
     cores = len(os.sched_getaffinity(0))
-    n = 2048 if wl["masked"] else 8192
+    softmax = wl.get("softmax", False)
+    n = 1024 if softmax else (2048 if wl["masked"] else 8192)
     q, k, v, do = (O.gen_slots(0, B, H, n, D, t, np.float32) for t in ("q", "k", "v", "do"))
+
+    def run():
+        if softmax:
+            O.cp_full(q, k, v, do, 1, True)
+        else:
+            O.lasp2_full(q, k, v, do, 1, wl["masked"], bc=BC)
+
     # warm-up once, then as many full fwd+bwd iterations of the sample as fit the budget
-    O.lasp2_full(q, k, v, do, 1, wl["masked"], bc=BC)
+    run()
     times = []
     t_end = time.perf_counter() + budget_s
     while time.perf_counter() < t_end or len(times) < 2:
         t0 = time.perf_counter()
-        O.lasp2_full(q, k, v, do, 1, wl["masked"], bc=BC)
+        run()
         times.append(time.perf_counter() - t0)
         if len(times) >= 50:
             break
     med = statistics.median(times)
     return {"value": n / med, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"numpy f32 oracle (oracle/lasp_oracle.py, restating lasp2.py:208-285 blocked at Bc={BC}) "
+            "sample": f"numpy f32 oracle (oracle/lasp_oracle.py, restating "
+                      f"{'standard_sp.py:37-76' if softmax else f'lasp2.py:208-285 blocked at Bc={BC}'}) "
                       f"on N={n} tokens of the same B=1 H=16 d=128 layer, T=1, median of {len(times)} "
                       f"iterations, OpenBLAS threads={os.environ.get('OPENBLAS_NUM_THREADS', 'default')}"}
 
@@ -195,6 +210,9 @@ def run_reference_arm(args) -> None:
 # GPU arm
 # ---------------------------------------------------------------------------
 
+seq_override: dict[str, int] = {}
+
+
 def measure_workload(workload: str, ctx, rank: int, world: int, steps: int, warmup: int, device,
                      use_graph: bool = True) -> dict:
     import torch
@@ -204,16 +222,25 @@ def measure_workload(workload: str, ctx, rank: int, world: int, steps: int, warm
     from paper_2502_07563_b200.datagen import gen_slots_device
     from paper_2502_07563_b200.lasp2 import rank_backward, rank_forward
 
+    from paper_2502_07563_b200.standard_sp import _cp_backward_rank, _cp_forward_rank
+
     wl = WORKLOADS[workload]
-    n, masked = wl["n"], wl["masked"]
+    n, masked, softmax = seq_override.get(workload, wl["n"]), wl["masked"], wl.get("softmax", False)
     c = n // world
     q, k, v, do = (gen_slots_device(0, B, H, c, D, t, torch.bfloat16, device=device, row_offset=rank * c)
                    for t in ("q", "k", "v", "do"))
 
-    def step():
-        out, cache = rank_forward(ctx, q, k, v, masked=masked)
-        g = rank_backward(ctx, cache, do)
+    def layer(bq, bk, bv, bdo):
+        if softmax:
+            out, cache = _cp_forward_rank(ctx, bq, bk, bv, True)
+            g = _cp_backward_rank(ctx, cache, bdo)
+        else:
+            out, cache = rank_forward(ctx, bq, bk, bv, masked=masked)
+            g = rank_backward(ctx, cache, bdo)
         return out, g.dq, g.dk, g.dv
+
+    def step():
+        return layer(q, k, v, do)
 
     def sync_all():
         torch.cuda.synchronize()
@@ -287,9 +314,7 @@ def measure_workload(workload: str, ctx, rank: int, world: int, steps: int, warm
         runners = []
         for bi, (bq, bk, bv, bdo) in enumerate(bufs):
             def make(bq=bq, bk=bk, bv=bv, bdo=bdo):
-                out, cache = rank_forward(ctx, bq, bk, bv, masked=masked)
-                g = rank_backward(ctx, cache, bdo)
-                return out, g.dq, g.dk, g.dv
+                return layer(bq, bk, bv, bdo)
             if graph is not None:
                 if bi == 0:
                     runners.append((graph.replay, outs))
@@ -347,9 +372,12 @@ def measure_workload(workload: str, ctx, rank: int, world: int, steps: int, warm
     dom_launch_ms = statistics.mean(durations[dom])
     unit_bytes = B * H * c * D * 2  # one bf16 (B,H,C,d) tensor
     algo_bytes = {"lasp2_causal_chunk": 4 * unit_bytes, "lasp2_apply_state": 2 * unit_bytes,
-                  "lasp2_segment_states": 2 * unit_bytes}.get(dom, 0)
-    return dict(workload=workload, n=n, c=c, masked=masked, ms=ms, e2e_ms=e2e_ms, per_kernel_ms=per_kernel, dominant=dom,
-                dom_launch_ms=dom_launch_ms, dom_algo_bytes=algo_bytes, launches_per_step=launches_per_step,
+                  "lasp2_segment_states": 2 * unit_bytes, "lasp2_dkdv_chunk": 6 * unit_bytes}.get(dom, 0)
+    # causal softmax useful FLOPs of one rank: queries [rC, (r+1)C) see keys <= position
+    pairs = H * (c * rank * c + c * (c + 1) / 2)
+    algo_flops = {"lasp2h_softmax_forward": 4 * D * pairs, "lasp2h_softmax_backward": 10 * D * pairs}.get(dom, 0)
+    return dict(workload=workload, n=n, c=c, masked=masked, softmax=softmax, ms=ms, e2e_ms=e2e_ms, per_kernel_ms=per_kernel, dominant=dom,
+                dom_launch_ms=dom_launch_ms, dom_algo_bytes=algo_bytes, dom_algo_flops=algo_flops, launches_per_step=launches_per_step,
                 h2d=4 * q.numel() * q.element_size() * world, d2h=4 * q.numel() * q.element_size() * world,
                 clocks=clk, e2e_steps=e2e_steps, graph=graph is not None,
                 kernel_sum_ms=sum(per_kernel.values()))
@@ -357,9 +385,11 @@ def measure_workload(workload: str, ctx, rank: int, world: int, steps: int, warm
 
 def summarize(r: dict, world: int, peaks: dict) -> dict:
     tok_s = r["n"] / (r["ms"] / 1e3)
-    flop_s = flops_per_token(r["masked"]) * tok_s
+    flop_s = flops_per_token(r["masked"], r.get("softmax", False), r["n"]) * tok_s
     byte_s = min_bytes_per_token() * tok_s
     achieved = r["dom_algo_bytes"] / (r["dom_launch_ms"] / 1e3) / 1e9
+    if r.get("softmax"):  # tensor-bound: useful FLOPs of the dominant kernel per launch
+        achieved = r["dom_algo_flops"] / (r["dom_launch_ms"] / 1e3) / 1e12
     return dict(
         value=tok_s, ms_per_step=r["ms"],
         tensor_tflops_per_gpu=flop_s / world / 1e12,
@@ -367,8 +397,10 @@ def summarize(r: dict, world: int, peaks: dict) -> dict:
         min_bytes_gbs_per_gpu=byte_s / world / 1e9,
         hbm_frac_of_peak=byte_s / world / (peaks["hbm"] * 1e9),
         per_kernel_ms_per_step=r["per_kernel_ms"],
-        roofline={"kernel": r["dominant"], "bound": "hbm", "achieved": achieved, "peak": peaks["hbm"],
-                  "unit": "GB/s", "frac": achieved / peaks["hbm"], "traffic": ncu_traffic(r["workload"], r["dominant"]),
+        roofline={"kernel": r["dominant"], "bound": "tensor" if r.get("softmax") else "hbm", "achieved": achieved,
+                  "peak": peaks["tensor"] if r.get("softmax") else peaks["hbm"],
+                  "unit": "TFLOP/s" if r.get("softmax") else "GB/s",
+                  "frac": achieved / (peaks["tensor"] if r.get("softmax") else peaks["hbm"]), "traffic": ncu_traffic(r["workload"], r["dominant"]),
                   "peak_source": peaks["source"],
                   "algorithmic_bytes_per_launch": r["dom_algo_bytes"], "avg_launch_ms": r["dom_launch_ms"]},
         e2e={"value": r["n"] / (r["e2e_ms"] / 1e3), "unit": UNIT, "h2d_bytes_per_step": r["h2d"],
@@ -447,9 +479,12 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--eager", action="store_true", help="time eager launches instead of CUDA-graph replay")
+    ap.add_argument("--seq-len", type=int, default=0, help="override N of the selected workload")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3 (timing rules)")
+    if args.seq_len:
+        seq_override[args.workload] = args.seq_len
     if args.impl == "reference":
         run_reference_arm(args)
     else:

@@ -77,6 +77,17 @@ int lasp2_causal_chunk(int dtype, const void* q, const void* k, const void* v, c
                        const void* base, void* out, int64_t slots, int64_t tokens, int dim, int nseg, int reverse,
                        int transpose_state, void* stream);
 
+/* Masked backward dK and dV of one rank's chunk in one pass:
+ *   dk_s = sum_{i>=s} (v_s.do_i) q_i + v_s G_s^T,  dv_s = sum_{i>=s} (k_s.q_i) do_i + k_s G_s
+ * with G_s = base + seg_states[seg(s)] + sum_{i>s, same segment} q_i^T do_i
+ * (seg_states = exclusive suffix of Q^T dO segment states, base = suffix fold of
+ * the gathered dM). Replaces the dk/dv halves of intra_backward
+ * (lasp2.py:199-202) plus lasp2.py:280-284. The bf16 path runs 2-CTA clusters
+ * that TMA-multicast Q and dO to both SMs (4 tile reads per block, not 6). */
+int lasp2_dkdv_chunk(int dtype, const void* q, const void* k, const void* v, const void* d_out, const void* seg_states,
+                     const void* base, void* dk, void* dv, int64_t slots, int64_t tokens, int dim, int nseg,
+                     void* stream);
+
 /* out (+)= x M (transpose=0) or x M^T (transpose=1) per slot.
  * Replaces apply_state / apply_state_t (lasp2.py:150-165). */
 int lasp2_apply_state(int dtype, const void* x, const void* m, void* out, int64_t slots, int64_t tokens, int dim,

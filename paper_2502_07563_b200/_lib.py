@@ -32,6 +32,7 @@ SIGNATURES = {
     "lasp2_scan_segments": (_int, [_int, _vp, _vp, _i64, _int, _int, _int, _vp]),
     "lasp2_fold_states": (_int, [_int, _vp, _vp, _int, _i64, _int, _int, _vp]),
     "lasp2_causal_chunk": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _int, _int, _int, _int, _vp]),
+    "lasp2_dkdv_chunk": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _int, _int, _vp]),
     "lasp2_apply_state": (_int, [_int, _vp, _vp, _vp, _i64, _i64, _int, _int, _int, _vp]),
     "lasp2h_softmax_forward": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _i64, _i64, _i64,
                                       _vp]),
@@ -98,7 +99,7 @@ class _Profiler:
 
 PROFILER = _Profiler()
 # kernels launched per call of each entry point (for gpu_launches accounting)
-KERNELS_PER_CALL = {"lasp2h_softmax_backward": 4}
+KERNELS_PER_CALL = {"lasp2h_softmax_backward": 4}  # bf16 tc path: delta, memset, main, finalize
 _NO_LAUNCH = {"lasp2_version", "lasp2_last_error", "lasp2_num_segments", "lasp2h_softmax_scratch_bytes"}
 
 

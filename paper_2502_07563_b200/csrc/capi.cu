@@ -131,6 +131,23 @@ int lasp2_causal_chunk(int dtype, const void* q, const void* k, const void* v, c
   return cuda_status(e, "causal_chunk");
 }
 
+int lasp2_dkdv_chunk(int dtype, const void* q, const void* k, const void* v, const void* d_out, const void* seg_states,
+                     const void* base, void* dk, void* dv, int64_t slots, int64_t tokens, int dim, int nseg,
+                     void* stream) {
+  CHECK(valid_dtype(dtype), "dkdv_chunk: unknown dtype");
+  CHECK(q && k && v && d_out && dk && dv, "dkdv_chunk: null pointer");
+  CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128, "dkdv_chunk: bad shape (1 <= dim <= 128)");
+  CHECK(nseg >= 1 && nseg <= (tokens + LASP_BLOCK_TOKENS - 1) / LASP_BLOCK_TOKENS, "dkdv_chunk: bad nseg");
+  CHECK(nseg == 1 || seg_states, "dkdv_chunk: nseg > 1 needs segment states");
+  if (use_tc(dtype, dim, tokens))
+    return cuda_status(lasp::tc_dkdv_pair(q, k, v, d_out, (const float*)seg_states, (const float*)base, dk, dv, slots,
+                                          tokens, dim, nseg, S(stream)),
+                       "dkdv_chunk");
+  int st = lasp2_causal_chunk(dtype, v, d_out, q, seg_states, base, dk, slots, tokens, dim, nseg, 1, 1, stream);
+  if (st != LASP2_OK) return st;
+  return lasp2_causal_chunk(dtype, k, q, d_out, seg_states, base, dv, slots, tokens, dim, nseg, 1, 0, stream);
+}
+
 int lasp2_apply_state(int dtype, const void* x, const void* m, void* out, int64_t slots, int64_t tokens, int dim,
                       int transpose, int accumulate, void* stream) {
   CHECK(valid_dtype(dtype), "apply_state: unknown dtype");

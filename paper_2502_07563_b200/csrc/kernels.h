@@ -43,6 +43,9 @@ cudaError_t tc_segment_states(const void* x, const void* y, float* out, int64_t 
 cudaError_t tc_causal_chunk(const void* q, const void* k, const void* v, const float* seg_states, const float* base,
                             void* out, int64_t slots, int64_t tokens, int dim, int nseg, int reverse,
                             int transpose_state, cudaStream_t s);
+cudaError_t tc_dkdv_pair(const void* q, const void* k, const void* v, const void* d_out, const float* seg_states,
+                         const float* base, void* dk, void* dv, int64_t slots, int64_t tokens, int dim, int nseg,
+                         cudaStream_t s);
 cudaError_t tc_apply_state(const void* x, const float* m, void* out, int64_t slots, int64_t tokens, int dim,
                            int transpose, int accumulate, int sm_count, cudaStream_t s);
 bool tc_softmax_supported(int dim, int64_t kv_chunk);

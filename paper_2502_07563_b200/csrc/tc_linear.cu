@@ -136,9 +136,20 @@ struct CausalArgs {
 
 constexpr int kCausalThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
 
+// kPair = false: one CTA per (slot, segment) computing causal_chunk(q, k, v).
+// kPair = true : a 2-CTA cluster per (slot, segment) computing the masked
+//   backward's dK (rank 0: anti-causal(V, dO, Q; G^T)) and dV (rank 1:
+//   anti-causal(K, Q, dO; G)) together. dO and Q are loaded once and TMA-
+//   multicast into both CTAs; ring slots are released by multicast
+//   tcgen05.commit from both CTAs (empty barriers count 2). HBM reads per
+//   block: V, K, dO, Q (4 tiles) instead of 6 for two separate passes.
+// Ring order per block: [a = q' (private), b, c]; single: (q, k, v);
+// pair: (V|K, dO, Q) with rank 0 using k'=b, v'=c and rank 1 k'=c, v'=b.
+template <bool kPair>
 __global__ void __launch_bounds__(kCausalThreads, 1)
-    tc_causal_chunk_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                           const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
+    tc_causal_chunk_kernel(const __grid_constant__ CUtensorMap tm_a0, const __grid_constant__ CUtensorMap tm_a1,
+                           const __grid_constant__ CUtensorMap tm_b, const __grid_constant__ CUtensorMap tm_c,
+                           const __grid_constant__ CUtensorMap tm_o0, const __grid_constant__ CUtensorMap tm_o1,
                            CausalArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -157,8 +168,11 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kRing + 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int seg = blockIdx.x;
+  const uint32_t role = kPair ? cluster_ctarank() : 0u;
+  const int seg = kPair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
   const int slot = blockIdx.y;
+  const int reverse = kPair ? 1 : a.reverse;
+  const int transpose_state = kPair ? (role == 0 ? 1 : 0) : a.transpose_state;
   int64_t lo, hi;
   seg_range(seg, a.nseg, a.tokens, &lo, &hi);
   const int nblk = (int)((hi - lo + kTile - 1) / kTile);
@@ -168,37 +182,50 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < kRing; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&empty[i], kPair ? 2 : 1);
     }
     for (int i = 0; i < 8; ++i) mbar_init(&s_full[i], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   // TMEM: S [0,128), O[0] [128,256), running state [256,384), O[1] [384,512)
   const uint32_t t_s = tmem, t_st = tmem + 256;
   auto t_o = [&](int b) { return tmem + (b ? 384u : 128u); };
+  auto release = [&](int s) {
+    if constexpr (kPair) mma_commit_mc(&empty[s], 0x3); else mma_commit(&empty[s]);
+  };
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (elect_one()) {
-      prefetch_tmap(&tm_q);
-      prefetch_tmap(&tm_k);
-      prefetch_tmap(&tm_v);
-      prefetch_tmap(&tm_o);
-      const CUtensorMap* maps[3] = {&tm_q, &tm_k, &tm_v};
+      const CUtensorMap* maps[3] = {role == 0 ? &tm_a0 : &tm_a1, &tm_b, &tm_c};
+      for (int w = 0; w < 3; ++w) prefetch_tmap(maps[w]);
+      const uint32_t bytes = nbox * kBoxBytes;
       for (int jj = 0; jj < nblk; ++jj) {
-        const int j = a.reverse ? nblk - 1 - jj : jj;
+        const int j = reverse ? nblk - 1 - jj : jj;
         const int row = (int)(lo + (int64_t)j * kTile);
         for (int w = 0; w < 3; ++w) {
           const int t = 3 * jj + w, s = t % kRing, u = t / kRing;
           if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
           uint8_t* dst = ring + s * kTileBytes;
-          mbar_arrive_expect_tx(&full[s], nbox * kBoxBytes);
-          for (int bx = 0; bx < nbox; ++bx) tma_load_3d(dst + bx * kBoxBytes, maps[w], &full[s], 64 * bx, row, slot);
+          mbar_arrive_expect_tx(&full[s], bytes);
+          if (!kPair || w == 0) {
+            for (int bx = 0; bx < nbox; ++bx) tma_load_3d(dst + bx * kBoxBytes, maps[w], &full[s], 64 * bx, row, slot);
+          } else if ((int)role == w - 1) {  // rank 0 multicasts b (dO), rank 1 multicasts c (Q)
+            for (int bx = 0; bx < nbox; ++bx)
+              tma_load_3d_mc(dst + bx * kBoxBytes, maps[w], &full[s], 64 * bx, row, slot, 0x3);
+          }
+        }
+      }
+      if constexpr (kPair) {  // drain: both CTAs' final releases of every used slot have arrived here
+        const int total = 3 * nblk;
+        for (int s = 0; s < kRing && s < total; ++s) {
+          const int uses = (total - s + kRing - 1) / kRing;
+          mbar_wait(&empty[s], (uses - 1) & 1);
         }
       }
     }
@@ -209,14 +236,17 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
     constexpr uint32_t id_kv = idesc_bf16_f32(128, 128, 1, 1);  // S += K^T V
     constexpr uint32_t id_pv = idesc_bf16_f32(128, 128, 0, 1);  // O += P V
     const uint32_t simg_a = smem_u32(simg), pimg_a = smem_u32(pimg);
+    const bool swap = kPair && role == 1;  // rank 1: k' = c, v' = b
     for (int jj = 0; jj < nblk; ++jj) {
-      const int tq = 3 * jj, tk = tq + 1, tv = tq + 2;
-      const int sq = tq % kRing, sk = tk % kRing, sv = tv % kRing;
+      const int t0 = 3 * jj;
+      const int sq = t0 % kRing, sb = (t0 + 1) % kRing, sc = (t0 + 2) % kRing;
+      const int sk = swap ? sc : sb, sv = swap ? sb : sc;
+      const int tk = swap ? t0 + 2 : t0 + 1, tv = swap ? t0 + 1 : t0 + 2;
       const int ob = jj & 1;
       const uint32_t qa = smem_u32(ring + sq * kTileBytes);
       const uint32_t ka = smem_u32(ring + sk * kTileBytes);
       const uint32_t va = smem_u32(ring + sv * kTileBytes);
-      mbar_wait(&full[sq], (tq / kRing) & 1);
+      mbar_wait(&full[sq], (t0 / kRing) & 1);
       mbar_wait(&full[sk], (tk / kRing) & 1);
       if (jj > 0) mbar_wait(p_ready, (jj - 1) & 1);  // S tile drained by the epilogue
       tc_fence_after();
@@ -233,7 +263,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
 #pragma unroll
         for (int kk = 0; kk < kfeat; ++kk)
           mma_bf16_ss(t_o(ob), desc_kmajor(qa, kk), desc_mnmajor(simg_a, kk), id_qs, kk > 0);
-        mma_commit(&empty[sq]);
+        release(sq);
       }
       __syncwarp();
       mbar_wait(&full[sv], (tv / kRing) & 1);
@@ -244,7 +274,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
           for (int kk = 0; kk < 8; ++kk) mma_bf16_ss(t_st, desc_mnmajor(ka, kk), desc_mnmajor(va, kk), id_kv, 1u);
           mma_commit(st_full);
         }
-        mma_commit(&empty[sk]);
+        release(sk);
       }
       __syncwarp();
       mbar_wait(p_ready, jj & 1);
@@ -252,7 +282,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) mma_bf16_ss(t_o(ob), desc_kmajor(pimg_a, kk), desc_mnmajor(va, kk), id_pv, 1u);
-        mma_commit(&empty[sv]);
+        release(sv);
         mma_commit(&o_full[ob]);
       }
       __syncwarp();
@@ -268,6 +298,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
     constexpr uint32_t kEpi = kCausalThreads - 64;
     const int dim = a.dim;
     const int64_t dd = (int64_t)dim * dim;
+    const CUtensorMap* tm_o = role == 0 ? &tm_o0 : &tm_o1;
     // initial state S0 = base + seg_states[seg] (optionally transposed), rows beyond dim are zero
     {
       const float* st = a.seg_states ? a.seg_states + ((int64_t)slot * a.nseg + seg) * dd : nullptr;
@@ -280,7 +311,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
           const int c = c0 + i;
           float x = 0.f;
           if ((int)row < dim && c < dim) {
-            const int64_t src = a.transpose_state ? (int64_t)c * dim + row : (int64_t)row * dim + c;
+            const int64_t src = transpose_state ? (int64_t)c * dim + row : (int64_t)row * dim + c;
             if (bs) x += bs[src];
             if (st) x += st[src];
           }
@@ -298,9 +329,9 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       named_bar_sync(1, kEpi);
       if (et == 0) mbar_arrive(sst_ready);
     }
-    const int pmask = a.reverse ? 2 : 1;
+    const int pmask = reverse ? 2 : 1;
     for (int jj = 0; jj < nblk; ++jj) {
-      const int j = a.reverse ? nblk - 1 - jj : jj;
+      const int j = reverse ? nblk - 1 - jj : jj;
       const int ob = jj & 1;
       // ---- P = mask(S) -> smem (after the previous O tile left the staging buffer)
       mbar_wait(s_full, jj & 1);
@@ -332,14 +363,14 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       if (et == 0) {
         mbar_arrive(&o_empty[ob]);
         const int orow = (int)(lo + (int64_t)j * kTile);
-        for (int bx = 0; bx < nbox; ++bx) tma_store_3d(&tm_o, pimg + bx * kBoxBytes, 64 * bx, orow, slot);
+        for (int bx = 0; bx < nbox; ++bx) tma_store_3d(tm_o, pimg + bx * kBoxBytes, 64 * bx, orow, slot);
         tma_store_commit();
       }
     }
     if (et == 0) tma_store_wait_all<0>();
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair) cluster_sync(); else __syncthreads();
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
@@ -569,11 +600,40 @@ cudaError_t tc_causal_chunk(const void* q, const void* k, const void* v, const f
   if ((e = make_tmap_3d(&mk, k, slots, tokens, dim)) != cudaSuccess) return e;
   if ((e = make_tmap_3d(&mv, v, slots, tokens, dim)) != cudaSuccess) return e;
   if ((e = make_tmap_3d(&mo, out, slots, tokens, dim)) != cudaSuccess) return e;
-  if ((e = set_smem_once((const void*)tc::tc_causal_chunk_kernel, tc::kCausalSmem)) != cudaSuccess) return e;
+  if ((e = set_smem_once((const void*)tc::tc_causal_chunk_kernel<false>, tc::kCausalSmem)) != cudaSuccess) return e;
   tc::CausalArgs a{seg_states, base, tokens, dim, nseg, reverse, transpose_state};
   dim3 grid(nseg, (unsigned)slots);
-  tc::tc_causal_chunk_kernel<<<grid, tc::kCausalThreads, tc::kCausalSmem, s>>>(mq, mk, mv, mo, a);
+  tc::tc_causal_chunk_kernel<false><<<grid, tc::kCausalThreads, tc::kCausalSmem, s>>>(mq, mq, mk, mv, mo, mo, a);
   return cudaGetLastError();
+}
+
+// Masked backward dK and dV in one pass over (Q, K, V, dO): 2-CTA clusters.
+cudaError_t tc_dkdv_pair(const void* q, const void* k, const void* v, const void* d_out, const float* seg_states,
+                         const float* base, void* dk, void* dv, int64_t slots, int64_t tokens, int dim, int nseg,
+                         cudaStream_t s) {
+  CUtensorMap mq, mk, mv, mdo, mdk, mdv;
+  cudaError_t e;
+  if ((e = make_tmap_3d(&mq, q, slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = make_tmap_3d(&mk, k, slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = make_tmap_3d(&mv, v, slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = make_tmap_3d(&mdo, d_out, slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = make_tmap_3d(&mdk, dk, slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = make_tmap_3d(&mdv, dv, slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = set_smem_once((const void*)tc::tc_causal_chunk_kernel<true>, tc::kCausalSmem)) != cudaSuccess) return e;
+  tc::CausalArgs a{seg_states, base, tokens, dim, nseg, 1, 0};
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * nseg, (unsigned)slots);
+  cfg.blockDim = dim3(tc::kCausalThreads);
+  cfg.dynamicSmemBytes = tc::kCausalSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, tc::tc_causal_chunk_kernel<true>, mv, mk, mdo, mq, mdk, mdv, a);
 }
 
 cudaError_t tc_apply_state(const void* x, const float* m, void* out, int64_t slots, int64_t tokens, int dim,

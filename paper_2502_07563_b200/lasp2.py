@@ -18,7 +18,8 @@ Inside a GPU the chunk is split again into segments (one CTA per segment of a
     dM segments (Q, dO), suffix scan, all_gather(dM_t)   [in flight ...]
     dQ = causal(dO, V, K; S^T)                            [... during dQ]
     R = suffix fold(gathered, t+1)
-    dK = anti-causal(V, dO, Q; G^T), dV = anti-causal(K, Q, dO; G)
+    dK = anti-causal(V, dO, Q; G^T), dV = anti-causal(K, Q, dO; G)   -> lasp2_dkdv_chunk
+                                          (one 2-CTA cluster pass, Q/dO multicast)
 
 Precision follows the data dtype: bfloat16 runs the tcgen05/TMEM/TMA kernels
 with fp32 states; float32 / float64 run the exact validation kernels.
@@ -253,9 +254,8 @@ def _backward_masked_rank(ctx, cache: ActivationCache, d_out: torch.Tensor) -> G
                           reverse=False, transpose_state=True)
     gathered = _unpack_gathered(pending.wait(), g_t)
     r = ops.suffix_states(gathered, t + 1) if t < world - 1 else None
-    # dk_s = sum_{i>=s}(v_s.do_i) q_i + v_s G_s^T ; dv_s = sum_{i>=s}(k_s.q_i) do_i + k_s G_s
-    dk = ops.causal_chunk(v, do, q, gseg, r, nseg, reverse=True, transpose_state=True)
-    dv = ops.causal_chunk(k, q, do, gseg, r, nseg, reverse=True, transpose_state=False)
+    # dk_s = sum_{i>=s}(v_s.do_i) q_i + v_s G_s^T ; dv_s = sum_{i>=s}(k_s.q_i) do_i + k_s G_s  (one pass)
+    dk, dv = ops.dkdv_chunk(q, k, v, do, gseg, r, nseg)
     return GradientBundle(dq=dq, dk=dk, dv=dv)
 
 
@@ -425,6 +425,5 @@ def intra_backward(qc: torch.Tensor, kc: torch.Tensor, vc: torch.Tensor, d_out: 
     gseg = ops.segment_states(q, do, nseg)
     ops.scan_segments(gseg, reverse=True, data_dtype=q.dtype)
     dq = ops.causal_chunk(do, v, k, seg, None, nseg, reverse=False, transpose_state=True)
-    dk = ops.causal_chunk(v, do, q, gseg, None, nseg, reverse=True, transpose_state=True)
-    dv = ops.causal_chunk(k, q, do, gseg, None, nseg, reverse=True, transpose_state=False)
+    dk, dv = ops.dkdv_chunk(q, k, v, do, gseg, None, nseg)
     return GradientBundle(dq=dq, dk=dk, dv=dv)

@@ -100,6 +100,19 @@ def causal_chunk(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, seg_states: 
     return out
 
 
+def dkdv_chunk(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, d_out: torch.Tensor,
+               seg_states: torch.Tensor | None, base: torch.Tensor | None, nseg: int) -> tuple[torch.Tensor, torch.Tensor]:
+    """Masked backward dK, dV in one pass (header: lasp2_dkdv_chunk)."""
+    require_cuda(q, k, v, d_out, seg_states, base)
+    if not (q.shape == k.shape == v.shape == d_out.shape):
+        raise ValueError("q/k/v/d_out shapes differ")
+    slots, n, d = _slots(q)
+    dk, dv = torch.empty_like(k), torch.empty_like(v)
+    call("lasp2_dkdv_chunk", dtype_code(q.dtype), ptr(q), ptr(k), ptr(v), ptr(d_out), ptr(seg_states), ptr(base),
+         ptr(dk), ptr(dv), slots, n, d, nseg, stream_ptr())
+    return dk, dv
+
+
 def apply_state(x: torch.Tensor, m: torch.Tensor, transpose: bool = False,
                 out: torch.Tensor | None = None, accumulate: bool = False) -> torch.Tensor:
     """out (+)= x M or x M^T per slot (lasp2.py:150-165)."""

@@ -176,3 +176,20 @@ def test_ops_reject_cpu_and_noncontiguous():
     y = torch.zeros((1, 1, 128, 256), dtype=torch.bfloat16, device="cuda")[..., ::2]
     with pytest.raises(ValueError, match="contiguous"):
         ops.apply_state(y, torch.zeros((1, 1, 128, 128), device="cuda"))
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32, torch.float64])
+@pytest.mark.parametrize("shape,nseg", [((1, 2, 1024, 128), 3), ((2, 1, 1000, 64), 2), ((1, 3, 2048, 128), 9),
+                                        ((1, 1, 77, 128), 1)])
+def test_dkdv_pair_matches_two_passes(dtype, shape, nseg):
+    q, k, v, do = (rand(shape, dtype, s) for s in (21, 22, 23, 24))
+    b, h, n, d = shape
+    sd = _lib.state_dtype(dtype)
+    seg = rand((b, h, nseg, d, d), sd, 25, scale=30.0)
+    base = rand((b, h, d, d), sd, 26, scale=30.0)
+    dk, dv = ops.dkdv_chunk(q, k, v, do, seg, base, nseg)
+    rk = ref_causal(v, do, q, seg, base, nseg, True, True)
+    rv = ref_causal(k, q, do, seg, base, nseg, True, False)
+    tol = {torch.bfloat16: 5e-3, torch.float32: F32_TOL, torch.float64: F64_TOL}[dtype]
+    assert nerr(dk, rk) <= tol
+    assert nerr(dv, rv) <= tol

@@ -36,6 +36,8 @@ def main():
     print(f"scan(+clone) {t:.3f} ms")
     t = timeit(lambda: ops.causal_chunk(q, k, v, seg, None, nseg))
     print(f"causal_chunk {t:.3f} ms  {4 * unit / t * 1e3:.0f} GB/s")
+    t = timeit(lambda: ops.dkdv_chunk(q, k, v, do, seg, None, nseg))
+    print(f"dkdv_chunk (pair) {t:.3f} ms  {6 * unit / t * 1e3:.0f} GB/s")
     m = torch.randn((1, h, d, d), device="cuda")
     t = timeit(lambda: ops.apply_state(q, m))
     print(f"apply_state {t:.3f} ms  {2 * unit / t * 1e3:.0f} GB/s")
