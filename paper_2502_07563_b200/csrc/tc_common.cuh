@@ -53,48 +53,47 @@ __device__ __forceinline__ void st_row32_bf16(uint8_t* img, uint32_t row, uint32
   }
 }
 
-// Load a 128-column fp32 row from TMEM (this thread's lane) in four x32 pieces,
-// convert to bf16 (optionally causal-masked) and write into a SW128 image.
-// mask: 0 none, 1 keep col<=row, 2 keep col>=row.
-__device__ __forceinline__ void tmem_row_to_image(uint32_t taddr_lane, uint8_t* img, uint32_t row, int mask) {
+// Columns [c_begin, c_begin + ncols) (multiple of 32) of this thread's TMEM lane
+// -> bf16 -> SW128 image. MASK 1 keeps col <= row, MASK 2 keeps col >= row
+// (the diagonal 128x128 block of a causal / anti-causal chunk). The mask is
+// resolved per 32-column chunk and warp: fully kept / fully dropped chunks
+// skip the per-element test (and dropped chunks skip the TMEM load).
+template <int MASK>
+__device__ __forceinline__ void tmem_cols_to_image(uint32_t taddr_lane, uint8_t* img, uint32_t row, int c_begin,
+                                                   int ncols) {
+  const int r_lo = (int)(row & ~31u), r_hi = r_lo + 31;  // rows of this warp
 #pragma unroll 1
-  for (int c0 = 0; c0 < 128; c0 += 32) {
-    uint32_t r[32];
-    tmem_ld_32x32b_x32(taddr_lane + c0, r);
-    tmem_ld_wait();
+  for (int c0 = c_begin; c0 < c_begin + ncols; c0 += 32) {
     float v[32];
+    const bool all_drop = (MASK == 1 && c0 > r_hi) || (MASK == 2 && c0 + 31 < r_lo);
+    if (all_drop) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      float x = __uint_as_float(r[i]);
-      const int col = c0 + i;
-      if (mask == 1 && col > (int)row) x = 0.f;
-      if (mask == 2 && col < (int)row) x = 0.f;
-      v[i] = x;
+      for (int i = 0; i < 32; ++i) v[i] = 0.f;
+    } else {
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(taddr_lane + c0, r);
+      tmem_ld_wait();
+      const bool all_keep = MASK == 0 || (MASK == 1 && c0 + 31 <= r_lo) || (MASK == 2 && c0 >= r_hi);
+      if (all_keep) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+      } else {
+        const int lim = (int)row - c0;  // column index (within chunk) of the diagonal
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const bool keep = MASK == 1 ? (i <= lim) : (i >= lim);
+          v[i] = keep ? __uint_as_float(r[i]) : 0.f;
+        }
+      }
     }
     st_row32_bf16(img, row, c0, v);
   }
 }
 
-// Columns [c_begin, c_begin + ncols) (multiple of 32) of this thread's TMEM lane
-// -> bf16 (optionally causal-masked: 1 keep col<=row, 2 keep col>=row) -> SW128 image.
-__device__ __forceinline__ void tmem_cols_to_image(uint32_t taddr_lane, uint8_t* img, uint32_t row, int c_begin,
-                                                   int ncols, int mask) {
-#pragma unroll 1
-  for (int c0 = c_begin; c0 < c_begin + ncols; c0 += 32) {
-    uint32_t r[32];
-    tmem_ld_32x32b_x32(taddr_lane + c0, r);
-    tmem_ld_wait();
-    float v[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      float x = __uint_as_float(r[i]);
-      const int col = c0 + i;
-      if (mask == 1 && col > (int)row) x = 0.f;
-      if (mask == 2 && col < (int)row) x = 0.f;
-      v[i] = x;
-    }
-    st_row32_bf16(img, row, c0, v);
-  }
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
 }  // namespace tc

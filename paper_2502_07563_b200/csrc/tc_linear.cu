@@ -329,7 +329,6 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       named_bar_sync(1, kEpi);
       if (et == 0) mbar_arrive(sst_ready);
     }
-    const int pmask = reverse ? 2 : 1;
     for (int jj = 0; jj < nblk; ++jj) {
       const int j = reverse ? nblk - 1 - jj : jj;
       const int ob = jj & 1;
@@ -338,7 +337,10 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       tc_fence_after();
       if (jj > 0 && et == 0) tma_store_wait_read<0>();
       named_bar_sync(1, kEpi);
-      tmem_cols_to_image(t_s + lane_off, pimg, row, cb, 64, pmask);
+      if (reverse)
+        tmem_cols_to_image<2>(t_s + lane_off, pimg, row, cb, 64);
+      else
+        tmem_cols_to_image<1>(t_s + lane_off, pimg, row, cb, 64);
       fence_proxy_async_smem();
       tc_fence_before();
       named_bar_sync(1, kEpi);
@@ -347,7 +349,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       if (jj < nblk - 1) {
         mbar_wait(st_full, jj & 1);
         tc_fence_after();
-        tmem_cols_to_image(t_st + lane_off, simg, row, cb, 64, 0);
+        tmem_cols_to_image<0>(t_st + lane_off, simg, row, cb, 64);
         fence_proxy_async_smem();
         tc_fence_before();
         named_bar_sync(1, kEpi);
@@ -356,7 +358,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       // ---- O tile -> staging -> TMA store
       mbar_wait(&o_full[ob], (jj >> 1) & 1);
       tc_fence_after();
-      tmem_cols_to_image(t_o(ob) + lane_off, pimg, row, cb, 64, 0);
+      tmem_cols_to_image<0>(t_o(ob) + lane_off, pimg, row, cb, 64);
       fence_proxy_async_smem();
       tc_fence_before();
       named_bar_sync(1, kEpi);

@@ -20,7 +20,8 @@ namespace lasp {
 namespace tc {
 
 constexpr int kKvRing = 4;  // K/V tile slots
-constexpr uint32_t kSmFwdSmem = (1 + kKvRing + 2) * kTileBytes + 1024 + 256;
+constexpr uint32_t kSmFwdSmem = (1 + kKvRing + 2) * kTileBytes + 1024 + 256 + 1024;
+constexpr int kSmFwdThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 softmax (2 per TMEM lane quarter)
 
 struct SmFwdArgs {
   float* lse;
@@ -38,7 +39,7 @@ __device__ __forceinline__ void kv_coords(int64_t key0, int64_t chunk, int* row,
   *row = (int)(key0 % chunk);
 }
 
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kSmFwdThreads, 1)
     tc_softmax_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                           const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
                           SmFwdArgs a) {
@@ -56,6 +57,7 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* o_full = q_full + 5;   // [2]
   uint64_t* o_empty = q_full + 7;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + 9);
+  float* xchg = reinterpret_cast<float*>(bars + 32);  // [2][128] partial row statistics
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qt = blockIdx.x, slot = blockIdx.y;
@@ -138,97 +140,105 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else {
     // ---------------- softmax / epilogue warps ----------------
+    // warp w owns TMEM lanes 32*(w%4).. (query rows) and columns [64*half, +64)
     const int qd = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int cb = 64 * half;
     const uint32_t row = qd * 32 + lane;
     const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
     const int et = threadIdx.x - 64;
+    constexpr uint32_t kSm = kSmFwdThreads - 64;
     const int64_t gq = a.row_offset + q0 + row;  // global query position
-    float o_acc[128];
+    float o_acc[64];
 #pragma unroll
-    for (int i = 0; i < 128; ++i) o_acc[i] = 0.f;
+    for (int i = 0; i < 64; ++i) o_acc[i] = 0.f;
     float m_run = -INFINITY, l_run = 0.f, corr_pending = 1.f;
     for (int j = 0; j <= nkb; ++j) {
       float corr_this = 1.f;
       if (j < nkb) {
         const int b = j & 1;
+        const int64_t k0 = (int64_t)j * kTile;
+        int lim = (int)lmin(kTile, a.kvtok - k0) - cb;  // valid columns of this row within my half
+        if (a.causal) lim = (int)lmin((int64_t)lim, gq - k0 + 1 - cb);
+        const bool full = __all_sync(0xffffffffu, lim >= 64);
         mbar_wait(&s_full[b], (j >> 1) & 1);
         tc_fence_after();
-        const int64_t k0 = (int64_t)j * kTile;
-        const uint32_t ts = tmem + b * 128 + lane_off;
-        // pass 1: masked row max of this block
-        float bmax = -INFINITY;
-#pragma unroll 1
-        for (int c0 = 0; c0 < 128; c0 += 32) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(ts + c0, r);
-          tmem_ld_wait();
+        const uint32_t ts = tmem + b * 128 + lane_off + cb;
+        uint32_t sr[64];
+        tmem_ld_32x32b_x32(ts, *reinterpret_cast<uint32_t(*)[32]>(sr));
+        tmem_ld_32x32b_x32(ts + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
+        tmem_ld_wait();
+        float pm = -INFINITY;
+        if (full) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int64_t kg = k0 + c0 + i;
-            const bool ok = kg < a.kvtok && (!a.causal || kg <= gq);
-            if (ok) bmax = fmaxf(bmax, __uint_as_float(r[i]));
-          }
+          for (int i = 0; i < 64; ++i) pm = fmaxf(pm, __uint_as_float(sr[i]));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 64; ++i)
+            if (i < lim) pm = fmaxf(pm, __uint_as_float(sr[i]));
         }
+        xchg[half * 128 + row] = pm;
+        named_bar_sync(1, kSm);
+        const float bmax = fmaxf(pm, xchg[(1 - half) * 128 + row]);
         const float m_new = fmaxf(m_run, bmax * a.scale_log2);
-        corr_this = (m_run == -INFINITY) ? 0.f : exp2f(m_run - m_new);
-        // pass 2: p = exp2(s*scale - m_new), row sum, bf16 -> P image
+        corr_this = (m_run == -INFINITY) ? 0.f : ex2_approx(m_run - m_new);
         uint8_t* pb = pimg + b * kTileBytes;
         float psum = 0.f;
-#pragma unroll 1
-        for (int c0 = 0; c0 < 128; c0 += 32) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(ts + c0, r);
-          tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < 64; c += 32) {
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
-            const int64_t kg = k0 + c0 + i;
-            const bool ok = kg < a.kvtok && (!a.causal || kg <= gq);
-            const float p = ok ? exp2f(fmaf(__uint_as_float(r[i]), a.scale_log2, -m_new)) : 0.f;
+            const bool ok = full || c + i < lim;
+            const float p = ok ? ex2_approx(fmaf(__uint_as_float(sr[c + i]), a.scale_log2, -m_new)) : 0.f;
             psum += p;
             v[i] = p;
           }
-          st_row32_bf16(pb, row, c0, v);
+          st_row32_bf16(pb, row, cb + c, v);
         }
         l_run = l_run * corr_this + psum;
         m_run = m_new;
         fence_proxy_async_smem();
         tc_fence_before();
-        named_bar_sync(1, 128);
+        named_bar_sync(1, kSm);  // P complete; xchg may be rewritten
         if (et == 0) mbar_arrive(&p_ready[b]);
       }
-      if (j >= 1) {  // fold O_{j-1} into the register accumulator
+      if (j >= 1) {  // fold O_{j-1} (my 64 columns) into the register accumulator
         const int jb = j - 1, b = jb & 1;
         mbar_wait(&o_full[b], (jb >> 1) & 1);
         tc_fence_after();
-        const uint32_t to = tmem + 256 + b * 128 + lane_off;
+        const uint32_t to = tmem + 256 + b * 128 + lane_off + cb;
+        uint32_t r0[32], r1[32];
+        tmem_ld_32x32b_x32(to, r0);
+        tmem_ld_32x32b_x32(to + 32, r1);
+        tmem_ld_wait();
 #pragma unroll
-        for (int c0 = 0; c0 < 128; c0 += 32) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(to + c0, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) o_acc[c0 + i] = fmaf(o_acc[c0 + i], corr_pending, __uint_as_float(r[i]));
+        for (int i = 0; i < 32; ++i) {
+          o_acc[i] = fmaf(o_acc[i], corr_pending, __uint_as_float(r0[i]));
+          o_acc[32 + i] = fmaf(o_acc[32 + i], corr_pending, __uint_as_float(r1[i]));
         }
         tc_fence_before();
-        named_bar_sync(1, 128);
+        named_bar_sync(1, kSm);
         if (et == 0) mbar_arrive(&o_empty[b]);
       }
       corr_pending = corr_this;
     }
-    // epilogue: O / l -> bf16 -> staging (P[0] is free: every PV has completed) -> TMA store
-    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+    // epilogue: row sum over both halves, O / l -> bf16 -> staging (P[0], every PV done) -> TMA store
+    xchg[half * 128 + row] = l_run;
+    named_bar_sync(1, kSm);
+    const float l_tot = l_run + xchg[(1 - half) * 128 + row];
+    const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
 #pragma unroll
-    for (int c0 = 0; c0 < 128; c0 += 32) {
+    for (int c = 0; c < 64; c += 32) {
       float v[32];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = o_acc[c0 + i] * inv;
-      st_row32_bf16(pimg, row, c0, v);
+      for (int i = 0; i < 32; ++i) v[i] = o_acc[c + i] * inv;
+      st_row32_bf16(pimg, row, cb + c, v);
     }
-    if (q0 + row < a.qtok)
-      a.lse[(int64_t)slot * a.qtok + q0 + row] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
+    if (half == 0 && q0 + row < a.qtok)
+      a.lse[(int64_t)slot * a.qtok + q0 + row] = (m_run + __log2f(l_tot)) * 0.69314718055994531f;
     fence_proxy_async_smem();
-    named_bar_sync(1, 128);
+    named_bar_sync(1, kSm);
     if (et == 0) {
       for (int bx = 0; bx < nbox; ++bx) tma_store_3d(&tm_o, pimg + bx * kBoxBytes, 64 * bx, (int)q0, slot);
       tma_store_commit();
@@ -390,12 +400,24 @@ __global__ void __launch_bounds__(192, 1)
     const uint32_t row = qd * 32 + lane;
     const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
     const int et = threadIdx.x - 64;
+    auto row_stats = [&](int i, float* lse2, float* dl) {
+      const int64_t ql = (int64_t)(qb0 + i) * kTile + row;
+      const bool ok = i < nq && ql < a.qtok;
+      *lse2 = ok ? a.lse[(int64_t)slot * a.qtok + ql] * 1.4426950408889634f : 0.f;
+      *dl = ok ? a.delta[(int64_t)slot * a.qtok + ql] : 0.f;
+    };
+    float lse2_next, dl_next;
+    row_stats(0, &lse2_next, &dl_next);
     for (int i = 0; i < nq; ++i) {
       const int64_t qloc = (int64_t)(qb0 + i) * kTile + row;  // local query row of this thread
       const bool qok = qloc < a.qtok;
       const int64_t gq = a.row_offset + qloc;
-      const float lse2 = qok ? a.lse[(int64_t)slot * a.qtok + qloc] * 1.4426950408889634f : 0.f;
-      const float dl = qok ? a.delta[(int64_t)slot * a.qtok + qloc] : 0.f;
+      const float lse2 = lse2_next, dl = dl_next;
+      row_stats(i + 1, &lse2_next, &dl_next);  // prefetch the next block's row statistics
+      // valid key columns for this query row in this key block
+      int lim = qok ? (int)lmin(kTile, a.kvtok - k0) : 0;
+      if (a.causal) lim = (int)lmax(0, lmin((int64_t)lim, gq - k0 + 1));
+      const bool full_blk = __all_sync(0xffffffffu, lim >= kTile);
       mbar_wait(sdp_full, i & 1);
       tc_fence_after();
       // P/dS images are free: the previous block's dq_full (all its MMAs) was waited below
@@ -408,14 +430,13 @@ __global__ void __launch_bounds__(192, 1)
         float pv[32], dsv[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
-          const int64_t kg = k0 + c0 + e;
-          const bool ok = qok && kg < a.kvtok && (!a.causal || kg <= gq);
-          const float p = ok ? exp2f(fmaf(__uint_as_float(rs[e]), a.scale_log2, -lse2)) : 0.f;
+          const bool ok = full_blk || c0 + e < lim;
+          const float p = ok ? ex2_approx(fmaf(__uint_as_float(rs[e]), a.scale_log2, -lse2)) : 0.f;
           pv[e] = p;
           dsv[e] = p * (__uint_as_float(rp[e]) - dl);
         }
         st_row32_bf16(pimg, row, c0, pv);
-        st_row32_bf16(dsimg, row, c0, dsv);
+      st_row32_bf16(dsimg, row, c0, dsv);
       }
       fence_proxy_async_smem();
       tc_fence_before();
@@ -507,7 +528,7 @@ cudaError_t tc_softmax_forward(const void* q, const void* kf, const void* vf, vo
   if ((e = set_smem_once((const void*)tc::tc_softmax_fwd_kernel, tc::kSmFwdSmem)) != cudaSuccess) return e;
   tc::SmFwdArgs a{lse, qtok, kvtok, kv_chunk, row_offset, dim, causal, 1.4426950408889634f / sqrtf((float)dim)};
   dim3 grid((unsigned)((qtok + 127) / 128), (unsigned)slots);
-  tc::tc_softmax_fwd_kernel<<<grid, 192, tc::kSmFwdSmem, s>>>(mq, mk, mv, mo, a);
+  tc::tc_softmax_fwd_kernel<<<grid, tc::kSmFwdThreads, tc::kSmFwdSmem, s>>>(mq, mk, mv, mo, a);
   return cudaGetLastError();
 }
 
