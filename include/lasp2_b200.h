@@ -93,6 +93,16 @@ int lasp2_dkdv_chunk(int dtype, const void* q, const void* k, const void* v, con
 int lasp2_apply_state(int dtype, const void* x, const void* m, void* out, int64_t slots, int64_t tokens, int dim,
                       int transpose, int accumulate, void* stream);
 
+/* Unmasked backward, fused (lasp2.py:256-267): seg_states[slot][g] = Q_g^T dO_g
+ * (the dM segments, scanned by lasp2_scan_segments) and dq = dO M^T, reading Q and
+ * dO once. `m` = the forward's M_{1:T} (states dtype). */
+int lasp2_state_apply(int dtype, const void* q, const void* d_out, const void* m, void* seg_states, void* dq,
+                      int64_t slots, int64_t tokens, int dim, int nseg, void* stream);
+
+/* Unmasked backward dk = v dM^T and dv = k dM in one pass (lasp2.py:265-266). */
+int lasp2_apply_state2(int dtype, const void* v, const void* k, const void* dm, void* dk, void* dv, int64_t slots,
+                       int64_t tokens, int dim, void* stream);
+
 /* LASP-2H softmax attention of one chunk of queries (global rows
  * [row_offset, row_offset+q_tokens)) against full-length keys/values.
  * Full-length tensors may be rank-major as the collectives produce them:

@@ -167,6 +167,35 @@ int lasp2_apply_state(int dtype, const void* x, const void* m, void* out, int64_
   return cuda_status(e, "apply_state");
 }
 
+int lasp2_state_apply(int dtype, const void* q, const void* d_out, const void* m, void* seg_states, void* dq,
+                      int64_t slots, int64_t tokens, int dim, int nseg, void* stream) {
+  CHECK(valid_dtype(dtype), "state_apply: unknown dtype");
+  CHECK(q && d_out && m && seg_states && dq, "state_apply: null pointer");
+  CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128, "state_apply: bad shape (1 <= dim <= 128)");
+  CHECK(nseg >= 1 && nseg <= (tokens + LASP_BLOCK_TOKENS - 1) / LASP_BLOCK_TOKENS, "state_apply: bad nseg");
+  if (use_tc(dtype, dim, tokens))
+    return cuda_status(lasp::tc_state_apply(q, d_out, (const float*)m, (float*)seg_states, dq, slots, tokens, dim, nseg,
+                                            S(stream)),
+                       "state_apply");
+  int st = lasp2_segment_states(dtype, q, d_out, seg_states, slots, tokens, dim, nseg, stream);
+  if (st != LASP2_OK) return st;
+  return lasp2_apply_state(dtype, d_out, m, dq, slots, tokens, dim, 1, 0, stream);
+}
+
+int lasp2_apply_state2(int dtype, const void* v, const void* k, const void* dm, void* dk, void* dv, int64_t slots,
+                       int64_t tokens, int dim, void* stream) {
+  CHECK(valid_dtype(dtype), "apply_state2: unknown dtype");
+  CHECK(v && k && dm && dk && dv, "apply_state2: null pointer");
+  CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128, "apply_state2: bad shape (1 <= dim <= 128)");
+  if (use_tc(dtype, dim, tokens))
+    return cuda_status(lasp::tc_apply2(v, k, (const float*)dm, dk, dv, slots, tokens, dim, sm_count_current(),
+                                       S(stream)),
+                       "apply_state2");
+  int st = lasp2_apply_state(dtype, v, dm, dk, slots, tokens, dim, 1, 0, stream);
+  if (st != LASP2_OK) return st;
+  return lasp2_apply_state(dtype, k, dm, dv, slots, tokens, dim, 0, 0, stream);
+}
+
 int lasp2h_softmax_forward(int dtype, const void* q, const void* k_full, const void* v_full, void* out, void* lse,
                            int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim, int causal, int64_t row_offset,
                            int64_t kv_chunk, int64_t kv_rank_stride, void* stream) {

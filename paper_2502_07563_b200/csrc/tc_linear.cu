@@ -519,6 +519,200 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 // ============================================================================
+// Fused unmasked-backward kernels (8 epilogue warps, 64 columns each):
+//   MODE 0 (state_apply): seg[slot][g] = X0_g^T X1_g and out0 = X1 M^T
+//          -> dM segments (Q^T dO) and dQ = dO M^T reading Q, dO once
+//   MODE 1 (apply2)     : out0 = X0 M^T, out1 = X1 M
+//          -> dK = V dM^T and dV = K dM from one bf16 image of dM
+// (reference lasp2.py:256-267)
+// ============================================================================
+constexpr int kFusedThreads = 320;
+constexpr int kFusedStages = 2;  // each stage holds the two input tiles of one block
+constexpr uint32_t kFusedSmem = (2 * kFusedStages + 3) * kTileBytes + 1024 + 256;
+
+template <int MODE>
+__global__ void __launch_bounds__(kFusedThreads, 1)
+    tc_fused_apply_kernel(const __grid_constant__ CUtensorMap tm_x0, const __grid_constant__ CUtensorMap tm_x1,
+                          const __grid_constant__ CUtensorMap tm_o0, const __grid_constant__ CUtensorMap tm_o1,
+                          const float* __restrict__ m, float* __restrict__ seg_out, int64_t tokens, int dim, int nseg,
+                          int blocks_per_cta) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* ring = smem;                                    // [stage][2] tiles
+  uint8_t* mimg = ring + 2 * kFusedStages * kTileBytes;   // bf16 state image
+  uint8_t* stg = mimg + kTileBytes;                        // [2] output staging
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stg + 2 * kTileBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kFusedStages;
+  uint64_t* acc_full = bars + 2 * kFusedStages;       // [2]
+  uint64_t* acc_empty = bars + 2 * kFusedStages + 2;  // [2]
+  uint64_t* m_ready = bars + 2 * kFusedStages + 4;
+  uint64_t* g_full = bars + 2 * kFusedStages + 5;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kFusedStages + 6);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot = blockIdx.y;
+  int64_t b0, b1;
+  if (MODE == 0) {
+    int64_t lo, hi;
+    seg_range(blockIdx.x, nseg, tokens, &lo, &hi);
+    b0 = lo / kTile;
+    b1 = (hi + kTile - 1) / kTile;
+  } else {
+    const int64_t nblk_all = (tokens + kTile - 1) / kTile;
+    b0 = (int64_t)blockIdx.x * blocks_per_cta;
+    b1 = lmin(nblk_all, b0 + blocks_per_cta);
+  }
+  const int nblk = (int)lmax(0, b1 - b0);
+  const int nbox = dim > 64 ? 2 : 1;
+  const int kfeat = (dim + 15) / 16;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kFusedStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 6; ++i) mbar_init(&acc_full[i], 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // MODE 0: G [0,128), out0[2] at 128/256.  MODE 1: out0[2] at 0/128, out1[2] at 256/384.
+  auto t_out0 = [&](int b) { return tmem + (MODE == 0 ? 128u + 128u * b : 128u * b); };
+  auto t_out1 = [&](int b) { return tmem + 256u + 128u * b; };
+
+  if (warp == 0) {
+    if (elect_one()) {
+      prefetch_tmap(&tm_x0);
+      prefetch_tmap(&tm_x1);
+      for (int b = 0; b < nblk; ++b) {
+        const int s = b % kFusedStages, u = b / kFusedStages;
+        if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+        uint8_t* d0 = ring + (2 * s) * kTileBytes;
+        uint8_t* d1 = d0 + kTileBytes;
+        mbar_arrive_expect_tx(&full[s], 2 * nbox * kBoxBytes);
+        const int row = (int)((b0 + b) * kTile);
+        for (int bx = 0; bx < nbox; ++bx) {
+          tma_load_3d(d0 + bx * kBoxBytes, &tm_x0, &full[s], 64 * bx, row, slot);
+          tma_load_3d(d1 + bx * kBoxBytes, &tm_x1, &full[s], 64 * bx, row, slot);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t id_g = idesc_bf16_f32(128, 128, 1, 1);    // X0^T X1
+    constexpr uint32_t id_mt = idesc_bf16_f32(128, 128, 0, 0);   // X M^T (B = image K-major)
+    constexpr uint32_t id_m = idesc_bf16_f32(128, 128, 0, 1);    // X M   (B = image MN-major)
+    const uint32_t ma = smem_u32(mimg);
+    mbar_wait(m_ready, 0);
+    for (int b = 0; b < nblk; ++b) {
+      const int s = b % kFusedStages, u = b / kFusedStages;
+      const int buf = b & 1;
+      mbar_wait(&full[s], u & 1);
+      if (b >= 2) mbar_wait(&acc_empty[buf], ((b >> 1) - 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t x0 = smem_u32(ring + (2 * s) * kTileBytes), x1 = x0 + kTileBytes;
+        if (MODE == 0) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            mma_bf16_ss(tmem, desc_mnmajor(x0, kk), desc_mnmajor(x1, kk), id_g, (b > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < kfeat; ++kk)
+            mma_bf16_ss(t_out0(buf), desc_kmajor(x1, kk), desc_kmajor(ma, kk), id_mt, kk > 0);
+        } else {
+          for (int kk = 0; kk < kfeat; ++kk)
+            mma_bf16_ss(t_out0(buf), desc_kmajor(x0, kk), desc_kmajor(ma, kk), id_mt, kk > 0);
+          for (int kk = 0; kk < kfeat; ++kk)
+            mma_bf16_ss(t_out1(buf), desc_kmajor(x1, kk), desc_mnmajor(ma, kk), id_m, kk > 0);
+        }
+        mma_commit(&empty[s]);
+        mma_commit(&acc_full[buf]);
+        if (MODE == 0 && b == nblk - 1) mma_commit(g_full);
+      }
+      __syncwarp();
+    }
+  } else {
+    const int qd = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int cb = 64 * half;
+    const uint32_t row = qd * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
+    const int et = threadIdx.x - 64;
+    constexpr uint32_t kEpi = kFusedThreads - 64;
+    const int64_t dd = (int64_t)dim * dim;
+    const float* mb = m + (int64_t)slot * dd;
+#pragma unroll 1
+    for (int c0 = cb; c0 < cb + 64; c0 += 32) {
+      float v[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int c = c0 + i;
+        v[i] = ((int)row < dim && c < dim) ? mb[(int64_t)row * dim + c] : 0.f;
+      }
+      st_row32_bf16(mimg, row, c0, v);
+    }
+    fence_proxy_async_smem();
+    named_bar_sync(1, kEpi);
+    if (et == 0) mbar_arrive(m_ready);
+    for (int b = 0; b < nblk; ++b) {
+      const int buf = b & 1;
+      mbar_wait(&acc_full[buf], (b >> 1) & 1);
+      tc_fence_after();
+      if (et == 0) {
+        if (MODE == 0 && b >= 2) tma_store_wait_read<1>();
+        if (MODE == 1 && b >= 1) tma_store_wait_read<0>();
+      }
+      named_bar_sync(1, kEpi);
+      if (MODE == 0) {
+        tmem_cols_to_image<0>(t_out0(buf) + lane_off, stg + buf * kTileBytes, row, cb, 64);
+      } else {
+        tmem_cols_to_image<0>(t_out0(buf) + lane_off, stg, row, cb, 64);
+        tmem_cols_to_image<0>(t_out1(buf) + lane_off, stg + kTileBytes, row, cb, 64);
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      named_bar_sync(1, kEpi);
+      if (et == 0) {
+        mbar_arrive(&acc_empty[buf]);
+        const int orow = (int)((b0 + b) * kTile);
+        if (MODE == 0) {
+          for (int bx = 0; bx < nbox; ++bx)
+            tma_store_3d(&tm_o0, stg + buf * kTileBytes + bx * kBoxBytes, 64 * bx, orow, slot);
+        } else {
+          for (int bx = 0; bx < nbox; ++bx) {
+            tma_store_3d(&tm_o0, stg + bx * kBoxBytes, 64 * bx, orow, slot);
+            tma_store_3d(&tm_o1, stg + kTileBytes + bx * kBoxBytes, 64 * bx, orow, slot);
+          }
+        }
+        tma_store_commit();
+      }
+    }
+    if (MODE == 0 && nblk > 0) {  // segment state G -> fp32 [slot][seg][dim][dim]
+      mbar_wait(g_full, 0);
+      tc_fence_after();
+      float* ob = seg_out + ((int64_t)slot * nseg + blockIdx.x) * dd;
+#pragma unroll 1
+      for (int c0 = cb; c0 < cb + 64; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem + lane_off + c0, r);
+        tmem_ld_wait();
+        if ((int)row < dim) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (c0 + i < dim) ob[(int64_t)row * dim + c0 + i] = __uint_as_float(r[i]);
+        }
+      }
+    }
+    if (et == 0) tma_store_wait_all<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+// ============================================================================
 // Debug probe: D = op(A) op(B)^T for one 128x128x128 tile, to pin descriptor
 // conventions on hardware (a_mn / b_mn select MN-major interpretation).
 // ============================================================================
@@ -655,6 +849,43 @@ cudaError_t tc_apply_state(const void* x, const float* m, void* out, int64_t slo
   dim3 grid((unsigned)ctas, (unsigned)slots);
   tc::tc_apply_state_kernel<<<grid, 192, tc::kApplySmem, s>>>(mx, mo, m, (__nv_bfloat16*)out, tokens, dim,
                                                               transpose, accumulate, bpc);
+  return cudaGetLastError();
+}
+
+// Unmasked backward, fused: dM segment states (Q^T dO) and dQ = dO M^T in one pass.
+cudaError_t tc_state_apply(const void* x0, const void* x1, const float* m, float* seg_out, void* out, int64_t slots,
+                           int64_t tokens, int dim, int nseg, cudaStream_t s) {
+  CUtensorMap m0, m1, mo;
+  cudaError_t e;
+  if ((e = make_tmap_3d(&m0, x0, slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = make_tmap_3d(&m1, x1, slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = make_tmap_3d(&mo, out, slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = set_smem_once((const void*)tc::tc_fused_apply_kernel<0>, tc::kFusedSmem)) != cudaSuccess) return e;
+  dim3 grid(nseg, (unsigned)slots);
+  tc::tc_fused_apply_kernel<0><<<grid, tc::kFusedThreads, tc::kFusedSmem, s>>>(m0, m1, mo, mo, m, seg_out, tokens,
+                                                                              dim, nseg, 0);
+  return cudaGetLastError();
+}
+
+// Unmasked backward dK = V dM^T and dV = K dM in one pass.
+cudaError_t tc_apply2(const void* x0, const void* x1, const float* m, void* out0, void* out1, int64_t slots,
+                      int64_t tokens, int dim, int sm_count, cudaStream_t s) {
+  CUtensorMap m0, m1, mo0, mo1;
+  cudaError_t e;
+  if ((e = make_tmap_3d(&m0, x0, slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = make_tmap_3d(&m1, x1, slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = make_tmap_3d(&mo0, out0, slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = make_tmap_3d(&mo1, out1, slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = set_smem_once((const void*)tc::tc_fused_apply_kernel<1>, tc::kFusedSmem)) != cudaSuccess) return e;
+  const int64_t nblk = (tokens + tc::kTile - 1) / tc::kTile;
+  int64_t ctas = sm_count / slots;
+  if (ctas < 1) ctas = 1;
+  if (ctas > nblk) ctas = nblk;
+  const int bpc = (int)((nblk + ctas - 1) / ctas);
+  ctas = (nblk + bpc - 1) / bpc;
+  dim3 grid((unsigned)ctas, (unsigned)slots);
+  tc::tc_fused_apply_kernel<1><<<grid, tc::kFusedThreads, tc::kFusedSmem, s>>>(m0, m1, mo0, mo1, m, nullptr, tokens,
+                                                                              dim, 1, bpc);
   return cudaGetLastError();
 }
 

@@ -264,6 +264,7 @@ __global__ void __launch_bounds__(kSmFwdThreads, 1)
 // ============================================================================
 constexpr int kQRing = 3;
 constexpr uint32_t kSmBwdSmem = (2 + kQRing + 2) * kTileBytes + 1024 + 256;
+constexpr int kSmBwdThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9: one query row x 64 columns each
 
 struct SmBwdArgs {
   const float* lse;    // [slots][qtok] natural log
@@ -282,7 +283,7 @@ struct SmBwdArgs {
   float scale_log2;  // log2(e)/sqrt(d)
 };
 
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kSmBwdThreads, 1)
     tc_softmax_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                           const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                           SmBwdArgs a) {
@@ -397,9 +398,12 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else {
     const int qd = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int cb = 64 * half;
     const uint32_t row = qd * 32 + lane;
     const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
     const int et = threadIdx.x - 64;
+    constexpr uint32_t kSm = kSmBwdThreads - 64;
     auto row_stats = [&](int i, float* lse2, float* dl) {
       const int64_t ql = (int64_t)(qb0 + i) * kTile + row;
       const bool ok = i < nq && ql < a.qtok;
@@ -414,40 +418,48 @@ __global__ void __launch_bounds__(192, 1)
       const int64_t gq = a.row_offset + qloc;
       const float lse2 = lse2_next, dl = dl_next;
       row_stats(i + 1, &lse2_next, &dl_next);  // prefetch the next block's row statistics
-      // valid key columns for this query row in this key block
-      int lim = qok ? (int)lmin(kTile, a.kvtok - k0) : 0;
-      if (a.causal) lim = (int)lmax(0, lmin((int64_t)lim, gq - k0 + 1));
-      const bool full_blk = __all_sync(0xffffffffu, lim >= kTile);
+      // valid key columns (within my 64-column half) for this query row
+      int lim = qok ? (int)lmin(kTile, a.kvtok - k0) - cb : 0;
+      if (a.causal) lim = (int)lmin((int64_t)lim, gq - k0 + 1 - cb);
+      const bool full = __all_sync(0xffffffffu, lim >= 64);
+      const bool none = __all_sync(0xffffffffu, lim <= 0);
       mbar_wait(sdp_full, i & 1);
       tc_fence_after();
       // P/dS images are free: the previous block's dq_full (all its MMAs) was waited below
 #pragma unroll 1
-      for (int c0 = 0; c0 < 128; c0 += 32) {
-        uint32_t rs[32], rp[32];
-        tmem_ld_32x32b_x32(t_s + lane_off + c0, rs);
-        tmem_ld_32x32b_x32(t_dp + lane_off + c0, rp);
-        tmem_ld_wait();
+      for (int c = 0; c < 64; c += 32) {
+        const int c0 = cb + c;
         float pv[32], dsv[32];
+        if (none) {
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const bool ok = full_blk || c0 + e < lim;
-          const float p = ok ? ex2_approx(fmaf(__uint_as_float(rs[e]), a.scale_log2, -lse2)) : 0.f;
-          pv[e] = p;
-          dsv[e] = p * (__uint_as_float(rp[e]) - dl);
+          for (int e = 0; e < 32; ++e) pv[e] = dsv[e] = 0.f;
+        } else {
+          uint32_t rs[32], rp[32];
+          tmem_ld_32x32b_x32(t_s + lane_off + c0, rs);
+          tmem_ld_32x32b_x32(t_dp + lane_off + c0, rp);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const bool ok = full || c + e < lim;
+            const float p = ok ? ex2_approx(fmaf(__uint_as_float(rs[e]), a.scale_log2, -lse2)) : 0.f;
+            pv[e] = p;
+            dsv[e] = p * (__uint_as_float(rp[e]) - dl);
+          }
         }
         st_row32_bf16(pimg, row, c0, pv);
-      st_row32_bf16(dsimg, row, c0, dsv);
+        st_row32_bf16(dsimg, row, c0, dsv);
       }
       fence_proxy_async_smem();
       tc_fence_before();
-      named_bar_sync(1, 128);
+      named_bar_sync(1, kSm);
       if (et == 0) mbar_arrive(ds_ready);
-      // dQ partial -> fp32 global accumulator
+      // dQ partial (my 64 columns) -> fp32 global accumulator
       mbar_wait(dq_full, i & 1);
       tc_fence_after();
       float* dqr = a.dq_acc + ((int64_t)slot * a.qtok + qloc) * a.dim;
 #pragma unroll 1
-      for (int c0 = 0; c0 < 128; c0 += 32) {
+      for (int c = 0; c < 64; c += 32) {
+        const int c0 = cb + c;
         uint32_t r[32];
         tmem_ld_32x32b_x32(t_s + lane_off + c0, r);
         tmem_ld_wait();
@@ -463,23 +475,23 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
       tc_fence_before();
-      named_bar_sync(1, 128);
+      named_bar_sync(1, kSm);
       if (et == 0) mbar_arrive(dq_empty);
     }
-    // dK / dV rows of this key block (one key per thread) -> fp32 contributions
+    // dK / dV rows of this key block (one key per thread, my 64 columns) -> fp32 contributions
     const int64_t key = k0 + row;
     if (key < a.kvtok) {
       const int64_t off = (key / a.chunk) * a.grad_rank_stride + ((int64_t)slot * a.chunk + key % a.chunk) * a.dim;
       float* dkr = a.dk_full + off;
       float* dvr = a.dv_full + off;
       if (nq == 0) {
-        for (int c = 0; c < a.dim; c += 4) {
+        for (int c = cb; c < cb + 64 && c < a.dim; c += 4) {
           *reinterpret_cast<float4*>(dkr + c) = make_float4(0.f, 0.f, 0.f, 0.f);
           *reinterpret_cast<float4*>(dvr + c) = make_float4(0.f, 0.f, 0.f, 0.f);
         }
       } else {
 #pragma unroll 1
-        for (int c0 = 0; c0 < 128; c0 += 32) {
+        for (int c0 = cb; c0 < cb + 64; c0 += 32) {
           uint32_t rk[32], rv[32];
           tmem_ld_32x32b_x32(t_dk + lane_off + c0, rk);
           tmem_ld_32x32b_x32(t_dv + lane_off + c0, rv);
@@ -556,7 +568,7 @@ cudaError_t tc_softmax_backward(const void* q, const void* kf, const void* vf, c
   tc::SmBwdArgs a{lse, delta, dq_acc, dk_full, dv_full, qtok, kvtok, kv_chunk, grad_rank_stride, row_offset, dim,
                   causal, 1.f / sqrtf((float)dim), 1.4426950408889634f / sqrtf((float)dim)};
   dim3 grid((unsigned)((kvtok + 127) / 128), (unsigned)slots);
-  tc::tc_softmax_bwd_kernel<<<grid, 192, tc::kSmBwdSmem, s>>>(mq, mdo, mk, mv, a);
+  tc::tc_softmax_bwd_kernel<<<grid, tc::kSmBwdThreads, tc::kSmBwdSmem, s>>>(mq, mdo, mk, mv, a);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const int64_t n = slots * qtok * dim;
   tc::dq_finalize_kernel<<<(unsigned)lmin(148 * 16, (n + 255) / 256), 256, 0, s>>>(dq_acc, (__nv_bfloat16*)dq, n);

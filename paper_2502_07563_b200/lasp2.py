@@ -228,16 +228,34 @@ def _require_cache(cache: ActivationCache, masked: bool) -> None:
 
 
 def _backward_nomask_rank(ctx, cache: ActivationCache, d_out: torch.Tensor) -> GradientBundle:
-    """One all_gather of Q^T dO; full-sum reduction (lasp2.py:256-267)."""
+    """One all_gather of Q^T dO; full-sum reduction (lasp2.py:256-267).
+
+    When the all_gather is free (one rank) or cheap next to a pass over the
+    chunk, dQ = dO M^T is fused into the dM segment pass (Q and dO read once);
+    otherwise dQ runs while the collective is in flight. dK and dV share one pass.
+    """
     _require_cache(cache, masked=False)
     (do,) = _contig(d_out)
-    _, g_t, _ = ops.chunk_states(cache.q, do)
-    pending = _gather_states(ctx, g_t, "state_grad", async_op=True)
-    dq = ops.apply_state(do, cache.m_full, transpose=True)  # independent of the collective
-    dm_full = ops.sum_states(_unpack_gathered(pending.wait(), g_t))
-    dk = ops.apply_state(cache.v, dm_full, transpose=True)
-    dv = ops.apply_state(cache.k, dm_full)
+    q = cache.q
+    unit_bytes = q.numel() * q.element_size()
+    if ctx.sp_size == 1 or unit_bytes >= _FUSE_DQ_MIN_BYTES:
+        nseg = ops.num_segments(q)
+        gseg, dq = ops.state_apply(q, do, cache.m_full, nseg)
+        g_t = ops.scan_segments(gseg, reverse=False, data_dtype=q.dtype)
+        gathered = _unpack_gathered(_gather_states(ctx, g_t, "state_grad"), g_t)
+    else:
+        _, g_t, _ = ops.chunk_states(q, do)
+        pending = _gather_states(ctx, g_t, "state_grad", async_op=True)
+        dq = ops.apply_state(do, cache.m_full, transpose=True)  # independent of the collective
+        gathered = _unpack_gathered(pending.wait(), g_t)
+    dm_full = ops.sum_states(gathered)
+    dk, dv = ops.apply_state2(cache.v, cache.k, dm_full)
     return GradientBundle(dq=dq, dk=dk, dv=dv)
+
+
+# a bf16 chunk tensor of >= 256 MB takes >= ~40 us to stream, more than a
+# state all_gather costs, so fusing dQ into the dM pass wins even with T > 1
+_FUSE_DQ_MIN_BYTES = 256 << 20
 
 
 def _backward_masked_rank(ctx, cache: ActivationCache, d_out: torch.Tensor) -> GradientBundle:

@@ -129,6 +129,28 @@ def apply_state(x: torch.Tensor, m: torch.Tensor, transpose: bool = False,
     return out
 
 
+def state_apply(q: torch.Tensor, d_out: torch.Tensor, m: torch.Tensor, nseg: int) -> tuple[torch.Tensor, torch.Tensor]:
+    """(dM segment states Q^T dO, dq = dO M^T) in one pass (header: lasp2_state_apply)."""
+    require_cuda(q, d_out, m)
+    slots, n, d = _slots(q)
+    b, h = q.shape[:2]
+    seg = torch.empty((b, h, nseg, d, d), dtype=state_dtype(q.dtype), device=q.device)
+    dq = torch.empty_like(d_out)
+    call("lasp2_state_apply", dtype_code(q.dtype), ptr(q), ptr(d_out), ptr(m), ptr(seg), ptr(dq), slots, n, d, nseg,
+         stream_ptr())
+    return seg, dq
+
+
+def apply_state2(v: torch.Tensor, k: torch.Tensor, dm: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    """(dk = v dM^T, dv = k dM) in one pass (header: lasp2_apply_state2)."""
+    require_cuda(v, k, dm)
+    slots, n, d = _slots(v)
+    dk, dv = torch.empty_like(v), torch.empty_like(k)
+    call("lasp2_apply_state2", dtype_code(v.dtype), ptr(v), ptr(k), ptr(dm), ptr(dk), ptr(dv), slots, n, d,
+         stream_ptr())
+    return dk, dv
+
+
 def softmax_forward(q: torch.Tensor, k_full: torch.Tensor, v_full: torch.Tensor, causal: bool, row_offset: int,
                     kv_tokens: int, kv_chunk: int, kv_rank_stride: int) -> tuple[torch.Tensor, torch.Tensor]:
     """Softmax attention of a query chunk against (possibly rank-major) full K/V (oracle.py:136-139)."""

@@ -193,3 +193,20 @@ def test_dkdv_pair_matches_two_passes(dtype, shape, nseg):
     tol = {torch.bfloat16: 5e-3, torch.float32: F32_TOL, torch.float64: F64_TOL}[dtype]
     assert nerr(dk, rk) <= tol
     assert nerr(dv, rv) <= tol
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32, torch.float64])
+@pytest.mark.parametrize("shape", [(1, 2, 4096, 128), (2, 1, 700, 64), (1, 3, 300, 32)])
+def test_state_apply_and_apply2(dtype, shape):
+    q, do, v, k = (rand(shape, dtype, s) for s in (31, 32, 33, 34))
+    b, h, n, d = shape
+    nseg = max(1, min(3, (n + 127) // 128))
+    m = rand((b, h, d, d), _lib.state_dtype(dtype), 35, scale=10.0)
+    seg, dq = ops.state_apply(q, do, m, nseg)
+    tol_s = {torch.bfloat16: 1e-5, torch.float32: 1e-5, torch.float64: F64_TOL}[dtype]
+    tol_o = {torch.bfloat16: 5e-3, torch.float32: F32_TOL, torch.float64: F64_TOL}[dtype]
+    assert nerr(seg, ref_segment_states(q, do, nseg)) <= tol_s
+    assert nerr(dq, do.double() @ m.double().transpose(-1, -2)) <= tol_o
+    dk, dv = ops.apply_state2(v, k, m)
+    assert nerr(dk, v.double() @ m.double().transpose(-1, -2)) <= tol_o
+    assert nerr(dv, k.double() @ m.double()) <= tol_o
