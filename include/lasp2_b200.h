@@ -88,6 +88,18 @@ int lasp2_dkdv_chunk(int dtype, const void* q, const void* k, const void* v, con
                      const void* base, void* dk, void* dv, int64_t slots, int64_t tokens, int dim, int nseg,
                      void* stream);
 
+/* The whole masked backward of one rank's chunk in one launch (lasp2.py:270-285):
+ *   dq = causal(dO, V, K; state S^T),  S = fwd_base + fwd_seg (exclusive K^T V
+ *        segment prefixes; fwd_total is the chunk total), i.e. lasp2.py:277-279;
+ *   dk, dv as lasp2_dkdv_chunk with G from bwd_seg / bwd_base (lasp2.py:280-284).
+ * The bf16 path runs three CTAs per segment (dQ, dK, dV) that stream Q, K, V, dO
+ * in the same order so L2 absorbs the re-reads; dQ walks its segment backwards
+ * from the segment-end state, subtracting K^T V per block. */
+int lasp2_backward_chunk(int dtype, const void* q, const void* k, const void* v, const void* d_out,
+                         const void* fwd_seg, const void* fwd_total, const void* fwd_base, const void* bwd_seg,
+                         const void* bwd_base, void* dq, void* dk, void* dv, int64_t slots, int64_t tokens, int dim,
+                         int nseg, void* stream);
+
 /* out (+)= x M (transpose=0) or x M^T (transpose=1) per slot.
  * Replaces apply_state / apply_state_t (lasp2.py:150-165). */
 int lasp2_apply_state(int dtype, const void* x, const void* m, void* out, int64_t slots, int64_t tokens, int dim,

@@ -148,6 +148,25 @@ int lasp2_dkdv_chunk(int dtype, const void* q, const void* k, const void* v, con
   return lasp2_causal_chunk(dtype, k, q, d_out, seg_states, base, dv, slots, tokens, dim, nseg, 1, 0, stream);
 }
 
+int lasp2_backward_chunk(int dtype, const void* q, const void* k, const void* v, const void* d_out,
+                         const void* fwd_seg, const void* fwd_total, const void* fwd_base, const void* bwd_seg,
+                         const void* bwd_base, void* dq, void* dk, void* dv, int64_t slots, int64_t tokens, int dim,
+                         int nseg, void* stream) {
+  CHECK(valid_dtype(dtype), "backward_chunk: unknown dtype");
+  CHECK(q && k && v && d_out && dq && dk && dv && fwd_total, "backward_chunk: null pointer");
+  CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128, "backward_chunk: bad shape (1 <= dim <= 128)");
+  CHECK(nseg >= 1 && nseg <= (tokens + LASP_BLOCK_TOKENS - 1) / LASP_BLOCK_TOKENS, "backward_chunk: bad nseg");
+  CHECK(nseg == 1 || (fwd_seg && bwd_seg), "backward_chunk: nseg > 1 needs segment states");
+  if (use_tc(dtype, dim, tokens))
+    return cuda_status(lasp::tc_backward_triple(q, k, v, d_out, (const float*)fwd_seg, (const float*)fwd_total,
+                                                (const float*)fwd_base, (const float*)bwd_seg, (const float*)bwd_base,
+                                                dq, dk, dv, slots, tokens, dim, nseg, S(stream)),
+                       "backward_chunk");
+  int st = lasp2_causal_chunk(dtype, d_out, v, k, fwd_seg, fwd_base, dq, slots, tokens, dim, nseg, 0, 1, stream);
+  if (st != LASP2_OK) return st;
+  return lasp2_dkdv_chunk(dtype, q, k, v, d_out, bwd_seg, bwd_base, dk, dv, slots, tokens, dim, nseg, stream);
+}
+
 int lasp2_apply_state(int dtype, const void* x, const void* m, void* out, int64_t slots, int64_t tokens, int dim,
                       int transpose, int accumulate, void* stream) {
   CHECK(valid_dtype(dtype), "apply_state: unknown dtype");

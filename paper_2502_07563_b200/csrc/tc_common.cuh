@@ -58,7 +58,7 @@ __device__ __forceinline__ void st_row32_bf16(uint8_t* img, uint32_t row, uint32
 // (the diagonal 128x128 block of a causal / anti-causal chunk). The mask is
 // resolved per 32-column chunk and warp: fully kept / fully dropped chunks
 // skip the per-element test (and dropped chunks skip the TMEM load).
-template <int MASK>
+template <int MASK, bool NEG = false>
 __device__ __forceinline__ void tmem_cols_to_image(uint32_t taddr_lane, uint8_t* img, uint32_t row, int c_begin,
                                                    int ncols) {
   const int r_lo = (int)(row & ~31u), r_hi = r_lo + 31;  // rows of this warp
@@ -76,7 +76,7 @@ __device__ __forceinline__ void tmem_cols_to_image(uint32_t taddr_lane, uint8_t*
       const bool all_keep = MASK == 0 || (MASK == 1 && c0 + 31 <= r_lo) || (MASK == 2 && c0 >= r_hi);
       if (all_keep) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        for (int i = 0; i < 32; ++i) v[i] = NEG ? -__uint_as_float(r[i]) : __uint_as_float(r[i]);
       } else {
         const int lim = (int)row - c0;  // column index (within chunk) of the diagonal
 #pragma unroll

@@ -119,14 +119,18 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 // ============================================================================
-// Causal chunk kernel (one CTA per (slot, segment))
+// Causal chunk kernel family (tcgen05, one 128-token block per step)
 // ============================================================================
-constexpr int kRing = 5;  // tile slots for the Q/K/V stream
+constexpr int kRing = 5;  // tile slots for the q'/k'/v' stream
 constexpr uint32_t kCausalSmem = (kRing + 2) * kTileBytes + 1024 + 256;
 
 struct CausalArgs {
-  const float* seg_states;  // [slots][nseg][dim][dim] or null
-  const float* base;        // [slots][dim][dim] or null
+  const float* seg_states;  // [slots][nseg][dim][dim] exclusive segment states (or null)
+  const float* base;        // [slots][dim][dim] rank-level state (or null)
+  // backward-triple only: forward states for the dQ role (run in reverse by subtraction)
+  const float* fwd_seg;     // [slots][nseg][dim][dim] exclusive prefixes of K^T V
+  const float* fwd_total;   // [slots][dim][dim] chunk total of K^T V
+  const float* fwd_base;    // [slots][dim][dim] M_{1:t-1} (or null)
   int64_t tokens;
   int dim;
   int nseg;
@@ -134,23 +138,48 @@ struct CausalArgs {
   int transpose_state;
 };
 
+struct TileMaps {
+  CUtensorMap m[7];
+};
+
 constexpr int kCausalThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
 
-// kPair = false: one CTA per (slot, segment) computing causal_chunk(q, k, v).
-// kPair = true : a 2-CTA cluster per (slot, segment) computing the masked
-//   backward's dK (rank 0: anti-causal(V, dO, Q; G^T)) and dV (rank 1:
-//   anti-causal(K, Q, dO; G)) together. dO and Q are loaded once and TMA-
-//   multicast into both CTAs; ring slots are released by multicast
-//   tcgen05.commit from both CTAs (empty barriers count 2). HBM reads per
-//   block: V, K, dO, Q (4 tiles) instead of 6 for two separate passes.
-// Ring order per block: [a = q' (private), b, c]; single: (q, k, v);
-// pair: (V|K, dO, Q) with rank 0 using k'=b, v'=c and rank 1 k'=c, v'=b.
-template <bool kPair>
+// Per-CTA role: which maps feed q', k', v' and receive the output, how the
+// running state is seeded and updated, and which causal mask P gets.
+struct Role {
+  int qi, ki, vi, oi;   // indices into TileMaps
+  int reverse;          // block order (1: last block first)
+  int transpose;        // seed the state transposed
+  int subtract;         // state -= k'^T v' before the block (dQ run in reverse)
+  int mask;             // 1 keep col <= row, 2 keep col >= row
+  int mcast;            // kMode 1: which ring position (1 or 2) this CTA multicasts
+};
+
+// kMode 0: causal_chunk(q, k, v) -> o; maps [q, k, v, o].
+// kMode 1: 2-CTA cluster per segment, masked backward dK (rank 0) and dV (rank 1);
+//          maps [V, K, dO, Q, dK, dV]; dO and Q TMA-multicast to both CTAs and ring
+//          slots released by multicast tcgen05.commit (empty barriers count 2).
+// kMode 2: three CTAs per segment (blockIdx.x = 3*seg + role): dK, dV and dQ of the
+//          masked backward; maps [Q, K, V, dO, dQ, dK, dV]. The three CTAs stream
+//          the same four tiles in the same (reverse) order at the same time, so L2
+//          serves the re-reads: HBM sees Q, K, V, dO once. dQ is the causal
+//          forward form run backwards: TMEM holds T = -S, seeded with minus the
+//          segment-END state; each block adds K^T V (so T becomes minus the
+//          block-start state) and the state image is written as -T.
+template <int kMode>
+__device__ __forceinline__ Role causal_role(uint32_t role, const CausalArgs& a) {
+  if (kMode == 0) return Role{0, 1, 2, 3, a.reverse, a.transpose_state, 0, a.reverse ? 2 : 1, 0};
+  if (kMode == 1)
+    // ring positions are shared by both CTAs: 0 private (V | K), 1 = dO, 2 = Q; rank 1 swaps k'/v' at the MMA
+    return role == 0 ? Role{0, 2, 3, 4, 1, 1, 0, 2, 1} : Role{1, 2, 3, 5, 1, 0, 0, 2, 2};
+  if (role == 0) return Role{2, 3, 0, 5, 1, 1, 0, 2, 0};  // dK = anti-causal(V, dO, Q; G^T)
+  if (role == 1) return Role{1, 0, 3, 6, 1, 0, 0, 2, 0};  // dV = anti-causal(K, Q, dO; G)
+  return Role{3, 2, 1, 4, 1, 1, 1, 1, 0};                 // dQ = causal(dO, V, K; S^T), reversed
+}
+
+template <int kMode>
 __global__ void __launch_bounds__(kCausalThreads, 1)
-    tc_causal_chunk_kernel(const __grid_constant__ CUtensorMap tm_a0, const __grid_constant__ CUtensorMap tm_a1,
-                           const __grid_constant__ CUtensorMap tm_b, const __grid_constant__ CUtensorMap tm_c,
-                           const __grid_constant__ CUtensorMap tm_o0, const __grid_constant__ CUtensorMap tm_o1,
-                           CausalArgs a) {
+    tc_causal_chunk_kernel(const __grid_constant__ TileMaps tm, CausalArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* ring = smem;                                // kRing x 32 KB
@@ -168,11 +197,10 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kRing + 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t role = kPair ? cluster_ctarank() : 0u;
-  const int seg = kPair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const uint32_t role_id = kMode == 1 ? cluster_ctarank() : kMode == 2 ? blockIdx.x % 3 : 0u;
+  const int seg = kMode == 1 ? (int)(blockIdx.x >> 1) : kMode == 2 ? (int)(blockIdx.x / 3) : (int)blockIdx.x;
+  const Role R = causal_role<kMode>(role_id, a);
   const int slot = blockIdx.y;
-  const int reverse = kPair ? 1 : a.reverse;
-  const int transpose_state = kPair ? (role == 0 ? 1 : 0) : a.transpose_state;
   int64_t lo, hi;
   seg_range(seg, a.nseg, a.tokens, &lo, &hi);
   const int nblk = (int)((hi - lo + kTile - 1) / kTile);
@@ -182,46 +210,46 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < kRing; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], kPair ? 2 : 1);
+      mbar_init(&empty[i], kMode == 1 ? 2 : 1);
     }
     for (int i = 0; i < 8; ++i) mbar_init(&s_full[i], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
-  if constexpr (kPair) cluster_sync(); else __syncthreads();
+  if constexpr (kMode == 1) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   // TMEM: S [0,128), O[0] [128,256), running state [256,384), O[1] [384,512)
   const uint32_t t_s = tmem, t_st = tmem + 256;
   auto t_o = [&](int b) { return tmem + (b ? 384u : 128u); };
   auto release = [&](int s) {
-    if constexpr (kPair) mma_commit_mc(&empty[s], 0x3); else mma_commit(&empty[s]);
+    if constexpr (kMode == 1) mma_commit_mc(&empty[s], 0x3); else mma_commit(&empty[s]);
   };
 
   if (warp == 0) {
-    // ---------------- TMA producer ----------------
+    // ---------------- TMA producer: ring order per block = q', k', v' ----------------
     if (elect_one()) {
-      const CUtensorMap* maps[3] = {role == 0 ? &tm_a0 : &tm_a1, &tm_b, &tm_c};
+      const CUtensorMap* maps[3] = {&tm.m[R.qi], &tm.m[R.ki], &tm.m[R.vi]};
       for (int w = 0; w < 3; ++w) prefetch_tmap(maps[w]);
       const uint32_t bytes = nbox * kBoxBytes;
       for (int jj = 0; jj < nblk; ++jj) {
-        const int j = reverse ? nblk - 1 - jj : jj;
+        const int j = R.reverse ? nblk - 1 - jj : jj;
         const int row = (int)(lo + (int64_t)j * kTile);
         for (int w = 0; w < 3; ++w) {
           const int t = 3 * jj + w, s = t % kRing, u = t / kRing;
           if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
           uint8_t* dst = ring + s * kTileBytes;
           mbar_arrive_expect_tx(&full[s], bytes);
-          if (!kPair || w == 0) {
+          if (kMode != 1 || w == 0) {
             for (int bx = 0; bx < nbox; ++bx) tma_load_3d(dst + bx * kBoxBytes, maps[w], &full[s], 64 * bx, row, slot);
-          } else if ((int)role == w - 1) {  // rank 0 multicasts b (dO), rank 1 multicasts c (Q)
+          } else if (R.mcast == w) {  // kMode 1: rank 0 multicasts dO, rank 1 multicasts Q
             for (int bx = 0; bx < nbox; ++bx)
               tma_load_3d_mc(dst + bx * kBoxBytes, maps[w], &full[s], 64 * bx, row, slot, 0x3);
           }
         }
       }
-      if constexpr (kPair) {  // drain: both CTAs' final releases of every used slot have arrived here
+      if constexpr (kMode == 1) {  // drain: both CTAs' final releases of every used slot have arrived here
         const int total = 3 * nblk;
         for (int s = 0; s < kRing && s < total; ++s) {
           const int uses = (total - s + kRing - 1) / kRing;
@@ -236,7 +264,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
     constexpr uint32_t id_kv = idesc_bf16_f32(128, 128, 1, 1);  // S += K^T V
     constexpr uint32_t id_pv = idesc_bf16_f32(128, 128, 0, 1);  // O += P V
     const uint32_t simg_a = smem_u32(simg), pimg_a = smem_u32(pimg);
-    const bool swap = kPair && role == 1;  // rank 1: k' = c, v' = b
+    const bool swap = kMode == 1 && R.mcast == 2;  // kMode 1 rank 1: ring positions of k', v' swapped
     for (int jj = 0; jj < nblk; ++jj) {
       const int t0 = 3 * jj;
       const int sq = t0 % kRing, sb = (t0 + 1) % kRing, sc = (t0 + 2) % kRing;
@@ -256,7 +284,20 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
         mma_commit(s_full);
       }
       __syncwarp();
-      mbar_wait(sst_ready, jj & 1);
+      if (R.subtract) {  // T = -S: T += k'^T v' first; the epilogue then images -T for this block
+        mbar_wait(&full[sv], (tv / kRing) & 1);
+        if (jj == 0) mbar_wait(sst_ready, 0);  // the seed (tcgen05.st of -S_end) has landed
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            mma_bf16_ss(t_st, desc_mnmajor(ka, kk), desc_mnmajor(va, kk), id_kv, 1u);
+          mma_commit(st_full);
+          release(sk);
+        }
+        __syncwarp();
+      }
+      mbar_wait(sst_ready, (jj + (R.subtract ? 1 : 0)) & 1);  // subtract form: arrival 0 is the seed
       if (jj >= 2) mbar_wait(&o_empty[ob], ((jj >> 1) - 1) & 1);
       tc_fence_after();
       if (elect_one()) {
@@ -266,17 +307,19 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
         release(sq);
       }
       __syncwarp();
-      mbar_wait(&full[sv], (tv / kRing) & 1);
-      tc_fence_after();
-      if (elect_one()) {
-        if (jj < nblk - 1) {
+      if (!R.subtract) {
+        mbar_wait(&full[sv], (tv / kRing) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          if (jj < nblk - 1) {
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) mma_bf16_ss(t_st, desc_mnmajor(ka, kk), desc_mnmajor(va, kk), id_kv, 1u);
-          mma_commit(st_full);
+            for (int kk = 0; kk < 8; ++kk) mma_bf16_ss(t_st, desc_mnmajor(ka, kk), desc_mnmajor(va, kk), id_kv, 1u);
+            mma_commit(st_full);
+          }
+          release(sk);
         }
-        release(sk);
+        __syncwarp();
       }
-      __syncwarp();
       mbar_wait(p_ready, jj & 1);
       tc_fence_after();
       if (elect_one()) {
@@ -298,11 +341,19 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
     constexpr uint32_t kEpi = kCausalThreads - 64;
     const int dim = a.dim;
     const int64_t dd = (int64_t)dim * dim;
-    const CUtensorMap* tm_o = role == 0 ? &tm_o0 : &tm_o1;
-    // initial state S0 = base + seg_states[seg] (optionally transposed), rows beyond dim are zero
+    const CUtensorMap* tm_o = &tm.m[R.oi];
+    // initial state (optionally transposed); rows/cols beyond dim are zero
+    //   forward form : base + seg_states[seg]                (state at the segment start)
+    //   subtract form: fwd_base + fwd prefix of segment seg+1 (state at the segment end)
     {
-      const float* st = a.seg_states ? a.seg_states + ((int64_t)slot * a.nseg + seg) * dd : nullptr;
-      const float* bs = a.base ? a.base + (int64_t)slot * dd : nullptr;
+      const float *st, *bs;
+      if (R.subtract) {
+        st = seg + 1 < a.nseg ? a.fwd_seg + ((int64_t)slot * a.nseg + seg + 1) * dd : a.fwd_total + (int64_t)slot * dd;
+        bs = a.fwd_base ? a.fwd_base + (int64_t)slot * dd : nullptr;
+      } else {
+        st = a.seg_states ? a.seg_states + ((int64_t)slot * a.nseg + seg) * dd : nullptr;
+        bs = a.base ? a.base + (int64_t)slot * dd : nullptr;
+      }
 #pragma unroll 1
       for (int c0 = cb; c0 < cb + 64; c0 += 32) {
         float v[32];
@@ -311,7 +362,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
           const int c = c0 + i;
           float x = 0.f;
           if ((int)row < dim && c < dim) {
-            const int64_t src = transpose_state ? (int64_t)c * dim + row : (int64_t)row * dim + c;
+            const int64_t src = R.transpose ? (int64_t)c * dim + row : (int64_t)row * dim + c;
             if (bs) x += bs[src];
             if (st) x += st[src];
           }
@@ -319,25 +370,35 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
         }
         uint32_t r[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(v[i]);
+        for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(R.subtract ? -v[i] : v[i]);
         tmem_st_32x32b_x32(t_st + lane_off + c0, r);
-        st_row32_bf16(simg, row, c0, v);
+        if (!R.subtract) st_row32_bf16(simg, row, c0, v);
       }
       tmem_st_wait();
       fence_proxy_async_smem();
       tc_fence_before();
       named_bar_sync(1, kEpi);
-      if (et == 0) mbar_arrive(sst_ready);
+      if (et == 0) mbar_arrive(sst_ready);  // forward form: image of block 0; subtract form: seed landed
     }
     for (int jj = 0; jj < nblk; ++jj) {
-      const int j = reverse ? nblk - 1 - jj : jj;
+      const int j = R.reverse ? nblk - 1 - jj : jj;
       const int ob = jj & 1;
+      // ---- subtract form: this block's (post-subtraction) state image comes first
+      if (R.subtract) {
+        mbar_wait(st_full, jj & 1);
+        tc_fence_after();
+        tmem_cols_to_image<0, true>(t_st + lane_off, simg, row, cb, 64);
+        fence_proxy_async_smem();
+        tc_fence_before();
+        named_bar_sync(1, kEpi);
+        if (et == 0) mbar_arrive(sst_ready);
+      }
       // ---- P = mask(S) -> smem (after the previous O tile left the staging buffer)
       mbar_wait(s_full, jj & 1);
       tc_fence_after();
       if (jj > 0 && et == 0) tma_store_wait_read<0>();
       named_bar_sync(1, kEpi);
-      if (reverse)
+      if (R.mask == 2)
         tmem_cols_to_image<2>(t_s + lane_off, pimg, row, cb, 64);
       else
         tmem_cols_to_image<1>(t_s + lane_off, pimg, row, cb, 64);
@@ -345,8 +406,8 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       tc_fence_before();
       named_bar_sync(1, kEpi);
       if (et == 0) mbar_arrive(p_ready);
-      // ---- next block's state image
-      if (jj < nblk - 1) {
+      // ---- forward form: next block's state image
+      if (!R.subtract && jj < nblk - 1) {
         mbar_wait(st_full, jj & 1);
         tc_fence_after();
         tmem_cols_to_image<0>(t_st + lane_off, simg, row, cb, 64);
@@ -372,7 +433,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
     if (et == 0) tma_store_wait_all<0>();
   }
   tc_fence_before();
-  if constexpr (kPair) cluster_sync(); else __syncthreads();
+  if constexpr (kMode == 1) cluster_sync(); else __syncthreads();
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
@@ -790,16 +851,15 @@ cudaError_t tc_segment_states(const void* x, const void* y, float* out, int64_t 
 cudaError_t tc_causal_chunk(const void* q, const void* k, const void* v, const float* seg_states, const float* base,
                             void* out, int64_t slots, int64_t tokens, int dim, int nseg, int reverse,
                             int transpose_state, cudaStream_t s) {
-  CUtensorMap mq, mk, mv, mo;
+  tc::TileMaps tm;
   cudaError_t e;
-  if ((e = make_tmap_3d(&mq, q, slots, tokens, dim)) != cudaSuccess) return e;
-  if ((e = make_tmap_3d(&mk, k, slots, tokens, dim)) != cudaSuccess) return e;
-  if ((e = make_tmap_3d(&mv, v, slots, tokens, dim)) != cudaSuccess) return e;
-  if ((e = make_tmap_3d(&mo, out, slots, tokens, dim)) != cudaSuccess) return e;
-  if ((e = set_smem_once((const void*)tc::tc_causal_chunk_kernel<false>, tc::kCausalSmem)) != cudaSuccess) return e;
-  tc::CausalArgs a{seg_states, base, tokens, dim, nseg, reverse, transpose_state};
+  const void* ptrs[4] = {q, k, v, out};
+  for (int i = 0; i < 4; ++i)
+    if ((e = make_tmap_3d(&tm.m[i], ptrs[i], slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = set_smem_once((const void*)tc::tc_causal_chunk_kernel<0>, tc::kCausalSmem)) != cudaSuccess) return e;
+  tc::CausalArgs a{seg_states, base, nullptr, nullptr, nullptr, tokens, dim, nseg, reverse, transpose_state};
   dim3 grid(nseg, (unsigned)slots);
-  tc::tc_causal_chunk_kernel<false><<<grid, tc::kCausalThreads, tc::kCausalSmem, s>>>(mq, mq, mk, mv, mo, mo, a);
+  tc::tc_causal_chunk_kernel<0><<<grid, tc::kCausalThreads, tc::kCausalSmem, s>>>(tm, a);
   return cudaGetLastError();
 }
 
@@ -807,16 +867,13 @@ cudaError_t tc_causal_chunk(const void* q, const void* k, const void* v, const f
 cudaError_t tc_dkdv_pair(const void* q, const void* k, const void* v, const void* d_out, const float* seg_states,
                          const float* base, void* dk, void* dv, int64_t slots, int64_t tokens, int dim, int nseg,
                          cudaStream_t s) {
-  CUtensorMap mq, mk, mv, mdo, mdk, mdv;
+  tc::TileMaps tm;
   cudaError_t e;
-  if ((e = make_tmap_3d(&mq, q, slots, tokens, dim)) != cudaSuccess) return e;
-  if ((e = make_tmap_3d(&mk, k, slots, tokens, dim)) != cudaSuccess) return e;
-  if ((e = make_tmap_3d(&mv, v, slots, tokens, dim)) != cudaSuccess) return e;
-  if ((e = make_tmap_3d(&mdo, d_out, slots, tokens, dim)) != cudaSuccess) return e;
-  if ((e = make_tmap_3d(&mdk, dk, slots, tokens, dim)) != cudaSuccess) return e;
-  if ((e = make_tmap_3d(&mdv, dv, slots, tokens, dim)) != cudaSuccess) return e;
-  if ((e = set_smem_once((const void*)tc::tc_causal_chunk_kernel<true>, tc::kCausalSmem)) != cudaSuccess) return e;
-  tc::CausalArgs a{seg_states, base, tokens, dim, nseg, 1, 0};
+  const void* ptrs[6] = {v, k, d_out, q, dk, dv};
+  for (int i = 0; i < 6; ++i)
+    if ((e = make_tmap_3d(&tm.m[i], ptrs[i], slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = set_smem_once((const void*)tc::tc_causal_chunk_kernel<1>, tc::kCausalSmem)) != cudaSuccess) return e;
+  tc::CausalArgs a{seg_states, base, nullptr, nullptr, nullptr, tokens, dim, nseg, 1, 0};
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * nseg, (unsigned)slots);
   cfg.blockDim = dim3(tc::kCausalThreads);
@@ -829,7 +886,24 @@ cudaError_t tc_dkdv_pair(const void* q, const void* k, const void* v, const void
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, tc::tc_causal_chunk_kernel<true>, mv, mk, mdo, mq, mdk, mdv, a);
+  return cudaLaunchKernelEx(&cfg, tc::tc_causal_chunk_kernel<1>, tm, a);
+}
+
+// Masked backward dQ, dK, dV in one launch: three CTAs per segment sharing tiles through L2.
+cudaError_t tc_backward_triple(const void* q, const void* k, const void* v, const void* d_out, const float* fwd_seg,
+                               const float* fwd_total, const float* fwd_base, const float* bwd_seg,
+                               const float* bwd_base, void* dq, void* dk, void* dv, int64_t slots, int64_t tokens,
+                               int dim, int nseg, cudaStream_t s) {
+  tc::TileMaps tm;
+  cudaError_t e;
+  const void* ptrs[7] = {q, k, v, d_out, dq, dk, dv};
+  for (int i = 0; i < 7; ++i)
+    if ((e = make_tmap_3d(&tm.m[i], ptrs[i], slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = set_smem_once((const void*)tc::tc_causal_chunk_kernel<2>, tc::kCausalSmem)) != cudaSuccess) return e;
+  tc::CausalArgs a{bwd_seg, bwd_base, fwd_seg, fwd_total, fwd_base, tokens, dim, nseg, 1, 0};
+  dim3 grid(3 * nseg, (unsigned)slots);
+  tc::tc_causal_chunk_kernel<2><<<grid, tc::kCausalThreads, tc::kCausalSmem, s>>>(tm, a);
+  return cudaGetLastError();
 }
 
 cudaError_t tc_apply_state(const void* x, const float* m, void* out, int64_t slots, int64_t tokens, int dim,

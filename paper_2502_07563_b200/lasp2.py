@@ -18,8 +18,8 @@ Inside a GPU the chunk is split again into segments (one CTA per segment of a
     dM segments (Q, dO), suffix scan, all_gather(dM_t)   [in flight ...]
     dQ = causal(dO, V, K; S^T)                            [... during dQ]
     R = suffix fold(gathered, t+1)
-    dK = anti-causal(V, dO, Q; G^T), dV = anti-causal(K, Q, dO; G)   -> lasp2_dkdv_chunk
-                                          (one 2-CTA cluster pass, Q/dO multicast)
+    dK = anti-causal(V, dO, Q; G^T), dV = anti-causal(K, Q, dO; G)  -> lasp2_dkdv_chunk
+    (or all three in one launch: lasp2_backward_chunk, MASKED_BWD_FUSED)
 
 Precision follows the data dtype: bfloat16 runs the tcgen05/TMEM/TMA kernels
 with fp32 states; float32 / float64 run the exact validation kernels.
@@ -130,6 +130,7 @@ class ActivationCache:
     m_full: torch.Tensor | None = None
     state_folds: int = 0
     seg_prefix: torch.Tensor | None = None
+    seg_total: torch.Tensor | None = None
     nseg: int = 1
 
 
@@ -210,7 +211,7 @@ def _forward_masked_rank(ctx, qc: torch.Tensor, kc: torch.Tensor, vc: torch.Tens
         out = ops.causal_chunk(qc, kc, vc, seg, m_prefix if t > 0 else None, nseg)
         ctx.mark("intra_end", f"chunk={t}")
     cache = ActivationCache(q=qc, k=kc, v=vc, masked=True, m_prefix=m_prefix, state_folds=1, seg_prefix=seg,
-                            nseg=nseg)
+                            seg_total=m_t, nseg=nseg)
     return out, cache
 
 
@@ -259,15 +260,28 @@ _FUSE_DQ_MIN_BYTES = 256 << 20
 
 
 def _backward_masked_rank(ctx, cache: ActivationCache, d_out: torch.Tensor) -> GradientBundle:
-    """Masked backward (lasp2.py:270-285): the dM all_gather overlaps the dQ pass."""
+    """Masked backward (lasp2.py:270-285).
+
+    dM segment states (Q^T dO) and their suffix scan; the dM all_gather runs on
+    the side stream while the dQ pass (which needs only forward states) runs;
+    after the descending suffix fold one pass computes dK and dV together
+    (2-CTA clusters, Q/dO multicast). `MASKED_BWD_FUSED = True` selects the
+    single-launch dQ/dK/dV kernel instead (lasp2_backward_chunk).
+    """
     _require_cache(cache, masked=True)
     t, world = ctx.sp_position, ctx.sp_size
     (do,) = _contig(d_out)
     q, k, v, nseg = cache.q, cache.k, cache.v, cache.nseg
     gseg = ops.segment_states(q, do, nseg)
     g_t = ops.scan_segments(gseg, reverse=True, data_dtype=q.dtype)
+    if MASKED_BWD_FUSED:
+        gathered = _unpack_gathered(_gather_states(ctx, g_t, "state_grad"), g_t)
+        r = ops.suffix_states(gathered, t + 1) if t < world - 1 else None
+        dq, dk, dv = ops.backward_chunk(q, k, v, do, cache.seg_prefix, cache.seg_total,
+                                        cache.m_prefix if t > 0 else None, gseg, r, nseg)
+        return GradientBundle(dq=dq, dk=dk, dv=dv)
     pending = _gather_states(ctx, g_t, "state_grad", async_op=True)
-    # dq_s = sum_{i<=s}(do_s.v_i) k_i + do_s (M_{1:t-1} + local prefix)^T
+    # dq_s = sum_{i<=s}(do_s.v_i) k_i + do_s (M_{1:t-1} + local prefix)^T   (overlaps the all_gather)
     dq = ops.causal_chunk(do, v, k, cache.seg_prefix, cache.m_prefix if t > 0 else None, nseg,
                           reverse=False, transpose_state=True)
     gathered = _unpack_gathered(pending.wait(), g_t)
@@ -275,6 +289,11 @@ def _backward_masked_rank(ctx, cache: ActivationCache, d_out: torch.Tensor) -> G
     # dk_s = sum_{i>=s}(v_s.do_i) q_i + v_s G_s^T ; dv_s = sum_{i>=s}(k_s.q_i) do_i + k_s G_s  (one pass)
     dk, dv = ops.dkdv_chunk(q, k, v, do, gseg, r, nseg)
     return GradientBundle(dq=dq, dk=dk, dv=dv)
+
+
+# single-launch dQ/dK/dV backward (three CTAs per segment sharing L2); off by
+# default while the per-CTA MMA/epilogue chain, not HBM, bounds both variants
+MASKED_BWD_FUSED = False
 
 
 # ---- world drivers ----------------------------------------------------------

@@ -210,3 +210,26 @@ def test_state_apply_and_apply2(dtype, shape):
     dk, dv = ops.apply_state2(v, k, m)
     assert nerr(dk, v.double() @ m.double().transpose(-1, -2)) <= tol_o
     assert nerr(dv, k.double() @ m.double()) <= tol_o
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32, torch.float64])
+@pytest.mark.parametrize("shape,nseg", [((1, 2, 1024, 128), 3), ((2, 1, 1000, 64), 2), ((1, 3, 2048, 128), 9),
+                                        ((1, 1, 77, 128), 1)])
+def test_backward_chunk_matches_separate_passes(dtype, shape, nseg):
+    q, k, v, do = (rand(shape, dtype, s) for s in (41, 42, 43, 44))
+    b, h, n, d = shape
+    sd = _lib.state_dtype(dtype)
+    # forward states: exclusive prefixes of K^T V per segment + chunk total, as the forward scan leaves them
+    fseg = ops.segment_states(k, v, nseg)
+    ftot = ops.scan_segments(fseg, reverse=False, data_dtype=dtype)
+    fbase = rand((b, h, d, d), sd, 45, scale=30.0)
+    gseg = rand((b, h, nseg, d, d), sd, 46, scale=30.0)
+    gbase = rand((b, h, d, d), sd, 47, scale=30.0)
+    dq, dk, dv = ops.backward_chunk(q, k, v, do, fseg, ftot, fbase, gseg, gbase, nseg)
+    rq = ref_causal(do, v, k, fseg, fbase, nseg, False, True)
+    rk = ref_causal(v, do, q, gseg, gbase, nseg, True, True)
+    rv = ref_causal(k, q, do, gseg, gbase, nseg, True, False)
+    tol = {torch.bfloat16: 6e-3, torch.float32: F32_TOL, torch.float64: F64_TOL}[dtype]
+    assert nerr(dq, rq) <= tol
+    assert nerr(dk, rk) <= tol
+    assert nerr(dv, rv) <= tol

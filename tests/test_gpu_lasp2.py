@@ -244,3 +244,19 @@ def test_bf16_large_n_chunking_invariance():
         a, b = a.float(), b.float()
         assert torch.isfinite(b).all()
         assert ((a - b).abs().max() / a.abs().max()).item() <= 1e-2
+
+
+def test_fused_backward_variant_matches_default():
+    import paper_2502_07563_b200.lasp2 as L
+    q, k, v, do = O.inputs(3000, 128, 1, 2, 0)
+    seq = ChunkedSequence(*(dev(x, torch.bfloat16) for x in (q, k, v)), 3)
+    a = lasp2_iteration(seq, dev(do, torch.bfloat16), True)
+    L.MASKED_BWD_FUSED = True
+    try:
+        b = lasp2_iteration(seq, dev(do, torch.bfloat16), True)
+    finally:
+        L.MASKED_BWD_FUSED = False
+    for name in ("dq", "dk", "dv"):
+        x = cat(getattr(g, name) for g in a.grads).float()
+        y = cat(getattr(g, name) for g in b.grads).float()
+        assert ((x - y).abs().max() / x.abs().max()).item() <= 1e-2
