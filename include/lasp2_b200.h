@@ -155,6 +155,10 @@ int lasp2_gen_slots(int dtype, uint64_t seed, const uint64_t* tag_words_device, 
  * UMMA descriptor convention of the fast path (a_mn / b_mn select MN-major). */
 int lasp2_debug_probe_gemm(const void* a, const void* b, void* d, int a_mn, int b_mn, void* stream);
 
+/* Test hook: record a clock64() timeline of CTA (0,0) of the causal kernels into
+ * `buffer` (4096 x {event, block, clock} uint64; NULL disables). */
+int lasp2_debug_trace(void* buffer);
+
 #ifdef __cplusplus
 }
 #endif

@@ -45,6 +45,7 @@ SIGNATURES = {
     "lasp2h_softmax_scratch_bytes": (_i64, [_int, _i64, _i64, _i64, _int]),
     "lasp2_gen_slots": (_int, [_int, _u64, _vp, _vp, _i64, _i64, _i64, _i64, _vp]),
     "lasp2_debug_probe_gemm": (_int, [_vp, _vp, _vp, _int, _int, _vp]),
+    "lasp2_debug_trace": (_int, [_vp]),
 }
 
 _lock = threading.Lock()
@@ -104,7 +105,8 @@ class _Profiler:
 PROFILER = _Profiler()
 # kernels launched per call of each entry point (for gpu_launches accounting)
 KERNELS_PER_CALL = {"lasp2h_softmax_backward": 4}  # bf16 tc path: delta, memset, main, finalize
-_NO_LAUNCH = {"lasp2_version", "lasp2_last_error", "lasp2_num_segments", "lasp2h_softmax_scratch_bytes"}
+_NO_LAUNCH = {"lasp2_version", "lasp2_last_error", "lasp2_num_segments", "lasp2h_softmax_scratch_bytes",
+              "lasp2_debug_trace"}
 
 
 def call(name: str, *args) -> int:

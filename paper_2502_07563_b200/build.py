@@ -21,7 +21,7 @@ BUILD = PKG.parent / "build"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-                     "-Xptxas", "-v", f"-I{INCLUDE}"]
+                     "-Xptxas", "-v", f"-I{INCLUDE}"] + (["-DLASP2_TRACE"] if os.environ.get("LASP2_TRACE") else [])
 
 
 def _nvcc() -> str:

@@ -300,6 +300,10 @@ int lasp2_gen_slots(int dtype, uint64_t seed, const uint64_t* tag_words_device, 
   return cuda_status(e, "gen_slots");
 }
 
+int lasp2_debug_trace(void* buffer) {
+  return cuda_status(lasp::tc_set_trace((unsigned long long*)buffer), "debug_trace");
+}
+
 int lasp2_debug_probe_gemm(const void* a, const void* b, void* d, int a_mn, int b_mn, void* stream) {
   CHECK(a && b && d, "probe_gemm: null pointer");
   return cuda_status(lasp::tc_probe_gemm(a, b, (float*)d, a_mn, b_mn, S(stream)), "probe_gemm");

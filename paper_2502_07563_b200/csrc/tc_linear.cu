@@ -22,9 +22,33 @@
 namespace lasp {
 namespace tc {
 
-// ============================================================================
-// Segment states: out[slot][seg] = X_seg^T Y_seg   (fp32 [dim][dim])
-// ============================================================================
+// Optional per-block timeline of CTA (0,0) for blocks [16, 24): each traced
+// thread stamps clock64() into a local array and flushes it once at exit, so
+// tracing costs a few cycles per point. Enabled when g_trace != nullptr.
+__device__ unsigned long long* g_trace = nullptr;
+#ifdef LASP2_TRACE
+struct Tracer {
+  unsigned long long rec[64];
+  int n = 0;
+  bool on;
+  __device__ Tracer() : on(g_trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0) {}
+  __device__ __forceinline__ void operator()(int ev, int blk) {
+    if (on && blk >= 16 && blk < 24 && n < 64)
+      rec[n++] = ((unsigned long long)ev << 56) | ((unsigned long long)blk << 48) |
+                 ((unsigned long long)clock64() & 0xFFFFFFFFFFFFull);
+  }
+  __device__ void flush(int region) {
+    if (!on) return;
+    for (int i = 0; i < n; ++i) g_trace[region * 64 + i] = rec[i];
+  }
+};
+#else
+struct Tracer {  // compiled out: build with -DLASP2_TRACE to record timelines
+  __device__ __forceinline__ void operator()(int, int) {}
+  __device__ __forceinline__ void flush(int) {}
+};
+#endif
+
 constexpr int kSegStages = 3;
 constexpr uint32_t kSegSmem = kSegStages * 2 * kTileBytes + 1024 + 256;
 
@@ -265,6 +289,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
     constexpr uint32_t id_pv = idesc_bf16_f32(128, 128, 0, 1);  // O += P V
     const uint32_t simg_a = smem_u32(simg), pimg_a = smem_u32(pimg);
     const bool swap = kMode == 1 && R.mcast == 2;  // kMode 1 rank 1: ring positions of k', v' swapped
+    Tracer tr;
     for (int jj = 0; jj < nblk; ++jj) {
       const int t0 = 3 * jj;
       const int sq = t0 % kRing, sb = (t0 + 1) % kRing, sc = (t0 + 2) % kRing;
@@ -274,10 +299,13 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       const uint32_t qa = smem_u32(ring + sq * kTileBytes);
       const uint32_t ka = smem_u32(ring + sk * kTileBytes);
       const uint32_t va = smem_u32(ring + sv * kTileBytes);
+      if (lane == 0) tr(10, jj);
       mbar_wait(&full[sq], (t0 / kRing) & 1);
       mbar_wait(&full[sk], (tk / kRing) & 1);
+      if (lane == 0) tr(11, jj);
       if (jj > 0) mbar_wait(p_ready, (jj - 1) & 1);  // S tile drained by the epilogue
       tc_fence_after();
+      if (lane == 0) tr(12, jj);
       if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < kfeat; ++kk) mma_bf16_ss(t_s, desc_kmajor(qa, kk), desc_kmajor(ka, kk), id_qk, kk > 0);
@@ -298,8 +326,10 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
         __syncwarp();
       }
       mbar_wait(sst_ready, (jj + (R.subtract ? 1 : 0)) & 1);  // subtract form: arrival 0 is the seed
+      if (lane == 0) tr(13, jj);
       if (jj >= 2) mbar_wait(&o_empty[ob], ((jj >> 1) - 1) & 1);
       tc_fence_after();
+      if (lane == 0) tr(14, jj);
       if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < kfeat; ++kk)
@@ -310,6 +340,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       if (!R.subtract) {
         mbar_wait(&full[sv], (tv / kRing) & 1);
         tc_fence_after();
+        if (lane == 0) tr(15, jj);
         if (elect_one()) {
           if (jj < nblk - 1) {
 #pragma unroll
@@ -322,6 +353,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       }
       mbar_wait(p_ready, jj & 1);
       tc_fence_after();
+      if (lane == 0) tr(16, jj);
       if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) mma_bf16_ss(t_o(ob), desc_kmajor(pimg_a, kk), desc_mnmajor(va, kk), id_pv, 1u);
@@ -330,6 +362,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       }
       __syncwarp();
     }
+    if (lane == 0) tr.flush(0);
   } else {
     // -------- epilogue: 8 warps; warp w owns TMEM lanes 32*(w%4).. and columns [64*half, +64) --------
     const int qd = warp & 3;
@@ -342,6 +375,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
     const int dim = a.dim;
     const int64_t dd = (int64_t)dim * dim;
     const CUtensorMap* tm_o = &tm.m[R.oi];
+    Tracer tr;
     // initial state (optionally transposed); rows/cols beyond dim are zero
     //   forward form : base + seg_states[seg]                (state at the segment start)
     //   subtract form: fwd_base + fwd prefix of segment seg+1 (state at the segment end)
@@ -394,10 +428,13 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
         if (et == 0) mbar_arrive(sst_ready);
       }
       // ---- P = mask(S) -> smem (after the previous O tile left the staging buffer)
+      if (et == 0) tr(20, jj);
       mbar_wait(s_full, jj & 1);
       tc_fence_after();
+      if (et == 0) tr(21, jj);
       if (jj > 0 && et == 0) tma_store_wait_read<0>();
       named_bar_sync(1, kEpi);
+      if (et == 0) tr(22, jj);
       if (R.mask == 2)
         tmem_cols_to_image<2>(t_s + lane_off, pimg, row, cb, 64);
       else
@@ -406,19 +443,23 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       tc_fence_before();
       named_bar_sync(1, kEpi);
       if (et == 0) mbar_arrive(p_ready);
+      if (et == 0) tr(23, jj);
       // ---- forward form: next block's state image
       if (!R.subtract && jj < nblk - 1) {
         mbar_wait(st_full, jj & 1);
         tc_fence_after();
+        if (et == 0) tr(24, jj);
         tmem_cols_to_image<0>(t_st + lane_off, simg, row, cb, 64);
         fence_proxy_async_smem();
         tc_fence_before();
         named_bar_sync(1, kEpi);
         if (et == 0) mbar_arrive(sst_ready);
+        if (et == 0) tr(25, jj);
       }
       // ---- O tile -> staging -> TMA store
       mbar_wait(&o_full[ob], (jj >> 1) & 1);
       tc_fence_after();
+      if (et == 0) tr(26, jj);
       tmem_cols_to_image<0>(t_o(ob) + lane_off, pimg, row, cb, 64);
       fence_proxy_async_smem();
       tc_fence_before();
@@ -428,9 +469,11 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
         const int orow = (int)(lo + (int64_t)j * kTile);
         for (int bx = 0; bx < nbox; ++bx) tma_store_3d(tm_o, pimg + bx * kBoxBytes, 64 * bx, orow, slot);
         tma_store_commit();
+        tr(27, jj);
       }
     }
     if (et == 0) tma_store_wait_all<0>();
+    if (et == 0) tr.flush(1);
   }
   tc_fence_before();
   if constexpr (kMode == 1) cluster_sync(); else __syncthreads();
@@ -961,6 +1004,10 @@ cudaError_t tc_apply2(const void* x0, const void* x1, const float* m, void* out0
   tc::tc_fused_apply_kernel<1><<<grid, tc::kFusedThreads, tc::kFusedSmem, s>>>(m0, m1, mo0, mo1, m, nullptr, tokens,
                                                                               dim, 1, bpc);
   return cudaGetLastError();
+}
+
+cudaError_t tc_set_trace(unsigned long long* buf) {
+  return cudaMemcpyToSymbol(tc::g_trace, &buf, sizeof(buf));
 }
 
 cudaError_t tc_probe_gemm(const void* a, const void* b, float* d, int a_mn, int b_mn, cudaStream_t s) {
