@@ -8,8 +8,8 @@
 //         descending for suffix); an empty fold is zeros.
 // gen   : bit-exact SplitMix64 counter-hash port of datagen.gen_data
 //         (datagen.py:14-57), so the bench can build 2M-token inputs on device.
-#include "common.cuh"
 #include "kernels.h"
+#include "tc_common.cuh"
 
 namespace lasp {
 
@@ -19,6 +19,8 @@ namespace lasp {
 template <typename A>
 __global__ void scan_states_kernel(A* __restrict__ seg, A* __restrict__ total, int64_t slots, int nseg, int64_t dd,
                                    int reverse) {
+  ptx::pdl_wait();
+  ptx::pdl_launch_dependents();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= slots * dd) return;
   const int64_t slot = idx / dd, el = idx % dd;
@@ -48,6 +50,8 @@ __global__ void scan_states_kernel(A* __restrict__ seg, A* __restrict__ total, i
 template <typename A>
 __global__ void fold_states_kernel(const A* __restrict__ gathered, A* __restrict__ out, int nstates, int64_t elems,
                                    int mode, int bound) {
+  ptx::pdl_wait();
+  ptx::pdl_launch_dependents();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= elems) return;
   A acc = A(0);
@@ -114,16 +118,15 @@ template <typename A>
 cudaError_t scan_states(void* seg, void* total, int64_t slots, int nseg, int dim, int reverse, cudaStream_t s) {
   const int64_t dd = (int64_t)dim * dim;
   const int64_t n = slots * dd;
-  scan_states_kernel<A><<<(unsigned)((n + 255) / 256), 256, 0, s>>>((A*)seg, (A*)total, slots, nseg, dd, reverse);
-  return cudaGetLastError();
+  return launch_pdl(scan_states_kernel<A>, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, 1, (A*)seg, (A*)total,
+                    slots, nseg, dd, reverse);
 }
 
 template <typename A>
 cudaError_t fold_states(const void* gathered, void* out, int nstates, int64_t elems, int mode, int bound,
                         cudaStream_t s) {
-  fold_states_kernel<A><<<(unsigned)((elems + 255) / 256), 256, 0, s>>>((const A*)gathered, (A*)out, nstates, elems,
-                                                                       mode, bound);
-  return cudaGetLastError();
+  return launch_pdl(fold_states_kernel<A>, dim3((unsigned)((elems + 255) / 256)), dim3(256), 0, s, 1,
+                    (const A*)gathered, (A*)out, nstates, elems, mode, bound);
 }
 
 template <typename T>

@@ -84,6 +84,8 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_launch_dependents();
 
   if (warp == 0) {
     if (elect_one()) {
@@ -244,6 +246,8 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
   if constexpr (kMode == 1) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_launch_dependents();
   // TMEM: S [0,128), O[0] [128,256), running state [256,384), O[1] [384,512)
   const uint32_t t_s = tmem, t_st = tmem + 256;
   auto t_o = [&](int b) { return tmem + (b ? 384u : 128u); };
@@ -525,6 +529,8 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_launch_dependents();
 
   if (warp == 0) {
     if (elect_one()) {
@@ -684,6 +690,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_launch_dependents();
   // MODE 0: G [0,128), out0[2] at 128/256.  MODE 1: out0[2] at 0/128, out1[2] at 256/384.
   auto t_out0 = [&](int b) { return tmem + (MODE == 0 ? 128u + 128u * b : 128u * b); };
   auto t_out1 = [&](int b) { return tmem + 256u + 128u * b; };
@@ -840,6 +848,8 @@ __global__ void __launch_bounds__(128, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_launch_dependents();
   if (threadIdx.x == 0) {
     mbar_arrive_expect_tx(&bars[0], 2 * kTileBytes);
     tma_load_3d(at, &tm_a, &bars[0], 0, 0, 0);
@@ -887,8 +897,7 @@ cudaError_t tc_segment_states(const void* x, const void* y, float* out, int64_t 
   if ((e = make_tmap_3d(&my, y, slots, tokens, dim)) != cudaSuccess) return e;
   if ((e = set_smem_once((const void*)tc::tc_segment_states_kernel, tc::kSegSmem)) != cudaSuccess) return e;
   dim3 grid(nseg, (unsigned)slots);
-  tc::tc_segment_states_kernel<<<grid, 192, tc::kSegSmem, s>>>(mx, my, out, tokens, dim, nseg);
-  return cudaGetLastError();
+  return launch_pdl(tc::tc_segment_states_kernel, grid, dim3(192), tc::kSegSmem, s, 1, mx, my, out, tokens, dim, nseg);
 }
 
 cudaError_t tc_causal_chunk(const void* q, const void* k, const void* v, const float* seg_states, const float* base,
@@ -902,8 +911,7 @@ cudaError_t tc_causal_chunk(const void* q, const void* k, const void* v, const f
   if ((e = set_smem_once((const void*)tc::tc_causal_chunk_kernel<0>, tc::kCausalSmem)) != cudaSuccess) return e;
   tc::CausalArgs a{seg_states, base, nullptr, nullptr, nullptr, tokens, dim, nseg, reverse, transpose_state};
   dim3 grid(nseg, (unsigned)slots);
-  tc::tc_causal_chunk_kernel<0><<<grid, tc::kCausalThreads, tc::kCausalSmem, s>>>(tm, a);
-  return cudaGetLastError();
+  return launch_pdl(tc::tc_causal_chunk_kernel<0>, grid, dim3(tc::kCausalThreads), tc::kCausalSmem, s, 1, tm, a);
 }
 
 // Masked backward dK and dV in one pass over (Q, K, V, dO): 2-CTA clusters.
@@ -917,19 +925,8 @@ cudaError_t tc_dkdv_pair(const void* q, const void* k, const void* v, const void
     if ((e = make_tmap_3d(&tm.m[i], ptrs[i], slots, tokens, dim)) != cudaSuccess) return e;
   if ((e = set_smem_once((const void*)tc::tc_causal_chunk_kernel<1>, tc::kCausalSmem)) != cudaSuccess) return e;
   tc::CausalArgs a{seg_states, base, nullptr, nullptr, nullptr, tokens, dim, nseg, 1, 0};
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(2 * nseg, (unsigned)slots);
-  cfg.blockDim = dim3(tc::kCausalThreads);
-  cfg.dynamicSmemBytes = tc::kCausalSmem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, tc::tc_causal_chunk_kernel<1>, tm, a);
+  return launch_pdl(tc::tc_causal_chunk_kernel<1>, dim3(2 * nseg, (unsigned)slots), dim3(tc::kCausalThreads),
+                    tc::kCausalSmem, s, 2, tm, a);
 }
 
 // Masked backward dQ, dK, dV in one launch: three CTAs per segment sharing tiles through L2.
@@ -945,8 +942,7 @@ cudaError_t tc_backward_triple(const void* q, const void* k, const void* v, cons
   if ((e = set_smem_once((const void*)tc::tc_causal_chunk_kernel<2>, tc::kCausalSmem)) != cudaSuccess) return e;
   tc::CausalArgs a{bwd_seg, bwd_base, fwd_seg, fwd_total, fwd_base, tokens, dim, nseg, 1, 0};
   dim3 grid(3 * nseg, (unsigned)slots);
-  tc::tc_causal_chunk_kernel<2><<<grid, tc::kCausalThreads, tc::kCausalSmem, s>>>(tm, a);
-  return cudaGetLastError();
+  return launch_pdl(tc::tc_causal_chunk_kernel<2>, grid, dim3(tc::kCausalThreads), tc::kCausalSmem, s, 1, tm, a);
 }
 
 cudaError_t tc_apply_state(const void* x, const float* m, void* out, int64_t slots, int64_t tokens, int dim,
@@ -964,9 +960,8 @@ cudaError_t tc_apply_state(const void* x, const float* m, void* out, int64_t slo
   const int bpc = (int)((nblk + ctas - 1) / ctas);
   ctas = (nblk + bpc - 1) / bpc;
   dim3 grid((unsigned)ctas, (unsigned)slots);
-  tc::tc_apply_state_kernel<<<grid, 192, tc::kApplySmem, s>>>(mx, mo, m, (__nv_bfloat16*)out, tokens, dim,
-                                                              transpose, accumulate, bpc);
-  return cudaGetLastError();
+  return launch_pdl(tc::tc_apply_state_kernel, grid, dim3(192), tc::kApplySmem, s, 1, mx, mo, m,
+                    (__nv_bfloat16*)out, tokens, dim, transpose, accumulate, bpc);
 }
 
 // Unmasked backward, fused: dM segment states (Q^T dO) and dQ = dO M^T in one pass.
@@ -979,9 +974,8 @@ cudaError_t tc_state_apply(const void* x0, const void* x1, const float* m, float
   if ((e = make_tmap_3d(&mo, out, slots, tokens, dim)) != cudaSuccess) return e;
   if ((e = set_smem_once((const void*)tc::tc_fused_apply_kernel<0>, tc::kFusedSmem)) != cudaSuccess) return e;
   dim3 grid(nseg, (unsigned)slots);
-  tc::tc_fused_apply_kernel<0><<<grid, tc::kFusedThreads, tc::kFusedSmem, s>>>(m0, m1, mo, mo, m, seg_out, tokens,
-                                                                              dim, nseg, 0);
-  return cudaGetLastError();
+  return launch_pdl(tc::tc_fused_apply_kernel<0>, grid, dim3(tc::kFusedThreads), tc::kFusedSmem, s, 1, m0, m1, mo, mo,
+                    m, seg_out, tokens, dim, nseg, 0);
 }
 
 // Unmasked backward dK = V dM^T and dV = K dM in one pass.
@@ -1001,9 +995,8 @@ cudaError_t tc_apply2(const void* x0, const void* x1, const float* m, void* out0
   const int bpc = (int)((nblk + ctas - 1) / ctas);
   ctas = (nblk + bpc - 1) / bpc;
   dim3 grid((unsigned)ctas, (unsigned)slots);
-  tc::tc_fused_apply_kernel<1><<<grid, tc::kFusedThreads, tc::kFusedSmem, s>>>(m0, m1, mo0, mo1, m, nullptr, tokens,
-                                                                              dim, 1, bpc);
-  return cudaGetLastError();
+  return launch_pdl(tc::tc_fused_apply_kernel<1>, grid, dim3(tc::kFusedThreads), tc::kFusedSmem, s, 1, m0, m1, mo0,
+                    mo1, m, (float*)nullptr, tokens, dim, 1, bpc);
 }
 
 cudaError_t tc_set_trace(unsigned long long* buf) {
