@@ -419,6 +419,7 @@ def run_gpu_arm(args) -> None:
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}; launch N>1 with torchrun")
+    local = local % torch.cuda.device_count()  # ranks may share a device (gloo smoke runs)
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     from paper_2502_07563_b200 import comm
@@ -426,7 +427,10 @@ def run_gpu_arm(args) -> None:
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=device)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(args.dist_backend)
         ctx = comm.DistRankContext()
     else:
         ctx = comm.LocalRankContext()
@@ -482,6 +486,7 @@ def main() -> None:
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--eager", action="store_true", help="time eager launches instead of CUDA-graph replay")
     ap.add_argument("--seq-len", type=int, default=0, help="override N of the selected workload")
+    ap.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo for multi-rank smoke runs on one GPU")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3 (timing rules)")
