@@ -301,7 +301,9 @@ int lasp2_gen_slots(int dtype, uint64_t seed, const uint64_t* tag_words_device, 
 }
 
 int lasp2_debug_trace(void* buffer) {
-  return cuda_status(lasp::tc_set_trace((unsigned long long*)buffer), "debug_trace");
+  cudaError_t e = lasp::tc_set_trace((unsigned long long*)buffer);
+  if (e == cudaSuccess) e = lasp::tc_set_trace_softmax((unsigned long long*)buffer);
+  return cuda_status(e, "debug_trace");
 }
 
 int lasp2_debug_probe_gemm(const void* a, const void* b, void* d, int a_mn, int b_mn, void* stream) {

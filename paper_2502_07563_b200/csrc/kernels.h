@@ -68,6 +68,7 @@ cudaError_t tc_state_apply(const void* x0, const void* x1, const float* m, float
 cudaError_t tc_apply2(const void* x0, const void* x1, const float* m, void* out0, void* out1, int64_t slots,
                       int64_t tokens, int dim, int sm_count, cudaStream_t s);
 cudaError_t tc_set_trace(unsigned long long* buf);
+cudaError_t tc_set_trace_softmax(unsigned long long* buf);
 cudaError_t tc_probe_gemm(const void* a, const void* b, float* d, int a_mn, int b_mn, cudaStream_t s);
 
 }  // namespace lasp

@@ -90,6 +90,33 @@ __device__ __forceinline__ void tmem_cols_to_image(uint32_t taddr_lane, uint8_t*
   }
 }
 
+// Optional per-block timeline of CTA (0,0) for blocks [16, 24): each traced
+// thread stamps clock64() into a local array and flushes it once at exit, so
+// tracing costs a few cycles per point. Enabled when g_trace != nullptr.
+static __device__ unsigned long long* g_trace = nullptr;  // one per translation unit
+#ifdef LASP2_TRACE
+struct Tracer {
+  unsigned long long rec[64];
+  int n = 0;
+  bool on;
+  __device__ Tracer() : on(g_trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0) {}
+  __device__ __forceinline__ void operator()(int ev, int blk) {
+    if (on && blk >= 16 && blk < 24 && n < 64)
+      rec[n++] = ((unsigned long long)ev << 56) | ((unsigned long long)blk << 48) |
+                 ((unsigned long long)clock64() & 0xFFFFFFFFFFFFull);
+  }
+  __device__ void flush(int region) {
+    if (!on) return;
+    for (int i = 0; i < n; ++i) g_trace[region * 64 + i] = rec[i];
+  }
+};
+#else
+struct Tracer {  // compiled out: build with -DLASP2_TRACE to record timelines
+  __device__ __forceinline__ void operator()(int, int) {}
+  __device__ __forceinline__ void flush(int) {}
+};
+#endif
+
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -141,6 +168,7 @@ inline cudaError_t set_smem_once(const void* kernel, uint32_t bytes) {
 // host: 3-D [slots][tokens][dim] and 4-D rank-major [ranks][slots][chunk][dim]
 // bf16 tensor maps with 64 x 128 SWIZZLE_128B boxes (tc_host.cu)
 cudaError_t make_tmap_3d(CUtensorMap* m, const void* ptr, int64_t slots, int64_t tokens, int dim);
+cudaError_t make_tmap_3d_f32(CUtensorMap* m, const void* ptr, int64_t slots, int64_t tokens, int dim);
 cudaError_t make_tmap_4d(CUtensorMap* m, const void* ptr, int64_t ranks, int64_t slots, int64_t chunk, int dim,
                          int64_t rank_stride_elems);
 

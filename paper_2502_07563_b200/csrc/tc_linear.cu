@@ -22,32 +22,6 @@
 namespace lasp {
 namespace tc {
 
-// Optional per-block timeline of CTA (0,0) for blocks [16, 24): each traced
-// thread stamps clock64() into a local array and flushes it once at exit, so
-// tracing costs a few cycles per point. Enabled when g_trace != nullptr.
-__device__ unsigned long long* g_trace = nullptr;
-#ifdef LASP2_TRACE
-struct Tracer {
-  unsigned long long rec[64];
-  int n = 0;
-  bool on;
-  __device__ Tracer() : on(g_trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0) {}
-  __device__ __forceinline__ void operator()(int ev, int blk) {
-    if (on && blk >= 16 && blk < 24 && n < 64)
-      rec[n++] = ((unsigned long long)ev << 56) | ((unsigned long long)blk << 48) |
-                 ((unsigned long long)clock64() & 0xFFFFFFFFFFFFull);
-  }
-  __device__ void flush(int region) {
-    if (!on) return;
-    for (int i = 0; i < n; ++i) g_trace[region * 64 + i] = rec[i];
-  }
-};
-#else
-struct Tracer {  // compiled out: build with -DLASP2_TRACE to record timelines
-  __device__ __forceinline__ void operator()(int, int) {}
-  __device__ __forceinline__ void flush(int) {}
-};
-#endif
 
 constexpr int kSegStages = 3;
 constexpr uint32_t kSegSmem = kSegStages * 2 * kTileBytes + 1024 + 256;

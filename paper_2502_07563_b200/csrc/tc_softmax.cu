@@ -286,7 +286,7 @@ struct SmBwdArgs {
 __global__ void __launch_bounds__(kSmBwdThreads, 1)
     tc_softmax_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                           const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
-                          SmBwdArgs a) {
+                          const __grid_constant__ CUtensorMap tm_dq, SmBwdArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* kimg = smem;
@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(kSmBwdThreads, 1)
           if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
           uint8_t* dst = ring + s * kTileBytes;
           mbar_arrive_expect_tx(&full[s], nbox * kBoxBytes);
-          const CUtensorMap* m = w == 0 ? &tm_q : &tm_do;
+          const CUtensorMap* m = w == 0 ? &tm_do : &tm_q;  // dO first: dP is issued first
           for (int bx = 0; bx < nbox; ++bx) tma_load_3d(dst + bx * kBoxBytes, m, &full[s], 64 * bx, qrow, slot);
         }
       }
@@ -363,23 +363,43 @@ __global__ void __launch_bounds__(kSmBwdThreads, 1)
       constexpr uint32_t id_km = idesc_bf16_f32(128, 128, 0, 1);  // dQ (A = dS, B = K)
       const uint32_t ka = smem_u32(kimg), va = smem_u32(vimg), pa = smem_u32(pimg), dsa = smem_u32(dsimg);
       mbar_wait(kv_full, 0);
-      for (int i = 0; i < nq; ++i) {
-        const int tq = 2 * i, tdo = tq + 1;
-        const int sq = tq % kQRing, sdo = tdo % kQRing;
-        const uint32_t qa = smem_u32(ring + sq * kTileBytes), doa = smem_u32(ring + sdo * kTileBytes);
-        mbar_wait(&full[sq], (tq / kQRing) & 1);
+      // S_i, dP_i -> [epilogue P, dS] -> dV, dK, dQ_i -> dP_{i+1} (overlaps the dQ_i drain) -> S_{i+1}
+      // ring order per query block: tile 2i = dO_i, tile 2i+1 = Q_i
+      auto issue_dp = [&](int i) {
+        const int tdo = 2 * i;
+        const int sdo = tdo % kQRing;
         mbar_wait(&full[sdo], (tdo / kQRing) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t doa = smem_u32(ring + sdo * kTileBytes);
+          for (int kk = 0; kk < kfeat; ++kk)
+            mma_bf16_ss(t_dp, desc_kmajor(doa, kk), desc_kmajor(va, kk), id_kk, kk > 0);
+        }
+        __syncwarp();
+      };
+      auto issue_s = [&](int i) {
+        const int tq = 2 * i + 1, sq = tq % kQRing;
+        mbar_wait(&full[sq], (tq / kQRing) & 1);
         if (i > 0) mbar_wait(dq_empty, (i - 1) & 1);  // S/dQ columns drained
         tc_fence_after();
         if (elect_one()) {
+          const uint32_t qa = smem_u32(ring + sq * kTileBytes);
           for (int kk = 0; kk < kfeat; ++kk) mma_bf16_ss(t_s, desc_kmajor(qa, kk), desc_kmajor(ka, kk), id_kk, kk > 0);
-          for (int kk = 0; kk < kfeat; ++kk)
-            mma_bf16_ss(t_dp, desc_kmajor(doa, kk), desc_kmajor(va, kk), id_kk, kk > 0);
           mma_commit(sdp_full);
         }
         __syncwarp();
+      };
+      Tracer tr;
+      issue_dp(0);
+      issue_s(0);
+      for (int i = 0; i < nq; ++i) {
+        if (lane == 0) tr(10, i);
+        const int tdo = 2 * i, tq = tdo + 1;
+        const int sq = tq % kQRing, sdo = tdo % kQRing;
+        const uint32_t qa = smem_u32(ring + sq * kTileBytes), doa = smem_u32(ring + sdo * kTileBytes);
         mbar_wait(ds_ready, i & 1);
         tc_fence_after();
+        if (lane == 0) tr(11, i);
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
@@ -394,7 +414,15 @@ __global__ void __launch_bounds__(kSmBwdThreads, 1)
           mma_commit(dq_full);
         }
         __syncwarp();
+        if (lane == 0) tr(12, i);
+        if (i + 1 < nq) {
+          issue_dp(i + 1);  // dP columns were drained at ds_ready(i)
+          if (lane == 0) tr(13, i);
+          issue_s(i + 1);
+          if (lane == 0) tr(14, i);
+        }
       }
+      if (lane == 0) tr.flush(0);
     }
   } else {
     const int qd = warp & 3;
@@ -404,27 +432,36 @@ __global__ void __launch_bounds__(kSmBwdThreads, 1)
     const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
     const int et = threadIdx.x - 64;
     constexpr uint32_t kSm = kSmBwdThreads - 64;
-    auto row_stats = [&](int i, float* lse2, float* dl) {
+    // raw row statistics of query block i (loads only: the values are consumed one block later)
+    auto row_stats = [&](int i, float* lse, float* dl) {
       const int64_t ql = (int64_t)(qb0 + i) * kTile + row;
       const bool ok = i < nq && ql < a.qtok;
-      *lse2 = ok ? a.lse[(int64_t)slot * a.qtok + ql] * 1.4426950408889634f : 0.f;
-      *dl = ok ? a.delta[(int64_t)slot * a.qtok + ql] : 0.f;
+      const int64_t idx = ok ? (int64_t)slot * a.qtok + ql : 0;
+      *lse = __ldg(a.lse + idx);
+      *dl = __ldg(a.delta + idx);
     };
     float lse2_next, dl_next;
+    Tracer tr;
     row_stats(0, &lse2_next, &dl_next);
     for (int i = 0; i < nq; ++i) {
       const int64_t qloc = (int64_t)(qb0 + i) * kTile + row;  // local query row of this thread
       const bool qok = qloc < a.qtok;
       const int64_t gq = a.row_offset + qloc;
-      const float lse2 = lse2_next, dl = dl_next;
+      const float lse2 = qok ? lse2_next * 1.4426950408889634f : 0.f, dl = qok ? dl_next : 0.f;
       row_stats(i + 1, &lse2_next, &dl_next);  // prefetch the next block's row statistics
       // valid key columns (within my 64-column half) for this query row
       int lim = qok ? (int)lmin(kTile, a.kvtok - k0) - cb : 0;
       if (a.causal) lim = (int)lmin((int64_t)lim, gq - k0 + 1 - cb);
       const bool full = __all_sync(0xffffffffu, lim >= 64);
       const bool none = __all_sync(0xffffffffu, lim <= 0);
+      if (et == 0) tr(20, i);
       mbar_wait(sdp_full, i & 1);
       tc_fence_after();
+      if (et == 0) tr(21, i);
+      if (i > 0) {  // the previous block's dQ reduce has finished reading the staging (= P/dS images)
+        if (et == 0) tma_store_wait_read<0>();
+        named_bar_sync(1, kSm);
+      }
       // P/dS images are free: the previous block's dq_full (all its MMAs) was waited below
 #pragma unroll 1
       for (int c = 0; c < 64; c += 32) {
@@ -453,30 +490,43 @@ __global__ void __launch_bounds__(kSmBwdThreads, 1)
       tc_fence_before();
       named_bar_sync(1, kSm);
       if (et == 0) mbar_arrive(ds_ready);
-      // dQ partial (my 64 columns) -> fp32 global accumulator
+      if (et == 0) tr(22, i);
+      // dQ partial (my 64 columns) -> fp32 SW128 staging in the (now free) P+dS region ->
+      // one TMA bulk reduce-add per 32-column box into the fp32 accumulator
       mbar_wait(dq_full, i & 1);
       tc_fence_after();
-      float* dqr = a.dq_acc + ((int64_t)slot * a.qtok + qloc) * a.dim;
+      if (et == 0) tr(23, i);
+      uint8_t* stg = pimg;  // P and dS images are contiguous: 64 KB = 4 boxes of 128 x 32 fp32
 #pragma unroll 1
       for (int c = 0; c < 64; c += 32) {
         const int c0 = cb + c;
         uint32_t r[32];
         tmem_ld_32x32b_x32(t_s + lane_off + c0, r);
         tmem_ld_wait();
-        if (qok && c0 < a.dim) {
+        uint8_t* box = stg + (c0 >> 5) * 16384 + row * 128;
 #pragma unroll
-          for (int e = 0; e < 32; e += 4) {
-            if (c0 + e < a.dim)
-              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dqr + c0 + e),
-                           "f"(__uint_as_float(r[e]) * a.scale), "f"(__uint_as_float(r[e + 1]) * a.scale),
-                           "f"(__uint_as_float(r[e + 2]) * a.scale), "f"(__uint_as_float(r[e + 3]) * a.scale)
-                           : "memory");
-          }
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t off = (uint32_t)((u ^ (row & 7)) * 16);
+          asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(smem_u32(box + off)),
+                       "f"(__uint_as_float(r[4 * u]) * a.scale), "f"(__uint_as_float(r[4 * u + 1]) * a.scale),
+                       "f"(__uint_as_float(r[4 * u + 2]) * a.scale), "f"(__uint_as_float(r[4 * u + 3]) * a.scale)
+                       : "memory");
         }
       }
+      fence_proxy_async_smem();
       tc_fence_before();
       named_bar_sync(1, kSm);
-      if (et == 0) mbar_arrive(dq_empty);
+      if (et == 0) {
+        mbar_arrive(dq_empty);
+        const int qrow = (qb0 + i) * kTile;
+        for (int bx = 0; bx < (a.dim + 31) / 32; ++bx) tma_reduce_add_3d(&tm_dq, stg + bx * 16384, 32 * bx, qrow, slot);
+        tma_store_commit();
+        tr(24, i);
+      }
+    }
+    if (et == 0) {
+      tma_store_wait_all<0>();
+      tr.flush(1);
     }
     // dK / dV rows of this key block (one key per thread, my 64 columns) -> fp32 contributions
     const int64_t key = k0 + row;
@@ -523,6 +573,10 @@ __global__ void dq_finalize_kernel(const float* __restrict__ acc, __nv_bfloat16*
 
 }  // namespace tc
 
+cudaError_t tc_set_trace_softmax(unsigned long long* buf) {
+  return cudaMemcpyToSymbol(tc::g_trace, &buf, sizeof(buf));
+}
+
 bool tc_softmax_supported(int dim, int64_t kv_chunk) {
   return dim >= 8 && dim <= 128 && dim % 8 == 0 && kv_chunk % 128 == 0;
 }
@@ -564,11 +618,13 @@ cudaError_t tc_softmax_backward(const void* q, const void* kf, const void* vf, c
   if ((e = make_tmap_3d(&mdo, d_out, slots, qtok, dim)) != cudaSuccess) return e;
   if ((e = make_tmap_4d(&mk, kf, ranks, slots, kv_chunk, dim, kv_rank_stride)) != cudaSuccess) return e;
   if ((e = make_tmap_4d(&mv, vf, ranks, slots, kv_chunk, dim, kv_rank_stride)) != cudaSuccess) return e;
+  CUtensorMap mdq;
+  if ((e = make_tmap_3d_f32(&mdq, dq_acc, slots, qtok, dim)) != cudaSuccess) return e;
   if ((e = set_smem_once((const void*)tc::tc_softmax_bwd_kernel, tc::kSmBwdSmem)) != cudaSuccess) return e;
   tc::SmBwdArgs a{lse, delta, dq_acc, dk_full, dv_full, qtok, kvtok, kv_chunk, grad_rank_stride, row_offset, dim,
                   causal, 1.f / sqrtf((float)dim), 1.4426950408889634f / sqrtf((float)dim)};
   dim3 grid((unsigned)((kvtok + 127) / 128), (unsigned)slots);
-  tc::tc_softmax_bwd_kernel<<<grid, tc::kSmBwdThreads, tc::kSmBwdSmem, s>>>(mq, mdo, mk, mv, a);
+  tc::tc_softmax_bwd_kernel<<<grid, tc::kSmBwdThreads, tc::kSmBwdSmem, s>>>(mq, mdo, mk, mv, mdq, a);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const int64_t n = slots * qtok * dim;
   tc::dq_finalize_kernel<<<(unsigned)lmin(148 * 16, (n + 255) / 256), 256, 0, s>>>(dq_acc, (__nv_bfloat16*)dq, n);

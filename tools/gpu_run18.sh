@@ -1,0 +1,7 @@
+#!/bin/bash
+cd "${GRAFT_REPO_ROOT:-.}"
+mkdir -p gpurun_out
+timeout -s KILL 300 python tools/trace_softmax.py > gpurun_out/trace18.log 2>&1
+timeout -s KILL 300 python tools/perf_probe.py 0 softmax 32768 > gpurun_out/perf18_softmax.log 2>&1
+timeout -s KILL 600 python -m pytest tests/test_gpu_softmax_kernels.py tests/test_gpu_cp.py -q -p no:cacheprovider -x > gpurun_out/t18.log 2>&1
+tail -2 gpurun_out/t18.log
