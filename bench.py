@@ -374,7 +374,10 @@ def measure_workload(workload: str, ctx, rank: int, world: int, steps: int, warm
     algo_bytes = {"lasp2_causal_chunk": 4 * unit_bytes, "lasp2_apply_state": 2 * unit_bytes,
                   "lasp2_segment_states": 2 * unit_bytes, "lasp2_dkdv_chunk": 6 * unit_bytes,
                   "lasp2_state_apply": 3 * unit_bytes, "lasp2_apply_state2": 4 * unit_bytes,
-                  "lasp2_backward_chunk": 7 * unit_bytes}.get(dom, 0)
+                  "lasp2_backward_chunk": 7 * unit_bytes,
+                  # world-of-one persistent kernels: K,V in + Q in, O out | Q,dO in, dQ out + V,K in, dK,dV out
+                  "lasp2_nomask_forward_local": 4 * unit_bytes,
+                  "lasp2_nomask_backward_local": 7 * unit_bytes}.get(dom, 0)
     # causal softmax useful FLOPs of one rank: queries [rC, (r+1)C) see keys <= position
     pairs = H * (c * rank * c + c * (c + 1) / 2)
     algo_flops = {"lasp2h_softmax_forward": 4 * D * pairs, "lasp2h_softmax_backward": 10 * D * pairs}.get(dom, 0)

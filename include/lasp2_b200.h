@@ -115,6 +115,26 @@ int lasp2_state_apply(int dtype, const void* q, const void* d_out, const void* m
 int lasp2_apply_state2(int dtype, const void* v, const void* k, const void* dm, void* dk, void* dv, int64_t slots,
                        int64_t tokens, int dim, void* stream);
 
+/* Unmasked layer on a world of ONE rank (T = 1: the state all_gather is the
+ * identity and sum_states of one state is a copy). Replaces
+ * _forward_nomask_rank (lasp2.py:208-216) and _backward_nomask_rank
+ * (lasp2.py:256-267) for sp_size == 1.
+ *   forward : m_full = K^T V (states dtype), out = q m_full
+ *   backward: dM = Q^T dO; dq = dO m_full^T; dk = v dM^T; dv = k dM
+ * bf16 runs one persistent launch per direction over all SMs (cooperative:
+ * it needs the whole GPU while it runs; in-kernel grid barrier + ordered
+ * reduction of per-CTA partial states). `workspace` must hold
+ * lasp2_local_workspace_bytes(...) bytes and be ZERO-FILLED before its first
+ * use; every call leaves it reusable. One workspace per concurrently running
+ * call. f32/f64 compose lasp2_segment_states / scan / apply entry points. */
+int64_t lasp2_local_workspace_bytes(int dtype, int64_t slots, int64_t tokens, int dim, int sm_count);
+int lasp2_nomask_forward_local(int dtype, const void* q, const void* k, const void* v, void* out, void* m_full,
+                               void* workspace, int64_t workspace_bytes, int64_t slots, int64_t tokens, int dim,
+                               void* stream);
+int lasp2_nomask_backward_local(int dtype, const void* q, const void* k, const void* v, const void* d_out,
+                                const void* m_full, void* dq, void* dk, void* dv, void* workspace,
+                                int64_t workspace_bytes, int64_t slots, int64_t tokens, int dim, void* stream);
+
 /* LASP-2H softmax attention of one chunk of queries (global rows
  * [row_offset, row_offset+q_tokens)) against full-length keys/values.
  * Full-length tensors may be rank-major as the collectives produce them:

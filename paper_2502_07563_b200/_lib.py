@@ -38,6 +38,10 @@ SIGNATURES = {
     "lasp2_backward_chunk": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64,
                                     _int, _int, _vp]),
     "lasp2_apply_state": (_int, [_int, _vp, _vp, _vp, _i64, _i64, _int, _int, _int, _vp]),
+    "lasp2_local_workspace_bytes": (_i64, [_int, _i64, _i64, _int, _int]),
+    "lasp2_nomask_forward_local": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _vp]),
+    "lasp2_nomask_backward_local": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64,
+                                           _int, _vp]),
     "lasp2h_softmax_forward": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _i64, _i64, _i64,
                                       _vp]),
     "lasp2h_softmax_backward": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int,
@@ -106,6 +110,7 @@ PROFILER = _Profiler()
 # kernels launched per call of each entry point (for gpu_launches accounting)
 KERNELS_PER_CALL = {"lasp2h_softmax_backward": 4}  # bf16 tc path: delta, memset, main, finalize
 _NO_LAUNCH = {"lasp2_version", "lasp2_last_error", "lasp2_num_segments", "lasp2h_softmax_scratch_bytes",
+              "lasp2_local_workspace_bytes",
               "lasp2_debug_trace"}
 
 

@@ -215,6 +215,64 @@ int lasp2_apply_state2(int dtype, const void* v, const void* k, const void* dm, 
   return lasp2_apply_state(dtype, k, dm, dv, slots, tokens, dim, 0, 0, stream);
 }
 
+// ---- unmasked layer on a world of one rank (lasp2.py:208-216, :256-267 with T = 1) ----
+namespace {
+int64_t simt_local_ws(int dtype, int64_t slots, int64_t tokens, int dim) {
+  const int64_t nseg = lasp2_num_segments(dtype, slots, tokens, dim, sm_count_current());
+  const int64_t elt = dtype == LASP2_F64 ? 8 : 4;
+  return (slots * nseg + slots) * (int64_t)dim * dim * elt;
+}
+}  // namespace
+
+int64_t lasp2_local_workspace_bytes(int dtype, int64_t slots, int64_t tokens, int dim, int sm_count) {
+  if (!valid_dtype(dtype) || slots < 1 || tokens < 1 || dim < 1 || dim > 128) return -1;
+  if (sm_count < 1) sm_count = sm_count_current();
+  if (use_tc(dtype, dim, tokens)) return lasp::tc_flat_workspace_bytes(slots, tokens, dim, sm_count);
+  return simt_local_ws(dtype, slots, tokens, dim);
+}
+
+int lasp2_nomask_forward_local(int dtype, const void* q, const void* k, const void* v, void* out, void* m_full,
+                               void* workspace, int64_t workspace_bytes, int64_t slots, int64_t tokens, int dim,
+                               void* stream) {
+  CHECK(valid_dtype(dtype), "nomask_forward_local: unknown dtype");
+  CHECK(q && k && v && out && m_full && workspace, "nomask_forward_local: null pointer");
+  CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128, "nomask_forward_local: bad shape (1 <= dim <= 128)");
+  const int sms = sm_count_current();
+  CHECK(workspace_bytes >= lasp2_local_workspace_bytes(dtype, slots, tokens, dim, sms),
+        "nomask_forward_local: workspace too small (lasp2_local_workspace_bytes)");
+  if (use_tc(dtype, dim, tokens))
+    return cuda_status(lasp::tc_flat_forward(q, k, v, out, (float*)m_full, workspace, slots, tokens, dim, sms,
+                                             S(stream)),
+                       "nomask_forward_local");
+  const int nseg = lasp2_num_segments(dtype, slots, tokens, dim, sms);
+  int st = lasp2_segment_states(dtype, k, v, workspace, slots, tokens, dim, nseg, stream);
+  if (st == LASP2_OK) st = lasp2_scan_segments(dtype, workspace, m_full, slots, nseg, dim, 0, stream);
+  if (st == LASP2_OK) st = lasp2_apply_state(dtype, q, m_full, out, slots, tokens, dim, 0, 0, stream);
+  return st;
+}
+
+int lasp2_nomask_backward_local(int dtype, const void* q, const void* k, const void* v, const void* d_out,
+                                const void* m_full, void* dq, void* dk, void* dv, void* workspace,
+                                int64_t workspace_bytes, int64_t slots, int64_t tokens, int dim, void* stream) {
+  CHECK(valid_dtype(dtype), "nomask_backward_local: unknown dtype");
+  CHECK(q && k && v && d_out && m_full && dq && dk && dv && workspace, "nomask_backward_local: null pointer");
+  CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128, "nomask_backward_local: bad shape (1 <= dim <= 128)");
+  const int sms = sm_count_current();
+  CHECK(workspace_bytes >= lasp2_local_workspace_bytes(dtype, slots, tokens, dim, sms),
+        "nomask_backward_local: workspace too small (lasp2_local_workspace_bytes)");
+  if (use_tc(dtype, dim, tokens))
+    return cuda_status(lasp::tc_flat_backward(q, k, v, d_out, (const float*)m_full, dq, dk, dv, workspace, slots,
+                                              tokens, dim, sms, S(stream)),
+                       "nomask_backward_local");
+  const int nseg = lasp2_num_segments(dtype, slots, tokens, dim, sms);
+  const int64_t elt = dtype == LASP2_F64 ? 8 : 4;
+  void* dm = (uint8_t*)workspace + slots * nseg * (int64_t)dim * dim * elt;
+  int st = lasp2_state_apply(dtype, q, d_out, m_full, workspace, dq, slots, tokens, dim, nseg, stream);
+  if (st == LASP2_OK) st = lasp2_scan_segments(dtype, workspace, dm, slots, nseg, dim, 0, stream);
+  if (st == LASP2_OK) st = lasp2_apply_state2(dtype, v, k, dm, dk, dv, slots, tokens, dim, stream);
+  return st;
+}
+
 int lasp2h_softmax_forward(int dtype, const void* q, const void* k_full, const void* v_full, void* out, void* lse,
                            int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim, int causal, int64_t row_offset,
                            int64_t kv_chunk, int64_t kv_rank_stride, void* stream) {
@@ -303,6 +361,7 @@ int lasp2_gen_slots(int dtype, uint64_t seed, const uint64_t* tag_words_device, 
 int lasp2_debug_trace(void* buffer) {
   cudaError_t e = lasp::tc_set_trace((unsigned long long*)buffer);
   if (e == cudaSuccess) e = lasp::tc_set_trace_softmax((unsigned long long*)buffer);
+  if (e == cudaSuccess) e = lasp::tc_set_trace_flat((unsigned long long*)buffer);
   return cuda_status(e, "debug_trace");
 }
 

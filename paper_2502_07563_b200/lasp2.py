@@ -176,6 +176,13 @@ def _forward_nomask_rank(ctx, qc: torch.Tensor, kc: torch.Tensor,
                          vc: torch.Tensor) -> tuple[torch.Tensor, ActivationCache]:
     """O_t = Q_t M_{1:T} after one state all_gather (lasp2.py:208-216)."""
     qc, kc, vc = _contig(qc, kc, vc)
+    if ctx.sp_size == 1 and LOCAL_FUSED:
+        # world of one: the gather is the identity and sum_states a copy, so both
+        # passes run as one persistent launch; the gather is still issued (1 launch,
+        # as the reference accounts it)
+        out, m_full = ops.nomask_forward_local(qc, kc, vc)
+        _gather_states(ctx, m_full, "state")
+        return out, ActivationCache(q=qc, k=kc, v=vc, masked=False, m_full=m_full, state_folds=1)
     _, m_t, _ = ops.chunk_states(kc, vc)
     gathered = _unpack_gathered(_gather_states(ctx, m_t, "state"), m_t)
     m_full = ops.sum_states(gathered)
@@ -238,6 +245,10 @@ def _backward_nomask_rank(ctx, cache: ActivationCache, d_out: torch.Tensor) -> G
     _require_cache(cache, masked=False)
     (do,) = _contig(d_out)
     q = cache.q
+    if ctx.sp_size == 1 and LOCAL_FUSED:
+        dq, dk, dv = ops.nomask_backward_local(q, cache.k, cache.v, do, cache.m_full)
+        _gather_states(ctx, cache.m_full, "state_grad")  # accounting only: identity at T = 1
+        return GradientBundle(dq=dq, dk=dk, dv=dv)
     unit_bytes = q.numel() * q.element_size()
     if ctx.sp_size == 1 or unit_bytes >= _FUSE_DQ_MIN_BYTES:
         nseg = ops.num_segments(q)
@@ -253,6 +264,10 @@ def _backward_nomask_rank(ctx, cache: ActivationCache, d_out: torch.Tensor) -> G
     dk, dv = ops.apply_state2(cache.v, cache.k, dm_full)
     return GradientBundle(dq=dq, dk=dk, dv=dv)
 
+
+# world of one rank: run the unmasked layer as one persistent launch per direction
+# (lasp2_nomask_forward_local / _backward_local); False keeps the per-step kernels
+LOCAL_FUSED = True
 
 # a bf16 chunk tensor of >= 256 MB takes >= ~40 us to stream, more than a
 # state all_gather costs, so fusing dQ into the dM pass wins even with T > 1

@@ -162,6 +162,53 @@ def apply_state2(v: torch.Tensor, k: torch.Tensor, dm: torch.Tensor) -> tuple[to
     return dk, dv
 
 
+_LOCAL_WS: dict[tuple[int, int], torch.Tensor] = {}
+
+
+def local_workspace(x: torch.Tensor) -> torch.Tensor:
+    """Zero-initialised workspace of the world-of-one kernels, one per (device, stream).
+
+    The kernels leave their grid-barrier words at zero, so the buffer is reused
+    across calls on the same stream (the header's contract)."""
+    slots, n, d = _slots(x)
+    need = int(_lib.load().lasp2_local_workspace_bytes(dtype_code(x.dtype), slots, n, d, sm_count(x.device)))
+    if need < 0:
+        raise ValueError(f"no world-of-one workspace for shape {tuple(x.shape)}")
+    key = (x.device.index, torch.cuda.current_stream(x.device).cuda_stream)
+    ws = _LOCAL_WS.get(key)
+    if ws is None or ws.numel() < need:
+        ws = torch.zeros(max(need, 256), dtype=torch.uint8, device=x.device)
+        _LOCAL_WS[key] = ws
+    return ws
+
+
+def nomask_forward_local(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    """(out = q M, M = k^T v) of a world of one rank (header: lasp2_nomask_forward_local)."""
+    require_cuda(q, k, v)
+    if not (q.shape == k.shape == v.shape):
+        raise ValueError(f"q/k/v shapes differ: {tuple(q.shape)} {tuple(k.shape)} {tuple(v.shape)}")
+    slots, n, d = _slots(q)
+    out = torch.empty_like(q)
+    m_full = torch.empty((*q.shape[:2], d, d), dtype=state_dtype(q.dtype), device=q.device)
+    ws = local_workspace(q)
+    call("lasp2_nomask_forward_local", dtype_code(q.dtype), ptr(q), ptr(k), ptr(v), ptr(out), ptr(m_full), ptr(ws),
+         ws.numel(), slots, n, d, stream_ptr())
+    return out, m_full
+
+
+def nomask_backward_local(q, k, v, d_out, m_full) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    """(dq, dk, dv) of a world of one rank (header: lasp2_nomask_backward_local)."""
+    require_cuda(q, k, v, d_out, m_full)
+    if not (q.shape == k.shape == v.shape == d_out.shape):
+        raise ValueError("q/k/v/d_out shapes differ")
+    slots, n, d = _slots(q)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    ws = local_workspace(q)
+    call("lasp2_nomask_backward_local", dtype_code(q.dtype), ptr(q), ptr(k), ptr(v), ptr(d_out), ptr(m_full),
+         ptr(dq), ptr(dk), ptr(dv), ptr(ws), ws.numel(), slots, n, d, stream_ptr())
+    return dq, dk, dv
+
+
 def softmax_forward(q: torch.Tensor, k_full: torch.Tensor, v_full: torch.Tensor, causal: bool, row_offset: int,
                     kv_tokens: int, kv_chunk: int, kv_rank_stride: int) -> tuple[torch.Tensor, torch.Tensor]:
     """Softmax attention of a query chunk against (possibly rank-major) full K/V (oracle.py:136-139)."""

@@ -233,3 +233,60 @@ def test_backward_chunk_matches_separate_passes(dtype, shape, nseg):
     assert nerr(dq, rq) <= tol
     assert nerr(dk, rk) <= tol
     assert nerr(dv, rv) <= tol
+
+
+def ref_nomask_local(q, k, v, do, m_in):
+    qd, kd, vd, dod = (x.double() for x in (q, k, v, do))
+    m = kd.transpose(-1, -2) @ vd
+    dm = qd.transpose(-1, -2) @ dod
+    mi = m_in.double()
+    return m, qd @ m, dod @ mi.transpose(-1, -2), vd @ dm.transpose(-1, -2), kd @ dm
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32, torch.float64])
+@pytest.mark.parametrize("shape", [(1, 16, 4096, 128), (2, 3, 1000, 64), (1, 2, 256, 128), (1, 1, 77, 128),
+                                   (3, 50, 128, 32), (1, 16, 16384, 128)])
+def test_nomask_local_forward_backward(dtype, shape):
+    """World-of-one persistent kernels: flat (slot, block) split over all SMs, pieces
+    crossing slot boundaries, ragged last blocks, fewer blocks than SMs."""
+    if dtype != torch.bfloat16 and shape[2] > 4096:
+        pytest.skip("validation kernels: small shapes only")
+    q, k, v, do = (rand(shape, dtype, s) for s in (51, 52, 53, 54))
+    out, m = ops.nomask_forward_local(q, k, v)
+    dq, dk, dv = ops.nomask_backward_local(q, k, v, do, m)
+    rm, ro, rdq, rdk, rdv = ref_nomask_local(q, k, v, do, m)
+    tol_s = {torch.bfloat16: 1e-5, torch.float32: 1e-5, torch.float64: F64_TOL}[dtype]
+    tol_o = {torch.bfloat16: 6e-3, torch.float32: F32_TOL, torch.float64: F64_TOL}[dtype]
+    assert nerr(m, rm) <= tol_s
+    for got, ref in ((out, ro), (dq, rdq), (dk, rdk), (dv, rdv)):
+        assert nerr(got, ref) <= tol_o
+
+
+def test_nomask_local_deterministic_and_barrier_reuse():
+    """Repeated calls with different grid sizes reuse the zeroed barrier words and
+    give bitwise identical results (ordered reduction, no float atomics)."""
+    shapes = [(1, 16, 4096, 128), (1, 2, 256, 128), (1, 16, 4096, 128), (2, 3, 1000, 64)]
+    first = {}
+    for rep in range(3):
+        for shape in shapes:
+            q, k, v, do = (rand(shape, torch.bfloat16, s) for s in (61, 62, 63, 64))
+            out, m = ops.nomask_forward_local(q, k, v)
+            grads = ops.nomask_backward_local(q, k, v, do, m)
+            res = [out, m, *grads]
+            if shape in first:
+                for a, b in zip(first[shape], res):
+                    assert torch.equal(a, b)
+            else:
+                first[shape] = res
+    ws = ops.local_workspace(torch.empty(1, 16, 4096, 128, dtype=torch.bfloat16, device="cuda"))
+    torch.cuda.synchronize()
+    assert int(ws[:8].view(torch.int32)[0]) == 0  # arrival counter back at zero
+
+
+def test_nomask_local_workspace_validation():
+    x = rand((1, 2, 256, 128), torch.bfloat16, 1)
+    m = torch.empty(1, 2, 128, 128, dtype=torch.float32, device="cuda")
+    small = torch.zeros(16, dtype=torch.uint8, device="cuda")
+    with pytest.raises(ValueError, match="workspace too small"):
+        ops.call("lasp2_nomask_forward_local", _lib.BF16, ops.ptr(x), ops.ptr(x), ops.ptr(x), ops.ptr(x),
+                 ops.ptr(m), ops.ptr(small), small.numel(), 2, 256, 128, ops.stream_ptr())

@@ -260,3 +260,21 @@ def test_fused_backward_variant_matches_default():
         x = cat(getattr(g, name) for g in a.grads).float()
         y = cat(getattr(g, name) for g in b.grads).float()
         assert ((x - y).abs().max() / x.abs().max()).item() <= 1e-2
+
+
+@pytest.mark.parametrize("n,d,h", [(4096, 128, 16), (1000, 64, 3)])
+def test_world_of_one_fused_unmasked_matches_per_step_kernels(n, d, h, monkeypatch):
+    """T = 1 unmasked layer: persistent local kernels == per-step kernels (bf16) and
+    the gather is still accounted once per pass (lasp2.py:208-216, :256-267)."""
+    from paper_2502_07563_b200 import lasp2 as L
+    q, k, v, do = O.inputs(n, d, 1, h, 9)
+    q, k, v, do = (dev(x, torch.bfloat16) for x in (q, k, v, do))
+    res = {}
+    for fused in (True, False):
+        monkeypatch.setattr(L, "LOCAL_FUSED", fused)
+        it = lasp2_iteration(ChunkedSequence(q, k, v, 1), do, False)
+        assert it.run.stats.allgather_launches == 2
+        res[fused] = [it.outputs[0]] + [getattr(it.grads[0], n_) for n_ in ("dq", "dk", "dv")]
+    for a, b in zip(res[True], res[False]):
+        scale = b.double().abs().max().item()
+        assert (a.double() - b.double()).abs().max().item() <= 6e-3 * scale  # <= 1.5 bf16 ulp

@@ -23,7 +23,8 @@ ENTRY = {"tc_causal_chunk_kernel<0>": "lasp2_causal_chunk", "tc_causal_chunk_ker
          "tc_causal_chunk_kernel<2>": "lasp2_backward_chunk", "tc_fused_apply_kernel<0>": "lasp2_state_apply",
          "tc_fused_apply_kernel<1>": "lasp2_apply_state2", "tc_apply_state": "lasp2_apply_state",
          "tc_segment_states": "lasp2_segment_states", "tc_softmax_fwd": "lasp2h_softmax_forward",
-         "tc_softmax_bwd": "lasp2h_softmax_backward"}
+         "tc_softmax_bwd": "lasp2h_softmax_backward", "tc_flat_kernel<0>": "lasp2_nomask_forward_local",
+         "tc_flat_kernel<1>": "lasp2_nomask_backward_local"}
 
 
 def raw(rep):
