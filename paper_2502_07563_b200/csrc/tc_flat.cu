@@ -40,7 +40,7 @@ struct FlatArgs {
   const float* m_in;  // KIND 1: forward state M [slots][dim][dim] (phase-1 operand)
   float* total;       // phase-1 result = phase-2 state [slots][dim][dim]
   float* part;        // [grid][kmax][dim][dim] per-piece partial states
-  unsigned* gbar;     // {arrivals, generation}; zero before first use, left reusable
+  unsigned* gbar;     // {arrivals, CTAs past barrier 2}; zero before first use, left reusable
   unsigned* done;     // phase-2 producers finished (reset to 0 by the last one)
   unsigned* ctr;      // [slots] phase-2 blocks handed out per slot (reset to 0 by the last producer)
   int64_t tokens;
@@ -74,28 +74,30 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   return v;
 }
 
-// Grid-wide barrier among the epilogue warps of every CTA (all CTAs are
-// co-resident: one per SM, cooperative launch). Sense by generation count, so
-// the arrival counter returns to zero and any grid size can reuse it.
-__device__ __forceinline__ void grid_barrier(unsigned* gbar, unsigned n, int et) {
+// Grid-wide barriers among the epilogue warps of every CTA (all CTAs are
+// co-resident: one per SM, cooperative launch). gbar[0] counts arrivals over
+// the launch's two barriers (targets n and 2n: one red.add and an acquire
+// spin each); gbar[1] counts CTAs past the second one, and the last of those
+// re-arms both words for the next launch, off the critical path.
+__device__ __forceinline__ void grid_barrier(unsigned* gbar, unsigned target, int et) {
   named_bar_sync(1, kFlatEpi);
   if (et == 0) {
-    const unsigned gen = ld_acquire_u32(gbar + 1);
-    __threadfence();
-    if (atomicAdd(gbar, 1u) == n - 1) {
-      atomicExch(gbar, 0u);
-      __threadfence();
-      atomicAdd(gbar + 1, 1u);
-    } else {
-      const long long t0 = clock64();
-      while (ld_acquire_u32(gbar + 1) == gen) {
-        __nanosleep(40);
-        if (clock64() - t0 > (1ll << 36)) __trap();  // a CTA never arrived: fail loudly, do not hang
-      }
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(gbar) : "memory");
+    const long long t0 = clock64();
+    while (ld_acquire_u32(gbar) < target) {
+      __nanosleep(32);
+      if (clock64() - t0 > (1ll << 36)) __trap();  // a CTA never arrived: fail loudly, do not hang
     }
-    __threadfence();
   }
   named_bar_sync(1, kFlatEpi);
+}
+
+__device__ __forceinline__ void grid_barrier_rearm(unsigned* gbar, unsigned n, int et) {
+  if (et == 0 && atomicAdd(gbar + 1, 1u) == n - 1) {  // every CTA has left both barriers
+    gbar[0] = 0;
+    gbar[1] = 0;
+    __threadfence();
+  }
 }
 
 __device__ __forceinline__ void st_shared_u64(uint64_t* p, uint64_t v) {
@@ -420,33 +422,56 @@ __global__ void __launch_bounds__(kFlatThreads, 1) tc_flat_kernel(const __grid_c
       const int64_t E4 = (int64_t)a.slots * dd / 4, dd4 = dd / 4;
       const int64_t cstride = (int64_t)a.kmax * dd4;  // float4s between consecutive CTAs' pieces
       const float4* part4 = reinterpret_cast<const float4*>(a.part);
-      for (int64_t e = (int64_t)blockIdx.x * kFlatEpi + et; e < E4; e += nthr) {
+      // each thread owns units e and e + nthr (~2 per thread at cfg sizes): both units'
+      // partial loads are issued before their adds
+      auto unit_src = [&](int64_t e, int64_t* c_lo, int64_t* c_hi, int64_t* first) {
         const int s = (int)(e / dd4);
         const int64_t r = e - (int64_t)s * dd4;
         const int64_t fs = (int64_t)s * nb, fe = fs + nb;
-        const int64_t c_lo = ((fs + 1) * n - 1) / F, c_hi = (fe * n - 1) / F;
-        float4 acc = __ldcg(part4 + c_lo * cstride + (s - flat_lo(c_lo, F, n) / nb) * dd4 + r);
-        const float4* p = part4 + r;  // copy-first, ascending (numerics.py:71-90)
-        for (int64_t c = c_lo + 1; c <= c_hi; c += 8) {
-          float4 v[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            v[j] = c + j <= c_hi ? __ldcg(p + (c + j) * cstride) : make_float4(0.f, 0.f, 0.f, 0.f);
+        *c_lo = ((fs + 1) * n - 1) / F;
+        *c_hi = (fe * n - 1) / F;
+        *first = *c_lo * cstride + (s - flat_lo(*c_lo, F, n) / nb) * dd4 + r;
+        return r;
+      };
+      for (int64_t e = (int64_t)blockIdx.x * kFlatEpi + et; e < E4; e += 2 * nthr) {
+        const bool two = e + nthr < E4;
+        int64_t lo0, hi0, first0, lo1 = 0, hi1 = -1, first1 = 0;
+        const int64_t r0 = unit_src(e, &lo0, &hi0, &first0);
+        const int64_t r1 = two ? unit_src(e + nthr, &lo1, &hi1, &first1) : 0;
+        float4 acc0 = __ldcg(part4 + first0);  // copy-first, ascending (numerics.py:71-90)
+        float4 acc1 = two ? __ldcg(part4 + first1) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const int64_t span = lmax(hi0 - lo0, hi1 - lo1);
+        for (int64_t j0 = 1; j0 <= span; j0 += 8) {
+          float4 v0[8], v1[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            if (c + j <= c_hi) {
-              acc.x += v[j].x;
-              acc.y += v[j].y;
-              acc.z += v[j].z;
-              acc.w += v[j].w;
+            const int64_t c0 = lo0 + j0 + j, c1 = lo1 + j0 + j;
+            v0[j] = c0 <= hi0 ? __ldcg(part4 + c0 * cstride + r0) : make_float4(0.f, 0.f, 0.f, 0.f);
+            v1[j] = c1 <= hi1 ? __ldcg(part4 + c1 * cstride + r1) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (lo0 + j0 + j <= hi0) {
+              acc0.x += v0[j].x;
+              acc0.y += v0[j].y;
+              acc0.z += v0[j].z;
+              acc0.w += v0[j].w;
+            }
+            if (lo1 + j0 + j <= hi1) {
+              acc1.x += v1[j].x;
+              acc1.y += v1[j].y;
+              acc1.z += v1[j].z;
+              acc1.w += v1[j].w;
             }
           }
         }
-        reinterpret_cast<float4*>(a.total)[e] = acc;
+        reinterpret_cast<float4*>(a.total)[e] = acc0;
+        if (two) reinterpret_cast<float4*>(a.total)[e + nthr] = acc1;
       }
     }
     trace(3);
-    grid_barrier(a.gbar, gridDim.x, et);
+    grid_barrier(a.gbar, 2 * gridDim.x, et);
+    grid_barrier_rearm(a.gbar, gridDim.x, et);
     trace(4);
 
     // ---- phase 2 (dynamic blocks, in the producer's record order) ----
