@@ -172,7 +172,8 @@ int lasp2_gen_slots(int dtype, uint64_t seed, const uint64_t* tag_words_device, 
                     int64_t cols, int64_t row_offset, void* stream);
 
 /* Test hook: d (f32 128x128) = op(a) op(b)^T for bf16 128x128 tiles with the
- * UMMA descriptor convention of the fast path (a_mn / b_mn select MN-major). */
+ * UMMA descriptor convention of the fast path (a_mn / b_mn select MN-major;
+ * a_mn = 2 stages A in TMEM and runs the TS-mode MMA). */
 int lasp2_debug_probe_gemm(const void* a, const void* b, void* d, int a_mn, int b_mn, void* stream);
 
 /* Test hook: record a clock64() timeline of CTA (0,0) of the causal kernels into

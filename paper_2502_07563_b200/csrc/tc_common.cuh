@@ -101,6 +101,7 @@ struct Tracer {
   int n = 0;
   bool on;
   __device__ Tracer() : on(g_trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0) {}
+  __device__ explicit Tracer(bool cta) : on(g_trace != nullptr && cta) {}
   __device__ __forceinline__ void operator()(int ev, int blk) {
     if (on && blk >= 16 && blk < 24 && n < 64)
       rec[n++] = ((unsigned long long)ev << 56) | ((unsigned long long)blk << 48) |
@@ -113,6 +114,8 @@ struct Tracer {
 };
 #else
 struct Tracer {  // compiled out: build with -DLASP2_TRACE to record timelines
+  __device__ Tracer() {}
+  __device__ explicit Tracer(bool) {}
   __device__ __forceinline__ void operator()(int, int) {}
   __device__ __forceinline__ void flush(int) {}
 };

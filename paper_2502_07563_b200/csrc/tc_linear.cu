@@ -817,7 +817,7 @@ __global__ void __launch_bounds__(128, 1)
     mbar_init(&bars[1], 1);
     fence_barrier_init();
   }
-  if (warp == 0) tmem_alloc<128>(tmem_slot);
+  if (warp == 0) tmem_alloc<256>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -830,14 +830,33 @@ __global__ void __launch_bounds__(128, 1)
     tma_load_3d(at + kBoxBytes, &tm_a, &bars[0], 64, 0, 0);
     tma_load_3d(bt, &tm_b, &bars[0], 0, 0, 0);
     tma_load_3d(bt + kBoxBytes, &tm_b, &bars[0], 64, 0, 0);
-    mbar_wait(&bars[0], 0);
-    tc_fence_after();
-    const uint32_t idesc = idesc_bf16_f32(128, 128, a_mn, b_mn);
+  }
+  mbar_wait(&bars[0], 0);
+  if (a_mn == 2) {  // TS mode: row r of A (this thread) packed bf16x2 along K into TMEM columns [128, 192)
+    const uint32_t r = warp * 32 + lane;
+    uint32_t pk[64];
+#pragma unroll
+    for (int c = 0; c < 64; ++c)
+      pk[c] = *reinterpret_cast<const uint32_t*>(at + sw128_offset(r, 2 * c));
+    const uint32_t lane_base = tmem + ((warp * 32) << 16) + 128;
+    tmem_st_32x32b_x32(lane_base, *reinterpret_cast<uint32_t(*)[32]>(pk));
+    tmem_st_32x32b_x32(lane_base + 32, *reinterpret_cast<uint32_t(*)[32]>(pk + 32));
+    tmem_st_wait();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = idesc_bf16_f32(128, 128, a_mn == 1 ? 1 : 0, b_mn);
     const uint32_t aa = smem_u32(at), ba = smem_u32(bt);
     for (int kk = 0; kk < 8; ++kk) {
-      const uint64_t ad = a_mn ? desc_mnmajor(aa, kk) : desc_kmajor(aa, kk);
       const uint64_t bd = b_mn ? desc_mnmajor(ba, kk) : desc_kmajor(ba, kk);
-      mma_bf16_ss(tmem, ad, bd, idesc, kk > 0);
+      if (a_mn == 2) {
+        mma_bf16_ts(tmem, tmem + 128 + kk * 8, bd, idesc, kk > 0);
+      } else {
+        const uint64_t ad = a_mn ? desc_mnmajor(aa, kk) : desc_kmajor(aa, kk);
+        mma_bf16_ss(tmem, ad, bd, idesc, kk > 0);
+      }
     }
     mma_commit(&bars[1]);
   }
@@ -853,7 +872,7 @@ __global__ void __launch_bounds__(128, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc<128>(tmem);
+  if (warp == 0) tmem_dealloc<256>(tmem);
 }
 
 }  // namespace tc

@@ -105,6 +105,7 @@ __global__ void __launch_bounds__(kSmFwdThreads, 1)
     constexpr uint32_t id_qk = idesc_bf16_f32(128, 128, 0, 0);
     constexpr uint32_t id_pv = idesc_bf16_f32(128, 128, 0, 1);
     const uint32_t qa = smem_u32(qimg);
+    Tracer tr(blockIdx.x == gridDim.x - 1 && blockIdx.y == 0);
     mbar_wait(q_full, 0);
     for (int j = 0; j <= nkb; ++j) {
       if (j < nkb) {  // S_j = Q K_j^T into S[j&1]
@@ -119,11 +120,13 @@ __global__ void __launch_bounds__(kSmFwdThreads, 1)
           mma_commit(&empty[s]);
         }
         __syncwarp();
+        if (lane == 0) tr(30, j);
       }
       if (j >= 1) {  // O_{j-1} = P_{j-1} V_{j-1} into O[(j-1)&1]
         const int jb = j - 1, b = jb & 1;
         const int t = 2 * jb + 1, s = t % kKvRing;
         mbar_wait(&p_ready[b], (jb >> 1) & 1);
+        if (lane == 0) tr(32, jb);
         if (jb >= 2) mbar_wait(&o_empty[b], ((jb >> 1) - 1) & 1);
         mbar_wait(&full[s], (t / kKvRing) & 1);
         tc_fence_after();
@@ -136,8 +139,10 @@ __global__ void __launch_bounds__(kSmFwdThreads, 1)
           mma_commit(&empty[s]);
         }
         __syncwarp();
+        if (lane == 0) tr(31, jb);
       }
     }
+    if (lane == 0) tr.flush(0);
   } else {
     // ---------------- softmax / epilogue warps ----------------
     // warp w owns TMEM lanes 32*(w%4).. (query rows) and columns [64*half, +64)
@@ -153,6 +158,7 @@ __global__ void __launch_bounds__(kSmFwdThreads, 1)
 #pragma unroll
     for (int i = 0; i < 64; ++i) o_acc[i] = 0.f;
     float m_run = -INFINITY, l_run = 0.f, corr_pending = 1.f;
+    Tracer tr(blockIdx.x == gridDim.x - 1 && blockIdx.y == 0 && et == 0);
     for (int j = 0; j <= nkb; ++j) {
       float corr_this = 1.f;
       if (j < nkb) {
@@ -161,8 +167,10 @@ __global__ void __launch_bounds__(kSmFwdThreads, 1)
         int lim = (int)lmin(kTile, a.kvtok - k0) - cb;  // valid columns of this row within my half
         if (a.causal) lim = (int)lmin((int64_t)lim, gq - k0 + 1 - cb);
         const bool full = __all_sync(0xffffffffu, lim >= 64);
+        tr(45, j);
         mbar_wait(&s_full[b], (j >> 1) & 1);
         tc_fence_after();
+        tr(40, j);
         const uint32_t ts = tmem + b * 128 + lane_off + cb;
         uint32_t sr[64];
         tmem_ld_32x32b_x32(ts, *reinterpret_cast<uint32_t(*)[32]>(sr));
@@ -179,6 +187,7 @@ __global__ void __launch_bounds__(kSmFwdThreads, 1)
         }
         xchg[half * 128 + row] = pm;
         named_bar_sync(1, kSm);
+        tr(41, j);
         const float bmax = fmaxf(pm, xchg[(1 - half) * 128 + row]);
         const float m_new = fmaxf(m_run, bmax * a.scale_log2);
         corr_this = (m_run == -INFINITY) ? 0.f : ex2_approx(m_run - m_new);
@@ -202,11 +211,13 @@ __global__ void __launch_bounds__(kSmFwdThreads, 1)
         tc_fence_before();
         named_bar_sync(1, kSm);  // P complete; xchg may be rewritten
         if (et == 0) mbar_arrive(&p_ready[b]);
+        tr(42, j);
       }
       if (j >= 1) {  // fold O_{j-1} (my 64 columns) into the register accumulator
         const int jb = j - 1, b = jb & 1;
         mbar_wait(&o_full[b], (jb >> 1) & 1);
         tc_fence_after();
+        tr(43, jb);
         const uint32_t to = tmem + 256 + b * 128 + lane_off + cb;
         uint32_t r0[32], r1[32];
         tmem_ld_32x32b_x32(to, r0);
@@ -220,9 +231,11 @@ __global__ void __launch_bounds__(kSmFwdThreads, 1)
         tc_fence_before();
         named_bar_sync(1, kSm);
         if (et == 0) mbar_arrive(&o_empty[b]);
+        tr(44, jb);
       }
       corr_pending = corr_this;
     }
+    tr.flush(1);
     // epilogue: row sum over both halves, O / l -> bf16 -> staging (P[0], every PV done) -> TMA store
     xchg[half * 128 + row] = l_run;
     named_bar_sync(1, kSm);
@@ -243,6 +256,235 @@ __global__ void __launch_bounds__(kSmFwdThreads, 1)
       for (int bx = 0; bx < nbox; ++bx) tma_store_3d(&tm_o, pimg + bx * kBoxBytes, 64 * bx, (int)q0, slot);
       tma_store_commit();
       tma_store_wait_all<0>();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+// ============================================================================
+// Forward, two query tiles per CTA (A = rows [256p, 256p+128), B = the next
+// 128). Each tile has its own softmax group of four warps (one query row per
+// thread, all 128 key columns: no cross-warp row exchange) and its own TMEM
+// S and O; K_j / V_j are loaded once for both tiles. Per key block j:
+//   S_t = Q_t K_j^T                      (SS-mode MMA, TMEM)
+//   P_t = exp2(S_t*scale*log2e - m_t)    bf16 written back over S_t in TMEM
+//   O_t += P_t V_j                       (TS-mode MMA: A = P_t from TMEM)
+// The MMA warp interleaves the tiles (PV_A, S_A, PV_B, S_B), so one tile's
+// softmax runs while the tensor core works on the other. O stays in TMEM; the
+// running max is raised lazily (only when a block max exceeds it by more than
+// 2^8), and only then are O rows rescaled in place.
+// ============================================================================
+constexpr int kF2Ring = 5;
+constexpr uint32_t kSmFwd2Smem = (2 + kF2Ring) * kTileBytes + 1024 + 256;
+constexpr float kLazyRescale = 8.f;  // log2 of the largest unnormalised P
+
+// 10 warps: three share an SMSP's 16K registers, so 168 per thread is the cap
+__global__ void __launch_bounds__(kSmFwdThreads, 1)
+    tc_softmax_fwd2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                           const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
+                           SmFwdArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* qimg = smem;  // [2] Q tiles, reused as O staging at the end
+  uint8_t* ring = qimg + 2 * kTileBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kF2Ring * kTileBytes);
+  uint64_t* full = bars;              // [kF2Ring]
+  uint64_t* empty = bars + kF2Ring;   // [kF2Ring]
+  uint64_t* q_full = bars + 2 * kF2Ring;
+  uint64_t* s_full = q_full + 1;   // [2] per tile
+  uint64_t* p_ready = q_full + 3;  // [2]
+  uint64_t* o_full = q_full + 5;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + 7);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot = blockIdx.y;
+  const int npairs = gridDim.x;
+  const int pair = npairs - 1 - (int)blockIdx.x;  // longest (causal) pairs first
+  const int ntiles = (int)((a.qtok + kTile - 1) / kTile);
+  const bool has_b = 2 * pair + 1 < ntiles;
+  auto nkb_of = [&](int tile) {
+    const int64_t q0 = (int64_t)tile * kTile;
+    const int64_t end = a.causal ? lmin(a.kvtok, a.row_offset + q0 + kTile) : a.kvtok;
+    return (int)((end + kTile - 1) / kTile);
+  };
+  const int nkb_a = nkb_of(2 * pair), nkb_b = has_b ? nkb_of(2 * pair + 1) : 0;
+  const int nkb = nkb_a > nkb_b ? nkb_a : nkb_b;
+  const int nbox = a.dim > 64 ? 2 : 1;
+  const int kfeat = (a.dim + 15) / 16;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kF2Ring; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 7; ++i) mbar_init(&q_full[i], 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;  // S_A 0, S_B 128 (P_t over S_t[0,64)), O_A 256, O_B 384
+  auto s_col = [](int t) { return 128u * t; };
+  auto o_col = [](int t) { return 256u + 128u * t; };
+
+  if (warp == 0) {
+    if (elect_one()) {
+      prefetch_tmap(&tm_q);
+      prefetch_tmap(&tm_k);
+      prefetch_tmap(&tm_v);
+      mbar_arrive_expect_tx(q_full, (has_b ? 2 : 1) * nbox * kBoxBytes);
+      for (int t = 0; t < (has_b ? 2 : 1); ++t)
+        for (int bx = 0; bx < nbox; ++bx)
+          tma_load_3d(qimg + t * kTileBytes + bx * kBoxBytes, &tm_q, q_full, 64 * bx, (2 * pair + t) * kTile, slot);
+      for (int j = 0; j < nkb; ++j) {
+        int row, rank;
+        kv_coords((int64_t)j * kTile, a.chunk, &row, &rank);
+        for (int w = 0; w < 2; ++w) {
+          const int t = 2 * j + w, s = t % kF2Ring, u = t / kF2Ring;
+          if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+          uint8_t* dst = ring + s * kTileBytes;
+          mbar_arrive_expect_tx(&full[s], nbox * kBoxBytes);
+          const CUtensorMap* m = w == 0 ? &tm_k : &tm_v;
+          for (int bx = 0; bx < nbox; ++bx) tma_load_4d(dst + bx * kBoxBytes, m, &full[s], 64 * bx, row, slot, rank);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t id_qk = idesc_bf16_f32(128, 128, 0, 0);
+    constexpr uint32_t id_pv = idesc_bf16_f32(128, 128, 0, 1);
+    mbar_wait(q_full, 0);
+    for (int j = 0; j <= nkb; ++j) {
+      for (int t = 0; t < 2; ++t) {
+        const int nkb_t = t ? nkb_b : nkb_a;
+        if (j >= 1 && j - 1 < nkb_t) {  // O_t += P_t V_{j-1}
+          const int jb = j - 1, tv = 2 * jb + 1, sv = tv % kF2Ring;
+          mbar_wait(&p_ready[t], jb & 1);
+          mbar_wait(&full[sv], (tv / kF2Ring) & 1);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t va = smem_u32(ring + sv * kTileBytes);
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+              mma_bf16_ts(tmem + o_col(t), tmem + s_col(t) + kk * 8, desc_mnmajor(va, kk), id_pv,
+                          (jb > 0 || kk > 0) ? 1u : 0u);
+            mma_commit(&o_full[t]);
+            if (t == 1 || jb >= nkb_b) mma_commit(&empty[sv]);  // last reader of V_{j-1}
+          }
+          __syncwarp();
+        }
+        if (j < nkb_t) {  // S_t = Q_t K_j^T (after PV_t(j-1), which read P_t from these columns)
+          const int tk = 2 * j, sk = tk % kF2Ring;
+          mbar_wait(&full[sk], (tk / kF2Ring) & 1);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t qa = smem_u32(qimg + t * kTileBytes), ka = smem_u32(ring + sk * kTileBytes);
+            for (int kk = 0; kk < kfeat; ++kk)
+              mma_bf16_ss(tmem + s_col(t), desc_kmajor(qa, kk), desc_kmajor(ka, kk), id_qk, kk > 0);
+            mma_commit(&s_full[t]);
+            if (t == 1 || j >= nkb_b) mma_commit(&empty[sk]);  // last reader of K_j
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else {
+    // ---------------- softmax groups: warps 2-5 tile A, 6-9 tile B ----------------
+    const int t = (warp - 2) >> 2;
+    const int nkb_t = t == 0 ? nkb_a : nkb_b;
+    const uint32_t qd = warp & 3;
+    const uint32_t row = qd * 32 + lane;
+    const uint32_t lane_off = (qd * 32) << 16;
+    const int gt = threadIdx.x - 64 - 128 * t;  // thread index within the group
+    const int64_t q0 = (int64_t)(2 * pair + t) * kTile;
+    const int64_t gq = a.row_offset + q0 + row;  // global query position
+    const uint32_t ts = tmem + s_col(t) + lane_off, to = tmem + o_col(t) + lane_off;
+    float m_run = -INFINITY, l_run = 0.f;
+    if (t == 0 || has_b) {
+      for (int j = 0; j < nkb_t; ++j) {
+        const int64_t k0 = (int64_t)j * kTile;
+        int lim = (int)lmin(kTile, a.kvtok - k0);
+        if (a.causal) lim = (int)lmin((int64_t)lim, gq - k0 + 1);
+        const bool full_blk = __all_sync(0xffffffffu, lim >= kTile);
+        mbar_wait(&s_full[t], j & 1);
+        tc_fence_after();
+        uint32_t sr[128];
+#pragma unroll
+        for (int c = 0; c < 128; c += 32) tmem_ld_32x32b_x32(ts + c, *reinterpret_cast<uint32_t(*)[32]>(sr + c));
+        tmem_ld_wait();
+        float bm = -INFINITY;
+        if (full_blk) {
+#pragma unroll
+          for (int i = 0; i < 128; ++i) bm = fmaxf(bm, __uint_as_float(sr[i]));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 128; ++i)
+            if (i < lim) bm = fmaxf(bm, __uint_as_float(sr[i]));
+        }
+        const float mc = bm * a.scale_log2;
+        const bool need = mc > m_run + kLazyRescale;
+        const float m_new = need ? mc : m_run;
+        const float corr = (need && m_run != -INFINITY) ? ex2_approx(m_run - m_new) : (need ? 0.f : 1.f);
+        float psum = 0.f;
+#pragma unroll
+        for (int c = 0; c < 128; c += 16) {
+          uint32_t pk[8];
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) {
+            const bool ok0 = full_blk || c + i < lim, ok1 = full_blk || c + i + 1 < lim;
+            const float p0 = ok0 ? ex2_approx(fmaf(__uint_as_float(sr[c + i]), a.scale_log2, -m_new)) : 0.f;
+            const float p1 = ok1 ? ex2_approx(fmaf(__uint_as_float(sr[c + i + 1]), a.scale_log2, -m_new)) : 0.f;
+            psum += p0 + p1;
+            pk[i >> 1] = pack_bf16x2(p0, p1);
+          }
+          tmem_st_32x32b_x8(ts + (c >> 1), pk);
+        }
+        if (j > 0 && __any_sync(0xffffffffu, need)) {  // raise this warp's rows' max: rescale O in TMEM
+          mbar_wait(&o_full[t], (j - 1) & 1);  // PV_t(j-1) complete
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < 128; c += 32) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(to + c, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * corr);
+            tmem_st_32x32b_x32(to + c, r);
+          }
+        }
+        l_run = l_run * corr + psum;
+        m_run = m_new;
+        tmem_st_wait();
+        tc_fence_before();
+        named_bar_sync(1 + t, 128);
+        if (gt == 0) mbar_arrive(&p_ready[t]);
+      }
+      // epilogue: O / l -> bf16 -> staging (this tile's Q image) -> TMA store
+      mbar_wait(&o_full[t], (nkb_t - 1) & 1);
+      tc_fence_after();
+      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+      uint8_t* stg = qimg + t * kTileBytes;
+#pragma unroll 1
+      for (int c = 0; c < 128; c += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(to + c, r);
+        tmem_ld_wait();
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * inv;
+        st_row32_bf16(stg, row, c, v);
+      }
+      if (q0 + row < a.qtok)
+        a.lse[(int64_t)slot * a.qtok + q0 + row] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
+      fence_proxy_async_smem();
+      named_bar_sync(1 + t, 128);
+      if (gt == 0) {
+        for (int bx = 0; bx < nbox; ++bx) tma_store_3d(&tm_o, stg + bx * kBoxBytes, 64 * bx, (int)q0, slot);
+        tma_store_commit();
+        tma_store_wait_all<0>();
+      }
     }
   }
   tc_fence_before();
@@ -591,10 +833,17 @@ cudaError_t tc_softmax_forward(const void* q, const void* kf, const void* vf, vo
   if ((e = make_tmap_4d(&mk, kf, ranks, slots, kv_chunk, dim, kv_rank_stride)) != cudaSuccess) return e;
   if ((e = make_tmap_4d(&mv, vf, ranks, slots, kv_chunk, dim, kv_rank_stride)) != cudaSuccess) return e;
   if ((e = make_tmap_3d(&mo, out, slots, qtok, dim)) != cudaSuccess) return e;
-  if ((e = set_smem_once((const void*)tc::tc_softmax_fwd_kernel, tc::kSmFwdSmem)) != cudaSuccess) return e;
   tc::SmFwdArgs a{lse, qtok, kvtok, kv_chunk, row_offset, dim, causal, 1.4426950408889634f / sqrtf((float)dim)};
-  dim3 grid((unsigned)((qtok + 127) / 128), (unsigned)slots);
-  tc::tc_softmax_fwd_kernel<<<grid, tc::kSmFwdThreads, tc::kSmFwdSmem, s>>>(mq, mk, mv, mo, a);
+  static const bool one_tile = std::getenv("LASP2_SOFTMAX_FWD1") != nullptr;  // previous kernel, for comparison
+  if (one_tile) {
+    if ((e = set_smem_once((const void*)tc::tc_softmax_fwd_kernel, tc::kSmFwdSmem)) != cudaSuccess) return e;
+    dim3 grid((unsigned)((qtok + 127) / 128), (unsigned)slots);
+    tc::tc_softmax_fwd_kernel<<<grid, tc::kSmFwdThreads, tc::kSmFwdSmem, s>>>(mq, mk, mv, mo, a);
+    return cudaGetLastError();
+  }
+  if ((e = set_smem_once((const void*)tc::tc_softmax_fwd2_kernel, tc::kSmFwd2Smem)) != cudaSuccess) return e;
+  dim3 grid((unsigned)((qtok + 255) / 256), (unsigned)slots);
+  tc::tc_softmax_fwd2_kernel<<<grid, tc::kSmFwdThreads, tc::kSmFwd2Smem, s>>>(mq, mk, mv, mo, a);
   return cudaGetLastError();
 }
 

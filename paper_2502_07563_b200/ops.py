@@ -242,7 +242,8 @@ def softmax_backward(q, k_full, v_full, out, lse, d_out, causal: bool, row_offse
     return dq
 
 
-def probe_gemm(a: torch.Tensor, b: torch.Tensor, a_mn: bool, b_mn: bool) -> torch.Tensor:
+def probe_gemm(a: torch.Tensor, b: torch.Tensor, a_mn: int, b_mn: bool) -> torch.Tensor:
+    """D = op(A) op(B)^T for one 128^3 tile; a_mn 0/1 = K/MN-major smem A, 2 = A from TMEM."""
     require_cuda(a, b)
     d = torch.empty((128, 128), dtype=torch.float32, device=a.device)
     call("lasp2_debug_probe_gemm", ptr(a), ptr(b), ptr(d), int(a_mn), int(b_mn), stream_ptr())

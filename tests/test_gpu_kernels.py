@@ -60,12 +60,13 @@ def ref_causal(q, k, v, seg, base, nseg, reverse, transpose):
     return out
 
 
-@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1), (2, 0), (2, 1)])
 def test_probe_gemm_descriptor_conventions(a_mn, b_mn):
+    """a_mn 2: A staged into TMEM (bf16 pairs along K) and read by the TS-mode MMA."""
     a = rand((128, 128), torch.bfloat16, 1)
     b = rand((128, 128), torch.bfloat16, 2)
-    d = ops.probe_gemm(a, b, bool(a_mn), bool(b_mn))
-    A = a.double().T if a_mn else a.double()  # op(A): [M][K]
+    d = ops.probe_gemm(a, b, a_mn, bool(b_mn))
+    A = a.double().T if a_mn == 1 else a.double()  # op(A): [M][K]
     B = b.double().T if b_mn else b.double()  # op(B): [N][K]
     ref = A @ B.T
     torch.cuda.synchronize()
