@@ -355,6 +355,7 @@ __global__ void __launch_bounds__(kSmFwdThreads, 1)
   } else if (warp == 1) {
     constexpr uint32_t id_qk = idesc_bf16_f32(128, 128, 0, 0);
     constexpr uint32_t id_pv = idesc_bf16_f32(128, 128, 0, 1);
+    Tracer tr(blockIdx.x == 0 && blockIdx.y == 0);
     mbar_wait(q_full, 0);
     for (int j = 0; j <= nkb; ++j) {
       for (int t = 0; t < 2; ++t) {
@@ -374,6 +375,7 @@ __global__ void __launch_bounds__(kSmFwdThreads, 1)
             if (t == 1 || jb >= nkb_b) mma_commit(&empty[sv]);  // last reader of V_{j-1}
           }
           __syncwarp();
+          if (lane == 0) tr(50 + 2 * t, jb);
         }
         if (j < nkb_t) {  // S_t = Q_t K_j^T (after PV_t(j-1), which read P_t from these columns)
           const int tk = 2 * j, sk = tk % kF2Ring;
@@ -387,9 +389,11 @@ __global__ void __launch_bounds__(kSmFwdThreads, 1)
             if (t == 1 || j >= nkb_b) mma_commit(&empty[sk]);  // last reader of K_j
           }
           __syncwarp();
+          if (lane == 0) tr(51 + 2 * t, j);
         }
       }
     }
+    if (lane == 0) tr.flush(0);
   } else {
     // ---------------- softmax groups: warps 2-5 tile A, 6-9 tile B ----------------
     const int t = (warp - 2) >> 2;
@@ -402,6 +406,7 @@ __global__ void __launch_bounds__(kSmFwdThreads, 1)
     const int64_t gq = a.row_offset + q0 + row;  // global query position
     const uint32_t ts = tmem + s_col(t) + lane_off, to = tmem + o_col(t) + lane_off;
     float m_run = -INFINITY, l_run = 0.f;
+    Tracer tr(blockIdx.x == 0 && blockIdx.y == 0 && gt == 0);
     if (t == 0 || has_b) {
       for (int j = 0; j < nkb_t; ++j) {
         const int64_t k0 = (int64_t)j * kTile;
@@ -410,24 +415,30 @@ __global__ void __launch_bounds__(kSmFwdThreads, 1)
         const bool full_blk = __all_sync(0xffffffffu, lim >= kTile);
         mbar_wait(&s_full[t], j & 1);
         tc_fence_after();
+        tr(60 + 2 * t, j);
         uint32_t sr[128];
 #pragma unroll
         for (int c = 0; c < 128; c += 32) tmem_ld_32x32b_x32(ts + c, *reinterpret_cast<uint32_t(*)[32]>(sr + c));
         tmem_ld_wait();
-        float bm = -INFINITY;
+        // row max as 8 independent chains (a single fmaxf chain is 128 dependent ops)
+        float mx[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) mx[u] = -INFINITY;
         if (full_blk) {
 #pragma unroll
-          for (int i = 0; i < 128; ++i) bm = fmaxf(bm, __uint_as_float(sr[i]));
+          for (int i = 0; i < 128; ++i) mx[i & 7] = fmaxf(mx[i & 7], __uint_as_float(sr[i]));
         } else {
 #pragma unroll
           for (int i = 0; i < 128; ++i)
-            if (i < lim) bm = fmaxf(bm, __uint_as_float(sr[i]));
+            if (i < lim) mx[i & 7] = fmaxf(mx[i & 7], __uint_as_float(sr[i]));
         }
+        const float bm = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                               fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
         const float mc = bm * a.scale_log2;
         const bool need = mc > m_run + kLazyRescale;
         const float m_new = need ? mc : m_run;
         const float corr = (need && m_run != -INFINITY) ? ex2_approx(m_run - m_new) : (need ? 0.f : 1.f);
-        float psum = 0.f;
+        float ps[4] = {0.f, 0.f, 0.f, 0.f};  // row sum as 4 independent chains
 #pragma unroll
         for (int c = 0; c < 128; c += 16) {
           uint32_t pk[8];
@@ -436,11 +447,12 @@ __global__ void __launch_bounds__(kSmFwdThreads, 1)
             const bool ok0 = full_blk || c + i < lim, ok1 = full_blk || c + i + 1 < lim;
             const float p0 = ok0 ? ex2_approx(fmaf(__uint_as_float(sr[c + i]), a.scale_log2, -m_new)) : 0.f;
             const float p1 = ok1 ? ex2_approx(fmaf(__uint_as_float(sr[c + i + 1]), a.scale_log2, -m_new)) : 0.f;
-            psum += p0 + p1;
+            ps[(i >> 1) & 3] += p0 + p1;
             pk[i >> 1] = pack_bf16x2(p0, p1);
           }
           tmem_st_32x32b_x8(ts + (c >> 1), pk);
         }
+        const float psum = (ps[0] + ps[1]) + (ps[2] + ps[3]);
         if (j > 0 && __any_sync(0xffffffffu, need)) {  // raise this warp's rows' max: rescale O in TMEM
           mbar_wait(&o_full[t], (j - 1) & 1);  // PV_t(j-1) complete
           tc_fence_after();
@@ -460,7 +472,9 @@ __global__ void __launch_bounds__(kSmFwdThreads, 1)
         tc_fence_before();
         named_bar_sync(1 + t, 128);
         if (gt == 0) mbar_arrive(&p_ready[t]);
+        tr(61 + 2 * t, j);
       }
+      tr.flush(1 + t);
       // epilogue: O / l -> bf16 -> staging (this tile's Q image) -> TMA store
       mbar_wait(&o_full[t], (nkb_t - 1) & 1);
       tc_fence_after();
@@ -525,6 +539,17 @@ struct SmBwdArgs {
   float scale_log2;  // log2(e)/sqrt(d)
 };
 
+// P and dS of this thread's row (64 columns from c0) as packed bf16 pairs -> SW128 image
+__device__ __forceinline__ void store_row64_packed(uint8_t* img, uint32_t row, int c0, const uint32_t* pk) {
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const uint32_t off = sw128_offset(row, c0 + 8 * u);
+    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(smem_u32(img + off)), "r"(pk[4 * u]),
+                 "r"(pk[4 * u + 1]), "r"(pk[4 * u + 2]), "r"(pk[4 * u + 3])
+                 : "memory");
+  }
+}
+
 __global__ void __launch_bounds__(kSmBwdThreads, 1)
     tc_softmax_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                           const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
@@ -533,18 +558,20 @@ __global__ void __launch_bounds__(kSmBwdThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* kimg = smem;
   uint8_t* vimg = kimg + kTileBytes;
-  uint8_t* ring = vimg + kTileBytes;
+  uint8_t* ring = vimg + kTileBytes;  // [kQRing]: Q_i, dO_i, Q_{i+1}, ...
   uint8_t* pimg = ring + kQRing * kTileBytes;
   uint8_t* dsimg = pimg + kTileBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(dsimg + kTileBytes);
   uint64_t* full = bars;              // [kQRing]
   uint64_t* empty = bars + kQRing;    // [kQRing]
   uint64_t* kv_full = bars + 2 * kQRing;
-  uint64_t* sdp_full = kv_full + 1;
-  uint64_t* ds_ready = kv_full + 2;
-  uint64_t* dq_full = kv_full + 3;
-  uint64_t* dq_empty = kv_full + 4;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_full + 5);
+  uint64_t* s_full = kv_full + 1;     // S_i in TMEM
+  uint64_t* dp_full = kv_full + 2;    // dP_i in TMEM
+  uint64_t* ds_ready = kv_full + 3;   // P_i / dS_i images written (one arrival per column half)
+  uint64_t* dq_full = kv_full + 4;    // dQ_i partial in TMEM (the S columns)
+  uint64_t* dq_empty = kv_full + 5;   // ... read out by both halves
+  uint64_t* pds_free = kv_full + 6;   // dV_i, dK_i done: images reusable as dQ staging
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_full + 7);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kb = blockIdx.x, slot = blockIdx.y;
@@ -565,14 +592,14 @@ __global__ void __launch_bounds__(kSmBwdThreads, 1)
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    for (int i = 0; i < 5; ++i) mbar_init(&kv_full[i], 1);
+    for (int i = 0; i < 7; ++i) mbar_init(&kv_full[i], (i == 3 || i == 5) ? 2 : 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;  // S/dQ 0, dP 128, dV 256, dK 384
+  const uint32_t tmem = *tmem_slot;  // S / dQ 0, dP 128, dV 256, dK 384
   const uint32_t t_s = tmem, t_dp = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 384;
 
   if (warp == 0) {
@@ -593,7 +620,7 @@ __global__ void __launch_bounds__(kSmBwdThreads, 1)
           if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
           uint8_t* dst = ring + s * kTileBytes;
           mbar_arrive_expect_tx(&full[s], nbox * kBoxBytes);
-          const CUtensorMap* m = w == 0 ? &tm_do : &tm_q;  // dO first: dP is issued first
+          const CUtensorMap* m = w == 0 ? &tm_q : &tm_do;  // Q_{i+1} lands while block i is in use
           for (int bx = 0; bx < nbox; ++bx) tma_load_3d(dst + bx * kBoxBytes, m, &full[s], 64 * bx, qrow, slot);
         }
       }
@@ -604,173 +631,183 @@ __global__ void __launch_bounds__(kSmBwdThreads, 1)
       constexpr uint32_t id_mm = idesc_bf16_f32(128, 128, 1, 1);  // dV, dK (A = P^T / dS^T, B = dO / Q)
       constexpr uint32_t id_km = idesc_bf16_f32(128, 128, 0, 1);  // dQ (A = dS, B = K)
       const uint32_t ka = smem_u32(kimg), va = smem_u32(vimg), pa = smem_u32(pimg), dsa = smem_u32(dsimg);
-      mbar_wait(kv_full, 0);
-      // S_i, dP_i -> [epilogue P, dS] -> dV, dK, dQ_i -> dP_{i+1} (overlaps the dQ_i drain) -> S_{i+1}
-      // ring order per query block: tile 2i = dO_i, tile 2i+1 = Q_i
-      auto issue_dp = [&](int i) {
-        const int tdo = 2 * i;
-        const int sdo = tdo % kQRing;
-        mbar_wait(&full[sdo], (tdo / kQRing) & 1);
-        tc_fence_after();
-        if (elect_one()) {
-          const uint32_t doa = smem_u32(ring + sdo * kTileBytes);
-          for (int kk = 0; kk < kfeat; ++kk)
-            mma_bf16_ss(t_dp, desc_kmajor(doa, kk), desc_kmajor(va, kk), id_kk, kk > 0);
-        }
-        __syncwarp();
+      auto tile = [&](int t) {
+        mbar_wait(&full[t % kQRing], (t / kQRing) & 1);
+        return smem_u32(ring + (t % kQRing) * kTileBytes);
       };
       auto issue_s = [&](int i) {
-        const int tq = 2 * i + 1, sq = tq % kQRing;
-        mbar_wait(&full[sq], (tq / kQRing) & 1);
-        if (i > 0) mbar_wait(dq_empty, (i - 1) & 1);  // S/dQ columns drained
+        const uint32_t qa = tile(2 * i);
         tc_fence_after();
         if (elect_one()) {
-          const uint32_t qa = smem_u32(ring + sq * kTileBytes);
           for (int kk = 0; kk < kfeat; ++kk) mma_bf16_ss(t_s, desc_kmajor(qa, kk), desc_kmajor(ka, kk), id_kk, kk > 0);
-          mma_commit(sdp_full);
+          mma_commit(s_full);
         }
         __syncwarp();
       };
-      Tracer tr;
-      issue_dp(0);
+      auto issue_dp = [&](int i) {
+        const uint32_t doa = tile(2 * i + 1);
+        tc_fence_after();
+        if (elect_one()) {
+          for (int kk = 0; kk < kfeat; ++kk)
+            mma_bf16_ss(t_dp, desc_kmajor(doa, kk), desc_kmajor(va, kk), id_kk, kk > 0);
+          mma_commit(dp_full);
+        }
+        __syncwarp();
+      };
+      mbar_wait(kv_full, 0);
       issue_s(0);
+      issue_dp(0);
+      // per query block: dQ_i first (the softmax warps drain it while dV_i / dK_i run), then
+      // S_{i+1} (Q_{i+1} is already resident) and dP_{i+1}
       for (int i = 0; i < nq; ++i) {
-        if (lane == 0) tr(10, i);
-        const int tdo = 2 * i, tq = tdo + 1;
-        const int sq = tq % kQRing, sdo = tdo % kQRing;
-        const uint32_t qa = smem_u32(ring + sq * kTileBytes), doa = smem_u32(ring + sdo * kTileBytes);
         mbar_wait(ds_ready, i & 1);
         tc_fence_after();
-        if (lane == 0) tr(11, i);
         if (elect_one()) {
+          const uint32_t qa = smem_u32(ring + ((2 * i) % kQRing) * kTileBytes);
+          const uint32_t doa = smem_u32(ring + ((2 * i + 1) % kQRing) * kTileBytes);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) mma_bf16_ss(t_s, desc_kmajor(dsa, kk), desc_mnmajor(ka, kk), id_km, kk > 0);
+          mma_commit(dq_full);
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
             mma_bf16_ss(t_dv, desc_mnmajor(pa, kk), desc_mnmajor(doa, kk), id_mm, (i > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
             mma_bf16_ss(t_dk, desc_mnmajor(dsa, kk), desc_mnmajor(qa, kk), id_mm, (i > 0 || kk > 0) ? 1u : 0u);
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) mma_bf16_ss(t_s, desc_kmajor(dsa, kk), desc_mnmajor(ka, kk), id_km, kk > 0);
-          mma_commit(&empty[sq]);
-          mma_commit(&empty[sdo]);
-          mma_commit(dq_full);
+          mma_commit(&empty[(2 * i) % kQRing]);
+          mma_commit(&empty[(2 * i + 1) % kQRing]);
+          mma_commit(pds_free);
         }
         __syncwarp();
-        if (lane == 0) tr(12, i);
         if (i + 1 < nq) {
-          issue_dp(i + 1);  // dP columns were drained at ds_ready(i)
-          if (lane == 0) tr(13, i);
+          mbar_wait(dq_empty, i & 1);  // dQ_i left the S columns
           issue_s(i + 1);
-          if (lane == 0) tr(14, i);
+          issue_dp(i + 1);
         }
       }
-      if (lane == 0) tr.flush(0);
     }
   } else {
+    // two independent column halves (warps 2-5: columns 0-63, warps 6-9: 64-127), one query row
+    // per thread. Half h stages its dQ columns into P box h and dS box h — exactly the smem it
+    // rewrites next — so it only ever waits on its own bulk reduce reads.
+    const int h = (warp - 2) >> 2;
     const int qd = warp & 3;
-    const int half = (warp - 2) >> 2;
-    const int cb = 64 * half;
+    const int cb = 64 * h;
     const uint32_t row = qd * 32 + lane;
     const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
-    const int et = threadIdx.x - 64;
-    constexpr uint32_t kSm = kSmBwdThreads - 64;
-    // raw row statistics of query block i (loads only: the values are consumed one block later)
-    auto row_stats = [&](int i, float* lse, float* dl) {
+    const int eh = threadIdx.x - 64 - 128 * h;  // thread index within the half
+    const uint32_t bar_id = 1 + h;
+    uint8_t* stg0 = pimg + h * kBoxBytes;   // dQ columns [cb, cb+32)
+    uint8_t* stg1 = dsimg + h * kBoxBytes;  // dQ columns [cb+32, cb+64)
+    float lse_next = 0.f, dl_next = 0.f;
+    auto row_stats = [&](int i) {
       const int64_t ql = (int64_t)(qb0 + i) * kTile + row;
-      const bool ok = i < nq && ql < a.qtok;
-      const int64_t idx = ok ? (int64_t)slot * a.qtok + ql : 0;
-      *lse = __ldg(a.lse + idx);
-      *dl = __ldg(a.delta + idx);
+      const int64_t idx = (i < nq && ql < a.qtok) ? (int64_t)slot * a.qtok + ql : 0;
+      lse_next = __ldg(a.lse + idx);
+      dl_next = __ldg(a.delta + idx);
     };
-    float lse2_next, dl_next;
-    Tracer tr;
-    row_stats(0, &lse2_next, &dl_next);
+    row_stats(0);
     for (int i = 0; i < nq; ++i) {
-      const int64_t qloc = (int64_t)(qb0 + i) * kTile + row;  // local query row of this thread
+      const int64_t qloc = (int64_t)(qb0 + i) * kTile + row;
       const bool qok = qloc < a.qtok;
-      const int64_t gq = a.row_offset + qloc;
-      const float lse2 = qok ? lse2_next * 1.4426950408889634f : 0.f, dl = qok ? dl_next : 0.f;
-      row_stats(i + 1, &lse2_next, &dl_next);  // prefetch the next block's row statistics
-      // valid key columns (within my 64-column half) for this query row
+      const float lse2 = qok ? lse_next * 1.4426950408889634f : 0.f, dl = qok ? dl_next : 0.f;
+      row_stats(i + 1);
       int lim = qok ? (int)lmin(kTile, a.kvtok - k0) - cb : 0;
-      if (a.causal) lim = (int)lmin((int64_t)lim, gq - k0 + 1 - cb);
+      if (a.causal) lim = (int)lmin((int64_t)lim, a.row_offset + qloc - k0 + 1 - cb);
       const bool full = __all_sync(0xffffffffu, lim >= 64);
       const bool none = __all_sync(0xffffffffu, lim <= 0);
-      if (et == 0) tr(20, i);
-      mbar_wait(sdp_full, i & 1);
+      // P = exp2(S*scale*log2e - lse*log2e) as bf16 pairs (needs only S)
+      uint32_t ppk[32], dpk[32];
+      mbar_wait(s_full, i & 1);
       tc_fence_after();
-      if (et == 0) tr(21, i);
-      if (i > 0) {  // the previous block's dQ reduce has finished reading the staging (= P/dS images)
-        if (et == 0) tma_store_wait_read<0>();
-        named_bar_sync(1, kSm);
-      }
-      // P/dS images are free: the previous block's dq_full (all its MMAs) was waited below
-#pragma unroll 1
-      for (int c = 0; c < 64; c += 32) {
-        const int c0 = cb + c;
-        float pv[32], dsv[32];
-        if (none) {
+      if (none) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) pv[e] = dsv[e] = 0.f;
-        } else {
-          uint32_t rs[32], rp[32];
-          tmem_ld_32x32b_x32(t_s + lane_off + c0, rs);
-          tmem_ld_32x32b_x32(t_dp + lane_off + c0, rp);
+        for (int e = 0; e < 32; ++e) ppk[e] = 0u;
+      } else {
+#pragma unroll
+        for (int c = 0; c < 64; c += 32) {
+          uint32_t rs[32];
+          tmem_ld_32x32b_x32(t_s + lane_off + cb + c, rs);
           tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const bool ok = full || c + e < lim;
-            const float p = ok ? ex2_approx(fmaf(__uint_as_float(rs[e]), a.scale_log2, -lse2)) : 0.f;
-            pv[e] = p;
-            dsv[e] = p * (__uint_as_float(rp[e]) - dl);
+          for (int e = 0; e < 32; e += 2) {
+            const bool ok0 = full || c + e < lim, ok1 = full || c + e + 1 < lim;
+            const float p0 = ok0 ? ex2_approx(fmaf(__uint_as_float(rs[e]), a.scale_log2, -lse2)) : 0.f;
+            const float p1 = ok1 ? ex2_approx(fmaf(__uint_as_float(rs[e + 1]), a.scale_log2, -lse2)) : 0.f;
+            ppk[(c + e) >> 1] = pack_bf16x2(p0, p1);
           }
         }
-        st_row32_bf16(pimg, row, c0, pv);
-        st_row32_bf16(dsimg, row, c0, dsv);
       }
-      fence_proxy_async_smem();
-      tc_fence_before();
-      named_bar_sync(1, kSm);
-      if (et == 0) mbar_arrive(ds_ready);
-      if (et == 0) tr(22, i);
-      // dQ partial (my 64 columns) -> fp32 SW128 staging in the (now free) P+dS region ->
-      // one TMA bulk reduce-add per 32-column box into the fp32 accumulator
-      mbar_wait(dq_full, i & 1);
+      // dS = P o (dP - D)
+      mbar_wait(dp_full, i & 1);
       tc_fence_after();
-      if (et == 0) tr(23, i);
-      uint8_t* stg = pimg;  // P and dS images are contiguous: 64 KB = 4 boxes of 128 x 32 fp32
-#pragma unroll 1
-      for (int c = 0; c < 64; c += 32) {
-        const int c0 = cb + c;
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(t_s + lane_off + c0, r);
-        tmem_ld_wait();
-        uint8_t* box = stg + (c0 >> 5) * 16384 + row * 128;
+      if (none) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint32_t off = (uint32_t)((u ^ (row & 7)) * 16);
-          asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(smem_u32(box + off)),
-                       "f"(__uint_as_float(r[4 * u]) * a.scale), "f"(__uint_as_float(r[4 * u + 1]) * a.scale),
-                       "f"(__uint_as_float(r[4 * u + 2]) * a.scale), "f"(__uint_as_float(r[4 * u + 3]) * a.scale)
-                       : "memory");
+        for (int e = 0; e < 32; ++e) dpk[e] = 0u;
+      } else {
+#pragma unroll
+        for (int c = 0; c < 64; c += 32) {
+          uint32_t rp[32];
+          tmem_ld_32x32b_x32(t_dp + lane_off + cb + c, rp);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            const uint32_t pp = ppk[(c + e) >> 1];
+            const float p0 = __uint_as_float(pp << 16), p1 = __uint_as_float(pp & 0xFFFF0000u);
+            dpk[(c + e) >> 1] =
+                pack_bf16x2(p0 * (__uint_as_float(rp[e]) - dl), p1 * (__uint_as_float(rp[e + 1]) - dl));
+          }
         }
       }
+      // the previous block's dQ reduce has read this half's staging (= its P / dS boxes)
+      if (i > 0) {
+        if (eh == 0) tma_store_wait_read<0>();
+        named_bar_sync(bar_id, 128);
+      }
+      store_row64_packed(pimg, row, cb, ppk);
+      store_row64_packed(dsimg, row, cb, dpk);
       fence_proxy_async_smem();
       tc_fence_before();
-      named_bar_sync(1, kSm);
-      if (et == 0) {
-        mbar_arrive(dq_empty);
+      named_bar_sync(bar_id, 128);
+      if (eh == 0) mbar_arrive(ds_ready);
+      // dQ_i partial (this half's 64 columns) out of TMEM: frees the S columns for S_{i+1}
+      mbar_wait(dq_full, i & 1);
+      tc_fence_after();
+      uint32_t dq0[32], dq1[32];
+      tmem_ld_32x32b_x32(t_s + lane_off + cb, dq0);
+      tmem_ld_32x32b_x32(t_s + lane_off + cb + 32, dq1);
+      tmem_ld_wait();
+      tc_fence_before();
+      named_bar_sync(bar_id, 128);
+      if (eh == 0) mbar_arrive(dq_empty);
+      // stage (fp32, SW128 boxes of 32 columns) once dV_i / dK_i have read the images, then
+      // one TMA bulk reduce-add per box into the fp32 accumulator
+      mbar_wait(pds_free, i & 1);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t off = row * 128 + (uint32_t)((u ^ (row & 7)) * 16);
+        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(smem_u32(stg0 + off)),
+                     "f"(__uint_as_float(dq0[4 * u]) * a.scale), "f"(__uint_as_float(dq0[4 * u + 1]) * a.scale),
+                     "f"(__uint_as_float(dq0[4 * u + 2]) * a.scale), "f"(__uint_as_float(dq0[4 * u + 3]) * a.scale)
+                     : "memory");
+        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(smem_u32(stg1 + off)),
+                     "f"(__uint_as_float(dq1[4 * u]) * a.scale), "f"(__uint_as_float(dq1[4 * u + 1]) * a.scale),
+                     "f"(__uint_as_float(dq1[4 * u + 2]) * a.scale), "f"(__uint_as_float(dq1[4 * u + 3]) * a.scale)
+                     : "memory");
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(bar_id, 128);
+      if (eh == 0) {
         const int qrow = (qb0 + i) * kTile;
-        for (int bx = 0; bx < (a.dim + 31) / 32; ++bx) tma_reduce_add_3d(&tm_dq, stg + bx * 16384, 32 * bx, qrow, slot);
+        if (cb < a.dim) tma_reduce_add_3d(&tm_dq, stg0, cb, qrow, slot);
+        if (cb + 32 < a.dim) tma_reduce_add_3d(&tm_dq, stg1, cb + 32, qrow, slot);
         tma_store_commit();
-        tr(24, i);
       }
     }
-    if (et == 0) {
-      tma_store_wait_all<0>();
-      tr.flush(1);
-    }
+    if (eh == 0) tma_store_wait_all<0>();
     // dK / dV rows of this key block (one key per thread, my 64 columns) -> fp32 contributions
+    // (pds_free of the last block was awaited above: every MMA is complete)
+    tc_fence_after();
     const int64_t key = k0 + row;
     if (key < a.kvtok) {
       const int64_t off = (key / a.chunk) * a.grad_rank_stride + ((int64_t)slot * a.chunk + key % a.chunk) * a.dim;
@@ -860,13 +897,13 @@ cudaError_t tc_softmax_backward(const void* q, const void* kf, const void* vf, c
   float* dq_acc = delta + ((slots * qtok + 63) / 64) * 64;
   cudaError_t e = softmax_delta_bf16(o, d_out, delta, slots * qtok, dim, s);
   if (e != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(dq_acc, 0, (size_t)slots * qtok * dim * 4, s)) != cudaSuccess) return e;
   CUtensorMap mq, mdo, mk, mv;
   const int64_t ranks = kvtok / kv_chunk;
   if ((e = make_tmap_3d(&mq, q, slots, qtok, dim)) != cudaSuccess) return e;
   if ((e = make_tmap_3d(&mdo, d_out, slots, qtok, dim)) != cudaSuccess) return e;
   if ((e = make_tmap_4d(&mk, kf, ranks, slots, kv_chunk, dim, kv_rank_stride)) != cudaSuccess) return e;
   if ((e = make_tmap_4d(&mv, vf, ranks, slots, kv_chunk, dim, kv_rank_stride)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(dq_acc, 0, (size_t)slots * qtok * dim * 4, s)) != cudaSuccess) return e;
   CUtensorMap mdq;
   if ((e = make_tmap_3d_f32(&mdq, dq_acc, slots, qtok, dim)) != cudaSuccess) return e;
   if ((e = set_smem_once((const void*)tc::tc_softmax_bwd_kernel, tc::kSmBwdSmem)) != cudaSuccess) return e;

@@ -8,11 +8,11 @@ sys.path.insert(0, ".")
 from paper_2502_07563_b200 import _lib, ops  # noqa: E402
 from paper_2502_07563_b200.datagen import gen_slots_device  # noqa: E402
 
-NAMES = {30: "mma:S_issued", 31: "mma:PV_issued", 32: "mma:p_ready_seen", 40: "sm:s_full", 41: "sm:xchg_bar",
-         42: "sm:p_ready", 43: "sm:o_full(prev)", 44: "sm:o_empty(prev)", 45: "sm:wait_s"}
+NAMES = {50: "mma:PV_A issued", 51: "mma:S_A issued", 52: "mma:PV_B issued", 53: "mma:S_B issued",
+         60: "smA:s_full", 61: "smA:p_ready", 62: "smB:s_full", 63: "smB:p_ready"}
 n, h, d = 32768, 16, 128
 q, k, v = (gen_slots_device(0, 1, h, n, d, t) for t in ("q", "k", "v"))
-buf = torch.zeros(128, dtype=torch.int64, device="cuda")
+buf = torch.zeros(256, dtype=torch.int64, device="cuda")
 ops.softmax_forward(q, k, v, True, 0, n, n, 0)
 torch.cuda.synchronize()
 _lib.call("lasp2_debug_trace", buf.data_ptr())
@@ -26,7 +26,7 @@ by_blk = defaultdict(dict)
 for ev, blk, clk in rec:
     by_blk[blk].setdefault(ev, clk - t0)
 blocks = sorted(by_blk)
-print("period (sm:p_ready deltas):", [by_blk[b + 1].get(42, 0) - by_blk[b].get(42, 0) for b in blocks[:-1]])
+print("period (smA:p_ready deltas):", [by_blk[b + 1].get(61, 0) - by_blk[b].get(61, 0) for b in blocks[:-1]])
 allev = sorted(((c, b, ev) for b in blocks for ev, c in by_blk[b].items()))
 for c, b, ev in allev:
     if 18 <= b <= 21:
