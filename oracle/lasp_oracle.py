@@ -320,6 +320,60 @@ def cp_full(q, k, v, d_out, chunks: int, causal: bool = True):
 
 
 # ---------------------------------------------------------------------------
+# hybrid layer stacks (hybrid.py:60-63, 136-160, 306-361)
+# ---------------------------------------------------------------------------
+
+def projection_weight(seed: int, layer: int, role: str, d: int) -> np.ndarray:
+    """(d, d) weight uniform in [-1/sqrt(d), 1/sqrt(d)) (datagen.py:82-85)."""
+    return gen_data(seed, d, d, tag=f"w{role}/layer{layer}") / np.sqrt(float(d))
+
+
+def stack_weights(layers: str, dim: int, seed: int, round_bf16: bool = False):
+    """layer_weights (hybrid.py:60-63); optionally bf16-rounded as the bf16 GPU path sees them."""
+    ws = [tuple(projection_weight(seed, i, role, dim) for role in "qkv") for i in range(len(layers))]
+    return [tuple(bf16_round(w) for w in t) for t in ws] if round_bf16 else ws
+
+
+def stack_iteration(layers: str, x, d_out, causal: bool = True, weights=None, seed: int = 0, bc: int = 256):
+    """Serial layer stack forward + analytic backward on the full sequence
+    (serial_stack_oracle, hybrid.py:306-361): L layers blocked (lasp2 T=1),
+    N layers per-slot softmax. Returns (out, d_x, d_weights, layer_outputs)."""
+    layers = layers.replace(" ", "")
+    weights = weights if weights is not None else stack_weights(layers, x.shape[-1], seed)
+    retained, layer_outputs = [], []
+    cur = x
+    for kind, (wq, wk, wv) in zip(layers, weights):
+        q, k, v = cur @ wq, cur @ wk, cur @ wv  # _project, hybrid.py:136-142
+        if kind == "L":
+            out = lasp2_forward(q, k, v, 1, causal, bc)[0][0]
+        else:
+            out = np.empty_like(q)
+            for bi in range(q.shape[0]):
+                for hi in range(q.shape[1]):
+                    out[bi, hi] = softmax_chunk_forward(q[bi, hi], k[bi, hi], v[bi, hi], causal, 0)
+        retained.append((cur, q, k, v))
+        layer_outputs.append(out)
+        cur = out
+    dy = d_out
+    d_weights = [()] * len(layers)
+    for i in range(len(layers) - 1, -1, -1):
+        inp, q, k, v = retained[i]
+        if layers[i] == "L":
+            dq, dk, dv = lasp2_backward(q, k, v, dy, 1, causal, bc)[0]
+        else:
+            dq, dk, dv = np.empty_like(q), np.empty_like(k), np.empty_like(v)
+            for bi in range(q.shape[0]):
+                for hi in range(q.shape[1]):
+                    dq[bi, hi], dk[bi, hi], dv[bi, hi] = softmax_chunk_backward(
+                        q[bi, hi], k[bi, hi], v[bi, hi], dy[bi, hi], causal, 0)
+        rows = lambda a: a.reshape(-1, a.shape[-1])  # noqa: E731  pack_slots
+        d_weights[i] = tuple(rows(inp).T @ rows(g) for g in (dq, dk, dv))  # _weight_grads, hybrid.py:154-160
+        wq, wk, wv = weights[i]
+        dy = dq @ wq.T + dk @ wk.T + dv @ wv.T  # hybrid.py:207-210
+    return layer_outputs[-1], dy, d_weights, layer_outputs
+
+
+# ---------------------------------------------------------------------------
 # error metrics (oracle.py:230-233; SURVEY §8a note P)
 # ---------------------------------------------------------------------------
 

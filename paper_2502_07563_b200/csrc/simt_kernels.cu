@@ -336,6 +336,44 @@ __device__ __forceinline__ void row_stats(const A* qrow, const T* kf, int64_t sl
   *out_sum = s;
 }
 
+// delta[row] = sum_j P[row][j] dP[row][j], dP[row][j] = dO[row] . v_j, exactly
+// as the reference forms it (oracle.py:155). Equal to dO . O in exact
+// arithmetic, but when |dP| is large next to dP - delta (deep stacks of
+// unnormalised linear layers feeding a softmax layer) the two roundings differ
+// far beyond f64 tolerance, so the f32/f64 validation path keeps the
+// reference's grouping. P comes from the exact row statistics (mx, sm).
+template <typename T, typename A>
+__global__ void __launch_bounds__(kSmThreads) simt_softmax_delta_exact_kernel(
+    const T* __restrict__ q, const T* __restrict__ kf, const T* __restrict__ vf, const T* __restrict__ d_out,
+    const A* __restrict__ mx, const A* __restrict__ sm, A* __restrict__ delta, int64_t qtok, int64_t kvtok, int dim,
+    int causal, int64_t row_offset, KvLayout kl) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  A* qrow = reinterpret_cast<A*>(smem_raw);  // [dim]
+  A* drow = qrow + dim;                      // [dim]
+  A* red = drow + dim;                       // [32]
+  const int64_t row = blockIdx.x, slot = blockIdx.y, r = slot * qtok + row;
+  for (int c = threadIdx.x; c < dim; c += blockDim.x) {
+    qrow[c] = load_as<A>(q + r * dim + c);
+    drow[c] = load_as<A>(d_out + r * dim + c);
+  }
+  __syncthreads();
+  const A scale = dev_rsqrt<A>(dim), m = mx[r], ssum = sm[r];
+  const int64_t limit = causal ? lmin(kvtok, row_offset + row + 1) : kvtok;
+  A acc = A(0);
+  for (int64_t j = threadIdx.x; j < limit; j += blockDim.x) {
+    const T* kr = kf + kl.row(slot, j, dim);
+    const T* vr = vf + kl.row(slot, j, dim);
+    A sdot = A(0), dp = A(0);
+    for (int a = 0; a < dim; ++a) {
+      sdot += qrow[a] * load_as<A>(kr + a);
+      dp += drow[a] * load_as<A>(vr + a);
+    }
+    acc += dev_exp<A>(sdot * scale - m) / ssum * dp;
+  }
+  acc = block_reduce_sum<A>(acc, red);
+  if (threadIdx.x == 0) delta[r] = acc;
+}
+
 // dq[row] = scale * sum_j dS[row][j] k_j, dS = P (dP - delta)   (oracle.py:150-157)
 template <typename T, typename A>
 __global__ void __launch_bounds__(kSmThreads) simt_softmax_bwd_dq_kernel(
@@ -519,14 +557,17 @@ cudaError_t simt_softmax_backward(const void* q, const void* kf, const void* vf,
   A* mx = delta + slots * qtok;
   A* sm = mx + slots * qtok;
   const int64_t rows = slots * qtok;
-  simt_softmax_delta_kernel<T, A><<<(unsigned)((rows + 7) / 8), dim3(32, 8), 0, s>>>((const T*)o, (const T*)d_out,
-                                                                                    delta, rows, dim);
+  (void)o;  // delta is formed from P and dP (reference grouping), not from the forward output
+  (void)rows;
   dim3 gq((unsigned)qtok, (unsigned)slots);
+  simt_softmax_rowstats_kernel<T, A><<<gq, kSmThreads, (size_t)(dim + 32) * sizeof(A), s>>>(
+      (const T*)q, (const T*)kf, mx, sm, qtok, kvtok, dim, causal, row_offset, kl);
+  simt_softmax_delta_exact_kernel<T, A><<<gq, kSmThreads, (size_t)(2 * dim + 32) * sizeof(A), s>>>(
+      (const T*)q, (const T*)kf, (const T*)vf, (const T*)d_out, mx, sm, delta, qtok, kvtok, dim, causal, row_offset,
+      kl);
   simt_softmax_bwd_dq_kernel<T, A><<<gq, kSmThreads, (size_t)(2 * dim + kSmKeys + 32) * sizeof(A), s>>>(
       (const T*)q, (const T*)kf, (const T*)vf, (const T*)d_out, delta, (T*)dq, qtok, kvtok, dim, causal,
       row_offset, kl);
-  simt_softmax_rowstats_kernel<T, A><<<gq, kSmThreads, (size_t)(dim + 32) * sizeof(A), s>>>(
-      (const T*)q, (const T*)kf, mx, sm, qtok, kvtok, dim, causal, row_offset, kl);
   dim3 gk((unsigned)kvtok, (unsigned)slots);
   simt_softmax_bwd_dkdv_kernel<T, A, G><<<gk, kSmThreads, (size_t)(2 * dim + 2 * kSmKeys) * sizeof(A), s>>>(
       (const T*)q, (const T*)kf, (const T*)vf, (const T*)d_out, delta, mx, sm, (G*)dk_full, (G*)dv_full, qtok,

@@ -32,3 +32,12 @@ def pytest_collection_modifyitems(config, items):
 def golden():
     with np.load(GOLDEN) as z:
         return {k: z[k] for k in z.files}
+
+
+HYBRID_GOLDEN = ROOT / "tests" / "golden" / "hybrid_cases.npz"
+
+
+@pytest.fixture(scope="session")
+def hybrid_golden():
+    with np.load(HYBRID_GOLDEN) as z:
+        return {k: z[k] for k in z.files}

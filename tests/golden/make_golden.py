@@ -69,7 +69,45 @@ def main() -> None:
     data["cfg1_rows"] = CFG1_ROWS
     np.savez_compressed(OUT, **data)
     print(f"wrote {OUT} ({OUT.stat().st_size} bytes, {len(data)} arrays)")
+    hybrid_cases()
+
+
+# (pattern, n, d, chunks, batch, heads, seed, causal): test_hybrid.py grids plus two larger stacks
+HYBRID_CASES = [(p, 16, 4, t, 1, 1, 2, True) for p in ("L", "N", "LN", "LLLN", "LNLN LNLN") for t in (1, 2, 4)] + [
+    ("LN", 8, 4, 2, 1, 1, 5, False), ("LN", 8, 4, 2, 2, 2, 6, True),
+    ("LLN", 256, 32, 2, 1, 2, 11, True), ("LN", 256, 32, 4, 1, 2, 12, False),
+]
+
+
+def hybrid_key(pattern, n, d, t, b, h, seed, causal):
+    return f"hy_{pattern.replace(' ', '_')}_{n}_{d}_{t}_{b}_{h}_{seed}_{'c' if causal else 'n'}"
+
+
+def hybrid_cases() -> None:
+    """Reference hybrid_iteration outputs (hybrid.py:284-303) -> tests/golden/hybrid_cases.npz."""
+    from laspsim.datagen import gen_slots
+    from laspsim.hybrid import ModelSpec, hybrid_iteration
+
+    out_path = OUT.parent / "hybrid_cases.npz"
+    data = {}
+    for case in HYBRID_CASES:
+        pattern, n, d, t, b, h, seed, causal = case
+        spec = ModelSpec(pattern, dim=d, heads=h, batch=b, seed=seed)
+        x = gen_slots(seed, b, h, n, d, "x")
+        dy = gen_slots(seed, b, h, n, d, "dy")
+        it = hybrid_iteration(spec, x, dy, t, causal=causal)
+        key = hybrid_key(*case)
+        data[key + "_out"] = np.concatenate(it.outputs, axis=2)
+        data[key + "_dx"] = np.concatenate(it.d_x, axis=2)
+        data[key + "_dw"] = np.stack([np.stack(w) for w in it.d_weights])
+        data[key + "_ledger"] = np.array([it.run.stats.allgather_launches, it.run.stats.p2p_sends])
+    np.savez_compressed(out_path, **data)
+    print(f"wrote {out_path} ({out_path.stat().st_size} bytes, {len(data)} arrays)")
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["hybrid"]:
+        sys.path.insert(0, str(REF))
+        hybrid_cases()
+    else:
+        main()

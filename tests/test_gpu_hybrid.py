@@ -1,0 +1,119 @@
+"""Hybrid L/N layer stacks on the GPU (reference pkg/tests/test_hybrid.py):
+the driver against outputs of the reference's own hybrid_iteration
+(tests/golden/hybrid_cases.npz) in f64, and against the stack oracle in the
+fp32 validation mode and the bf16 tensor-core mode."""
+import importlib.util
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import lasp_oracle as O
+from paper_2502_07563_b200.hybrid import ModelSpec, hybrid_backward, hybrid_forward, hybrid_iteration
+
+pytestmark = pytest.mark.gpu
+
+_spec = importlib.util.spec_from_file_location("make_golden", Path(__file__).parent / "golden" / "make_golden.py")
+_mg = importlib.util.module_from_spec(_spec)
+_spec.loader.exec_module(_mg)
+HYBRID_CASES, hybrid_key = _mg.HYBRID_CASES, _mg.hybrid_key
+
+STACK_TOL = 1e-9  # test_hybrid.py:16
+
+
+def cat(xs):
+    return torch.cat(list(xs), dim=2).double().cpu().numpy()
+
+
+def dw_np(d_weights):
+    return np.stack([np.stack([w.double().cpu().numpy() for w in t]) for t in d_weights])
+
+
+def xy(case, dtype=torch.float64):
+    pattern, n, d, t, b, h, seed, causal = case
+    x = O.gen_slots(seed, b, h, n, d, "x")
+    dy = O.gen_slots(seed, b, h, n, d, "dy")
+    return x, dy, torch.from_numpy(x).to("cuda", dtype), torch.from_numpy(dy).to("cuda", dtype)
+
+
+@pytest.mark.parametrize("case", HYBRID_CASES, ids=lambda c: hybrid_key(*c))
+def test_f64_stack_matches_reference(hybrid_golden, case):
+    pattern, n, d, t, b, h, seed, causal = case
+    _, _, x, dy = xy(case)
+    it = hybrid_iteration(ModelSpec(pattern, dim=d, heads=h, batch=b, seed=seed), x, dy, t, causal=causal)
+    key = hybrid_key(*case)
+    assert O.relative_error(cat(it.outputs), hybrid_golden[key + "_out"]) <= STACK_TOL
+    assert O.relative_error(cat(it.d_x), hybrid_golden[key + "_dx"]) <= STACK_TOL
+    assert O.relative_error(dw_np(it.d_weights), hybrid_golden[key + "_dw"]) <= STACK_TOL
+    # 2 launches per L layer, 3 per N layer (the N layer's third is a reduce_scatter here)
+    layers = pattern.replace(" ", "")
+    st = it.run.stats
+    assert st.allgather_launches + st.reduce_scatter_launches == hybrid_golden[key + "_ledger"][0]
+    assert st.p2p_sends == 0
+
+
+@pytest.mark.parametrize("dtype,tol", [(torch.float32, 1e-4), (torch.bfloat16, 2e-2)])
+@pytest.mark.parametrize("case,shift", [(("LLN", 256, 32, 2, 1, 2, 11, True), 2),
+                                        (("LN", 256, 32, 4, 1, 2, 12, False), 1),
+                                        (("LNLN", 1024, 128, 2, 1, 2, 13, True), 2)])
+def test_lowp_stack_matches_oracle(case, shift, dtype, tol):
+    """fp32 validation mode (<= 1e-4) and bf16 tensor-core mode vs the f64 stack
+    oracle on the same rounded inputs/weights, normalised error per tensor
+    (SURVEY §8a note P). bf16 rounds every layer's q/k/v/output, so a stack of
+    L layers compounds the per-layer 1e-2 budget: 2e-2 here for <= 4 layers.
+    Unnormalised linear layers grow activations like n*d per layer (the
+    reference has no norm), so x is scaled by 2^-shift (exact) to keep every
+    layer finite in bf16/fp32."""
+    pattern, n, d, t, b, h, seed, causal = case
+    x, dy, xd, dyd = xy(case, dtype)
+    x, xd = x * 2.0 ** -shift, xd * 2.0 ** -shift
+    bf = dtype == torch.bfloat16
+    if bf:
+        x, dy = O.bf16_round(x), O.bf16_round(dy)
+    ws = O.stack_weights(pattern.replace(" ", ""), d, seed, round_bf16=bf)
+    out, dx, dw, _ = O.stack_iteration(pattern, x, dy, causal, weights=ws)
+    it = hybrid_iteration(ModelSpec(pattern, dim=d, heads=h, batch=b, seed=seed), xd, dyd, t, causal=causal)
+    assert O.normalized_error(cat(it.outputs), out) <= tol
+    assert O.normalized_error(cat(it.d_x), dx) <= tol
+    got_dw = dw_np(it.d_weights)
+    for i, layer in enumerate(dw):
+        for j, want in enumerate(layer):
+            assert O.normalized_error(got_dw[i, j], want) <= tol, (i, j)
+    if bf:
+        assert all(w.dtype == torch.float32 for t3 in it.d_weights for w in t3)
+
+
+def test_forward_then_backward_equals_iteration():
+    case = ("LN", 256, 32, 2, 1, 2, 11, True)
+    pattern, n, d, t, b, h, seed, causal = case
+    _, _, x, dy = xy(case)
+    spec = ModelSpec(pattern, dim=d, heads=h, batch=b, seed=seed)
+    fwd = hybrid_forward(spec, x, t, causal)
+    bwd = hybrid_backward(spec, x, dy, t, fwd.caches)
+    it = hybrid_iteration(spec, x, dy, t, causal)
+    assert np.array_equal(cat(fwd.outputs), cat(it.outputs))
+    assert np.array_equal(cat(bwd.d_x), cat(it.d_x))
+    assert np.array_equal(dw_np(bwd.d_weights), dw_np(it.d_weights))
+
+
+def test_zero_input_and_zero_upstream():
+    spec = ModelSpec("LN", dim=4, seed=7)
+    x = torch.zeros((1, 1, 8, 4), dtype=torch.float64, device="cuda")
+    it = hybrid_iteration(spec, x, torch.zeros_like(x), 2)
+    assert not cat(it.outputs).any() and not cat(it.d_x).any()
+    assert not dw_np(it.d_weights).any()
+
+
+def test_validation_errors():
+    spec = ModelSpec("LN", dim=4)
+    x = torch.zeros((1, 1, 8, 4), dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError):
+        hybrid_forward(ModelSpec("L", dim=8), x, 2)  # dim mismatch
+    with pytest.raises(ValueError):
+        hybrid_iteration(spec, x, torch.zeros((1, 1, 4, 4), dtype=torch.float64, device="cuda"), 2)
+    with pytest.raises(ValueError):
+        hybrid_forward(spec, x, 3)  # 3 does not divide 8
+    fwd = hybrid_forward(spec, x, 2)
+    with pytest.raises(ValueError):
+        hybrid_backward(spec, x, torch.zeros_like(x), 2, fwd.caches[:1])
