@@ -77,6 +77,17 @@ int lasp2_causal_chunk(int dtype, const void* q, const void* k, const void* v, c
                        const void* base, void* out, int64_t slots, int64_t tokens, int dim, int nseg, int reverse,
                        int transpose_state, void* stream);
 
+/* Masked backward dQ of one rank's chunk plus the dM segment states, one pass:
+ *   dq_s = sum_{i<=s} (do_s.v_i) k_i + do_s S_s^T,  S_s = fwd_base + fwd_seg[seg(s)]
+ *          + sum_{i<s, same segment} k_i^T v_i   (lasp2.py:198, :277-279)
+ *   g_seg[slot][g] = Q_g^T dO_g  (chunk_state_grad per segment, lasp2.py:140-147;
+ *          unscanned, the caller's lasp2_scan_segments turns it into suffixes).
+ * Replaces the dq half of intra_backward and chunk_state_grad; the bf16 path
+ * reads dO, V, K and Q once (one tcgen05 pass instead of two). */
+int lasp2_dq_chunk(int dtype, const void* q, const void* k, const void* v, const void* d_out, const void* fwd_seg,
+                   const void* fwd_base, void* g_seg, void* dq, int64_t slots, int64_t tokens, int dim, int nseg,
+                   void* stream);
+
 /* Masked backward dK and dV of one rank's chunk in one pass:
  *   dk_s = sum_{i>=s} (v_s.do_i) q_i + v_s G_s^T,  dv_s = sum_{i>=s} (k_s.q_i) do_i + k_s G_s
  * with G_s = base + seg_states[seg(s)] + sum_{i>s, same segment} q_i^T do_i

@@ -32,6 +32,7 @@ SIGNATURES = {
     "lasp2_scan_segments": (_int, [_int, _vp, _vp, _i64, _int, _int, _int, _vp]),
     "lasp2_fold_states": (_int, [_int, _vp, _vp, _int, _i64, _int, _int, _vp]),
     "lasp2_causal_chunk": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _int, _int, _int, _int, _vp]),
+    "lasp2_dq_chunk": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _int, _int, _vp]),
     "lasp2_dkdv_chunk": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _int, _int, _vp]),
     "lasp2_state_apply": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _int, _int, _vp]),
     "lasp2_apply_state2": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _int, _vp]),

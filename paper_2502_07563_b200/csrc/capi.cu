@@ -131,6 +131,23 @@ int lasp2_causal_chunk(int dtype, const void* q, const void* k, const void* v, c
   return cuda_status(e, "causal_chunk");
 }
 
+int lasp2_dq_chunk(int dtype, const void* q, const void* k, const void* v, const void* d_out, const void* fwd_seg,
+                   const void* fwd_base, void* g_seg, void* dq, int64_t slots, int64_t tokens, int dim, int nseg,
+                   void* stream) {
+  CHECK(valid_dtype(dtype), "dq_chunk: unknown dtype");
+  CHECK(q && k && v && d_out && g_seg && dq, "dq_chunk: null pointer");
+  CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128, "dq_chunk: bad shape (1 <= dim <= 128)");
+  CHECK(nseg >= 1 && nseg <= (tokens + LASP_BLOCK_TOKENS - 1) / LASP_BLOCK_TOKENS, "dq_chunk: bad nseg");
+  CHECK(nseg == 1 || fwd_seg, "dq_chunk: nseg > 1 needs segment states");
+  if (use_tc(dtype, dim, tokens))
+    return cuda_status(lasp::tc_dq_chunk(q, k, v, d_out, (const float*)fwd_seg, (const float*)fwd_base,
+                                         (float*)g_seg, dq, slots, tokens, dim, nseg, S(stream)),
+                       "dq_chunk");
+  int st = lasp2_segment_states(dtype, q, d_out, g_seg, slots, tokens, dim, nseg, stream);
+  if (st != LASP2_OK) return st;
+  return lasp2_causal_chunk(dtype, d_out, v, k, fwd_seg, fwd_base, dq, slots, tokens, dim, nseg, 0, 1, stream);
+}
+
 int lasp2_dkdv_chunk(int dtype, const void* q, const void* k, const void* v, const void* d_out, const void* seg_states,
                      const void* base, void* dk, void* dv, int64_t slots, int64_t tokens, int dim, int nseg,
                      void* stream) {

@@ -43,6 +43,9 @@ cudaError_t tc_segment_states(const void* x, const void* y, float* out, int64_t 
 cudaError_t tc_causal_chunk(const void* q, const void* k, const void* v, const float* seg_states, const float* base,
                             void* out, int64_t slots, int64_t tokens, int dim, int nseg, int reverse,
                             int transpose_state, cudaStream_t s);
+cudaError_t tc_dq_chunk(const void* q, const void* k, const void* v, const void* d_out, const float* fwd_seg,
+                        const float* fwd_base, float* g_out, void* dq, int64_t slots, int64_t tokens, int dim,
+                        int nseg, cudaStream_t s);
 cudaError_t tc_dkdv_pair(const void* q, const void* k, const void* v, const void* d_out, const float* seg_states,
                          const float* base, void* dk, void* dv, int64_t slots, int64_t tokens, int dim, int nseg,
                          cudaStream_t s);

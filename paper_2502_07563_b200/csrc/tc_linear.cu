@@ -131,6 +131,7 @@ struct CausalArgs {
   const float* fwd_seg;     // [slots][nseg][dim][dim] exclusive prefixes of K^T V
   const float* fwd_total;   // [slots][dim][dim] chunk total of K^T V
   const float* fwd_base;    // [slots][dim][dim] M_{1:t-1} (or null)
+  float* g_out;             // kMode 3: [slots][nseg][dim][dim] segment states X^T q' (unscanned)
   int64_t tokens;
   int dim;
   int nseg;
@@ -166,9 +167,13 @@ struct Role {
 //          forward form run backwards: TMEM holds T = -S, seeded with minus the
 //          segment-END state; each block adds K^T V (so T becomes minus the
 //          block-start state) and the state image is written as -T.
+// kMode 3: kMode 0 plus one more tile per block, X (maps[4]), and the segment
+//          state G = X^T q' accumulated in TMEM [384,512) (O single-buffered):
+//          the masked backward's dQ pass (q' = dO, k' = V, v' = K) also yields
+//          the dM segment states (X = Q), so Q^T dO needs no pass of its own.
 template <int kMode>
 __device__ __forceinline__ Role causal_role(uint32_t role, const CausalArgs& a) {
-  if (kMode == 0) return Role{0, 1, 2, 3, a.reverse, a.transpose_state, 0, a.reverse ? 2 : 1, 0};
+  if (kMode == 0 || kMode == 3) return Role{0, 1, 2, 3, a.reverse, a.transpose_state, 0, a.reverse ? 2 : 1, 0};
   if (kMode == 1)
     // ring positions are shared by both CTAs: 0 private (V | K), 1 = dO, 2 = Q; rank 1 swaps k'/v' at the MMA
     return role == 0 ? Role{0, 2, 3, 4, 1, 1, 0, 2, 1} : Role{1, 2, 3, 5, 1, 0, 0, 2, 2};
@@ -194,7 +199,10 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
   uint64_t* sst_ready = bars + 2 * kRing + 3;
   uint64_t* o_full = bars + 2 * kRing + 4;   // [2]
   uint64_t* o_empty = bars + 2 * kRing + 6;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kRing + 8);
+  uint64_t* g_full = bars + 2 * kRing + 8;   // kMode 3
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kRing + 9);
+  constexpr int kTPB = kMode == 3 ? 4 : 3;   // ring tiles per block: q', k', v' (+ X)
+  constexpr bool kOneO = kMode == 3;         // TMEM [384,512) holds G, so O is single-buffered
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t role_id = kMode == 1 ? cluster_ctarank() : kMode == 2 ? blockIdx.x % 3 : 0u;
@@ -212,7 +220,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], kMode == 1 ? 2 : 1);
     }
-    for (int i = 0; i < 8; ++i) mbar_init(&s_full[i], 1);
+    for (int i = 0; i < 9; ++i) mbar_init(&s_full[i], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -222,9 +230,10 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
   const uint32_t tmem = *tmem_slot;
   pdl_wait();
   pdl_launch_dependents();
-  // TMEM: S [0,128), O[0] [128,256), running state [256,384), O[1] [384,512)
-  const uint32_t t_s = tmem, t_st = tmem + 256;
+  // TMEM: S [0,128), O[0] [128,256), running state [256,384), O[1] (kMode 3: G) [384,512)
+  const uint32_t t_s = tmem, t_st = tmem + 256, t_g = tmem + 384;
   auto t_o = [&](int b) { return tmem + (b ? 384u : 128u); };
+  auto o_buf = [&](int jj) { return kOneO ? 0 : (jj & 1); };
   auto release = [&](int s) {
     if constexpr (kMode == 1) mma_commit_mc(&empty[s], 0x3); else mma_commit(&empty[s]);
   };
@@ -232,14 +241,14 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
   if (warp == 0) {
     // ---------------- TMA producer: ring order per block = q', k', v' ----------------
     if (elect_one()) {
-      const CUtensorMap* maps[3] = {&tm.m[R.qi], &tm.m[R.ki], &tm.m[R.vi]};
-      for (int w = 0; w < 3; ++w) prefetch_tmap(maps[w]);
+      const CUtensorMap* maps[4] = {&tm.m[R.qi], &tm.m[R.ki], &tm.m[R.vi], &tm.m[4]};
+      for (int w = 0; w < kTPB; ++w) prefetch_tmap(maps[w]);
       const uint32_t bytes = nbox * kBoxBytes;
       for (int jj = 0; jj < nblk; ++jj) {
         const int j = R.reverse ? nblk - 1 - jj : jj;
         const int row = (int)(lo + (int64_t)j * kTile);
-        for (int w = 0; w < 3; ++w) {
-          const int t = 3 * jj + w, s = t % kRing, u = t / kRing;
+        for (int w = 0; w < kTPB; ++w) {
+          const int t = kTPB * jj + w, s = t % kRing, u = t / kRing;
           if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
           uint8_t* dst = ring + s * kTileBytes;
           mbar_arrive_expect_tx(&full[s], bytes);
@@ -252,7 +261,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
         }
       }
       if constexpr (kMode == 1) {  // drain: both CTAs' final releases of every used slot have arrived here
-        const int total = 3 * nblk;
+        const int total = kTPB * nblk;
         for (int s = 0; s < kRing && s < total; ++s) {
           const int uses = (total - s + kRing - 1) / kRing;
           mbar_wait(&empty[s], (uses - 1) & 1);
@@ -269,11 +278,11 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
     const bool swap = kMode == 1 && R.mcast == 2;  // kMode 1 rank 1: ring positions of k', v' swapped
     Tracer tr;
     for (int jj = 0; jj < nblk; ++jj) {
-      const int t0 = 3 * jj;
+      const int t0 = kTPB * jj;
       const int sq = t0 % kRing, sb = (t0 + 1) % kRing, sc = (t0 + 2) % kRing;
       const int sk = swap ? sc : sb, sv = swap ? sb : sc;
       const int tk = swap ? t0 + 2 : t0 + 1, tv = swap ? t0 + 1 : t0 + 2;
-      const int ob = jj & 1;
+      const int ob = o_buf(jj);
       const uint32_t qa = smem_u32(ring + sq * kTileBytes);
       const uint32_t ka = smem_u32(ring + sk * kTileBytes);
       const uint32_t va = smem_u32(ring + sv * kTileBytes);
@@ -305,16 +314,31 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       }
       mbar_wait(sst_ready, (jj + (R.subtract ? 1 : 0)) & 1);  // subtract form: arrival 0 is the seed
       if (lane == 0) tr(13, jj);
-      if (jj >= 2) mbar_wait(&o_empty[ob], ((jj >> 1) - 1) & 1);
+      if (kOneO ? jj >= 1 : jj >= 2) mbar_wait(&o_empty[ob], (kOneO ? jj - 1 : (jj >> 1) - 1) & 1);
       tc_fence_after();
       if (lane == 0) tr(14, jj);
       if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < kfeat; ++kk)
           mma_bf16_ss(t_o(ob), desc_kmajor(qa, kk), desc_mnmajor(simg_a, kk), id_qs, kk > 0);
-        release(sq);
+        if constexpr (kMode != 3) release(sq);
       }
       __syncwarp();
+      if constexpr (kMode == 3) {  // G += X^T q' (token contraction, both MN-major views)
+        const int sx = (t0 + 3) % kRing;
+        mbar_wait(&full[sx], ((t0 + 3) / kRing) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t xa = smem_u32(ring + sx * kTileBytes);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            mma_bf16_ss(t_g, desc_mnmajor(xa, kk), desc_mnmajor(qa, kk), id_kv, (jj > 0 || kk > 0) ? 1u : 0u);
+          release(sq);
+          release(sx);
+          if (jj == nblk - 1) mma_commit(g_full);
+        }
+        __syncwarp();
+      }
       if (!R.subtract) {
         mbar_wait(&full[sv], (tv / kRing) & 1);
         tc_fence_after();
@@ -394,7 +418,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
     }
     for (int jj = 0; jj < nblk; ++jj) {
       const int j = R.reverse ? nblk - 1 - jj : jj;
-      const int ob = jj & 1;
+      const int ob = o_buf(jj);
       // ---- subtract form: this block's (post-subtraction) state image comes first
       if (R.subtract) {
         mbar_wait(st_full, jj & 1);
@@ -435,7 +459,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
         if (et == 0) tr(25, jj);
       }
       // ---- O tile -> staging -> TMA store
-      mbar_wait(&o_full[ob], (jj >> 1) & 1);
+      mbar_wait(&o_full[ob], (kOneO ? jj : jj >> 1) & 1);
       tc_fence_after();
       if (et == 0) tr(26, jj);
       tmem_cols_to_image<0>(t_o(ob) + lane_off, pimg, row, cb, 64);
@@ -448,6 +472,31 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
         for (int bx = 0; bx < nbox; ++bx) tma_store_3d(tm_o, pimg + bx * kBoxBytes, 64 * bx, orow, slot);
         tma_store_commit();
         tr(27, jj);
+      }
+    }
+    if constexpr (kMode == 3) {  // segment state G -> fp32 [slot][seg][dim][dim]
+      if (nblk > 0) {
+        mbar_wait(g_full, 0);
+        tc_fence_after();
+        float* gb = a.g_out + ((int64_t)slot * a.nseg + seg) * dd + (int64_t)row * dim;
+#pragma unroll 1
+        for (int c0 = cb; c0 < cb + 64; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(t_g + lane_off + c0, r);
+          tmem_ld_wait();
+          if ((int)row < dim && c0 < dim) {
+            if (c0 + 32 <= dim) {
+#pragma unroll
+              for (int i = 0; i < 32; i += 4)
+                *reinterpret_cast<float4*>(gb + c0 + i) = make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]),
+                                                                      __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (c0 + i < dim) gb[c0 + i] = __uint_as_float(r[i]);
+            }
+          }
+        }
       }
     }
     if (et == 0) tma_store_wait_all<0>();
@@ -902,9 +951,24 @@ cudaError_t tc_causal_chunk(const void* q, const void* k, const void* v, const f
   for (int i = 0; i < 4; ++i)
     if ((e = make_tmap_3d(&tm.m[i], ptrs[i], slots, tokens, dim)) != cudaSuccess) return e;
   if ((e = set_smem_once((const void*)tc::tc_causal_chunk_kernel<0>, tc::kCausalSmem)) != cudaSuccess) return e;
-  tc::CausalArgs a{seg_states, base, nullptr, nullptr, nullptr, tokens, dim, nseg, reverse, transpose_state};
+  tc::CausalArgs a{seg_states, base, nullptr, nullptr, nullptr, nullptr, tokens, dim, nseg, reverse, transpose_state};
   dim3 grid(nseg, (unsigned)slots);
   return launch_pdl(tc::tc_causal_chunk_kernel<0>, grid, dim3(tc::kCausalThreads), tc::kCausalSmem, s, 1, tm, a);
+}
+
+// Masked backward dQ = causal(dO, V, K; S^T) plus the dM segment states Q_g^T dO_g in one pass.
+cudaError_t tc_dq_chunk(const void* q, const void* k, const void* v, const void* d_out, const float* fwd_seg,
+                        const float* fwd_base, float* g_out, void* dq, int64_t slots, int64_t tokens, int dim,
+                        int nseg, cudaStream_t s) {
+  tc::TileMaps tm;
+  cudaError_t e;
+  const void* ptrs[5] = {d_out, v, k, dq, q};
+  for (int i = 0; i < 5; ++i)
+    if ((e = make_tmap_3d(&tm.m[i], ptrs[i], slots, tokens, dim)) != cudaSuccess) return e;
+  if ((e = set_smem_once((const void*)tc::tc_causal_chunk_kernel<3>, tc::kCausalSmem)) != cudaSuccess) return e;
+  tc::CausalArgs a{fwd_seg, fwd_base, nullptr, nullptr, nullptr, g_out, tokens, dim, nseg, 0, 1};
+  dim3 grid(nseg, (unsigned)slots);
+  return launch_pdl(tc::tc_causal_chunk_kernel<3>, grid, dim3(tc::kCausalThreads), tc::kCausalSmem, s, 1, tm, a);
 }
 
 // Masked backward dK and dV in one pass over (Q, K, V, dO): 2-CTA clusters.
@@ -917,7 +981,7 @@ cudaError_t tc_dkdv_pair(const void* q, const void* k, const void* v, const void
   for (int i = 0; i < 6; ++i)
     if ((e = make_tmap_3d(&tm.m[i], ptrs[i], slots, tokens, dim)) != cudaSuccess) return e;
   if ((e = set_smem_once((const void*)tc::tc_causal_chunk_kernel<1>, tc::kCausalSmem)) != cudaSuccess) return e;
-  tc::CausalArgs a{seg_states, base, nullptr, nullptr, nullptr, tokens, dim, nseg, 1, 0};
+  tc::CausalArgs a{seg_states, base, nullptr, nullptr, nullptr, nullptr, tokens, dim, nseg, 1, 0};
   return launch_pdl(tc::tc_causal_chunk_kernel<1>, dim3(2 * nseg, (unsigned)slots), dim3(tc::kCausalThreads),
                     tc::kCausalSmem, s, 2, tm, a);
 }
@@ -933,7 +997,7 @@ cudaError_t tc_backward_triple(const void* q, const void* k, const void* v, cons
   for (int i = 0; i < 7; ++i)
     if ((e = make_tmap_3d(&tm.m[i], ptrs[i], slots, tokens, dim)) != cudaSuccess) return e;
   if ((e = set_smem_once((const void*)tc::tc_causal_chunk_kernel<2>, tc::kCausalSmem)) != cudaSuccess) return e;
-  tc::CausalArgs a{bwd_seg, bwd_base, fwd_seg, fwd_total, fwd_base, tokens, dim, nseg, 1, 0};
+  tc::CausalArgs a{bwd_seg, bwd_base, fwd_seg, fwd_total, fwd_base, nullptr, tokens, dim, nseg, 1, 0};
   dim3 grid(3 * nseg, (unsigned)slots);
   return launch_pdl(tc::tc_causal_chunk_kernel<2>, grid, dim3(tc::kCausalThreads), tc::kCausalSmem, s, 1, tm, a);
 }

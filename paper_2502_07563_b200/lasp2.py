@@ -277,16 +277,27 @@ _FUSE_DQ_MIN_BYTES = 256 << 20
 def _backward_masked_rank(ctx, cache: ActivationCache, d_out: torch.Tensor) -> GradientBundle:
     """Masked backward (lasp2.py:270-285).
 
-    dM segment states (Q^T dO) and their suffix scan; the dM all_gather runs on
-    the side stream while the dQ pass (which needs only forward states) runs;
-    after the descending suffix fold one pass computes dK and dV together
-    (2-CTA clusters, Q/dO multicast). `MASKED_BWD_FUSED = True` selects the
-    single-launch dQ/dK/dV kernel instead (lasp2_backward_chunk).
+    One pass computes dQ (it needs only forward states) together with the dM
+    segment states Q_g^T dO_g (lasp2_dq_chunk); their suffix scan gives M_t's
+    gradient for the all_gather; after the descending suffix fold one pass
+    computes dK and dV together (2-CTA clusters, Q/dO multicast).
+    `MASKED_DQ_WITH_STATES = False` runs Q^T dO as its own pass with the gather
+    in flight during dQ; `MASKED_BWD_FUSED = True` selects the single-launch
+    dQ/dK/dV kernel (lasp2_backward_chunk).
     """
     _require_cache(cache, masked=True)
     t, world = ctx.sp_position, ctx.sp_size
     (do,) = _contig(d_out)
     q, k, v, nseg = cache.q, cache.k, cache.v, cache.nseg
+    if MASKED_DQ_WITH_STATES and not MASKED_BWD_FUSED:
+        # dq_s = sum_{i<=s}(do_s.v_i) k_i + do_s (M_{1:t-1} + local prefix)^T, and in the same
+        # pass over (dO, V, K, Q) the dM segment states Q_g^T dO_g (lasp2.py:273-279)
+        dq, gseg = ops.dq_chunk(q, k, v, do, cache.seg_prefix, cache.m_prefix if t > 0 else None, nseg)
+        g_t = ops.scan_segments(gseg, reverse=True, data_dtype=q.dtype)
+        gathered = _unpack_gathered(_gather_states(ctx, g_t, "state_grad"), g_t)
+        r = ops.suffix_states(gathered, t + 1) if t < world - 1 else None
+        dk, dv = ops.dkdv_chunk(q, k, v, do, gseg, r, nseg)
+        return GradientBundle(dq=dq, dk=dk, dv=dv)
     gseg = ops.segment_states(q, do, nseg)
     g_t = ops.scan_segments(gseg, reverse=True, data_dtype=q.dtype)
     if MASKED_BWD_FUSED:
@@ -309,6 +320,12 @@ def _backward_masked_rank(ctx, cache: ActivationCache, d_out: torch.Tensor) -> G
 # single-launch dQ/dK/dV backward (three CTAs per segment sharing L2); off by
 # default while the per-CTA MMA/epilogue chain, not HBM, bounds both variants
 MASKED_BWD_FUSED = False
+
+# masked backward default: the dQ pass also accumulates the dM segment states
+# (lasp2_dq_chunk: Q, dO, V, K read once, 5 units instead of 2 + 4), so the dM
+# all_gather follows the dQ pass; False restores the separate Q^T dO pass with
+# the gather in flight during dQ
+MASKED_DQ_WITH_STATES = True
 
 
 # ---- world drivers ----------------------------------------------------------

@@ -100,6 +100,21 @@ def causal_chunk(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, seg_states: 
     return out
 
 
+def dq_chunk(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, d_out: torch.Tensor, fwd_seg: torch.Tensor | None,
+             fwd_base: torch.Tensor | None, nseg: int) -> tuple[torch.Tensor, torch.Tensor]:
+    """Masked backward dQ plus the unscanned dM segment states Q_g^T dO_g (header: lasp2_dq_chunk)."""
+    require_cuda(q, k, v, d_out, fwd_seg, fwd_base)
+    if not (q.shape == k.shape == v.shape == d_out.shape):
+        raise ValueError("q/k/v/d_out shapes differ")
+    slots, n, d = _slots(q)
+    b, h = q.shape[:2]
+    gseg = torch.empty((b, h, nseg, d, d), dtype=state_dtype(q.dtype), device=q.device)
+    dq = torch.empty_like(q)
+    call("lasp2_dq_chunk", dtype_code(q.dtype), ptr(q), ptr(k), ptr(v), ptr(d_out), ptr(fwd_seg), ptr(fwd_base),
+         ptr(gseg), ptr(dq), slots, n, d, nseg, stream_ptr())
+    return dq, gseg
+
+
 def dkdv_chunk(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, d_out: torch.Tensor,
                seg_states: torch.Tensor | None, base: torch.Tensor | None, nseg: int) -> tuple[torch.Tensor, torch.Tensor]:
     """Masked backward dK, dV in one pass (header: lasp2_dkdv_chunk)."""

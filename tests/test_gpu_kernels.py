@@ -197,6 +197,29 @@ def test_dkdv_pair_matches_two_passes(dtype, shape, nseg):
 
 
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32, torch.float64])
+@pytest.mark.parametrize("shape,nseg", [((1, 2, 1024, 128), 3), ((2, 1, 1000, 64), 2), ((1, 3, 2048, 128), 9),
+                                        ((1, 1, 77, 128), 1), ((1, 2, 300, 32), 2)])
+def test_dq_chunk_matches_separate_passes(dtype, shape, nseg):
+    """lasp2_dq_chunk = causal_chunk(dO, V, K; S^T) and segment_states(Q, dO) in one pass."""
+    q, k, v, do = (rand(shape, dtype, s) for s in (41, 42, 43, 44))
+    b, h, n, d = shape
+    sd = _lib.state_dtype(dtype)
+    seg = rand((b, h, nseg, d, d), sd, 45, scale=30.0)
+    base = rand((b, h, d, d), sd, 46, scale=30.0)
+    for bs in (base, None):
+        dq, gseg = ops.dq_chunk(q, k, v, do, seg, bs, nseg)
+        rq = ref_causal(do, v, k, seg, bs, nseg, False, True)
+        tol = {torch.bfloat16: 5e-3, torch.float32: F32_TOL, torch.float64: F64_TOL}[dtype]
+        tol_s = {torch.bfloat16: 1e-5, torch.float32: 1e-5, torch.float64: F64_TOL}[dtype]
+        assert nerr(dq, rq) <= tol
+        assert nerr(gseg, ref_segment_states(q, do, nseg)) <= tol_s
+    if dtype == torch.bfloat16:  # bitwise the same dQ as the standalone causal pass
+        dq2 = ops.causal_chunk(do, v, k, seg, base, nseg, reverse=False, transpose_state=True)
+        dq, _ = ops.dq_chunk(q, k, v, do, seg, base, nseg)
+        assert torch.equal(dq, dq2)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32, torch.float64])
 @pytest.mark.parametrize("shape", [(1, 2, 4096, 128), (2, 1, 700, 64), (1, 3, 300, 32)])
 def test_state_apply_and_apply2(dtype, shape):
     q, do, v, k = (rand(shape, dtype, s) for s in (31, 32, 33, 34))
