@@ -91,6 +91,43 @@ __device__ __forceinline__ void tmem_cols_to_image(uint32_t taddr_lane, uint8_t*
   }
 }
 
+// Same conversion, but the bf16 result goes back to TMEM as the A operand of a
+// TS-mode MMA: column pair (c, c+1) of this thread's row packed into one 32-bit
+// column at taddr_dst_lane + c/2 (low half = column c). Caller: tcgen05.wait::st
+// + fence before signalling the MMA warp.
+template <int MASK>
+__device__ __forceinline__ void tmem_cols_to_tmem_bf16(uint32_t taddr_lane, uint32_t taddr_dst_lane, uint32_t row,
+                                                       int c_begin, int ncols) {
+  const int r_lo = (int)(row & ~31u), r_hi = r_lo + 31;
+#pragma unroll 1
+  for (int c0 = c_begin; c0 < c_begin + ncols; c0 += 32) {
+    uint32_t pk[16];
+    const bool all_drop = (MASK == 1 && c0 > r_hi) || (MASK == 2 && c0 + 31 < r_lo);
+    if (all_drop) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) pk[i] = 0u;
+    } else {
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(taddr_lane + c0, r);
+      tmem_ld_wait();
+      const bool all_keep = MASK == 0 || (MASK == 1 && c0 + 31 <= r_lo) || (MASK == 2 && c0 >= r_hi);
+      if (all_keep) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+      } else {
+        const int lim = (int)row - c0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int a = 2 * i, b = 2 * i + 1;
+          const bool ka = MASK == 1 ? (a <= lim) : (a >= lim), kb = MASK == 1 ? (b <= lim) : (b >= lim);
+          pk[i] = pack_bf16x2(ka ? __uint_as_float(r[a]) : 0.f, kb ? __uint_as_float(r[b]) : 0.f);
+        }
+      }
+    }
+    tmem_st_32x32b_x16(taddr_dst_lane + (uint32_t)(c0 >> 1), pk);
+  }
+}
+
 // Optional per-block timeline of CTA (0,0) for blocks [16, 24): each traced
 // thread stamps clock64() into a local array and flushes it once at exit, so
 // tracing costs a few cycles per point. Enabled when g_trace != nullptr.

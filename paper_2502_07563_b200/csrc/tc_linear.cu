@@ -202,7 +202,8 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
   uint64_t* g_full = bars + 2 * kRing + 8;   // kMode 3
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kRing + 9);
   constexpr int kTPB = kMode == 3 ? 4 : 3;   // ring tiles per block: q', k', v' (+ X)
-  constexpr bool kOneO = kMode == 3;         // TMEM [384,512) holds G, so O is single-buffered
+  constexpr bool kPT = kMode == 1;           // P goes back to TMEM [384,448) (TS-mode P.v' MMA)
+  constexpr bool kOneO = kMode == 3 || kPT;  // TMEM [384,512) holds G or P, so O is single-buffered
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t role_id = kMode == 1 ? cluster_ctarank() : kMode == 2 ? blockIdx.x % 3 : 0u;
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
   pdl_wait();
   pdl_launch_dependents();
   // TMEM: S [0,128), O[0] [128,256), running state [256,384), O[1] (kMode 3: G) [384,512)
-  const uint32_t t_s = tmem, t_st = tmem + 256, t_g = tmem + 384;
+  const uint32_t t_s = tmem, t_st = tmem + 256, t_g = tmem + 384, t_p = tmem + 384;
   auto t_o = [&](int b) { return tmem + (b ? 384u : 128u); };
   auto o_buf = [&](int jj) { return kOneO ? 0 : (jj & 1); };
   auto release = [&](int s) {
@@ -358,7 +359,12 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       if (lane == 0) tr(16, jj);
       if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) mma_bf16_ss(t_o(ob), desc_kmajor(pimg_a, kk), desc_mnmajor(va, kk), id_pv, 1u);
+        for (int kk = 0; kk < 8; ++kk) {
+          if constexpr (kPT)
+            mma_bf16_ts(t_o(ob), t_p + kk * 8, desc_mnmajor(va, kk), id_pv, 1u);
+          else
+            mma_bf16_ss(t_o(ob), desc_kmajor(pimg_a, kk), desc_mnmajor(va, kk), id_pv, 1u);
+        }
         release(sv);
         mma_commit(&o_full[ob]);
       }
@@ -434,14 +440,20 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       mbar_wait(s_full, jj & 1);
       tc_fence_after();
       if (et == 0) tr(21, jj);
-      if (jj > 0 && et == 0) tma_store_wait_read<0>();
-      named_bar_sync(1, kEpi);
-      if (et == 0) tr(22, jj);
-      if (R.mask == 2)
-        tmem_cols_to_image<2>(t_s + lane_off, pimg, row, cb, 64);
-      else
-        tmem_cols_to_image<1>(t_s + lane_off, pimg, row, cb, 64);
-      fence_proxy_async_smem();
+      if constexpr (kPT) {  // P -> TMEM (the previous block's P.v' MMA completed before its o_full)
+        if (et == 0) tr(22, jj);
+        tmem_cols_to_tmem_bf16<2>(t_s + lane_off, t_p + lane_off, row, cb, 64);
+        tmem_st_wait();
+      } else {
+        if (jj > 0 && et == 0) tma_store_wait_read<0>();
+        named_bar_sync(1, kEpi);
+        if (et == 0) tr(22, jj);
+        if (R.mask == 2)
+          tmem_cols_to_image<2>(t_s + lane_off, pimg, row, cb, 64);
+        else
+          tmem_cols_to_image<1>(t_s + lane_off, pimg, row, cb, 64);
+        fence_proxy_async_smem();
+      }
       tc_fence_before();
       named_bar_sync(1, kEpi);
       if (et == 0) mbar_arrive(p_ready);
@@ -462,6 +474,10 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       mbar_wait(&o_full[ob], (kOneO ? jj : jj >> 1) & 1);
       tc_fence_after();
       if (et == 0) tr(26, jj);
+      if (kPT && jj > 0) {  // staging is O-only here: the previous O store must have left it
+        if (et == 0) tma_store_wait_read<0>();
+        named_bar_sync(1, kEpi);
+      }
       tmem_cols_to_image<0>(t_o(ob) + lane_off, pimg, row, cb, 64);
       fence_proxy_async_smem();
       tc_fence_before();
