@@ -266,6 +266,33 @@ def lasp2_full(q, k, v, d_out, chunks: int, masked: bool, bc: int = 256):
     return cat(outs), cat([g[0] for g in grads]), cat([g[1] for g in grads]), cat([g[2] for g in grads])
 
 
+def lasp1_nomask_full(q, k, v, d_out, chunks: int):
+    """Concatenated (out, dq, dk, dv) of the literal exclusive-prefix ring
+    (lasp1.py:43-72, 110-140): O_t = Q_t M_{1:t-1}, rank 0 zeros; the last
+    chunk's k/v reach no output."""
+    qs, ks, vs, ds = (_chunks(x, chunks) for x in (q, k, v, d_out))
+    states = [np.swapaxes(kc, -1, -2) @ vc for kc, vc in zip(ks, vs)]
+    grads = [np.swapaxes(qc, -1, -2) @ dc for qc, dc in zip(qs, ds)]
+    out, dq, dk, dv = [], [], [], []
+    for t in range(chunks):
+        if t == 0:
+            out.append(np.zeros_like(qs[t]))
+            dq.append(np.zeros_like(qs[t]))
+        else:
+            m = prefix_sum_states(states, t)
+            out.append(qs[t] @ m)
+            dq.append(ds[t] @ np.swapaxes(m, -1, -2))
+        if t == chunks - 1:
+            dk.append(np.zeros_like(ks[t]))
+            dv.append(np.zeros_like(vs[t]))
+        else:
+            g = suffix_sum_states(grads, t + 1)
+            dk.append(vs[t] @ np.swapaxes(g, -1, -2))
+            dv.append(ks[t] @ g)
+    cat = lambda xs: np.concatenate(xs, axis=2)  # noqa: E731
+    return cat(out), cat(dq), cat(dk), cat(dv)
+
+
 # ---------------------------------------------------------------------------
 # softmax / LASP-2H (oracle.py:111-158, standard_sp.py:37-76)
 # ---------------------------------------------------------------------------

@@ -16,12 +16,14 @@ RankContext that the hot path calls, comm.py:251-436):
 Interface: ``sp_position``, ``sp_size``, ``all_gather_async(t) -> Pending``,
 ``all_gather(t)`` (returns the rank-ordered contributions stacked on a new
 leading axis — the NCCL all_gather_into_tensor layout), ``reduce_scatter(t)``,
-``mark(kind)``, ``stats`` (CommStats) and ``trace``.
+``send(dst, t)`` / ``recv(src)`` (the LASP-1 ring baseline's matched pairs;
+NCCL P2P under torchrun), ``mark(kind)``, ``stats`` (CommStats) and ``trace``.
 """
 from __future__ import annotations
 
 import threading
 import time
+from collections import deque
 from collections.abc import Callable, Sequence
 from dataclasses import dataclass, field
 from typing import Any
@@ -180,6 +182,7 @@ class _World:
         t = cfg.sp_size
         self.groups = [tuple(range(g * t, (g + 1) * t)) for g in range(cfg.dp_size)]
         self.gens: dict[tuple[int, int], _Gen] = {}
+        self.queues: dict[tuple[int, int], deque] = {}  # (src, dst) -> FIFO of (snapshot, event)
         self.t0 = time.perf_counter()
 
     def record(self, rank: int, kind: str, detail: str) -> None:
@@ -350,6 +353,47 @@ class RankContext(_ContextBase):
             acc += p[pos]
         self._device_mark("reduce_scatter_complete")
         return acc
+
+    def send(self, dst: int, payload: torch.Tensor, tag: str = "") -> None:
+        """Deposit a frozen snapshot for global rank dst; non-blocking. The
+        matched pair is one communication step on the sender's ledger (comm.py:324-343)."""
+        if not 0 <= dst < self.world_size:
+            raise ValueError(f"destination {dst} outside world of {self.world_size}")
+        if not payload.is_cuda:
+            raise ValueError("p2p payloads must be CUDA tensors")
+        snap = payload.detach().clone()
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        nbytes = snap.numel() * snap.element_size()
+        world = self.world
+        with world.cond:
+            if world.abort_error is not None:
+                raise WorldAbortedError(f"rank {self.rank}: aborted by {world.abort_error!r}")
+            world.record(self.rank, "send", f"dst={dst} tag={tag} bytes={nbytes}")
+            self.stats.p2p_sends += 1
+            self.stats.communication_steps += 1
+            self.stats._account("send", nbytes)
+            world.queues.setdefault((self.rank, dst), deque()).append((snap, ev))
+            world.cond.notify_all()
+        self._device_mark("send")
+
+    def recv(self, src: int, tag: str = "") -> torch.Tensor:
+        """Next message from global rank src (FIFO per channel; the tag labels,
+        it does not filter), ordered after the sender's stream (comm.py:345-365)."""
+        if not 0 <= src < self.world_size:
+            raise ValueError(f"source {src} outside world of {self.world_size}")
+        if src == self.rank:
+            raise ValueError(f"rank {self.rank} cannot receive from itself")
+        world = self.world
+        with world.cond:
+            queue = world.queues.setdefault((src, self.rank), deque())
+            self._wait_locked(lambda: len(queue) > 0, lambda: f"recv from rank {src} found no matching send")
+            snap, ev = queue.popleft()
+            self.stats.p2p_recvs += 1
+            world.record(self.rank, "recv", f"src={src} tag={tag} bytes={snap.numel() * snap.element_size()}")
+        torch.cuda.current_stream().wait_event(ev)
+        self._device_mark("recv")
+        return snap
 
     def barrier(self) -> None:
         self.all_gather(torch.zeros(1, device=self.world.device), tag="barrier")
@@ -552,6 +596,33 @@ class DistRankContext(_ContextBase):
         self.dist.reduce_scatter_tensor(out.view(-1), flat_in, group=self._group)
         return out
 
+    @property
+    def sp_peers(self) -> tuple[int, ...]:
+        g = self.rank // self._sp_size
+        return tuple(range(g * self._sp_size, (g + 1) * self._sp_size))
+
+    def send(self, dst: int, payload: torch.Tensor, tag: str = "") -> None:
+        """Point-to-point send to global rank dst (NCCL P2P over NVLink / gloo on CPU)."""
+        payload = payload.contiguous()
+        nbytes = payload.numel() * payload.element_size()
+        self.stats.p2p_sends += 1
+        self.stats.communication_steps += 1
+        self.stats._account("send", nbytes)
+        self.trace.append(TraceEvent(len(self.trace), self.rank, time.perf_counter(), "send",
+                                     f"dst={dst} tag={tag} bytes={nbytes}"))
+        self.dist.send(payload, dst)
+
+    def recv(self, src: int, tag: str = "", like: torch.Tensor | None = None) -> torch.Tensor:
+        """Receive into a fresh tensor shaped like ``like`` (the ring's payloads
+        have the sender's shape and dtype, known to the receiver)."""
+        if like is None:
+            raise ValueError("DistRankContext.recv needs a template tensor (like=)")
+        out = torch.empty_like(like)
+        self.dist.recv(out, src)
+        self.stats.p2p_recvs += 1
+        self.trace.append(TraceEvent(len(self.trace), self.rank, time.perf_counter(), "recv", f"src={src} tag={tag}"))
+        return out
+
     def barrier(self) -> None:
         self.dist.barrier(group=self._group)
 
@@ -596,6 +667,14 @@ class LocalRankContext(_ContextBase):
     def reduce_scatter(self, stacked: torch.Tensor, tag: str = "") -> torch.Tensor:
         self._account("reduce_scatter", stacked)
         return stacked[0]
+
+    sp_peers = (0,)
+
+    def send(self, dst: int, payload: torch.Tensor, tag: str = "") -> None:
+        raise ValueError(f"destination {dst} outside world of 1")
+
+    def recv(self, src: int, tag: str = "", like: torch.Tensor | None = None) -> torch.Tensor:
+        raise ValueError(f"source {src} outside world of 1")
 
     def barrier(self) -> None:
         pass

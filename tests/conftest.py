@@ -41,3 +41,12 @@ HYBRID_GOLDEN = ROOT / "tests" / "golden" / "hybrid_cases.npz"
 def hybrid_golden():
     with np.load(HYBRID_GOLDEN) as z:
         return {k: z[k] for k in z.files}
+
+
+LASP1_GOLDEN = ROOT / "tests" / "golden" / "lasp1_cases.npz"
+
+
+@pytest.fixture(scope="session")
+def lasp1_golden():
+    with np.load(LASP1_GOLDEN) as z:
+        return {k: z[k] for k in z.files}

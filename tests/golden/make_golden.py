@@ -70,6 +70,7 @@ def main() -> None:
     np.savez_compressed(OUT, **data)
     print(f"wrote {OUT} ({OUT.stat().st_size} bytes, {len(data)} arrays)")
     hybrid_cases()
+    lasp1_cases()
 
 
 # (pattern, n, d, chunks, batch, heads, seed, causal): test_hybrid.py grids plus two larger stacks
@@ -105,9 +106,43 @@ def hybrid_cases() -> None:
     print(f"wrote {out_path} ({out_path.stat().st_size} bytes, {len(data)} arrays)")
 
 
+# (n, d, t, batch, heads, seed): test_lasp1.py grids plus a multi-slot and a larger case
+LASP1_CASES = [(8, 4, 2, 1, 1, 0), (8, 8, 4, 1, 1, 0), (16, 4, 4, 1, 1, 0), (16, 8, 8, 1, 1, 0),
+               (16, 4, 4, 2, 3, 2), (256, 32, 4, 1, 2, 9)]
+
+
+def lasp1_cases() -> None:
+    """Reference lasp1_iteration outputs (lasp1.py:191-210) -> tests/golden/lasp1_cases.npz."""
+    from laspsim.datagen import gen_slots, qkv_slots
+    from laspsim.lasp1 import lasp1_iteration
+    from laspsim.lasp2 import ChunkedSequence
+
+    out_path = OUT.parent / "lasp1_cases.npz"
+    data = {}
+    cat = lambda xs: np.concatenate(xs, axis=2)  # noqa: E731
+    for masked in (True, False):
+        for (n, d, t, b, h, seed) in LASP1_CASES:
+            q, k, v = qkv_slots(seed, b, h, n, d)
+            do = gen_slots(seed, b, h, n, d, "do")
+            it = lasp1_iteration(ChunkedSequence(q, k, v, t), do, masked)
+            key = f"l1_{'m' if masked else 'u'}_{n}_{d}_{t}_{b}_{h}_{seed}"
+            data[key + "_out"] = cat(it.outputs)
+            for nm in ("dq", "dk", "dv"):
+                data[f"{key}_{nm}"] = cat([getattr(g, nm) for g in it.grads])
+            data[key + "_through"] = it.caches[-1].state_through
+            st = it.run.stats
+            data[key + "_ledger"] = np.array([st.p2p_sends, st.allgather_launches, st.communication_steps,
+                                              st.bytes_sent])
+    np.savez_compressed(out_path, **data)
+    print(f"wrote {out_path} ({out_path.stat().st_size} bytes, {len(data)} arrays)")
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["hybrid"]:
         sys.path.insert(0, str(REF))
         hybrid_cases()
+    elif sys.argv[1:] == ["lasp1"]:
+        sys.path.insert(0, str(REF))
+        lasp1_cases()
     else:
         main()

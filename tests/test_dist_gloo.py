@@ -87,3 +87,60 @@ def test_two_rank_gloo_lasp2_exchange_matches_oracle():
         assert ag == 2 and rs == 1  # 2 state all_gathers per iteration (+1 LASP-2H reduce_scatter)
         state_bytes = 1 * 2 * 4 * 4 * 8
         assert nbytes == 2 * state_bytes + world * 2 * 1 * 2 * c * 4 * 8
+
+
+def _ring_worker(rank, world, port, results):
+    """LASP-1 ring plumbing (lasp1.py:43-72, 82-107) through DistRankContext.send/recv."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ctx = DistRankContext()
+        n, d, b, h = 24, 4, 1, 2
+        q, k, v, do = O.inputs(n, d, b, h, seed=4)
+        c = n // world
+        sl = slice(rank * c, (rank + 1) * c)
+        kc, vc, qc, dc = (torch.from_numpy(np.ascontiguousarray(x[:, :, sl])) for x in (k, v, q, do))
+        r, peers = ctx.sp_position, ctx.sp_peers
+        own = (kc.transpose(-1, -2) @ vc).reshape(b * h * d, d)
+        if r == 0:
+            prefix, upd = torch.zeros_like(own), own.clone()
+        else:
+            prefix = ctx.recv(peers[r - 1], tag="state", like=own)
+            upd = prefix.clone()
+            upd += own
+        if r < world - 1:
+            ctx.send(peers[r + 1], upd, tag="state")
+        g = (qc.transpose(-1, -2) @ dc).reshape(b * h * d, d)
+        if r < world - 1:
+            suffix = ctx.recv(peers[r + 1], tag="state_grad", like=g)
+            gup = suffix.clone()
+            gup += g
+        else:
+            suffix, gup = torch.zeros_like(g), g.clone()
+        if r > 0:
+            ctx.send(peers[r - 1], gup, tag="state_grad")
+        results[rank] = dict(prefix=prefix.numpy(), suffix=suffix.numpy(), through=upd.numpy(),
+                             stats=(ctx.stats.p2p_sends, ctx.stats.p2p_recvs, ctx.stats.bytes_sent))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_three_rank_gloo_ring_send_recv():
+    world = 3
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_ring_worker, args=(world, _free_port(), results), nprocs=world, join=True)
+    q, k, v, do = O.inputs(24, 4, 1, 2, seed=4)
+    c = 8
+    chunk = lambda x, i: x[:, :, i * c:(i + 1) * c]  # noqa: E731
+    states = [(np.swapaxes(chunk(k, i), -1, -2) @ chunk(v, i)).reshape(8, 4) for i in range(world)]
+    grads = [(np.swapaxes(chunk(q, i), -1, -2) @ chunk(do, i)).reshape(8, 4) for i in range(world)]
+    for r in range(world):
+        res = results[r]
+        assert np.allclose(res["prefix"], O.prefix_sum_states(states, r), rtol=0, atol=1e-12)
+        assert np.allclose(res["suffix"], O.suffix_sum_states(grads, r + 1), rtol=0, atol=1e-12)
+        sends, recvs, nbytes = res["stats"]
+        want = (r < world - 1) + (r > 0)  # one hop each way except at the ends
+        assert sends == recvs == want and nbytes == want * 8 * 4 * 8
+    assert np.allclose(results[world - 1]["through"], O.sum_states(states), rtol=0, atol=1e-12)
