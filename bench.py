@@ -375,6 +375,7 @@ def measure_workload(workload: str, ctx, rank: int, world: int, steps: int, warm
                   "lasp2_segment_states": 2 * unit_bytes, "lasp2_dkdv_chunk": 6 * unit_bytes,
                   "lasp2_state_apply": 3 * unit_bytes, "lasp2_apply_state2": 4 * unit_bytes,
                   "lasp2_backward_chunk": 7 * unit_bytes,
+                  "lasp2_dq_chunk": 5 * unit_bytes,  # dO, V, K, Q in, dQ out
                   # world-of-one persistent kernels: K,V in + Q in, O out | Q,dO in, dQ out + V,K in, dK,dV out
                   "lasp2_nomask_forward_local": 4 * unit_bytes,
                   "lasp2_nomask_backward_local": 7 * unit_bytes}.get(dom, 0)

@@ -20,7 +20,8 @@ KEYS = [
     "lts__t_bytes.sum", "l1tex__throughput.avg.pct_of_peak_sustained_active",
 ]
 ENTRY = {"tc_causal_chunk_kernel<0>": "lasp2_causal_chunk", "tc_causal_chunk_kernel<1>": "lasp2_dkdv_chunk",
-         "tc_causal_chunk_kernel<2>": "lasp2_backward_chunk", "tc_fused_apply_kernel<0>": "lasp2_state_apply",
+         "tc_causal_chunk_kernel<2>": "lasp2_backward_chunk",
+         "tc_causal_chunk_kernel<3>": "lasp2_dq_chunk", "tc_fused_apply_kernel<0>": "lasp2_state_apply",
          "tc_fused_apply_kernel<1>": "lasp2_apply_state2", "tc_apply_state": "lasp2_apply_state",
          "tc_segment_states": "lasp2_segment_states", "tc_softmax_fwd": "lasp2h_softmax_forward",
          "tc_softmax_bwd": "lasp2h_softmax_backward", "tc_flat_kernel<0>": "lasp2_nomask_forward_local",
