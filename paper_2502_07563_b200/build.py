@@ -22,6 +22,8 @@ BUILD = PKG.parent / "build"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
                      "-Xptxas", "-v", f"-I{INCLUDE}"] + (["-DLASP2_TRACE"] if os.environ.get("LASP2_TRACE") else [])
+# experiment knobs for A/B builds, e.g. LASP2_DEFINES="LASP2_POLY_FROM=10"
+NVCC_FLAGS += [f"-D{d}" for d in os.environ.get("LASP2_DEFINES", "").split()]
 
 
 def _nvcc() -> str:

@@ -164,6 +164,45 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
+// sm_100 paired fp32 arithmetic (FFMA2 / FADD2) and the 3-input max (FMNMX3):
+// half the issue slots of the scalar forms in the softmax inner loops.
+__device__ __forceinline__ void ffma2_bc(float& d0, float& d1, float a0, float a1, float b, float c) {
+  uint64_t d;
+  asm("{\n\t.reg .b64 pa, pb, pc;\n\tmov.b64 pa, {%1, %2};\n\tmov.b64 pb, {%3, %3};\n\t"
+      "mov.b64 pc, {%4, %4};\n\tfma.rn.f32x2 %0, pa, pb, pc;\n\t}"
+      : "=l"(d)
+      : "f"(a0), "f"(a1), "f"(b), "f"(c));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(d));
+}
+__device__ __forceinline__ void fadd2(float& a0, float& a1, float b0, float b1) {
+  uint64_t d;
+  asm("{\n\t.reg .b64 pa, pb;\n\tmov.b64 pa, {%1, %2};\n\tmov.b64 pb, {%3, %4};\n\t"
+      "add.rn.f32x2 %0, pa, pb;\n\t}"
+      : "=l"(d)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(d));
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// 2^x on the FMA pipe (the SFU's ex2 rate on sm_100 equals the tensor core's
+// per-element rate of an attention block, so part of the exponentials move
+// here): round-to-nearest split x = j + f, f in [-0.5, 0.5], degree-3
+// relative-minimax polynomial for 2^f (max rel. error 7.5e-5, far below the
+// bf16 rounding of P), exponent added as integer bits. x is clamped at -125 so
+// the result stays a normal float (a masked-out score underflows to ~1e-38
+// instead of 0; masked elements are zeroed by the caller anyway).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -125.f);
+  const float t = x + 12582912.f;  // 1.5 * 2^23: round(x) lands in the low mantissa bits
+  const float f = x - (t - 12582912.f);
+  const float p = fmaf(fmaf(fmaf(0.05517160520f, f, 0.24261111021f), f, 0.69326096773f), f, 0.99992805719f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 }  // namespace tc
 
 // host: launch with programmatic stream serialization (PDL) and an optional

@@ -279,6 +279,14 @@ __global__ void __launch_bounds__(kSmFwdThreads, 1)
 constexpr int kF2Ring = 5;
 constexpr uint32_t kSmFwd2Smem = (2 + kF2Ring) * kTileBytes + 1024 + 256;
 constexpr float kLazyRescale = 8.f;  // log2 of the largest unnormalised P
+// Share of the exponentials evaluated by ex2_poly on the FMA pipe: pairs
+// i >= kPolyFrom of every 16 columns. Measured at N=32K (profiles/r01b_softmax_poly.log):
+// 0 % 1177 TFLOP/s, 25 % 1139, 37.5 % 986, 50 % 885 — the softmax warps are
+// issue-bound, not SFU-bound, on sm_100, so the default keeps every exp2 on the SFU.
+#ifndef LASP2_POLY_FROM
+#define LASP2_POLY_FROM 16
+#endif
+constexpr int kPolyFrom = LASP2_POLY_FROM;
 
 // 10 warps: three share an SMSP's 16K registers, so 168 per thread is the cap
 __global__ void __launch_bounds__(kSmFwdThreads, 1)
@@ -420,39 +428,47 @@ __global__ void __launch_bounds__(kSmFwdThreads, 1)
 #pragma unroll
         for (int c = 0; c < 128; c += 32) tmem_ld_32x32b_x32(ts + c, *reinterpret_cast<uint32_t(*)[32]>(sr + c));
         tmem_ld_wait();
-        // row max as 8 independent chains (a single fmaxf chain is 128 dependent ops)
+        // row max as 8 independent chains of 3-input max (two new columns per FMNMX3)
         float mx[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) mx[u] = -INFINITY;
         if (full_blk) {
 #pragma unroll
-          for (int i = 0; i < 128; ++i) mx[i & 7] = fmaxf(mx[i & 7], __uint_as_float(sr[i]));
+          for (int i = 0; i < 128; i += 2)
+            mx[(i >> 1) & 7] = fmax3(mx[(i >> 1) & 7], __uint_as_float(sr[i]), __uint_as_float(sr[i + 1]));
         } else {
 #pragma unroll
           for (int i = 0; i < 128; ++i)
             if (i < lim) mx[i & 7] = fmaxf(mx[i & 7], __uint_as_float(sr[i]));
         }
-        const float bm = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                               fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+        const float bm = fmaxf(fmax3(mx[0], mx[1], mx[2]), fmax3(fmax3(mx[3], mx[4], mx[5]), mx[6], mx[7]));
         const float mc = bm * a.scale_log2;
         const bool need = mc > m_run + kLazyRescale;
         const float m_new = need ? mc : m_run;
         const float corr = (need && m_run != -INFINITY) ? ex2_approx(m_run - m_new) : (need ? 0.f : 1.f);
-        float ps[4] = {0.f, 0.f, 0.f, 0.f};  // row sum as 4 independent chains
+        float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // row sum as 4 independent pair chains
 #pragma unroll
         for (int c = 0; c < 128; c += 16) {
           uint32_t pk[8];
 #pragma unroll
           for (int i = 0; i < 16; i += 2) {
             const bool ok0 = full_blk || c + i < lim, ok1 = full_blk || c + i + 1 < lim;
-            const float p0 = ok0 ? ex2_approx(fmaf(__uint_as_float(sr[c + i]), a.scale_log2, -m_new)) : 0.f;
-            const float p1 = ok1 ? ex2_approx(fmaf(__uint_as_float(sr[c + i + 1]), a.scale_log2, -m_new)) : 0.f;
-            ps[(i >> 1) & 3] += p0 + p1;
+            float x0, x1;  // x = s * scale * log2(e) - m for two columns in one FFMA2
+            ffma2_bc(x0, x1, __uint_as_float(sr[c + i]), __uint_as_float(sr[c + i + 1]), a.scale_log2, -m_new);
+            // this share of the exponentials runs on the FMA pipe; evaluated unconditionally
+            // and selected after, so the compiler interleaves elements instead of branching
+            const bool poly = i >= kPolyFrom;
+            const float e0 = poly ? ex2_poly(x0) : ex2_approx(x0);
+            const float e1 = poly ? ex2_poly(x1) : ex2_approx(x1);
+            const float p0 = ok0 ? e0 : 0.f;
+            const float p1 = ok1 ? e1 : 0.f;
+            const int ch = 2 * ((i >> 1) & 3);
+            fadd2(ps[ch], ps[ch + 1], p0, p1);
             pk[i >> 1] = pack_bf16x2(p0, p1);
           }
           tmem_st_32x32b_x8(ts + (c >> 1), pk);
         }
-        const float psum = (ps[0] + ps[1]) + (ps[2] + ps[3]);
+        const float psum = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
         if (j > 0 && __any_sync(0xffffffffu, need)) {  // raise this warp's rows' max: rescale O in TMEM
           mbar_wait(&o_full[t], (j - 1) & 1);  // PV_t(j-1) complete
           tc_fence_after();
