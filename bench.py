@@ -336,7 +336,9 @@ def measure_workload(workload: str, ctx, rank: int, world: int, steps: int, warm
         h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
         ev = lambda: torch.cuda.Event()  # noqa: E731
         h2d_done, comp_done, d2h_done = [ev(), ev()], [ev(), ev()], [ev(), ev()]
-        e2e_steps = max(4, min(steps, 8))
+        # the pipeline fills once and drains once per measurement (one H2D and one D2H not
+        # overlapped): 16 steps keep that to ~1/16 of the steady-state PCIe-bound period
+        e2e_steps = max(4, min(2 * steps, 16))
         sync_all()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(h2d_s)
