@@ -437,7 +437,11 @@ def run_gpu_arm(args) -> None:
             dist.init_process_group("nccl", device_id=device)
         else:
             dist.init_process_group(args.dist_backend)
-        ctx = comm.DistRankContext()
+        peer = args.state_exchange == "peer"
+        ctx = comm.DistRankContext(peer_exchange=peer)
+        if peer:  # fused state exchange over NVLink peer memory
+            from paper_2502_07563_b200 import lasp2 as _l2
+            _l2.STATE_EXCHANGE = "peer"
     else:
         ctx = comm.LocalRankContext()
     peaks = load_peaks()
@@ -488,6 +492,8 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--state-exchange", default="collective", choices=["collective", "peer"],
+                    help="N>1: NCCL all_gather of the states, or the fused put into symmetric-memory peers")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--eager", action="store_true", help="time eager launches instead of CUDA-graph replay")

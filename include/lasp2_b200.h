@@ -57,6 +57,29 @@ int lasp2_segment_states(int dtype, const void* x, const void* y, void* seg_stat
 int lasp2_scan_segments(int dtype, void* seg_states, void* chunk_total, int64_t slots, int nseg, int dim, int reverse,
                         void* stream);
 
+/* Fused state exchange over peer memory (replaces the NCCL
+ * AllGather of RankContext.all_gather, comm.py:367-412, for the state payload).
+ * lasp2_scan_put = lasp2_scan_segments plus: the chunk total is stored into
+ * slot `rank` of half (epoch & 1) of every rank's receive buffer
+ * ([2][nranks][slots*dim*dim], states dtype; `peer_recv` is a DEVICE array of
+ * nranks pointers, one per rank, e.g. symmetric-memory peer addresses over
+ * NVLink) and, once every element is stored, flag[rank] of every rank
+ * (`peer_flags`, device array of nranks pointers to uint64[nranks]) is set to
+ * `epoch` with a system-scope release. `done` is a zeroed uint32 the launch
+ * re-arms. Epochs start at 1 and grow per exchange. lasp2_exchange_wait
+ * blocks the stream until flags[lo..hi) (a uint64 array) carry `epoch`; after
+ * waiting on this rank's flags, half (epoch & 1) of the receive buffer is
+ * folded with lasp2_fold_states exactly like an all_gather result, and
+ * lasp2_exchange_ack then sets acks[rank] = epoch on every rank (`peer_acks`,
+ * device array of nranks pointers to uint64[nranks]). Before a put of epoch
+ * e > 2 the caller waits on its own acks[0..nranks) for e - 2, so no reader
+ * still needs the half being overwritten. */
+int lasp2_scan_put(int dtype, void* seg_states, void* chunk_total, int64_t slots, int nseg, int dim, int reverse,
+                   const void* peer_recv, const void* peer_flags, int rank, int nranks, uint64_t epoch, void* done,
+                   void* stream);
+int lasp2_exchange_wait(const void* flags, int lo, int hi, uint64_t epoch, void* stream);
+int lasp2_exchange_ack(const void* peer_acks, int rank, int nranks, uint64_t epoch, void* stream);
+
 /* out = ordered fold of `nstates` gathered states, each `elems` elements,
  * stored rank-major ([nstates][elems], the all_gather layout):
  *   PREFIX(bound): states[0:bound] ascending  = prefix_sum_states (numerics.py:71-90)

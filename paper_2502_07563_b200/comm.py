@@ -116,6 +116,36 @@ class GroupInfo:
     sp_position: int
 
 
+class PeerExchange:
+    """One rank's handle on a fused peer-memory state exchange.
+
+    ``recv`` [2, T, *state] is this rank's receive buffer, double-buffered by
+    epoch parity (slot j = rank j's chunk total), ``flags`` [T] its
+    epoch-stamped arrival flags, ``acks`` [T] the epochs each reader has
+    finished folding (back-pressure for this rank's puts), ``*_table`` device
+    arrays of every rank's buffer / flag / ack addresses (peer addresses over
+    NVLink with symmetric memory; same-device addresses in the threads-as-ranks
+    world), ``done`` the put kernel's completion counter. ``ops.scan_put``
+    writes, ``ops.exchange_fold`` waits, folds and acknowledges.
+    """
+
+    def __init__(self, rank: int, nranks: int, recv: torch.Tensor, flags: torch.Tensor, acks: torch.Tensor,
+                 done: torch.Tensor, recv_table: torch.Tensor, flag_table: torch.Tensor,
+                 ack_table: torch.Tensor) -> None:
+        self.rank, self.nranks = rank, nranks
+        self.recv, self.flags, self.acks, self.done = recv, flags, acks, done
+        self.recv_table, self.flag_table, self.ack_table = recv_table, flag_table, ack_table
+        self.epoch = 0
+
+    def next_epoch(self) -> int:
+        self.epoch += 1
+        return self.epoch
+
+
+def _ptr_table(tensors: Sequence[torch.Tensor], device) -> torch.Tensor:
+    return torch.tensor([t.data_ptr() for t in tensors], dtype=torch.int64, device=device)
+
+
 def process_groups(cfg: WorldConfig) -> dict[int, GroupInfo]:
     """Contiguous SP groups, strided DP peers (comm.py:143-158)."""
     t = cfg.sp_size
@@ -183,6 +213,8 @@ class _World:
         self.groups = [tuple(range(g * t, (g + 1) * t)) for g in range(cfg.dp_size)]
         self.gens: dict[tuple[int, int], _Gen] = {}
         self.queues: dict[tuple[int, int], deque] = {}  # (src, dst) -> FIFO of (snapshot, event)
+        self.exchanges: dict[tuple, list[PeerExchange]] = {}  # (group, tag, shape, dtype) -> per-position handles
+        self.exchange_calls: dict[tuple[int, int], int] = {}  # (group, call) -> ranks that exchanged
         self.t0 = time.perf_counter()
 
     def record(self, rank: int, kind: str, detail: str) -> None:
@@ -354,6 +386,44 @@ class RankContext(_ContextBase):
         self._device_mark("reduce_scatter_complete")
         return acc
 
+    def peer_exchange(self, tag: str, like: torch.Tensor) -> PeerExchange:
+        """This rank's handle on the fused state exchange for states shaped like
+        ``like`` (allocated once per group, tag, shape and dtype; every rank of
+        the group shares the address tables)."""
+        world = self.world
+        key = (self._group_index, tag, tuple(like.shape), like.dtype)
+        with world.cond:
+            handles = world.exchanges.get(key)
+            if handles is None:
+                t, dev = self.sp_size, world.device
+                recv = [torch.zeros((2, t, *like.shape), dtype=like.dtype, device=dev) for _ in range(t)]
+                flags = [torch.zeros(t, dtype=torch.int64, device=dev) for _ in range(t)]
+                acks = [torch.zeros(t, dtype=torch.int64, device=dev) for _ in range(t)]
+                done = [torch.zeros(1, dtype=torch.int32, device=dev) for _ in range(t)]
+                tables = [_ptr_table(x, dev) for x in (recv, flags, acks)]
+                torch.cuda.synchronize(dev)  # zero-filled before any rank's kernels touch them
+                handles = [PeerExchange(p, t, recv[p], flags[p], acks[p], done[p], *tables) for p in range(t)]
+                world.exchanges[key] = handles
+        return handles[self.sp_position]
+
+    def account_exchange(self, ex: PeerExchange, tag: str = "") -> None:
+        """Ledger of one fused exchange: one all_gather launch per group per call,
+        this rank's contribution in bytes (comm.py:395-397)."""
+        nbytes = ex.recv[0, 0].numel() * ex.recv.element_size()
+        world = self.world
+        with world.cond:
+            call = self._calls
+            self._calls += 1
+            k = (self._group_index, call)
+            world.exchange_calls[k] = world.exchange_calls.get(k, 0) + 1
+            if world.exchange_calls[k] == self.sp_size:
+                world.collective_launches += 1
+            world.record(self.rank, "all_gather_issue", f"call={call} tag={tag} bytes={nbytes} peer")
+        self.stats.allgather_launches += 1
+        self.stats.communication_steps += 1
+        self.stats._account("all_gather", nbytes)
+        self._device_mark("all_gather_issue")
+
     def send(self, dst: int, payload: torch.Tensor, tag: str = "") -> None:
         """Deposit a frozen snapshot for global rank dst; non-blocking. The
         matched pair is one communication step on the sender's ledger (comm.py:324-343)."""
@@ -519,10 +589,12 @@ class DistRankContext(_ContextBase):
     every process must construct its context (new_group is collective).
     """
 
-    def __init__(self, sp_size: int | None = None) -> None:
+    def __init__(self, sp_size: int | None = None, peer_exchange: bool = False) -> None:
         import torch.distributed as dist
 
         self._init_common()
+        self._peer = peer_exchange
+        self._exchanges: dict[tuple, PeerExchange] = {}
         self.dist = dist
         self.rank = dist.get_rank()
         world = dist.get_world_size()
@@ -601,6 +673,43 @@ class DistRankContext(_ContextBase):
         g = self.rank // self._sp_size
         return tuple(range(g * self._sp_size, (g + 1) * self._sp_size))
 
+    def peer_exchange(self, tag: str, like: torch.Tensor) -> PeerExchange | None:
+        """Fused state exchange over NVLink peer memory (torch symmetric memory),
+        opted in with ``DistRankContext(peer_exchange=True)``; None keeps the
+        NCCL all_gather. Buffers are allocated once per (tag, shape, dtype)."""
+        if not self._peer or not like.is_cuda:
+            return None
+        key = (tag, tuple(like.shape), like.dtype)
+        ex = self._exchanges.get(key)
+        if ex is None:
+            import torch.distributed._symmetric_memory as symm_mem
+
+            t, dev = self._sp_size, like.device
+            group_name = self._group.group_name
+            bufs = [symm_mem.empty((2, t, *like.shape), dtype=like.dtype, device=dev),
+                    symm_mem.empty((t,), dtype=torch.int64, device=dev),
+                    symm_mem.empty((t,), dtype=torch.int64, device=dev)]
+            tables = []
+            for buf in bufs:
+                buf.zero_()
+                hdl = symm_mem.rendezvous(buf, group_name)
+                if hdl.buffer_ptrs[hdl.rank] != buf.data_ptr():
+                    raise RuntimeError("symmetric-memory buffer is not at the start of its allocation")
+                tables.append(torch.tensor(list(hdl.buffer_ptrs), dtype=torch.int64, device=dev))
+            torch.cuda.synchronize(dev)
+            self.dist.barrier(group=self._group)  # every rank's zero-fill precedes any put
+            ex = PeerExchange(self.sp_position, t, *bufs, torch.zeros(1, dtype=torch.int32, device=dev), *tables)
+            self._exchanges[key] = ex
+        return ex
+
+    def account_exchange(self, ex: PeerExchange, tag: str = "") -> None:
+        nbytes = ex.recv[0, 0].numel() * ex.recv.element_size()
+        self.stats.allgather_launches += 1
+        self.stats.communication_steps += 1
+        self.stats._account("all_gather", nbytes)
+        self.trace.append(TraceEvent(len(self.trace), self.rank, time.perf_counter(), "all_gather_issue",
+                                     f"bytes={nbytes} peer tag={tag}"))
+
     def send(self, dst: int, payload: torch.Tensor, tag: str = "") -> None:
         """Point-to-point send to global rank dst (NCCL P2P over NVLink / gloo on CPU)."""
         payload = payload.contiguous()
@@ -669,6 +778,9 @@ class LocalRankContext(_ContextBase):
         return stacked[0]
 
     sp_peers = (0,)
+
+    def peer_exchange(self, tag: str, like: torch.Tensor) -> None:
+        return None  # a world of one exchanges nothing (the all_gather is the identity)
 
     def send(self, dst: int, payload: torch.Tensor, tag: str = "") -> None:
         raise ValueError(f"destination {dst} outside world of 1")

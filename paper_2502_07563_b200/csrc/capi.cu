@@ -94,6 +94,34 @@ int lasp2_scan_segments(int dtype, void* seg_states, void* chunk_total, int64_t 
   return cuda_status(e, "scan_segments");
 }
 
+int lasp2_scan_put(int dtype, void* seg_states, void* chunk_total, int64_t slots, int nseg, int dim, int reverse,
+                   const void* peer_recv, const void* peer_flags, int rank, int nranks, uint64_t epoch, void* done,
+                   void* stream) {
+  CHECK(valid_dtype(dtype), "scan_put: unknown dtype");
+  CHECK(seg_states && peer_recv && peer_flags && done, "scan_put: null pointer");
+  CHECK(slots >= 1 && nseg >= 1 && dim >= 1, "scan_put: bad shape");
+  CHECK(nranks >= 1 && rank >= 0 && rank < nranks, "scan_put: rank outside [0, nranks)");
+  CHECK(epoch >= 1, "scan_put: epochs start at 1");
+  cudaError_t e = dtype == LASP2_F64
+                      ? lasp::scan_put<double>(seg_states, chunk_total, slots, nseg, dim, reverse, peer_recv,
+                                               peer_flags, rank, nranks, epoch, (unsigned*)done, S(stream))
+                      : lasp::scan_put<float>(seg_states, chunk_total, slots, nseg, dim, reverse, peer_recv,
+                                              peer_flags, rank, nranks, epoch, (unsigned*)done, S(stream));
+  return cuda_status(e, "scan_put");
+}
+
+int lasp2_exchange_wait(const void* flags, int lo, int hi, uint64_t epoch, void* stream) {
+  CHECK(flags, "exchange_wait: null pointer");
+  CHECK(lo >= 0 && hi >= lo, "exchange_wait: bad range");
+  return cuda_status(lasp::exchange_wait(flags, lo, hi, epoch, S(stream)), "exchange_wait");
+}
+
+int lasp2_exchange_ack(const void* peer_acks, int rank, int nranks, uint64_t epoch, void* stream) {
+  CHECK(peer_acks, "exchange_ack: null pointer");
+  CHECK(nranks >= 1 && rank >= 0 && rank < nranks, "exchange_ack: rank outside [0, nranks)");
+  return cuda_status(lasp::exchange_ack(peer_acks, rank, nranks, epoch, S(stream)), "exchange_ack");
+}
+
 int lasp2_fold_states(int dtype, const void* gathered, void* out, int nstates, int64_t elems, int mode, int bound,
                       void* stream) {
   CHECK(valid_dtype(dtype), "fold_states: unknown dtype");

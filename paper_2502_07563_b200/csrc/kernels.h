@@ -30,6 +30,12 @@ cudaError_t simt_softmax_backward(const void* q, const void* kf, const void* vf,
 template <typename A>
 cudaError_t scan_states(void* seg, void* total, int64_t slots, int nseg, int dim, int reverse, cudaStream_t s);
 template <typename A>
+cudaError_t scan_put(void* seg, void* total, int64_t slots, int nseg, int dim, int reverse, const void* peer_recv,
+                     const void* peer_flags, int rank, int nranks, unsigned long long epoch, unsigned* done,
+                     cudaStream_t s);
+cudaError_t exchange_wait(const void* flags, int lo, int hi, unsigned long long epoch, cudaStream_t s);
+cudaError_t exchange_ack(const void* peer_acks, int rank, int nranks, unsigned long long epoch, cudaStream_t s);
+template <typename A>
 cudaError_t fold_states(const void* gathered, void* out, int nstates, int64_t elems, int mode, int bound,
                         cudaStream_t s);
 template <typename T>

@@ -46,6 +46,96 @@ __global__ void scan_states_kernel(A* __restrict__ seg, A* __restrict__ total, i
   if (total) total[slot * dd + el] = run;
 }
 
+// ---- fused state exchange over peer memory -------------------
+// scan_put: the scan above, and the chunk total (this rank's M_t / dM_t, the
+// all_gather payload) is stored straight into slot `rank` of every rank's
+// receive buffer [2][nranks][slots*dd] (double-buffered by epoch parity) —
+// P2P stores over NVLink when the buffers are symmetric-memory peers, plain
+// stores in the one-GPU threads world. The last block to finish (device-wide
+// counter, re-armed by that block) releases one epoch-stamped flag per rank at
+// system scope after a system fence, so a reader that acquires flag[rank]
+// sees every element of the slot. Back-pressure: before the put of epoch e the
+// caller waits (exchange_wait on its own acks) until every reader has
+// acknowledged epoch e-2 (exchange_ack after its fold), so a rank that runs
+// ahead (a forward-only loop needs nothing from its successors) never
+// clobbers the half another rank has not folded yet. The wait is its own
+// one-thread kernel: spinning inside the put's grid could starve the other
+// ranks' kernels of SM slots when ranks share one GPU.
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ void wait_epochs(const unsigned long long* flags, int lo, int hi, unsigned long long epoch) {
+  for (int j = lo; j < hi; ++j) {
+    const long long t0 = clock64();
+    while (ld_acquire_sys_u64(flags + j) < epoch) {
+      __nanosleep(64);
+      if (clock64() - t0 > (1ll << 36)) __trap();  // a peer never arrived: fail loudly, do not hang
+    }
+  }
+}
+
+template <typename A>
+__global__ void scan_put_kernel(A* __restrict__ seg, A* __restrict__ total, int64_t slots, int nseg, int64_t dd,
+                                int reverse, A* const* __restrict__ peer_recv,
+                                unsigned long long* const* __restrict__ peer_flags, int rank, int nranks,
+                                unsigned long long epoch, unsigned* __restrict__ done) {
+  ptx::pdl_wait();
+  ptx::pdl_launch_dependents();
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = slots * dd;
+  const int64_t off = ((int64_t)(epoch & 1) * nranks + rank) * n;
+  if (idx < n) {
+    const int64_t slot = idx / dd, el = idx % dd;
+    A* base = seg + slot * nseg * dd + el;
+    A run = A(0);
+    for (int i0 = 0; i0 < nseg; i0 += 8) {
+      A vals[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u;
+        if (i < nseg) vals[u] = base[(int64_t)(reverse ? nseg - 1 - i : i) * dd];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u;
+        if (i < nseg) {
+          base[(int64_t)(reverse ? nseg - 1 - i : i) * dd] = run;
+          run = (i == 0) ? vals[u] : run + vals[u];
+        }
+      }
+    }
+    if (total) total[idx] = run;
+    for (int r = 0; r < nranks; ++r) peer_recv[r][off + idx] = run;
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(done, 1u) == gridDim.x - 1) {
+    *done = 0;  // every block has stored and fenced: re-arm for the next exchange
+    __threadfence_system();
+    for (int r = 0; r < nranks; ++r) st_release_sys_u64(peer_flags[r] + rank, epoch);
+  }
+}
+
+// Block until flags[lo..hi) all carry `epoch` (or a later one). One thread; a
+// peer that never arrives traps after ~2^36 cycles instead of hanging the GPU.
+__global__ void exchange_wait_kernel(const unsigned long long* __restrict__ flags, int lo, int hi,
+                                     unsigned long long epoch) {
+  wait_epochs(flags, lo, hi, epoch);
+}
+
+// After this rank's fold of `epoch` (stream order): acks[rank] = epoch on every rank.
+__global__ void exchange_ack_kernel(unsigned long long* const* __restrict__ peer_acks, int rank, int nranks,
+                                    unsigned long long epoch) {
+  __threadfence_system();
+  for (int r = 0; r < nranks; ++r) st_release_sys_u64(peer_acks[r] + rank, epoch);
+}
+
 // gathered: [nstates][elems]. mode 0 = prefix(bound), 1 = suffix(bound), 2 = full.
 template <typename A>
 __global__ void fold_states_kernel(const A* __restrict__ gathered, A* __restrict__ out, int nstates, int64_t elems,
@@ -123,6 +213,28 @@ cudaError_t scan_states(void* seg, void* total, int64_t slots, int nseg, int dim
 }
 
 template <typename A>
+cudaError_t scan_put(void* seg, void* total, int64_t slots, int nseg, int dim, int reverse, const void* peer_recv,
+                     const void* peer_flags, int rank, int nranks, unsigned long long epoch, unsigned* done,
+                     cudaStream_t s) {
+  const int64_t dd = (int64_t)dim * dim;
+  const int64_t n = slots * dd;
+  return launch_pdl(scan_put_kernel<A>, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, 1, (A*)seg, (A*)total,
+                    slots, nseg, dd, reverse, (A* const*)peer_recv, (unsigned long long* const*)peer_flags, rank,
+                    nranks, epoch, done);
+}
+
+cudaError_t exchange_wait(const void* flags, int lo, int hi, unsigned long long epoch, cudaStream_t s) {
+  if (hi <= lo) return cudaSuccess;
+  exchange_wait_kernel<<<1, 1, 0, s>>>((const unsigned long long*)flags, lo, hi, epoch);
+  return cudaGetLastError();
+}
+
+cudaError_t exchange_ack(const void* peer_acks, int rank, int nranks, unsigned long long epoch, cudaStream_t s) {
+  exchange_ack_kernel<<<1, 1, 0, s>>>((unsigned long long* const*)peer_acks, rank, nranks, epoch);
+  return cudaGetLastError();
+}
+
+template <typename A>
 cudaError_t fold_states(const void* gathered, void* out, int nstates, int64_t elems, int mode, int bound,
                         cudaStream_t s) {
   return launch_pdl(fold_states_kernel<A>, dim3((unsigned)((elems + 255) / 256)), dim3(256), 0, s, 1,
@@ -141,6 +253,10 @@ cudaError_t gen_slots(uint64_t seed, const uint64_t* tag_words, void* out, int64
 
 template cudaError_t scan_states<float>(void*, void*, int64_t, int, int, int, cudaStream_t);
 template cudaError_t scan_states<double>(void*, void*, int64_t, int, int, int, cudaStream_t);
+template cudaError_t scan_put<float>(void*, void*, int64_t, int, int, int, const void*, const void*, int, int,
+                                     unsigned long long, unsigned*, cudaStream_t);
+template cudaError_t scan_put<double>(void*, void*, int64_t, int, int, int, const void*, const void*, int, int,
+                                      unsigned long long, unsigned*, cudaStream_t);
 template cudaError_t fold_states<float>(const void*, void*, int, int64_t, int, int, cudaStream_t);
 template cudaError_t fold_states<double>(const void*, void*, int, int64_t, int, int, cudaStream_t);
 template cudaError_t gen_slots<float>(uint64_t, const uint64_t*, void*, int64_t, int64_t, int64_t, int64_t, cudaStream_t);

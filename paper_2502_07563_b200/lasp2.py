@@ -172,6 +172,32 @@ def _unpack_gathered(gathered: torch.Tensor, like: torch.Tensor) -> torch.Tensor
     return gathered.view(t, *like.shape)
 
 
+# How a rank's chunk total reaches the other ranks. "collective": ctx.all_gather
+# (NCCL all_gather_into_tensor on a side stream under torchrun). "peer": the scan
+# kernel that produces M_t stores it straight into every rank's receive buffer
+# (symmetric-memory peer addresses over NVLink) and releases a flag per rank;
+# the fold waits on the flags it needs (lasp2_scan_put / lasp2_exchange_wait,
+# SURVEY §8f.2). Both count one all_gather launch per exchange, same bytes.
+STATE_EXCHANGE = "collective"
+
+
+def _peer(ctx, tag: str, like: torch.Tensor):
+    if STATE_EXCHANGE != "peer" or ctx.sp_size == 1:
+        return None
+    fn = getattr(ctx, "peer_exchange", None)
+    return fn(tag, like) if fn is not None else None
+
+
+def _share_total(ctx, seg: torch.Tensor, reverse: bool, data_dtype: torch.dtype, tag: str):
+    """Scan the segment states; returns (chunk total, exchange handle or None)."""
+    ex = _peer(ctx, tag, seg[:, :, 0])
+    if ex is None:
+        return ops.scan_segments(seg, reverse=reverse, data_dtype=data_dtype), None
+    total = ops.scan_put(seg, reverse, data_dtype, ex)
+    ctx.account_exchange(ex, tag)
+    return total, ex
+
+
 def _forward_nomask_rank(ctx, qc: torch.Tensor, kc: torch.Tensor,
                          vc: torch.Tensor) -> tuple[torch.Tensor, ActivationCache]:
     """O_t = Q_t M_{1:T} after one state all_gather (lasp2.py:208-216)."""
@@ -183,7 +209,12 @@ def _forward_nomask_rank(ctx, qc: torch.Tensor, kc: torch.Tensor,
         out, m_full = ops.nomask_forward_local(qc, kc, vc)
         _gather_states(ctx, m_full, "state")
         return out, ActivationCache(q=qc, k=kc, v=vc, masked=False, m_full=m_full, state_folds=1)
-    _, m_t, _ = ops.chunk_states(kc, vc)
+    nseg = ops.num_segments(kc)
+    m_t, ex = _share_total(ctx, ops.segment_states(kc, vc, nseg), False, kc.dtype, "state")
+    if ex is not None:
+        m_full = ops.exchange_fold(ex, ops.FOLD_FULL)
+        out = ops.apply_state(qc, m_full)
+        return out, ActivationCache(q=qc, k=kc, v=vc, masked=False, m_full=m_full, state_folds=1)
     gathered = _unpack_gathered(_gather_states(ctx, m_t, "state"), m_t)
     m_full = ops.sum_states(gathered)
     out = ops.apply_state(qc, m_full)
@@ -201,7 +232,24 @@ def _forward_masked_rank(ctx, qc: torch.Tensor, kc: torch.Tensor, vc: torch.Tens
     """
     qc, kc, vc = _contig(qc, kc, vc)
     t = ctx.sp_position
-    seg, m_t, nseg = ops.chunk_states(kc, vc)
+    nseg = ops.num_segments(kc)
+    seg = ops.segment_states(kc, vc, nseg)
+    m_t, ex = _share_total(ctx, seg, False, kc.dtype, "state")
+    if ex is not None:  # fused peer exchange: M_t is already on its way to every rank
+        if overlap:
+            ctx.mark("intra_start", f"chunk={t}")
+            out = ops.causal_chunk(qc, kc, vc, seg, None, nseg)
+            ctx.mark("intra_end", f"chunk={t}")
+            m_prefix = ops.exchange_fold(ex, ops.FOLD_PREFIX, t)
+            if t > 0:
+                ops.apply_state(qc, m_prefix, out=out, accumulate=True)
+        else:
+            m_prefix = ops.exchange_fold(ex, ops.FOLD_PREFIX, t)
+            ctx.mark("intra_start", f"chunk={t}")
+            out = ops.causal_chunk(qc, kc, vc, seg, m_prefix if t > 0 else None, nseg)
+            ctx.mark("intra_end", f"chunk={t}")
+        return out, ActivationCache(q=qc, k=kc, v=vc, masked=True, m_prefix=m_prefix, state_folds=1,
+                                    seg_prefix=seg, seg_total=m_t, nseg=nseg)
     if overlap:
         pending = _gather_states(ctx, m_t, "state", async_op=True)
         ctx.mark("intra_start", f"chunk={t}")
@@ -250,10 +298,14 @@ def _backward_nomask_rank(ctx, cache: ActivationCache, d_out: torch.Tensor) -> G
         _gather_states(ctx, cache.m_full, "state_grad")  # accounting only: identity at T = 1
         return GradientBundle(dq=dq, dk=dk, dv=dv)
     unit_bytes = q.numel() * q.element_size()
-    if ctx.sp_size == 1 or unit_bytes >= _FUSE_DQ_MIN_BYTES:
+    if ctx.sp_size == 1 or unit_bytes >= _FUSE_DQ_MIN_BYTES or STATE_EXCHANGE == "peer":
         nseg = ops.num_segments(q)
         gseg, dq = ops.state_apply(q, do, cache.m_full, nseg)
-        g_t = ops.scan_segments(gseg, reverse=False, data_dtype=q.dtype)
+        g_t, ex = _share_total(ctx, gseg, False, q.dtype, "state_grad")
+        if ex is not None:
+            dm_full = ops.exchange_fold(ex, ops.FOLD_FULL)
+            dk, dv = ops.apply_state2(cache.v, cache.k, dm_full)
+            return GradientBundle(dq=dq, dk=dk, dv=dv)
         gathered = _unpack_gathered(_gather_states(ctx, g_t, "state_grad"), g_t)
     else:
         _, g_t, _ = ops.chunk_states(q, do)
@@ -293,9 +345,13 @@ def _backward_masked_rank(ctx, cache: ActivationCache, d_out: torch.Tensor) -> G
         # dq_s = sum_{i<=s}(do_s.v_i) k_i + do_s (M_{1:t-1} + local prefix)^T, and in the same
         # pass over (dO, V, K, Q) the dM segment states Q_g^T dO_g (lasp2.py:273-279)
         dq, gseg = ops.dq_chunk(q, k, v, do, cache.seg_prefix, cache.m_prefix if t > 0 else None, nseg)
-        g_t = ops.scan_segments(gseg, reverse=True, data_dtype=q.dtype)
-        gathered = _unpack_gathered(_gather_states(ctx, g_t, "state_grad"), g_t)
-        r = ops.suffix_states(gathered, t + 1) if t < world - 1 else None
+        g_t, ex = _share_total(ctx, gseg, True, q.dtype, "state_grad")
+        if ex is not None:  # every rank folds (and acknowledges) the exchange, the last one gets zeros
+            r = ops.exchange_fold(ex, ops.FOLD_SUFFIX, t + 1)
+            r = r if t < world - 1 else None
+        else:
+            gathered = _unpack_gathered(_gather_states(ctx, g_t, "state_grad"), g_t)
+            r = ops.suffix_states(gathered, t + 1) if t < world - 1 else None
         dk, dv = ops.dkdv_chunk(q, k, v, do, gseg, r, nseg)
         return GradientBundle(dq=dq, dk=dk, dv=dv)
     gseg = ops.segment_states(q, do, nseg)

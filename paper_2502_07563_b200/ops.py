@@ -63,6 +63,35 @@ def chunk_states(x: torch.Tensor, y: torch.Tensor, reverse: bool = False) -> tup
     return seg, total, nseg
 
 
+def scan_put(seg: torch.Tensor, reverse: bool, data_dtype: torch.dtype, ex) -> torch.Tensor:
+    """scan_segments that also stores the chunk total into slot ex.rank of every
+    rank's receive buffer and releases the flags (header: lasp2_scan_put)."""
+    require_cuda(seg)
+    b, h, nseg, d, _ = seg.shape
+    total = torch.empty((b, h, d, d), dtype=seg.dtype, device=seg.device)
+    if tuple(ex.recv.shape[2:]) != tuple(total.shape) or ex.recv.dtype != seg.dtype:
+        raise ValueError(f"exchange buffer {tuple(ex.recv.shape)} {ex.recv.dtype} does not fit state "
+                         f"{tuple(total.shape)} {seg.dtype}")
+    epoch = ex.next_epoch()
+    if epoch > 2:  # every reader has folded the half this put overwrites
+        call("lasp2_exchange_wait", ptr(ex.acks), 0, ex.nranks, epoch - 2, stream_ptr())
+    call("lasp2_scan_put", dtype_code(data_dtype), ptr(seg), ptr(total), b * h, nseg, d, int(reverse),
+         ptr(ex.recv_table), ptr(ex.flag_table), ex.rank, ex.nranks, epoch, ptr(ex.done), stream_ptr())
+    return total
+
+
+def exchange_fold(ex, mode: int, bound: int = 0) -> torch.Tensor:
+    """Wait for the ranks a fold needs (header: lasp2_exchange_wait), fold this
+    epoch's half of the rank-major receive buffer exactly like an all_gather
+    result, then acknowledge the epoch to every writer (lasp2_exchange_ack).
+    Every rank must call it once per exchange, also when it needs no state."""
+    lo, hi = {FOLD_PREFIX: (0, bound), FOLD_SUFFIX: (bound, ex.nranks), FOLD_FULL: (0, ex.nranks)}[mode]
+    call("lasp2_exchange_wait", ptr(ex.flags), lo, hi, ex.epoch, stream_ptr())
+    out = fold(ex.recv[ex.epoch & 1], mode, bound)
+    call("lasp2_exchange_ack", ptr(ex.ack_table), ex.rank, ex.nranks, ex.epoch, stream_ptr())
+    return out
+
+
 def fold(gathered: torch.Tensor, mode: int, bound: int = 0) -> torch.Tensor:
     """Ordered fold of rank-major gathered states [T, ...] (numerics.py:71-121)."""
     require_cuda(gathered)
