@@ -206,6 +206,10 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
   constexpr bool kOneO = kMode == 3 || kPT;  // TMEM [384,512) holds G or P, so O is single-buffered
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifndef LASP2_TRACE
+  unsigned long long t_begin = 0;  // per-CTA globaltimer span when the debug buffer is set (tools/cta_span_probe.py)
+  if (g_trace != nullptr && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
+#endif
   const uint32_t role_id = kMode == 1 ? cluster_ctarank() : kMode == 2 ? blockIdx.x % 3 : 0u;
   const int seg = kMode == 1 ? (int)(blockIdx.x >> 1) : kMode == 2 ? (int)(blockIdx.x / 3) : (int)blockIdx.x;
   const Role R = causal_role<kMode>(role_id, a);
@@ -521,6 +525,15 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
   tc_fence_before();
   if constexpr (kMode == 1) cluster_sync(); else __syncthreads();
   if (warp == 1) tmem_dealloc<512>(tmem);
+#ifndef LASP2_TRACE
+  if (g_trace != nullptr && threadIdx.x == 0) {
+    unsigned long long t_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    const uint32_t cta = blockIdx.y * gridDim.x + blockIdx.x;
+    g_trace[2 * cta] = t_begin;
+    g_trace[2 * cta + 1] = t_end;
+  }
+#endif
 }
 
 // ============================================================================
