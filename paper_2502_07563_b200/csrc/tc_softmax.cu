@@ -13,6 +13,8 @@
 // Only key blocks at or below the diagonal are visited (causal), the diagonal
 // block is masked by global position exactly as softmax_probs
 // (oracle.py:111-133). Output O / l in bf16, LSE (natural log) in fp32.
+#include <type_traits>
+
 #include "kernels.h"
 #include "tc_common.cuh"
 
@@ -447,12 +449,15 @@ __global__ void __launch_bounds__(kSmFwdThreads, 1)
         const float m_new = need ? mc : m_run;
         const float corr = (need && m_run != -INFINITY) ? ex2_approx(m_run - m_new) : (need ? 0.f : 1.f);
         float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // row sum as 4 independent pair chains
+        // full blocks (all but the diagonal one) get a mask-free copy of the loop
+        auto exp_block = [&](auto full_tag) {
+          constexpr bool kFull = decltype(full_tag)::value;
 #pragma unroll
         for (int c = 0; c < 128; c += 16) {
           uint32_t pk[8];
 #pragma unroll
           for (int i = 0; i < 16; i += 2) {
-            const bool ok0 = full_blk || c + i < lim, ok1 = full_blk || c + i + 1 < lim;
+            const bool ok0 = kFull || c + i < lim, ok1 = kFull || c + i + 1 < lim;
             float x0, x1;  // x = s * scale * log2(e) - m for two columns in one FFMA2
             ffma2_bc(x0, x1, __uint_as_float(sr[c + i]), __uint_as_float(sr[c + i + 1]), a.scale_log2, -m_new);
             // this share of the exponentials runs on the FMA pipe; evaluated unconditionally
@@ -468,6 +473,11 @@ __global__ void __launch_bounds__(kSmFwdThreads, 1)
           }
           tmem_st_32x32b_x8(ts + (c >> 1), pk);
         }
+        };
+        if (full_blk)
+          exp_block(std::true_type{});
+        else
+          exp_block(std::false_type{});
         const float psum = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
         if (j > 0 && __any_sync(0xffffffffu, need)) {  // raise this warp's rows' max: rescale O in TMEM
           mbar_wait(&o_full[t], (j - 1) & 1);  // PV_t(j-1) complete
