@@ -408,7 +408,7 @@ def summarize(r: dict, world: int, peaks: dict) -> dict:
         roofline={"kernel": r["dominant"], "bound": "tensor" if r.get("softmax") else "hbm", "achieved": achieved,
                   "peak": peaks["tensor"] if r.get("softmax") else peaks["hbm"],
                   "unit": "TFLOP/s" if r.get("softmax") else "GB/s",
-                  "frac": achieved / (peaks["tensor"] if r.get("softmax") else peaks["hbm"]), "traffic": ncu_traffic(r["workload"], r["dominant"]),
+                  "frac": achieved / (peaks["tensor"] if r.get("softmax") else peaks["hbm"]), "traffic": ncu_traffic(r["workload"], r["dominant"]) if world == 1 else None,
                   "peak_source": peaks["source"],
                   "algorithmic_bytes_per_launch": r["dom_algo_bytes"], "avg_launch_ms": r["dom_launch_ms"]},
         e2e={"value": r["n"] / (r["e2e_ms"] / 1e3), "unit": UNIT, "h2d_bytes_per_step": r["h2d"],
