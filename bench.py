@@ -92,8 +92,10 @@ class ClockSampler:
     summary(t0, t1) keeps only samples taken inside [t0, t1] (host clock).
     """
 
-    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
-               "sw_power_cap": 0x4}
+    # every NVML clocks-event reason bit (nvmlClocksEventReasons), so a clock below max is explained
+    REASONS = {"gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+               "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100}
 
     def __init__(self, index: int, period: float = 0.005) -> None:
         self.index = index
@@ -137,9 +139,9 @@ class ClockSampler:
         rows = [r for r in self.samples if (t0 is None or r[0] >= t0) and (t1 is None or r[0] <= t1)]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "samples": 0}
-        reasons = sorted({n for _, _, rs in rows for n, bit in self.REASONS.items() if rs & bit})
-        return {"sm_mhz": statistics.median(r[1] for r in rows), "sm_max_mhz": self.max_mhz, "reasons": reasons,
-                "samples": len(rows)}
+        reasons = sorted({n for _, _, rs in rows for n, bit in self.REASONS.items() if rs & bit} - {"gpu_idle"})
+        return {"sm_mhz": statistics.median(r[1] for r in rows), "sm_max_mhz": self.max_mhz,
+                "sm_min_mhz": min(r[1] for r in rows), "reasons": reasons, "samples": len(rows)}
 
 
 # ---------------------------------------------------------------------------
