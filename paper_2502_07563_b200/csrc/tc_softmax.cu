@@ -1,18 +1,19 @@
 // tcgen05 flash-style causal softmax attention for LASP-2H (bf16 in, fp32
 // accumulate), sm_100a only.
 //
-// Forward, one CTA per (128-query tile, slot): queries are the rank's chunk at
-// global rows row_offset + [q0, q0+128); keys/values are the full gathered
-// sequence, read straight from the rank-major all_gather layout through a 4-D
-// TMA map {d, row-in-chunk, slot, rank}. Per 128-key block j:
-//   S_j = Q K_j^T           (tcgen05, TMEM, double-buffered)
-//   P_j = exp2(S_j*scale*log2e - m_j), online max/sum per row (softmax warps,
-//         one row per thread), bf16 -> SW128 smem (double-buffered)
-//   O_j = P_j V_j           (tcgen05, fresh TMEM accumulator, double-buffered)
-//   O  <- O * exp2(m_{j-1} - m_j) + O_j   (registers)
-// Only key blocks at or below the diagonal are visited (causal), the diagonal
-// block is masked by global position exactly as softmax_probs
-// (oracle.py:111-133). Output O / l in bf16, LSE (natural log) in fp32.
+// Queries are the rank's chunk at global rows row_offset + [q0, ...); keys /
+// values are the full gathered sequence, read straight from the rank-major
+// all_gather layout through a 4-D TMA map {d, row-in-chunk, slot, rank}. Only
+// key blocks at or below the diagonal are visited (causal); the diagonal block
+// is masked by global position exactly as softmax_probs (oracle.py:111-133).
+//
+// tc_softmax_fwd2_kernel (default forward): two 128-query tiles per CTA, P back
+//   to TMEM and O += P V as a TS-mode MMA accumulating in TMEM (see its header).
+// tc_softmax_fwd_kernel (LASP2_SOFTMAX_FWD1=1, kept for comparison): one tile,
+//   P through shared memory, O rescaled in registers.
+// tc_softmax_bwd_kernel: one CTA per 128-key block, dV / dK in TMEM, dQ reduced
+//   into an fp32 accumulator with TMA bulk reduce-adds (see its header).
+// Output O / l in bf16, LSE (natural log) in fp32.
 #include <type_traits>
 
 #include "kernels.h"
@@ -538,9 +539,10 @@ __global__ void __launch_bounds__(kSmFwdThreads, 1)
 // position):
 //   S = Q_i K^T, dP = dO_i V^T                         (tcgen05 -> TMEM)
 //   P = exp2(S*scale*log2e - lse_i*log2e), dS = P o (dP - D_i)   (one query row per thread)
+//   dQ_i = dS K * scale    (TMEM, drained while dV / dK run, staged in fp32 over the
+//                           P / dS boxes and added into dq_acc by TMA bulk reduce-add)
 //   dV += P^T dO_i, dK += dS^T Q_i                      (TMEM accumulators; P / dS
 //                                                        images read MN-major)
-//   dQ_i += dS K * scale                               (TMEM -> red.global.add.v4.f32)
 // D_i = rowsum(dO_i o O_i) (oracle.py:155). dK*scale and dV are written in
 // fp32 to the rank-major contribution buffer for the reduce-scatter.
 // ============================================================================
