@@ -100,6 +100,23 @@ int lasp2_causal_chunk(int dtype, const void* q, const void* k, const void* v, c
                        const void* base, void* out, int64_t slots, int64_t tokens, int dim, int nseg, int reverse,
                        int transpose_state, void* stream);
 
+/* bf16 lasp2_causal_chunk / lasp2_dkdv_chunk that consume a fused peer
+ * exchange (lasp2_scan_put) in their prologue instead of a folded `base`: each
+ * CTA waits until the uint64 flags[lo..hi) carry `epoch`, folds those ranks'
+ * states from the receive half `xrecv` ([T][slots][dim][dim]: ascending with
+ * the first term copied, descending for dK/dV's suffix — numerics.py:71-116)
+ * and seeds its state with it. base_out (causal_chunk_x, may be NULL)
+ * receives the folded base ([slots][dim][dim], the cache's M_{1:t-1}). The
+ * caller acknowledges the epoch afterwards (lasp2_exchange_ack). This removes
+ * the wait and fold launches between the collective and its consumer. */
+int lasp2_causal_chunk_x(const void* q, const void* k, const void* v, const void* seg_states, const void* xrecv,
+                         const void* xflags, int lo, int hi, int descending, uint64_t epoch, void* base_out, void* out,
+                         int64_t slots, int64_t tokens, int dim, int nseg, int reverse, int transpose_state,
+                         void* stream);
+int lasp2_dkdv_chunk_x(const void* q, const void* k, const void* v, const void* d_out, const void* seg_states,
+                       const void* xrecv, const void* xflags, int lo, int hi, uint64_t epoch, void* dk, void* dv,
+                       int64_t slots, int64_t tokens, int dim, int nseg, void* stream);
+
 /* Masked backward dQ of one rank's chunk plus the dM segment states, one pass:
  *   dq_s = sum_{i<=s} (do_s.v_i) k_i + do_s S_s^T,  S_s = fwd_base + fwd_seg[seg(s)]
  *          + sum_{i<s, same segment} k_i^T v_i   (lasp2.py:198, :277-279)

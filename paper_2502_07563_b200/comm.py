@@ -589,6 +589,8 @@ class DistRankContext(_ContextBase):
     every process must construct its context (new_group is collective).
     """
 
+    one_gpu_per_rank = True  # consumers may wait for peers inside their kernels
+
     def __init__(self, sp_size: int | None = None, peer_exchange: bool = False) -> None:
         import torch.distributed as dist
 

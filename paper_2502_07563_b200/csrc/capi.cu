@@ -159,6 +159,38 @@ int lasp2_causal_chunk(int dtype, const void* q, const void* k, const void* v, c
   return cuda_status(e, "causal_chunk");
 }
 
+int lasp2_causal_chunk_x(const void* q, const void* k, const void* v, const void* seg_states, const void* xrecv,
+                         const void* xflags, int lo, int hi, int descending, uint64_t epoch, void* base_out, void* out,
+                         int64_t slots, int64_t tokens, int dim, int nseg, int reverse, int transpose_state,
+                         void* stream) {
+  CHECK(q && k && v && out && xrecv && xflags, "causal_chunk_x: null pointer");
+  CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128, "causal_chunk_x: bad shape (1 <= dim <= 128)");
+  CHECK(nseg >= 1 && nseg <= (tokens + LASP_BLOCK_TOKENS - 1) / LASP_BLOCK_TOKENS, "causal_chunk_x: bad nseg");
+  CHECK(nseg == 1 || seg_states, "causal_chunk_x: nseg > 1 needs segment states");
+  CHECK(lo >= 0 && hi >= lo, "causal_chunk_x: bad rank range");
+  CHECK(use_tc(LASP2_BF16, dim, tokens), "causal_chunk_x: bf16 tensor-core path only (fold, then lasp2_causal_chunk)");
+  const lasp::XFold x{(const float*)xrecv, (const unsigned long long*)xflags, lo, hi, descending, epoch,
+                      (float*)base_out};
+  return cuda_status(lasp::tc_causal_chunk(q, k, v, (const float*)seg_states, nullptr, out, slots, tokens, dim, nseg,
+                                           reverse, transpose_state, S(stream), &x),
+                     "causal_chunk_x");
+}
+
+int lasp2_dkdv_chunk_x(const void* q, const void* k, const void* v, const void* d_out, const void* seg_states,
+                       const void* xrecv, const void* xflags, int lo, int hi, uint64_t epoch, void* dk, void* dv,
+                       int64_t slots, int64_t tokens, int dim, int nseg, void* stream) {
+  CHECK(q && k && v && d_out && dk && dv && xrecv && xflags, "dkdv_chunk_x: null pointer");
+  CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128, "dkdv_chunk_x: bad shape (1 <= dim <= 128)");
+  CHECK(nseg >= 1 && nseg <= (tokens + LASP_BLOCK_TOKENS - 1) / LASP_BLOCK_TOKENS, "dkdv_chunk_x: bad nseg");
+  CHECK(nseg == 1 || seg_states, "dkdv_chunk_x: nseg > 1 needs segment states");
+  CHECK(lo >= 0 && hi >= lo, "dkdv_chunk_x: bad rank range");
+  CHECK(use_tc(LASP2_BF16, dim, tokens), "dkdv_chunk_x: bf16 tensor-core path only (fold, then lasp2_dkdv_chunk)");
+  const lasp::XFold x{(const float*)xrecv, (const unsigned long long*)xflags, lo, hi, 1, epoch, nullptr};
+  return cuda_status(lasp::tc_dkdv_pair(q, k, v, d_out, (const float*)seg_states, nullptr, dk, dv, slots, tokens, dim,
+                                        nseg, S(stream), &x),
+                     "dkdv_chunk_x");
+}
+
 int lasp2_dq_chunk(int dtype, const void* q, const void* k, const void* v, const void* d_out, const void* fwd_seg,
                    const void* fwd_base, void* g_seg, void* dq, int64_t slots, int64_t tokens, int dim, int nseg,
                    void* stream) {

@@ -46,15 +46,26 @@ cudaError_t gen_slots(uint64_t seed, const uint64_t* tag_words, void* out, int64
 bool tc_supported(int dim, int64_t tokens);
 cudaError_t tc_segment_states(const void* x, const void* y, float* out, int64_t slots, int64_t tokens, int dim,
                               int nseg, cudaStream_t s);
+// In-kernel consumer of the fused peer state exchange (lasp2_scan_put): the
+// rank-level base is folded from this epoch's receive half once the flags of
+// ranks [lo, hi) carry `epoch` (see CausalArgs in tc_linear.cu).
+struct XFold {
+  const float* recv;                // [T][slots][dim][dim]
+  const unsigned long long* flags;  // [T]
+  int lo, hi, descending;
+  unsigned long long epoch;
+  float* base_out;                  // folded base per slot, or null
+};
 cudaError_t tc_causal_chunk(const void* q, const void* k, const void* v, const float* seg_states, const float* base,
                             void* out, int64_t slots, int64_t tokens, int dim, int nseg, int reverse,
-                            int transpose_state, cudaStream_t s);
+                            int transpose_state, cudaStream_t s,
+                            const XFold* xfold = nullptr);
 cudaError_t tc_dq_chunk(const void* q, const void* k, const void* v, const void* d_out, const float* fwd_seg,
                         const float* fwd_base, float* g_out, void* dq, int64_t slots, int64_t tokens, int dim,
                         int nseg, cudaStream_t s);
 cudaError_t tc_dkdv_pair(const void* q, const void* k, const void* v, const void* d_out, const float* seg_states,
                          const float* base, void* dk, void* dv, int64_t slots, int64_t tokens, int dim, int nseg,
-                         cudaStream_t s);
+                         cudaStream_t s, const XFold* xfold = nullptr);
 cudaError_t tc_apply_state(const void* x, const float* m, void* out, int64_t slots, int64_t tokens, int dim,
                            int transpose, int accumulate, int sm_count, cudaStream_t s);
 bool tc_softmax_supported(int dim, int64_t kv_chunk);

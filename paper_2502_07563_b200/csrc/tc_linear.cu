@@ -137,7 +137,21 @@ struct CausalArgs {
   int nseg;
   int reverse;
   int transpose_state;
+  // fused peer-exchange consumer (kModes 0 / 1): the rank-level base is folded in the
+  // prologue from this epoch's receive half [T][slots][dim][dim] once flags[xlo, xhi)
+  // carry xepoch (ascending for a prefix, descending when xdesc); replaces `base`
+  const float* xrecv = nullptr;
+  const unsigned long long* xflags = nullptr;
+  int xlo = 0, xhi = 0, xdesc = 0;
+  unsigned long long xepoch = 0;
+  float* base_out = nullptr;  // the folded base of each slot (written by its segment-0 CTA), or null
 };
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 
 struct TileMaps {
   CUtensorMap m[7];
@@ -400,6 +414,23 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
         st = a.seg_states ? a.seg_states + ((int64_t)slot * a.nseg + seg) * dd : nullptr;
         bs = a.base ? a.base + (int64_t)slot * dd : nullptr;
       }
+      const bool fold = a.xrecv != nullptr && a.xhi > a.xlo;
+      if (a.xrecv != nullptr) {  // wait for the ranks this fold needs (the TMA / MMA warps run ahead)
+        if (et == 0) {
+          for (int j = a.xlo; j < a.xhi; ++j) {
+            const long long t0 = clock64();
+            while (ld_acquire_sys_u64(a.xflags + j) < a.xepoch) {
+              __nanosleep(64);
+              if (clock64() - t0 > (1ll << 36)) __trap();  // a peer never arrived: fail loudly
+            }
+          }
+        }
+        named_bar_sync(1, kEpi);
+      }
+      const int64_t xstride = (int64_t)gridDim.y * dd;  // one rank's [slots][dim][dim] in the receive half
+      const float* xb = a.xrecv + (int64_t)slot * dd;
+      float* bo = (a.base_out != nullptr && seg == 0 && (kMode != 1 || R.mcast == 1)) ? a.base_out + (int64_t)slot * dd
+                                                                                        : nullptr;
 #pragma unroll 1
       for (int c0 = cb; c0 < cb + 64; c0 += 32) {
         float v[32];
@@ -409,7 +440,21 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
           float x = 0.f;
           if ((int)row < dim && c < dim) {
             const int64_t src = R.transpose ? (int64_t)c * dim + row : (int64_t)row * dim + c;
-            if (bs) x += bs[src];
+            if (fold) {  // first term copied, the rest in rank order (numerics.py:71-116)
+              float b = 0.f;
+              if (a.xdesc) {
+                b = __ldcg(xb + (a.xhi - 1) * xstride + src);
+                for (int j = a.xhi - 2; j >= a.xlo; --j) b += __ldcg(xb + j * xstride + src);
+              } else {
+                b = __ldcg(xb + a.xlo * xstride + src);
+                for (int j = a.xlo + 1; j < a.xhi; ++j) b += __ldcg(xb + j * xstride + src);
+              }
+              if (bo != nullptr) bo[src] = b;
+              x += b;
+            } else {
+              if (bs) x += bs[src];
+              if (bo != nullptr) bo[src] = 0.f;
+            }
             if (st) x += st[src];
           }
           v[i] = x;
@@ -971,9 +1016,23 @@ cudaError_t tc_segment_states(const void* x, const void* y, float* out, int64_t 
   return launch_pdl(tc::tc_segment_states_kernel, grid, dim3(192), tc::kSegSmem, s, 1, mx, my, out, tokens, dim, nseg);
 }
 
+namespace {
+void set_xfold(tc::CausalArgs* a, const XFold* x) {
+  if (x == nullptr) return;
+  a->base = nullptr;
+  a->xrecv = x->recv;
+  a->xflags = x->flags;
+  a->xlo = x->lo;
+  a->xhi = x->hi;
+  a->xdesc = x->descending;
+  a->xepoch = x->epoch;
+  a->base_out = x->base_out;
+}
+}  // namespace
+
 cudaError_t tc_causal_chunk(const void* q, const void* k, const void* v, const float* seg_states, const float* base,
                             void* out, int64_t slots, int64_t tokens, int dim, int nseg, int reverse,
-                            int transpose_state, cudaStream_t s) {
+                            int transpose_state, cudaStream_t s, const XFold* xfold) {
   tc::TileMaps tm;
   cudaError_t e;
   const void* ptrs[4] = {q, k, v, out};
@@ -981,6 +1040,7 @@ cudaError_t tc_causal_chunk(const void* q, const void* k, const void* v, const f
     if ((e = make_tmap_3d(&tm.m[i], ptrs[i], slots, tokens, dim)) != cudaSuccess) return e;
   if ((e = set_smem_once((const void*)tc::tc_causal_chunk_kernel<0>, tc::kCausalSmem)) != cudaSuccess) return e;
   tc::CausalArgs a{seg_states, base, nullptr, nullptr, nullptr, nullptr, tokens, dim, nseg, reverse, transpose_state};
+  set_xfold(&a, xfold);
   dim3 grid(nseg, (unsigned)slots);
   return launch_pdl(tc::tc_causal_chunk_kernel<0>, grid, dim3(tc::kCausalThreads), tc::kCausalSmem, s, 1, tm, a);
 }
@@ -1003,7 +1063,7 @@ cudaError_t tc_dq_chunk(const void* q, const void* k, const void* v, const void*
 // Masked backward dK and dV in one pass over (Q, K, V, dO): 2-CTA clusters.
 cudaError_t tc_dkdv_pair(const void* q, const void* k, const void* v, const void* d_out, const float* seg_states,
                          const float* base, void* dk, void* dv, int64_t slots, int64_t tokens, int dim, int nseg,
-                         cudaStream_t s) {
+                         cudaStream_t s, const XFold* xfold) {
   tc::TileMaps tm;
   cudaError_t e;
   const void* ptrs[6] = {v, k, d_out, q, dk, dv};
@@ -1011,6 +1071,7 @@ cudaError_t tc_dkdv_pair(const void* q, const void* k, const void* v, const void
     if ((e = make_tmap_3d(&tm.m[i], ptrs[i], slots, tokens, dim)) != cudaSuccess) return e;
   if ((e = set_smem_once((const void*)tc::tc_causal_chunk_kernel<1>, tc::kCausalSmem)) != cudaSuccess) return e;
   tc::CausalArgs a{seg_states, base, nullptr, nullptr, nullptr, nullptr, tokens, dim, nseg, 1, 0};
+  set_xfold(&a, xfold);
   return launch_pdl(tc::tc_causal_chunk_kernel<1>, dim3(2 * nseg, (unsigned)slots), dim3(tc::kCausalThreads),
                     tc::kCausalSmem, s, 2, tm, a);
 }

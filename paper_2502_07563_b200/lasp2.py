@@ -188,6 +188,20 @@ def _peer(ctx, tag: str, like: torch.Tensor):
     return fn(tag, like) if fn is not None else None
 
 
+# with the peer exchange, the bf16 chunk / dK-dV kernels wait for the ranks they need and
+# fold the base in their own prologue (lasp2_causal_chunk_x / lasp2_dkdv_chunk_x): no wait or
+# fold launch between the collective and its consumer. False: wait + fold kernels first.
+PEER_FUSED_CONSUMER = True
+
+
+def _fused_consumer(ctx, x: torch.Tensor) -> bool:
+    # Only with one GPU per rank: in the threads-as-ranks world several ranks' kernels share
+    # one GPU, and consumers spinning in-kernel could occupy every SM a producer still needs.
+    d = x.shape[-1]
+    return (PEER_FUSED_CONSUMER and getattr(ctx, "one_gpu_per_rank", False) and x.dtype == torch.bfloat16
+            and 8 <= d <= 128 and d % 8 == 0)
+
+
 def _share_total(ctx, seg: torch.Tensor, reverse: bool, data_dtype: torch.dtype, tag: str):
     """Scan the segment states; returns (chunk total, exchange handle or None)."""
     ex = _peer(ctx, tag, seg[:, :, 0])
@@ -236,7 +250,12 @@ def _forward_masked_rank(ctx, qc: torch.Tensor, kc: torch.Tensor, vc: torch.Tens
     seg = ops.segment_states(kc, vc, nseg)
     m_t, ex = _share_total(ctx, seg, False, kc.dtype, "state")
     if ex is not None:  # fused peer exchange: M_t is already on its way to every rank
-        if overlap:
+        if _fused_consumer(ctx, qc) and not overlap:  # the chunk kernel waits and folds M_{1:t-1} itself
+            m_prefix = torch.empty_like(m_t)
+            ctx.mark("intra_start", f"chunk={t}")
+            out = ops.causal_chunk_x(qc, kc, vc, seg, ex, t, nseg, base_out=m_prefix)
+            ctx.mark("intra_end", f"chunk={t}")
+        elif overlap:
             ctx.mark("intra_start", f"chunk={t}")
             out = ops.causal_chunk(qc, kc, vc, seg, None, nseg)
             ctx.mark("intra_end", f"chunk={t}")
@@ -346,6 +365,9 @@ def _backward_masked_rank(ctx, cache: ActivationCache, d_out: torch.Tensor) -> G
         # pass over (dO, V, K, Q) the dM segment states Q_g^T dO_g (lasp2.py:273-279)
         dq, gseg = ops.dq_chunk(q, k, v, do, cache.seg_prefix, cache.m_prefix if t > 0 else None, nseg)
         g_t, ex = _share_total(ctx, gseg, True, q.dtype, "state_grad")
+        if ex is not None and _fused_consumer(ctx, q):  # dK/dV kernel waits for ranks > t, folds their dM itself
+            dk, dv = ops.dkdv_chunk_x(q, k, v, do, gseg, ex, t + 1, nseg)
+            return GradientBundle(dq=dq, dk=dk, dv=dv)
         if ex is not None:  # every rank folds (and acknowledges) the exchange, the last one gets zeros
             r = ops.exchange_fold(ex, ops.FOLD_SUFFIX, t + 1)
             r = r if t < world - 1 else None

@@ -88,8 +88,38 @@ def exchange_fold(ex, mode: int, bound: int = 0) -> torch.Tensor:
     lo, hi = {FOLD_PREFIX: (0, bound), FOLD_SUFFIX: (bound, ex.nranks), FOLD_FULL: (0, ex.nranks)}[mode]
     call("lasp2_exchange_wait", ptr(ex.flags), lo, hi, ex.epoch, stream_ptr())
     out = fold(ex.recv[ex.epoch & 1], mode, bound)
-    call("lasp2_exchange_ack", ptr(ex.ack_table), ex.rank, ex.nranks, ex.epoch, stream_ptr())
+    exchange_ack(ex)
     return out
+
+
+def exchange_ack(ex) -> None:
+    """This rank is done with the current epoch's half (header: lasp2_exchange_ack)."""
+    call("lasp2_exchange_ack", ptr(ex.ack_table), ex.rank, ex.nranks, ex.epoch, stream_ptr())
+
+
+def causal_chunk_x(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, seg_states: torch.Tensor, ex, upto: int,
+                   nseg: int, base_out: torch.Tensor | None = None) -> torch.Tensor:
+    """causal_chunk whose base M_{1:upto} is folded in-kernel from the peer exchange
+    (header: lasp2_causal_chunk_x); acknowledges the epoch. bf16 only."""
+    require_cuda(q, k, v, seg_states, base_out)
+    slots, n, d = _slots(q)
+    out = torch.empty_like(q)
+    call("lasp2_causal_chunk_x", ptr(q), ptr(k), ptr(v), ptr(seg_states), ptr(ex.recv[ex.epoch & 1]), ptr(ex.flags),
+         0, upto, 0, ex.epoch, ptr(base_out), ptr(out), slots, n, d, nseg, 0, 0, stream_ptr())
+    exchange_ack(ex)
+    return out
+
+
+def dkdv_chunk_x(q, k, v, d_out, seg_states, ex, start: int, nseg: int) -> tuple[torch.Tensor, torch.Tensor]:
+    """dkdv_chunk whose base (suffix of ranks >= start, descending) is folded in-kernel
+    from the peer exchange (header: lasp2_dkdv_chunk_x); acknowledges the epoch."""
+    require_cuda(q, k, v, d_out, seg_states)
+    slots, n, d = _slots(q)
+    dk, dv = torch.empty_like(k), torch.empty_like(v)
+    call("lasp2_dkdv_chunk_x", ptr(q), ptr(k), ptr(v), ptr(d_out), ptr(seg_states), ptr(ex.recv[ex.epoch & 1]),
+         ptr(ex.flags), start, ex.nranks, ex.epoch, ptr(dk), ptr(dv), slots, n, d, nseg, stream_ptr())
+    exchange_ack(ex)
+    return dk, dv
 
 
 def fold(gathered: torch.Tensor, mode: int, bound: int = 0) -> torch.Tensor:

@@ -154,3 +154,44 @@ def test_forward_only_loop_with_a_rank_running_ahead(peer_mode):
     for r in range(t):
         for a, bb in zip(run.results[r], want.results[r]):
             assert torch.equal(a, bb)
+
+
+def test_fused_consumers_equal_wait_fold_then_kernel():
+    """lasp2_causal_chunk_x / lasp2_dkdv_chunk_x (in-kernel flag wait + fold of the
+    exchanged states) against exchange_fold + the plain kernels, bit for bit. All
+    puts are issued first on one stream, so no consumer can spin on a producer
+    that has no SM left (the drivers use the fused consumers only with one GPU per rank)."""
+    t_world, n, d, h = 3, 2048, 128, 2
+    dev = torch.device("cuda")
+    g = torch.Generator(device="cuda").manual_seed(11)
+    mk = lambda: ((torch.rand((1, h, n, d), generator=g, device=dev) * 2 - 1)).to(torch.bfloat16)  # noqa: E731
+    data = [tuple(mk() for _ in range(4)) for _ in range(t_world)]  # q, k, v, do per rank
+    nseg = ops.num_segments(data[0][0])
+
+    def exchange(tag_dtype=torch.float32):
+        recv = [torch.zeros((2, t_world, 1, h, d, d), dtype=tag_dtype, device=dev) for _ in range(t_world)]
+        flags = [torch.zeros(t_world, dtype=torch.int64, device=dev) for _ in range(t_world)]
+        acks = [torch.zeros(t_world, dtype=torch.int64, device=dev) for _ in range(t_world)]
+        done = [torch.zeros(1, dtype=torch.int32, device=dev) for _ in range(t_world)]
+        tables = [comm._ptr_table(x, dev) for x in (recv, flags, acks)]
+        return [comm.PeerExchange(r, t_world, recv[r], flags[r], acks[r], done[r], *tables) for r in range(t_world)]
+
+    ex_f, ex_b = exchange(), exchange()
+    segs = [ops.segment_states(k, v, nseg) for (_, k, v, _) in data]
+    totals = [ops.scan_put(s, False, torch.bfloat16, e) for s, e in zip(segs, ex_f)]
+    gsegs = [ops.segment_states(q, do, nseg) for (q, _, _, do) in data]
+    gtot = [ops.scan_put(s, True, torch.bfloat16, e) for s, e in zip(gsegs, ex_b)]
+    gathered, ggathered = torch.stack(totals), torch.stack(gtot)
+    for r, (q, k, v, do) in enumerate(data):
+        base_out = torch.empty((1, h, d, d), dtype=torch.float32, device=dev)
+        got = ops.causal_chunk_x(q, k, v, segs[r], ex_f[r], r, nseg, base_out=base_out)
+        m_prefix = ops.fold(gathered, FOLD_PREFIX, r)
+        want = ops.causal_chunk(q, k, v, segs[r], m_prefix if r > 0 else None, nseg)
+        assert torch.equal(got, want) and torch.equal(base_out, m_prefix), r
+        dk, dv = ops.dkdv_chunk_x(q, k, v, do, gsegs[r], ex_b[r], r + 1, nseg)
+        rr = ops.fold(ggathered, FOLD_SUFFIX, r + 1)
+        wk, wv = ops.dkdv_chunk(q, k, v, do, gsegs[r], rr if r < t_world - 1 else None, nseg)
+        assert torch.equal(dk, wk) and torch.equal(dv, wv), r
+    torch.cuda.synchronize()
+    for e in ex_f + ex_b:
+        assert e.acks.tolist() == [1] * t_world  # every consumer acknowledged the epoch
