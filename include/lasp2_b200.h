@@ -194,8 +194,9 @@ int lasp2_nomask_backward_local(int dtype, const void* q, const void* k, const v
  * plain [slots][kv_tokens][dim] layout). The dk/dv contributions use the
  * same indexing with grad_rank_stride, so a [T][2][slots][chunk][dim] buffer
  * feeds one reduce-scatter.
- * out = softmax(q k^T / sqrt(d), causal by global position) v; lse (f32,
- * [slots][q_tokens]) receives the row log-sum-exp. Replaces
+ * out = softmax(q k^T / sqrt(d), causal by global position) v; lse (states
+ * dtype: f64 for f64 data, else f32; [slots][q_tokens]) receives the row
+ * log-sum-exp (natural log). Replaces
  * softmax_chunk_forward (oracle.py:136-139) as called by _cp_forward_rank
  * (standard_sp.py:44-49). */
 int lasp2h_softmax_forward(int dtype, const void* q, const void* k_full, const void* v_full, void* out, void* lse,
@@ -212,6 +213,19 @@ int lasp2h_softmax_backward(int dtype, const void* q, const void* k_full, const 
                             int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim, int causal,
                             int64_t row_offset, int64_t kv_chunk, int64_t kv_rank_stride, int64_t grad_rank_stride,
                             void* stream);
+
+/* The same over a key SUB-RANGE of a larger softmax (the balanced LASP-2H
+ * schedule splits one query chunk's keys between two ranks): P uses the
+ * forward's lse of the whole key set and delta = rowsum(dO o O) with the
+ * final O, so partial dQ and dK/dV contributions of disjoint ranges add up
+ * to the full gradients. Identical to lasp2h_softmax_backward on the bf16
+ * tensor-core path; the f32/f64 path would otherwise renormalise over its
+ * range. lse must be given (states dtype). */
+int lasp2h_softmax_backward_range(int dtype, const void* q, const void* k_full, const void* v_full, const void* out,
+                                  const void* lse, const void* d_out, void* dq, void* dk_full, void* dv_full,
+                                  void* scratch, int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim,
+                                  int causal, int64_t row_offset, int64_t kv_chunk, int64_t kv_rank_stride,
+                                  int64_t grad_rank_stride, void* stream);
 int64_t lasp2h_softmax_scratch_bytes(int dtype, int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim);
 
 /* Deterministic inputs: out[slot] = rows [row_offset, row_offset+rows) of

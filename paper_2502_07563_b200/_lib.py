@@ -54,6 +54,8 @@ SIGNATURES = {
                                       _vp]),
     "lasp2h_softmax_backward": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int,
                                        _int, _i64, _i64, _i64, _i64, _vp]),
+    "lasp2h_softmax_backward_range": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64,
+                                             _i64, _int, _int, _i64, _i64, _i64, _i64, _vp]),
     "lasp2h_softmax_scratch_bytes": (_i64, [_int, _i64, _i64, _i64, _int]),
     "lasp2_gen_slots": (_int, [_int, _u64, _vp, _vp, _i64, _i64, _i64, _i64, _vp]),
     "lasp2_debug_probe_gemm": (_int, [_vp, _vp, _vp, _int, _int, _vp]),
@@ -116,7 +118,8 @@ class _Profiler:
 
 PROFILER = _Profiler()
 # kernels launched per call of each entry point (for gpu_launches accounting)
-KERNELS_PER_CALL = {"lasp2h_softmax_backward": 4}  # bf16 tc path: delta, memset, main, finalize
+KERNELS_PER_CALL = {"lasp2h_softmax_backward": 4,  # bf16 tc path: delta, memset, main, finalize
+                    "lasp2h_softmax_backward_range": 4}
 _NO_LAUNCH = {"lasp2_version", "lasp2_last_error", "lasp2_num_segments", "lasp2h_softmax_scratch_bytes",
               "lasp2_local_workspace_bytes",
               "lasp2_debug_trace"}

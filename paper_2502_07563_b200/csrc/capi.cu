@@ -363,13 +363,13 @@ int lasp2h_softmax_forward(int dtype, const void* q, const void* k_full, const v
     e = lasp::tc_softmax_forward(q, k_full, v_full, out, (float*)lse, slots, q_tokens, kv_tokens, dim, causal,
                                  row_offset, kv_chunk, kv_rank_stride, S(stream));
   else if (dtype == LASP2_F32)
-    e = lasp::simt_softmax_forward<float, float>(q, k_full, v_full, out, (float*)lse, slots, q_tokens, kv_tokens, dim,
+    e = lasp::simt_softmax_forward<float, float>(q, k_full, v_full, out, lse, slots, q_tokens, kv_tokens, dim,
                                                  causal, row_offset, kv_chunk, kv_rank_stride, S(stream));
   else if (dtype == LASP2_F64)
-    e = lasp::simt_softmax_forward<double, double>(q, k_full, v_full, out, (float*)lse, slots, q_tokens, kv_tokens,
+    e = lasp::simt_softmax_forward<double, double>(q, k_full, v_full, out, lse, slots, q_tokens, kv_tokens,
                                                    dim, causal, row_offset, kv_chunk, kv_rank_stride, S(stream));
   else
-    e = lasp::simt_softmax_forward<__nv_bfloat16, float>(q, k_full, v_full, out, (float*)lse, slots, q_tokens,
+    e = lasp::simt_softmax_forward<__nv_bfloat16, float>(q, k_full, v_full, out, lse, slots, q_tokens,
                                                          kv_tokens, dim, causal, row_offset, kv_chunk, kv_rank_stride,
                                                          S(stream));
   return cuda_status(e, "softmax_forward");
@@ -386,11 +386,13 @@ int64_t lasp2h_softmax_scratch_bytes(int dtype, int64_t slots, int64_t q_tokens,
   return n;
 }
 
-int lasp2h_softmax_backward(int dtype, const void* q, const void* k_full, const void* v_full, const void* out,
+static int softmax_backward_impl(bool range, int dtype, const void* q, const void* k_full, const void* v_full, const void* out,
                             const void* lse, const void* d_out, void* dq, void* dk_full, void* dv_full, void* scratch,
                             int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim, int causal,
                             int64_t row_offset, int64_t kv_chunk, int64_t kv_rank_stride, int64_t grad_rank_stride,
                             void* stream) {
+  CHECK(!range || lse, "softmax_backward_range: needs the forward's lse of the whole key set");
+  const void* lse_range = range ? lse : nullptr;
   CHECK(valid_dtype(dtype), "softmax_backward: unknown dtype");
   CHECK(q && k_full && v_full && out && d_out && dq && dk_full && dv_full && scratch,
         "softmax_backward: null pointer");
@@ -406,19 +408,39 @@ int lasp2h_softmax_backward(int dtype, const void* q, const void* k_full, const 
   } else if (dtype == LASP2_F32)
     e = lasp::simt_softmax_backward<float, float, float>(q, k_full, v_full, out, d_out, dq, dk_full, dv_full, scratch,
                                                          slots, q_tokens, kv_tokens, dim, causal, row_offset,
-                                                         kv_chunk, kv_rank_stride, grad_rank_stride, S(stream));
+                                                         kv_chunk, kv_rank_stride, grad_rank_stride, S(stream), lse_range);
   else if (dtype == LASP2_F64)
     e = lasp::simt_softmax_backward<double, double, double>(q, k_full, v_full, out, d_out, dq, dk_full, dv_full,
                                                             scratch, slots, q_tokens, kv_tokens, dim, causal,
                                                             row_offset, kv_chunk, kv_rank_stride, grad_rank_stride,
-                                                            S(stream));
+                                                            S(stream), lse_range);
   else
     e = lasp::simt_softmax_backward<__nv_bfloat16, float, float>(q, k_full, v_full, out, d_out, dq, dk_full, dv_full,
                                                                  scratch, slots, q_tokens, kv_tokens, dim, causal,
                                                                  row_offset, kv_chunk, kv_rank_stride, grad_rank_stride,
-                                                                 S(stream));
+                                                                 S(stream), lse_range);
   return cuda_status(e, "softmax_backward");
 }
+int lasp2h_softmax_backward(int dtype, const void* q, const void* k_full, const void* v_full, const void* out,
+                            const void* lse, const void* d_out, void* dq, void* dk_full, void* dv_full, void* scratch,
+                            int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim, int causal,
+                            int64_t row_offset, int64_t kv_chunk, int64_t kv_rank_stride, int64_t grad_rank_stride,
+                            void* stream) {
+  return softmax_backward_impl(false, dtype, q, k_full, v_full, out, lse, d_out, dq, dk_full, dv_full, scratch, slots,
+                               q_tokens, kv_tokens, dim, causal, row_offset, kv_chunk, kv_rank_stride,
+                               grad_rank_stride, stream);
+}
+
+int lasp2h_softmax_backward_range(int dtype, const void* q, const void* k_full, const void* v_full, const void* out,
+                                  const void* lse, const void* d_out, void* dq, void* dk_full, void* dv_full,
+                                  void* scratch, int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim,
+                                  int causal, int64_t row_offset, int64_t kv_chunk, int64_t kv_rank_stride,
+                                  int64_t grad_rank_stride, void* stream) {
+  return softmax_backward_impl(true, dtype, q, k_full, v_full, out, lse, d_out, dq, dk_full, dv_full, scratch, slots,
+                               q_tokens, kv_tokens, dim, causal, row_offset, kv_chunk, kv_rank_stride,
+                               grad_rank_stride, stream);
+}
+
 
 int lasp2_gen_slots(int dtype, uint64_t seed, const uint64_t* tag_words_device, void* out, int64_t slots, int64_t rows,
                     int64_t cols, int64_t row_offset, void* stream) {

@@ -17,14 +17,15 @@ template <typename T, typename A>
 cudaError_t simt_apply_state(const void* x, const void* m, void* out, int64_t slots, int64_t tokens, int dim,
                              int transpose, int accumulate, cudaStream_t s);
 template <typename T, typename A>
-cudaError_t simt_softmax_forward(const void* q, const void* kf, const void* vf, void* out, float* lse, int64_t slots,
+cudaError_t simt_softmax_forward(const void* q, const void* kf, const void* vf, void* out, void* lse, int64_t slots,
                                  int64_t qtok, int64_t kvtok, int dim, int causal, int64_t row_offset, int64_t kv_chunk,
                                  int64_t kv_rank_stride, cudaStream_t s);
 template <typename T, typename A, typename G>
 cudaError_t simt_softmax_backward(const void* q, const void* kf, const void* vf, const void* o, const void* d_out,
                                   void* dq, void* dk_full, void* dv_full, void* scratch, int64_t slots, int64_t qtok,
                                   int64_t kvtok, int dim, int causal, int64_t row_offset, int64_t kv_chunk,
-                                  int64_t kv_rank_stride, int64_t grad_rank_stride, cudaStream_t s);
+                                  int64_t kv_rank_stride, int64_t grad_rank_stride, cudaStream_t s,
+                                  const void* lse = nullptr);
 
 // shared state reductions / datagen
 template <typename A>

@@ -256,7 +256,7 @@ template <typename T, typename A>
 __global__ void __launch_bounds__(kSmThreads) simt_softmax_fwd_kernel(const T* __restrict__ q,
                                                                       const T* __restrict__ kf,
                                                                       const T* __restrict__ vf, T* __restrict__ out,
-                                                                      float* __restrict__ lse, int64_t qtok,
+                                                                      A* __restrict__ lse, int64_t qtok,
                                                                       int64_t kvtok, int dim, int causal,
                                                                       int64_t row_offset, KvLayout kl) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(kSmThreads) simt_softmax_fwd_kernel(const T* _
     __syncthreads();
   }
   if (threadIdx.x < dim) store_as<T, A>(out + (slot * qtok + row) * dim + threadIdx.x, acc / run_sum);
-  if (threadIdx.x == 0) lse[slot * qtok + row] = (float)(run_max + dev_log<A>(run_sum));
+  if (threadIdx.x == 0) lse[slot * qtok + row] = run_max + dev_log<A>(run_sum);  // f64 data: f64 lse
 }
 
 // delta[row] = sum_c dO[row][c] * O[row][c]  (== rowsum(dP o P), oracle.py:155)
@@ -374,12 +374,23 @@ __global__ void __launch_bounds__(kSmThreads) simt_softmax_delta_exact_kernel(
   if (threadIdx.x == 0) delta[r] = acc;
 }
 
+// Row statistics from the forward's log-sum-exp (max = lse, sum = 1): P over a key
+// sub-range normalised by the whole key set, as the balanced LASP-2H schedule needs.
+template <typename A>
+__global__ void stats_from_lse_kernel(const A* __restrict__ lse, A* __restrict__ mx, A* __restrict__ sm, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    mx[i] = lse[i];
+    sm[i] = A(1);
+  }
+}
+
 // dq[row] = scale * sum_j dS[row][j] k_j, dS = P (dP - delta)   (oracle.py:150-157)
 template <typename T, typename A>
 __global__ void __launch_bounds__(kSmThreads) simt_softmax_bwd_dq_kernel(
     const T* __restrict__ q, const T* __restrict__ kf, const T* __restrict__ vf, const T* __restrict__ d_out,
     const A* __restrict__ delta, T* __restrict__ dq, int64_t qtok, int64_t kvtok, int dim, int causal,
-    int64_t row_offset, KvLayout kl) {
+    int64_t row_offset, KvLayout kl, const A* __restrict__ mx_in, const A* __restrict__ sm_in) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   A* qrow = reinterpret_cast<A*>(smem_raw);
   A* dorow = qrow + dim;
@@ -394,7 +405,12 @@ __global__ void __launch_bounds__(kSmThreads) simt_softmax_bwd_dq_kernel(
   const A scale = dev_rsqrt<A>(dim);
   const int64_t limit = causal ? lmin(kvtok, row_offset + row + 1) : kvtok;
   A mx, sm;
-  row_stats<T, A>(qrow, kf, slot, kl, limit, dim, scale, red, &mx, &sm);
+  if (mx_in != nullptr) {  // statistics of the full key set (a key sub-range of a larger softmax)
+    mx = mx_in[slot * qtok + row];
+    sm = sm_in[slot * qtok + row];
+  } else {
+    row_stats<T, A>(qrow, kf, slot, kl, limit, dim, scale, red, &mx, &sm);
+  }
   const A dl = delta[slot * qtok + row];
   A acc = A(0);
   for (int64_t j0 = 0; j0 < limit; j0 += kSmKeys) {
@@ -536,14 +552,14 @@ cudaError_t simt_apply_state(const void* x, const void* m, void* out, int64_t sl
 }
 
 template <typename T, typename A>
-cudaError_t simt_softmax_forward(const void* q, const void* kf, const void* vf, void* out, float* lse, int64_t slots,
+cudaError_t simt_softmax_forward(const void* q, const void* kf, const void* vf, void* out, void* lse, int64_t slots,
                                  int64_t qtok, int64_t kvtok, int dim, int causal, int64_t row_offset, int64_t kv_chunk,
                                  int64_t kv_rank_stride, cudaStream_t s) {
   const KvLayout kl{kv_chunk, kv_rank_stride};
   const size_t smem = (size_t)(dim + kSmKeys + 32) * sizeof(A);
   dim3 grid((unsigned)qtok, (unsigned)slots);
   simt_softmax_fwd_kernel<T, A><<<grid, kSmThreads, smem, s>>>((const T*)q, (const T*)kf, (const T*)vf, (T*)out,
-                                                               lse, qtok, kvtok, dim, causal, row_offset, kl);
+                                                               (A*)lse, qtok, kvtok, dim, causal, row_offset, kl);
   return cudaGetLastError();
 }
 
@@ -551,23 +567,30 @@ template <typename T, typename A, typename G>
 cudaError_t simt_softmax_backward(const void* q, const void* kf, const void* vf, const void* o, const void* d_out,
                                   void* dq, void* dk_full, void* dv_full, void* scratch, int64_t slots, int64_t qtok,
                                   int64_t kvtok, int dim, int causal, int64_t row_offset, int64_t kv_chunk,
-                                  int64_t kv_rank_stride, int64_t grad_rank_stride, cudaStream_t s) {
+                                  int64_t kv_rank_stride, int64_t grad_rank_stride, cudaStream_t s, const void* lse) {
   const KvLayout kl{kv_chunk, kv_rank_stride}, gl{kv_chunk, grad_rank_stride};
   A* delta = reinterpret_cast<A*>(scratch);
   A* mx = delta + slots * qtok;
   A* sm = mx + slots * qtok;
   const int64_t rows = slots * qtok;
-  (void)o;  // delta is formed from P and dP (reference grouping), not from the forward output
-  (void)rows;
   dim3 gq((unsigned)qtok, (unsigned)slots);
-  simt_softmax_rowstats_kernel<T, A><<<gq, kSmThreads, (size_t)(dim + 32) * sizeof(A), s>>>(
-      (const T*)q, (const T*)kf, mx, sm, qtok, kvtok, dim, causal, row_offset, kl);
-  simt_softmax_delta_exact_kernel<T, A><<<gq, kSmThreads, (size_t)(2 * dim + 32) * sizeof(A), s>>>(
-      (const T*)q, (const T*)kf, (const T*)vf, (const T*)d_out, mx, sm, delta, qtok, kvtok, dim, causal, row_offset,
-      kl);
+  if (lse != nullptr) {
+    // the keys are a sub-range of the softmax: P from the forward's lse, delta = rowsum(dO o O)
+    // over the whole key set (reference grouping needs every key, this call sees only its range)
+    stats_from_lse_kernel<A><<<(unsigned)((rows + 255) / 256), 256, 0, s>>>((const A*)lse, mx, sm, rows);
+    simt_softmax_delta_kernel<T, A><<<(unsigned)((rows + 7) / 8), dim3(32, 8), 0, s>>>((const T*)o, (const T*)d_out,
+                                                                                      delta, rows, dim);
+  } else {
+    // delta formed from P and dP (reference grouping, oracle.py:155), exact row statistics
+    simt_softmax_rowstats_kernel<T, A><<<gq, kSmThreads, (size_t)(dim + 32) * sizeof(A), s>>>(
+        (const T*)q, (const T*)kf, mx, sm, qtok, kvtok, dim, causal, row_offset, kl);
+    simt_softmax_delta_exact_kernel<T, A><<<gq, kSmThreads, (size_t)(2 * dim + 32) * sizeof(A), s>>>(
+        (const T*)q, (const T*)kf, (const T*)vf, (const T*)d_out, mx, sm, delta, qtok, kvtok, dim, causal, row_offset,
+        kl);
+  }
   simt_softmax_bwd_dq_kernel<T, A><<<gq, kSmThreads, (size_t)(2 * dim + kSmKeys + 32) * sizeof(A), s>>>(
       (const T*)q, (const T*)kf, (const T*)vf, (const T*)d_out, delta, (T*)dq, qtok, kvtok, dim, causal,
-      row_offset, kl);
+      row_offset, kl, lse != nullptr ? mx : nullptr, sm);
   dim3 gk((unsigned)kvtok, (unsigned)slots);
   simt_softmax_bwd_dkdv_kernel<T, A, G><<<gk, kSmThreads, (size_t)(2 * dim + 2 * kSmKeys) * sizeof(A), s>>>(
       (const T*)q, (const T*)kf, (const T*)vf, (const T*)d_out, delta, mx, sm, (G*)dk_full, (G*)dv_full, qtok,
@@ -590,7 +613,7 @@ cudaError_t softmax_delta_bf16(const void* o, const void* d_out, float* delta, i
                                                void*, int64_t, int64_t, int, int, int, int, cudaStream_t);      \
   template cudaError_t simt_apply_state<T, A>(const void*, const void*, void*, int64_t, int64_t, int, int, int, \
                                               cudaStream_t);                                                    \
-  template cudaError_t simt_softmax_forward<T, A>(const void*, const void*, const void*, void*, float*, int64_t, \
+  template cudaError_t simt_softmax_forward<T, A>(const void*, const void*, const void*, void*, void*, int64_t, \
                                                   int64_t, int64_t, int, int, int64_t, int64_t, int64_t,         \
                                                   cudaStream_t);
 LASP_INST(float, float)
@@ -598,15 +621,17 @@ LASP_INST(double, double)
 LASP_INST(__nv_bfloat16, float)
 template cudaError_t simt_softmax_backward<float, float, float>(const void*, const void*, const void*, const void*,
                                                                 const void*, void*, void*, void*, void*, int64_t,
-                                                                int64_t, int64_t, int, int, int64_t, int64_t, int64_t, int64_t, cudaStream_t);
+                                                                int64_t, int64_t, int, int, int64_t, int64_t, int64_t,
+                                                                int64_t, cudaStream_t, const void*);
 template cudaError_t simt_softmax_backward<double, double, double>(const void*, const void*, const void*,
                                                                    const void*, const void*, void*, void*, void*,
                                                                    void*, int64_t, int64_t, int64_t, int, int,
-                                                                   int64_t, int64_t, int64_t, int64_t, cudaStream_t);
+                                                                   int64_t, int64_t, int64_t, int64_t, cudaStream_t,
+                                                                   const void*);
 template cudaError_t simt_softmax_backward<__nv_bfloat16, float, float>(const void*, const void*, const void*,
                                                                         const void*, const void*, void*, void*,
                                                                         void*, void*, int64_t, int64_t, int64_t,
                                                                         int, int, int64_t, int64_t, int64_t, int64_t,
-                                                                        cudaStream_t);
+                                                                        cudaStream_t, const void*);
 
 }  // namespace lasp

@@ -289,7 +289,7 @@ def softmax_forward(q: torch.Tensor, k_full: torch.Tensor, v_full: torch.Tensor,
     require_cuda(q, k_full, v_full)
     slots, qn, d = _slots(q)
     out = torch.empty_like(q)
-    lse = torch.empty(q.shape[:3], dtype=torch.float32, device=q.device)
+    lse = torch.empty(q.shape[:3], dtype=state_dtype(q.dtype), device=q.device)  # f64 data: f64 lse
     call("lasp2h_softmax_forward", dtype_code(q.dtype), ptr(q), ptr(k_full), ptr(v_full), ptr(out), ptr(lse), slots,
          qn, kv_tokens, d, int(causal), row_offset, kv_chunk, kv_rank_stride, stream_ptr())
     return out, lse
@@ -303,6 +303,17 @@ def softmax_backward(q, k_full, v_full, out, lse, d_out, causal: bool, row_offse
     dk contribution of key j lands at grads.view(-1)[(j//chunk)*grad_rank_stride + (slot*chunk + j%chunk)*d],
     dv at the same index + dv_offset.
     """
+    return softmax_backward_acc(q, k_full, v_full, out, lse, d_out, causal, row_offset, kv_tokens, kv_chunk,
+                                kv_rank_stride, grads, grad_rank_stride, dv_offset)[0]
+
+
+def softmax_backward_acc(q, k_full, v_full, out, lse, d_out, causal: bool, row_offset: int, kv_tokens: int,
+                         kv_chunk: int, kv_rank_stride: int, grads: torch.Tensor, grad_rank_stride: int,
+                         dv_offset: int, key_range: bool = False) -> tuple[torch.Tensor, torch.Tensor | None]:
+    """softmax_backward that also returns the fp32 dQ accumulator the bf16 tensor-core
+    path reduces into (None on the other paths, whose dq is already exact): partial
+    dQs of one query chunk from several key ranges then add with one rounding.
+    key_range: the keys are a sub-range of the softmax (lasp2h_softmax_backward_range)."""
     require_cuda(q, k_full, v_full, out, d_out, grads)
     slots, qn, d = _slots(q)
     dq = torch.empty_like(q)
@@ -310,10 +321,16 @@ def softmax_backward(q, k_full, v_full, out, lse, d_out, causal: bool, row_offse
     nbytes = int(_lib.load().lasp2h_softmax_scratch_bytes(code, slots, qn, kv_tokens, d))
     scratch = torch.empty(nbytes, dtype=torch.uint8, device=q.device)
     flat = grads.view(-1)
-    call("lasp2h_softmax_backward", code, ptr(q), ptr(k_full), ptr(v_full), ptr(out), ptr(lse), ptr(d_out), ptr(dq),
+    entry = "lasp2h_softmax_backward_range" if key_range else "lasp2h_softmax_backward"
+    call(entry, code, ptr(q), ptr(k_full), ptr(v_full), ptr(out), ptr(lse), ptr(d_out), ptr(dq),
          flat.data_ptr(), flat.data_ptr() + dv_offset * flat.element_size(), ptr(scratch), slots, qn, kv_tokens, d,
          int(causal), row_offset, kv_chunk, kv_rank_stride, grad_rank_stride, stream_ptr())
-    return dq
+    acc = None
+    if q.dtype == torch.bfloat16 and 8 <= d <= 128 and d % 8 == 0 and kv_chunk % 128 == 0:
+        # tc_softmax_backward's scratch: delta [slots*qtok] (padded to 64) then dq_acc [slots][qtok][d] fp32
+        off = ((slots * qn + 63) // 64) * 64
+        acc = scratch.view(torch.float32)[off:off + slots * qn * d].view(q.shape)
+    return dq, acc
 
 
 def probe_gemm(a: torch.Tensor, b: torch.Tensor, a_mn: int, b_mn: bool) -> torch.Tensor:

@@ -90,3 +90,39 @@ def test_low_precision_modes(dtype, tol):
     got = [to_np(cat(it.outputs))] + [to_np(cat(getattr(g, n) for g in it.grads)) for n in ("dq", "dk", "dv")]
     for name, g, r in zip(("out", "dq", "dk", "dv"), got, ref):
         assert O.normalized_error(g, r) <= tol, name
+
+
+@pytest.mark.parametrize("t", [3, 4, 5, 8])
+def test_balanced_schedule_f64_matches_oracle(t, monkeypatch):
+    """Causal load balance (standard_sp.BALANCED): helpers compute leading key chunks of the
+    upper ranks' queries; outputs / grads still match the reference math, with P2P sends."""
+    import paper_2502_07563_b200.standard_sp as sp
+    monkeypatch.setattr(sp, "BALANCED", True)
+    n, d, b, h = 8 * t, 8, 1, 2
+    q, k, v, do = O.inputs(n, d, b, h, 4)
+    it = cp_iteration(ChunkedSequence(q, k, v, t), do, True)
+    out, dq, dk, dv = O.cp_full(q, k, v, do, t, True)
+    assert np.max(np.abs(to_np(cat(it.outputs)) - out)) <= 1e-12
+    for name, ref in (("dq", dq), ("dk", dk), ("dv", dv)):
+        assert O.relative_error(to_np(cat(getattr(g, name) for g in it.grads)), ref) <= 1e-10, name
+    pairs = sum(1 for r in range(t) if sp._pairing(r, t)[0] >= 0)
+    assert it.run.stats.p2p_sends == 7 * pairs  # fwd: Q, O, lse; bwd: O, lse, dO, dQ
+    assert it.run.stats.allgather_launches == 2 and it.run.stats.reduce_scatter_launches == 1
+
+
+@pytest.mark.parametrize("t", [4, 8])
+def test_balanced_schedule_bf16_matches_unbalanced(t, monkeypatch):
+    import paper_2502_07563_b200.standard_sp as sp
+    n, d, b, h = 256 * t, 128, 1, 2
+    q, k, v, do = (O.bf16_round(x) for x in O.inputs(n, d, b, h, 5))
+    seq = ChunkedSequence(*(torch.from_numpy(x).to("cuda", torch.bfloat16) for x in (q, k, v)), t)
+    dod = torch.from_numpy(do).to("cuda", torch.bfloat16)
+    plain = cp_iteration(seq, dod, True)
+    monkeypatch.setattr(sp, "BALANCED", True)
+    bal = cp_iteration(seq, dod, True)
+    ref = O.cp_full(q, k, v, do, t, True)
+    for got, want, r in zip([cat(bal.outputs)] + [cat(getattr(g, nm) for g in bal.grads) for nm in ("dq", "dk", "dv")],
+                            [cat(plain.outputs)] + [cat(getattr(g, nm) for g in plain.grads)
+                                                    for nm in ("dq", "dk", "dv")], ref):
+        assert O.normalized_error(to_np(got), r) <= 1e-2
+        assert O.normalized_error(to_np(got), to_np(want)) <= 1e-2
