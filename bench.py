@@ -422,6 +422,10 @@ def summarize(r: dict, world: int, peaks: dict) -> dict:
 def run_gpu_arm(args) -> None:
     import torch
 
+    if args.balanced:
+        from paper_2502_07563_b200 import standard_sp as _sp
+        _sp.BALANCED = True
+
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -494,6 +498,8 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--balanced", action="store_true",
+                    help="cfg4 (LASP-2H): causal load balance across ranks (standard_sp.BALANCED)")
     ap.add_argument("--state-exchange", default="collective", choices=["collective", "peer"],
                     help="N>1: NCCL all_gather of the states, or the fused put into symmetric-memory peers")
     ap.add_argument("--no-cpu-baseline", action="store_true")
