@@ -464,7 +464,9 @@ def run_gpu_arm(args) -> None:
                 "config": {"workload": WORKLOADS[args.workload]["name"], "global_batch": B,
                            "seq_len": main["n"], "chunk_per_gpu": main["c"], "heads": H, "dim": D,
                            "parallelism": f"sp{world}", "masked": main["masked"],
-                           "l2": "inputs >= 2 GiB per step >> 126 MB L2; no flush needed"},
+                           "l2": "inputs >= 2 GiB per step >> 126 MB L2; no flush needed",
+                           "state_exchange": args.state_exchange if world > 1 else "none (one rank)",
+                           "lasp2h_schedule": "balanced" if args.balanced else "contiguous"},
                 "tensor_frac_of_peak": s["tensor_frac_of_peak"], "tensor_tflops_per_gpu": s["tensor_tflops_per_gpu"],
                 "hbm_frac_of_peak_min_bytes": s["hbm_frac_of_peak"], "roofline": s["roofline"],
                 "e2e": s["e2e"], "gpu_launches": int(round(s["gpu_launches_per_step"] * args.steps)),
