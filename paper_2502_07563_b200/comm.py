@@ -54,7 +54,9 @@ class WorldConfig:
     world_size ranks form contiguous SP groups of sp_size; ranks at the same
     position across groups are DP peers. element_bytes is the data element
     size: 8 (f64), 4 (f32) or 2 (bf16, which exchanges f32 states). The
-    latency fields exist for signature compatibility; real time is measured.
+    latency fields drive the threads-as-ranks world's simulated clock
+    (``WorldRun.simulated_time``, reference comm.py:7-12); real time is
+    measured on the device (bench.py, ``WorldRun.device_timelines``).
     """
 
     world_size: int
@@ -189,7 +191,7 @@ class _ContextBase:
 # ----------------------------------------------------------------------------
 
 class _Gen:
-    __slots__ = ("shape", "dtype", "contributions", "complete", "error", "kind")
+    __slots__ = ("shape", "dtype", "contributions", "complete", "error", "kind", "clocks", "completion_clock")
 
     def __init__(self, kind: str) -> None:
         self.kind = kind
@@ -198,6 +200,20 @@ class _Gen:
         self.contributions: dict[int, tuple[torch.Tensor, Any]] = {}
         self.complete = False
         self.error: CollectiveError | None = None
+        self.clocks: dict[int, float] = {}  # simulated issue clock per rank
+        self.completion_clock = 0.0
+
+
+class _ClockGen:
+    """Ledger-only generation of a collective (barriers, fused peer exchanges):
+    issue clocks only, completion at the latest issue plus the transfer cost."""
+
+    __slots__ = ("clocks", "completion_clock", "complete")
+
+    def __init__(self) -> None:
+        self.clocks: dict[int, float] = {}
+        self.completion_clock = 0.0
+        self.complete = False
 
 
 class _World:
@@ -212,9 +228,9 @@ class _World:
         t = cfg.sp_size
         self.groups = [tuple(range(g * t, (g + 1) * t)) for g in range(cfg.dp_size)]
         self.gens: dict[tuple[int, int], _Gen] = {}
-        self.queues: dict[tuple[int, int], deque] = {}  # (src, dst) -> FIFO of (snapshot, event)
+        self.queues: dict[tuple[int, int], deque] = {}  # (src, dst) -> FIFO of (snapshot, event, sent clock)
         self.exchanges: dict[tuple, list[PeerExchange]] = {}  # (group, tag, shape, dtype) -> per-position handles
-        self.exchange_calls: dict[tuple[int, int], int] = {}  # (group, call) -> ranks that exchanged
+        self.clock_gens: dict[tuple, _ClockGen] = {}  # (group, kind, call) -> barrier / peer-exchange generation
         self.t0 = time.perf_counter()
 
     def record(self, rank: int, kind: str, detail: str) -> None:
@@ -224,6 +240,10 @@ class _World:
         if self.abort_error is None:
             self.abort_error = err
         self.cond.notify_all()
+
+    def transfer_cost(self, nbytes: int) -> float:
+        """Simulated cost of one step moving nbytes (reference comm.py:359-360, 403-404)."""
+        return self.cfg.latency_per_launch + nbytes * self.cfg.latency_per_byte
 
 
 class PendingGather:
@@ -248,6 +268,7 @@ class PendingGather:
             if gen.error is not None:
                 raise CollectiveError(*gen.error.args)
             parts = [gen.contributions[r] for r in ctx.sp_peers]
+            ctx.clock = max(ctx.clock, gen.completion_clock)
         stream = torch.cuda.current_stream()
         for _, ev in parts:
             stream.wait_event(ev)
@@ -268,6 +289,8 @@ class RankContext(_ContextBase):
         self.rank = rank
         self._group_index = rank // world.cfg.sp_size
         self._calls = 0
+        self._barrier_calls = 0
+        self.clock = 0.0  # simulated: only communication moves it (reference comm.py:7-12)
         self.stream = torch.cuda.Stream(device=world.device)
 
     @property
@@ -340,7 +363,9 @@ class RankContext(_ContextBase):
                 raise gen.error
             world.record(self.rank, f"{kind}_issue", f"call={call} tag={tag} bytes={nbytes}")
             gen.contributions[self.rank] = (snap, ev)
+            gen.clocks[self.rank] = self.clock
             if len(gen.contributions) == len(self.sp_peers):
+                gen.completion_clock = max(gen.clocks.values()) + world.transfer_cost(nbytes)
                 gen.complete = True
                 if kind == "all_gather":
                     world.collective_launches += 1
@@ -376,6 +401,7 @@ class RankContext(_ContextBase):
             if gen.error is not None:
                 raise CollectiveError(*gen.error.args)
             parts = [gen.contributions[r] for r in self.sp_peers]
+            self.clock = max(self.clock, gen.completion_clock)
         stream = torch.cuda.current_stream()
         for _, ev in parts:
             stream.wait_event(ev)
@@ -406,19 +432,40 @@ class RankContext(_ContextBase):
                 world.exchanges[key] = handles
         return handles[self.sp_position]
 
+    def _clock_collective(self, kind: str, call: int, nbytes: int | None, on_complete=None) -> None:
+        """Join ledger-only generation (group, kind, call) and advance this rank's
+        simulated clock to its completion: the latest issue plus, when nbytes is
+        given, one transfer (a barrier aligns clocks at no cost, comm.py:414-431).
+        Called with world.cond held."""
+        world = self.world
+        gen = world.clock_gens.setdefault((self._group_index, kind, call), _ClockGen())
+        gen.clocks[self.rank] = self.clock
+        if len(gen.clocks) == self.sp_size:
+            latest = max(gen.clocks.values())
+            gen.completion_clock = latest if nbytes is None else latest + world.transfer_cost(nbytes)
+            gen.complete = True
+            if on_complete is not None:
+                on_complete()
+            world.cond.notify_all()
+        self._wait_locked(lambda: gen.complete, lambda: f"{kind} call {call} stalled: arrived {sorted(gen.clocks)}")
+        self.clock = max(self.clock, gen.completion_clock)
+
     def account_exchange(self, ex: PeerExchange, tag: str = "") -> None:
         """Ledger of one fused exchange: one all_gather launch per group per call,
-        this rank's contribution in bytes (comm.py:395-397)."""
+        this rank's contribution in bytes (comm.py:395-397); the simulated clock
+        advances as for a blocking all_gather (the consumers' in-kernel waits
+        are the device-side join)."""
         nbytes = ex.recv[0, 0].numel() * ex.recv.element_size()
         world = self.world
         with world.cond:
             call = self._calls
             self._calls += 1
-            k = (self._group_index, call)
-            world.exchange_calls[k] = world.exchange_calls.get(k, 0) + 1
-            if world.exchange_calls[k] == self.sp_size:
-                world.collective_launches += 1
             world.record(self.rank, "all_gather_issue", f"call={call} tag={tag} bytes={nbytes} peer")
+
+            def launched() -> None:
+                world.collective_launches += 1
+
+            self._clock_collective("peer_exchange", call, nbytes, launched)
         self.stats.allgather_launches += 1
         self.stats.communication_steps += 1
         self.stats._account("all_gather", nbytes)
@@ -443,7 +490,7 @@ class RankContext(_ContextBase):
             self.stats.p2p_sends += 1
             self.stats.communication_steps += 1
             self.stats._account("send", nbytes)
-            world.queues.setdefault((self.rank, dst), deque()).append((snap, ev))
+            world.queues.setdefault((self.rank, dst), deque()).append((snap, ev, self.clock))
             world.cond.notify_all()
         self._device_mark("send")
 
@@ -458,15 +505,24 @@ class RankContext(_ContextBase):
         with world.cond:
             queue = world.queues.setdefault((src, self.rank), deque())
             self._wait_locked(lambda: len(queue) > 0, lambda: f"recv from rank {src} found no matching send")
-            snap, ev = queue.popleft()
+            snap, ev, sent_clock = queue.popleft()
+            nbytes = snap.numel() * snap.element_size()
+            self.clock = max(self.clock, sent_clock + world.transfer_cost(nbytes))
             self.stats.p2p_recvs += 1
-            world.record(self.rank, "recv", f"src={src} tag={tag} bytes={snap.numel() * snap.element_size()}")
+            world.record(self.rank, "recv", f"src={src} tag={tag} bytes={nbytes}")
         torch.cuda.current_stream().wait_event(ev)
         self._device_mark("recv")
         return snap
 
     def barrier(self) -> None:
-        self.all_gather(torch.zeros(1, device=self.world.device), tag="barrier")
+        """Synchronise the SP group host-side: clocks align, no bytes or steps
+        accrue (comm.py:414-431). Device order is the callers' business."""
+        world = self.world
+        with world.cond:
+            call = self._barrier_calls
+            self._barrier_calls += 1
+            world.record(self.rank, "barrier", f"call={call}")
+            self._clock_collective("barrier", call, None)
 
     def mark(self, kind: str, detail: str = "") -> None:
         with self.world.cond:
@@ -485,6 +541,7 @@ class WorldRun:
     trace: list[TraceEvent]
     device_timelines: list[dict[str, list[float]]]
     wall_seconds: float
+    simulated_time: float | None = None  # threads-as-ranks world only: max final rank clock (comm.py:530)
 
 
 def _merge_stats(rank_stats: Sequence[CommStats], ag_launches: int, rs_launches: int) -> CommStats:
@@ -549,7 +606,7 @@ def world_spawn(cfg: WorldConfig, program: Callable[..., Any], rank_args: Sequen
                     stats=_merge_stats([c.stats for c in ctxs], world.collective_launches,
                                        world.reduce_scatter_launches),
                     trace=list(world.trace), device_timelines=[c.device_timeline() for c in ctxs],
-                    wall_seconds=wall)
+                    wall_seconds=wall, simulated_time=max(c.clock for c in ctxs))
 
 
 # ----------------------------------------------------------------------------

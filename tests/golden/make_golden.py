@@ -137,8 +137,74 @@ def lasp1_cases() -> None:
     print(f"wrote {out_path} ({out_path.stat().st_size} bytes, {len(data)} arrays)")
 
 
+# Simulated-clock cases: (method, n, d, t, world, batch, heads, masked/causal, pattern,
+# latency_per_launch, latency_per_byte). The reference clock depends only on the
+# schedule and the payload sizes, so these pin comm.py:7-12's model for every driver.
+CLOCK_CASES = [
+    ("lasp2", 16, 4, 4, 4, 1, 1, True, "", 10.0, 1 / 1024), ("lasp2", 16, 4, 4, 4, 1, 1, False, "", 10.0, 1 / 1024),
+    ("lasp2", 32, 8, 8, 8, 2, 3, True, "", 10.0, 1 / 1024), ("lasp2", 32, 4, 4, 8, 1, 1, True, "", 3.0, 0.25),
+    ("lasp2", 32, 4, 8, 8, 1, 1, True, "", 10.0, 0.0), ("lasp2_overlap", 16, 4, 4, 4, 1, 1, True, "", 10.0, 1 / 1024),
+    ("lasp1", 16, 4, 4, 4, 1, 1, True, "", 10.0, 1 / 1024), ("lasp1", 16, 4, 4, 4, 1, 1, False, "", 10.0, 1 / 1024),
+    ("lasp1", 32, 8, 8, 8, 2, 3, True, "", 10.0, 1 / 1024), ("lasp1", 32, 4, 8, 8, 1, 1, True, "", 10.0, 0.0),
+    ("lasp1", 32, 4, 4, 8, 1, 1, True, "", 3.0, 0.25),
+    ("cp", 16, 4, 4, 4, 1, 1, True, "", 10.0, 1 / 1024), ("cp", 16, 4, 2, 4, 2, 2, False, "", 10.0, 1 / 1024),
+    ("hybrid", 16, 4, 4, 4, 1, 1, True, "LLLN", 10.0, 1 / 1024), ("hybrid", 16, 8, 2, 2, 1, 2, True, "LN LN", 2.0, 0.5),
+]
+
+
+def clock_cases() -> None:
+    """Reference WorldRun.simulated_time for every driver -> tests/golden/clock_cases.json."""
+    import json
+
+    from laspsim import comm
+    from laspsim.datagen import gen_slots, qkv_slots
+    from laspsim.hybrid import ModelSpec, hybrid_iteration
+    from laspsim.lasp1 import lasp1_iteration
+    from laspsim.lasp2 import ChunkedSequence, lasp2_iteration
+    from laspsim.standard_sp import cp_iteration
+
+    rows = []
+    for case in CLOCK_CASES:
+        method, n, d, t, world, b, h, masked, pattern, lat_l, lat_b = case
+        cfg = comm.WorldConfig(world_size=world, sp_size=t, element_bytes=8,
+                               latency_per_launch=lat_l, latency_per_byte=lat_b)
+        if method == "hybrid":
+            spec = ModelSpec(pattern, dim=d, heads=h, batch=b, seed=0)
+            x, dy = gen_slots(0, b, h, n, d, "x"), gen_slots(0, b, h, n, d, "dy")
+            run = hybrid_iteration(spec, x, dy, t, masked, cfg).run
+        else:
+            q, k, v = qkv_slots(0, b, h, n, d)
+            do = gen_slots(0, b, h, n, d, "do")
+            seq = ChunkedSequence(q, k, v, t)
+            if method == "lasp2_overlap":
+                run = lasp2_iteration(seq, do, masked, cfg, overlap=True).run
+            else:
+                driver = {"lasp2": lasp2_iteration, "lasp1": lasp1_iteration, "cp": cp_iteration}[method]
+                run = driver(seq, do, masked, cfg).run
+        rows.append({"case": list(case), "simulated_time": run.simulated_time,
+                     "communication_steps": run.stats.communication_steps, "bytes_sent": run.stats.bytes_sent})
+    out_path = OUT.parent / "clock_cases.json"
+    out_path.write_text("[\n" + ",\n".join(json.dumps(r) for r in rows) + "\n]\n")
+    print(f"wrote {out_path} ({len(rows)} cases)")
+
+
+def costmodel_table() -> None:
+    """The reference CLI's default cost table (cli.py:765-810) -> tests/golden/costmodel_default.csv."""
+    from laspsim.cli import main as cli_main
+
+    out_path = OUT.parent / "costmodel_default.csv"
+    assert cli_main(["costmodel", "--out", str(out_path)]) == 0
+    print(f"wrote {out_path}")
+
+
 if __name__ == "__main__":
-    if sys.argv[1:] == ["hybrid"]:
+    if sys.argv[1:] == ["costmodel"]:
+        sys.path.insert(0, str(REF))
+        costmodel_table()
+    elif sys.argv[1:] == ["clock"]:
+        sys.path.insert(0, str(REF))
+        clock_cases()
+    elif sys.argv[1:] == ["hybrid"]:
         sys.path.insert(0, str(REF))
         hybrid_cases()
     elif sys.argv[1:] == ["lasp1"]:

@@ -4,8 +4,9 @@ the oracle restatement (itself pinned to the reference's outputs in
 test_oracle.py). Deviations, documented in DESIGN.md §6: bit-identity claims
 of the reference (T = 1 forward, ring vs gather, overlap vs sequential) hold
 here to rounding (<= 1e-12 relative), because the GPU kernels group the sums
-differently from numpy. Criterion 9 (the simulator's latency model) has no
-B200 counterpart: real time is measured by bench.py instead."""
+differently from numpy. Criterion 9 (the simulated latency model's
+ordering) is in tests/test_gpu_clock.py with the clock's reference goldens;
+real time is measured by bench.py."""
 import numpy as np
 import pytest
 import torch
