@@ -19,7 +19,10 @@ GPU instead of through one numpy BLAS:
   serial oracle, LASP-1 vs LASP-2, the ring's exclusive-prefix form) use the
   forward / gradient tolerance of the precision instead;
 * precision "bf16" (the tensor-core path) is added; its errors are normalised,
-  max|got - ref| / max|ref| per tensor, against 1e-2 (SURVEY §8a note P);
+  max|got - ref| / max|ref| per tensor, against 1e-2 (SURVEY §8a note P).
+  A bf16 L/N stack is only checkable for well-conditioned patterns: an
+  unnormalised L layer (no norm, as in the reference) gives the next softmax
+  logits of size ~N, where bf16 rounding flips row maxima;
 * method "oracle" (the reference checking its own serial oracles) is not a
   B200 path and is refused.
 ``simulated_time`` is the threads-as-ranks world's simulated clock
