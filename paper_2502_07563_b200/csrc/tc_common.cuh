@@ -54,6 +54,24 @@ __device__ __forceinline__ void st_row32_bf16(uint8_t* img, uint32_t row, uint32
   }
 }
 
+// v[i] += bf16 element (row, c0 + i) of a SW128 image (the read side of st_row32_bf16).
+__device__ __forceinline__ void ld_row32_add_bf16(const uint8_t* img, uint32_t row, uint32_t c0, float* v) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    uint32_t w[4];
+    const uint32_t off = sw128_offset(row, c0 + 8 * u);
+    asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                 : "r"(smem_u32(img + off))
+                 : "memory");
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      v[8 * u + 2 * j] += __uint_as_float(w[j] << 16);
+      v[8 * u + 2 * j + 1] += __uint_as_float(w[j] & 0xffff0000u);
+    }
+  }
+}
+
 // Columns [c_begin, c_begin + ncols) (multiple of 32) of this thread's TMEM lane
 // -> bf16 -> SW128 image. MASK 1 keeps col <= row, MASK 2 keeps col >= row
 // (the diagonal 128x128 block of a causal / anti-causal chunk). The mask is

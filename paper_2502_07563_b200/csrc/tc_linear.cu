@@ -602,7 +602,8 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* acc_full = bars + 2 * kApplyRing;       // [2]
   uint64_t* acc_empty = bars + 2 * kApplyRing + 2;  // [2]
   uint64_t* m_ready = bars + 2 * kApplyRing + 4;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kApplyRing + 5);
+  uint64_t* o_full = bars + 2 * kApplyRing + 5;  // [2] accumulate: the old O tile landed in stage[buf]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kApplyRing + 7);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slot = blockIdx.y;
@@ -618,7 +619,7 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    for (int i = 0; i < 5; ++i) mbar_init(&acc_full[i], 1);
+    for (int i = 0; i < 7; ++i) mbar_init(&acc_full[i], 1);  // acc_full, acc_empty, m_ready, o_full
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<256>(tmem_slot);
@@ -684,14 +685,26 @@ __global__ void __launch_bounds__(192, 1)
     fence_proxy_async_smem();
     named_bar_sync(1, 128);
     if (et == 0) mbar_arrive(m_ready);
+    // accumulate: the old O tile of block b is TMA-loaded into stage[buf] (once the store
+    // of block b-2 has read it) and added from shared memory, coalesced like the stores
+    auto load_old = [&](int b) {
+      const int buf = b & 1;
+      if (b >= 2) tma_store_wait_read<0>();  // the store of block b-2 (the latest group) has read stage[buf]
+      mbar_arrive_expect_tx(&o_full[buf], nbox * kBoxBytes);
+      const int orow = (int)((b0 + b) * kTile);
+      for (int bx = 0; bx < nbox; ++bx)
+        tma_load_3d(stage + buf * kTileBytes + bx * kBoxBytes, &tm_o, &o_full[buf], 64 * bx, orow, slot);
+    };
+    if (accumulate && et == 0 && nblk > 0) load_old(0);
     for (int b = 0; b < nblk; ++b) {
       const int buf = b & 1;
+      if (accumulate && et == 0 && b + 1 < nblk) load_old(b + 1);
       mbar_wait(&acc_full[buf], (b >> 1) & 1);
       tc_fence_after();
-      if (b >= 2 && et == 0) tma_store_wait_read<1>();
+      if (accumulate) mbar_wait(&o_full[buf], (b >> 1) & 1);
+      else if (b >= 2 && et == 0) tma_store_wait_read<1>();
       named_bar_sync(1, 128);
       uint8_t* st = stage + buf * kTileBytes;
-      const int64_t grow = (b0 + b) * kTile + row;
 #pragma unroll 1
       for (int c0 = 0; c0 < 128; c0 += 32) {
         uint32_t r[32];
@@ -700,12 +713,7 @@ __global__ void __launch_bounds__(192, 1)
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        if (accumulate && grow < tokens) {
-          const __nv_bfloat16* orow = out + ((int64_t)slot * tokens + grow) * dim;
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (c0 + i < dim) v[i] += __bfloat162float(orow[c0 + i]);
-        }
+        if (accumulate) ld_row32_add_bf16(st, row, c0, v);
         st_row32_bf16(st, row, c0, v);
       }
       fence_proxy_async_smem();

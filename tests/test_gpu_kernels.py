@@ -122,7 +122,7 @@ def test_causal_chunk_without_states():
 
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32, torch.float64])
 @pytest.mark.parametrize("transpose", [False, True])
-@pytest.mark.parametrize("shape", [(1, 2, 4096, 128), (2, 2, 300, 64), (1, 1, 3, 16)])
+@pytest.mark.parametrize("shape", [(1, 2, 4096, 128), (2, 2, 300, 64), (1, 1, 3, 16), (1, 2, 65536 + 77, 128)])
 def test_apply_state(dtype, transpose, shape):
     x = rand(shape, dtype, 13)
     b, h, n, d = shape
