@@ -84,6 +84,26 @@ def run(n: int, t: int, overlap: bool, iters: int = 5):
             seen[kind] = i + 1
             key = f"{kind}#{i}"
             acc[key] = acc.get(key, 0.0) + t0.elapsed_time(ev) / iters
+    # the same step captured in a CUDA graph (how bench.py runs it): no launch gaps
+    ctx.mark = lambda kind, detail="": None
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        step()
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        step()
+    graph.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(iters * 4):
+        graph.replay()
+    b.record()
+    torch.cuda.synchronize()
+    acc["graph_step"] = a.elapsed_time(b) / (iters * 4)
     return c, acc
 
 
@@ -103,6 +123,10 @@ def main() -> None:
                       f"bwd {step - fwd:7.3f} ms (before dM AG {ag2 - fwd:6.3f}) step {step:7.3f} ms  "
                       f"{c / step / 1e3:8.2f} M tok/s/GPU  {n / step / 1e3:8.1f} M tok/s x{W}  "
                       f"{flops / step / 1e9:6.0f} TFLOP/s/GPU")
+                g = ev["graph_step"]
+                print(f"{'':>27}graph-captured step {g:7.3f} ms  {c / g / 1e3:8.2f} M tok/s/GPU  "
+                      f"{n / g / 1e3:8.1f} M tok/s x{W}  {flops / g / 1e9:6.0f} TFLOP/s/GPU  "
+                      f"{22 * D * H * c / g / 1e6:6.0f} GB/s minimal-bytes")
 
 
 if __name__ == "__main__":
