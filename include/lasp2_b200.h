@@ -186,6 +186,23 @@ int lasp2_nomask_backward_local(int dtype, const void* q, const void* k, const v
                                 const void* m_full, void* dq, void* dk, void* dv, void* workspace,
                                 int64_t workspace_bytes, int64_t slots, int64_t tokens, int dim, void* stream);
 
+/* The same persistent kernels split around the state all_gather of a world
+ * of T > 1 ranks (the unmasked rank programs, lasp2.py:208-216, :256-267):
+ *   forward  phase 1: m = K^T V, this rank's chunk state M_t (the payload);
+ *            phase 2: out = Q m, m = the folded M_{1:T} (sum_states).
+ *   backward phase 1: dq = dO m_full^T and dm = Q^T dO (this rank's dM_t);
+ *            phase 2: dk = V dm^T, dv = K dm, dm = the folded dM_{1:T}.
+ * One launch per phase over all SMs (phase 1 with its in-kernel ordered
+ * reduction, phase 2 dynamically scheduled); same workspace contract as the
+ * _local entries; phase 3 = both (the world-of-one call). */
+int lasp2_nomask_forward_phase(int dtype, const void* q, const void* k, const void* v, void* out, void* m,
+                               void* workspace, int64_t workspace_bytes, int64_t slots, int64_t tokens, int dim,
+                               int phase, void* stream);
+int lasp2_nomask_backward_phase(int dtype, const void* q, const void* k, const void* v, const void* d_out,
+                                const void* m_full, void* dm, void* dq, void* dk, void* dv, void* workspace,
+                                int64_t workspace_bytes, int64_t slots, int64_t tokens, int dim, int phase,
+                                void* stream);
+
 /* LASP-2H softmax attention of one chunk of queries (global rows
  * [row_offset, row_offset+q_tokens)) against full-length keys/values.
  * Full-length tensors may be rank-major as the collectives produce them:

@@ -350,6 +350,58 @@ int lasp2_nomask_backward_local(int dtype, const void* q, const void* k, const v
   return st;
 }
 
+int lasp2_nomask_forward_phase(int dtype, const void* q, const void* k, const void* v, void* out, void* m,
+                               void* workspace, int64_t workspace_bytes, int64_t slots, int64_t tokens, int dim,
+                               int phase, void* stream) {
+  CHECK(valid_dtype(dtype), "nomask_forward_phase: unknown dtype");
+  CHECK(phase >= 1 && phase <= 3, "nomask_forward_phase: phase must be 1, 2 or 3");
+  CHECK(m && workspace && ((phase & 1) ? (k && v) : true) && ((phase & 2) ? (q && out) : true),
+        "nomask_forward_phase: null pointer");
+  CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128, "nomask_forward_phase: bad shape (1 <= dim <= 128)");
+  const int sms = sm_count_current();
+  CHECK(workspace_bytes >= lasp2_local_workspace_bytes(dtype, slots, tokens, dim, sms),
+        "nomask_forward_phase: workspace too small (lasp2_local_workspace_bytes)");
+  if (use_tc(dtype, dim, tokens))
+    return cuda_status(lasp::tc_flat_forward(q, k, v, out, (float*)m, workspace, slots, tokens, dim, sms, S(stream),
+                                             phase),
+                       "nomask_forward_phase");
+  int st = LASP2_OK;
+  if (phase & 1) {
+    const int nseg = lasp2_num_segments(dtype, slots, tokens, dim, sms);
+    st = lasp2_segment_states(dtype, k, v, workspace, slots, tokens, dim, nseg, stream);
+    if (st == LASP2_OK) st = lasp2_scan_segments(dtype, workspace, m, slots, nseg, dim, 0, stream);
+  }
+  if (st == LASP2_OK && (phase & 2)) st = lasp2_apply_state(dtype, q, m, out, slots, tokens, dim, 0, 0, stream);
+  return st;
+}
+
+int lasp2_nomask_backward_phase(int dtype, const void* q, const void* k, const void* v, const void* d_out,
+                                const void* m_full, void* dm, void* dq, void* dk, void* dv, void* workspace,
+                                int64_t workspace_bytes, int64_t slots, int64_t tokens, int dim, int phase,
+                                void* stream) {
+  CHECK(valid_dtype(dtype), "nomask_backward_phase: unknown dtype");
+  CHECK(phase >= 1 && phase <= 3, "nomask_backward_phase: phase must be 1, 2 or 3");
+  CHECK(dm && workspace && ((phase & 1) ? (q && d_out && m_full && dq) : true) &&
+            ((phase & 2) ? (k && v && dk && dv) : true),
+        "nomask_backward_phase: null pointer");
+  CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128, "nomask_backward_phase: bad shape (1 <= dim <= 128)");
+  const int sms = sm_count_current();
+  CHECK(workspace_bytes >= lasp2_local_workspace_bytes(dtype, slots, tokens, dim, sms),
+        "nomask_backward_phase: workspace too small (lasp2_local_workspace_bytes)");
+  if (use_tc(dtype, dim, tokens))
+    return cuda_status(lasp::tc_flat_backward(q, k, v, d_out, (const float*)m_full, dq, dk, dv, workspace, slots,
+                                              tokens, dim, sms, S(stream), (float*)dm, phase),
+                       "nomask_backward_phase");
+  int st = LASP2_OK;
+  if (phase & 1) {
+    const int nseg = lasp2_num_segments(dtype, slots, tokens, dim, sms);
+    st = lasp2_state_apply(dtype, q, d_out, m_full, workspace, dq, slots, tokens, dim, nseg, stream);
+    if (st == LASP2_OK) st = lasp2_scan_segments(dtype, workspace, dm, slots, nseg, dim, 0, stream);
+  }
+  if (st == LASP2_OK && (phase & 2)) st = lasp2_apply_state2(dtype, v, k, dm, dk, dv, slots, tokens, dim, stream);
+  return st;
+}
+
 int lasp2h_softmax_forward(int dtype, const void* q, const void* k_full, const void* v_full, void* out, void* lse,
                            int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim, int causal, int64_t row_offset,
                            int64_t kv_chunk, int64_t kv_rank_stride, void* stream) {

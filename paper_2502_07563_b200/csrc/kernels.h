@@ -90,10 +90,10 @@ cudaError_t tc_apply2(const void* x0, const void* x1, const float* m, void* out0
                       int64_t tokens, int dim, int sm_count, cudaStream_t s);
 int64_t tc_flat_workspace_bytes(int64_t slots, int64_t tokens, int dim, int sm_count);
 cudaError_t tc_flat_forward(const void* q, const void* k, const void* v, void* out, float* m_full, void* workspace,
-                            int64_t slots, int64_t tokens, int dim, int sm_count, cudaStream_t s);
+                            int64_t slots, int64_t tokens, int dim, int sm_count, cudaStream_t s, int phases = 3);
 cudaError_t tc_flat_backward(const void* q, const void* k, const void* v, const void* d_out, const float* m_full,
                              void* dq, void* dk, void* dv, void* workspace, int64_t slots, int64_t tokens, int dim,
-                             int sm_count, cudaStream_t s);
+                             int sm_count, cudaStream_t s, float* dm = nullptr, int phases = 3);
 cudaError_t tc_set_trace(unsigned long long* buf);
 cudaError_t tc_set_trace_flat(unsigned long long* buf);
 cudaError_t tc_set_trace_softmax(unsigned long long* buf);

@@ -47,6 +47,7 @@ struct FlatArgs {
   int dim;
   int slots;
   int kmax;
+  int phases;  // bit 0: phase 1 + reduction (total = this rank's chunk state); bit 1: phase 2 (state = total)
 };
 
 template <int KIND>
@@ -136,6 +137,8 @@ __global__ void __launch_bounds__(kFlatThreads, 1) tc_flat_kernel(const __grid_c
   const int64_t F = nb * a.slots;
   const int64_t f0 = flat_lo(blockIdx.x, F, gridDim.x), f1 = flat_lo(blockIdx.x + 1, F, gridDim.x);
   const int nblk = (int)(f1 - f0);
+  const bool run1 = a.phases & 1, run2 = a.phases & 2;
+  const int nblk1 = run1 ? nblk : 0;  // phase-1 blocks of this CTA
   const int slot0 = (int)(f0 / nb);
   const int nbox = a.dim > 64 ? 2 : 1;
   const int kfeat = (a.dim + 15) / 16;
@@ -180,47 +183,51 @@ __global__ void __launch_bounds__(kFlatThreads, 1) tc_flat_kernel(const __grid_c
         for (int bx = 0; bx < nbox; ++bx) tma_load_3d(dst + bx * kBoxBytes, m, &full[s], 64 * bx, row, sl);
         ++tcount;
       };
-      prefetch_tmap(&tm.p1_in0);
-      prefetch_tmap(&tm.p1_in1);
-      for (int b = 0; b < nblk; ++b) {
+      if (run1) {
+        prefetch_tmap(&tm.p1_in0);
+        prefetch_tmap(&tm.p1_in1);
+      }
+      for (int b = 0; b < nblk1; ++b) {
         load(&tm.p1_in0, f0 + b);
         load(&tm.p1_in1, f0 + b);
       }
-      prefetch_tmap(&tm.p2_in0);
-      if (Tr::p2_nin > 1) prefetch_tmap(&tm.p2_in1);
-      uint32_t seq = 0;
-      int s = (int)lmin(((f0 + f1) / 2) / nb, a.slots - 1), exhausted = 0;
-      while (exhausted < a.slots) {
-        unsigned got = (unsigned)nb;
-        if (*(volatile unsigned*)(a.ctr + s) < (unsigned)nb) got = atomicAdd(a.ctr + s, kGrab);
-        if (got >= (unsigned)nb) {
-          ++exhausted;
-          s = s + 1 == a.slots ? 0 : s + 1;
-          continue;
+      if (run2) {
+        prefetch_tmap(&tm.p2_in0);
+        if (Tr::p2_nin > 1) prefetch_tmap(&tm.p2_in1);
+        uint32_t seq = 0;
+        int s = (int)lmin(((f0 + f1) / 2) / nb, a.slots - 1), exhausted = 0;
+        while (exhausted < a.slots) {
+          unsigned got = (unsigned)nb;
+          if (*(volatile unsigned*)(a.ctr + s) < (unsigned)nb) got = atomicAdd(a.ctr + s, kGrab);
+          if (got >= (unsigned)nb) {
+            ++exhausted;
+            s = s + 1 == a.slots ? 0 : s + 1;
+            continue;
+          }
+          exhausted = 0;  // found work here: the scan restarts after this slot drains
+          const unsigned hi = got + kGrab < (unsigned)nb ? got + kGrab : (unsigned)nb;
+          for (unsigned j = got; j < hi; ++j) {
+            const int64_t f = (int64_t)s * nb + j;
+            // the record is visible to whoever waits on this block's first tile
+            const int rs = tcount % kFlatRing;
+            if (tcount >= kFlatRing) mbar_wait(&empty[rs], ((tcount / kFlatRing) - 1) & 1);
+            st_shared_u64(recs + seq % kRecs, ((uint64_t)seq << 32) | (uint32_t)f);
+            load(&tm.p2_in0, f);
+            if (Tr::p2_nin > 1) load(&tm.p2_in1, f);
+            ++seq;
+          }
         }
-        exhausted = 0;  // found work here: the scan restarts after this slot drains
-        const unsigned hi = got + kGrab < (unsigned)nb ? got + kGrab : (unsigned)nb;
-        for (unsigned j = got; j < hi; ++j) {
-          const int64_t f = (int64_t)s * nb + j;
-          // the record is visible to whoever waits on this block's first tile
-          const int rs = tcount % kFlatRing;
-          if (tcount >= kFlatRing) mbar_wait(&empty[rs], ((tcount / kFlatRing) - 1) & 1);
-          st_shared_u64(recs + seq % kRecs, ((uint64_t)seq << 32) | (uint32_t)f);
-          load(&tm.p2_in0, f);
-          if (Tr::p2_nin > 1) load(&tm.p2_in1, f);
-          ++seq;
-        }
-      }
-      const int rs = slot_wait();  // end record: one ring position, released by a plain arrive
-      st_shared_u64(recs + seq % kRecs, ((uint64_t)seq << 32) | 0xffffffffu);
-      mbar_arrive(&full[rs]);
-      ++tcount;
-      // the last CTA to finish grabbing re-arms the counters for the next launch
-      __threadfence();
-      if (atomicAdd(a.done, 1u) == gridDim.x - 1) {
-        for (int i = 0; i < a.slots; ++i) a.ctr[i] = 0;
-        *a.done = 0;
+        const int rs = slot_wait();  // end record: one ring position, released by a plain arrive
+        st_shared_u64(recs + seq % kRecs, ((uint64_t)seq << 32) | 0xffffffffu);
+        mbar_arrive(&full[rs]);
+        ++tcount;
+        // the last CTA to finish grabbing re-arms the counters for the next launch
         __threadfence();
+        if (atomicAdd(a.done, 1u) == gridDim.x - 1) {
+          for (int i = 0; i < a.slots; ++i) a.ctr[i] = 0;
+          *a.done = 0;
+          __threadfence();
+        }
       }
     }
   } else if (warp == 1) {
@@ -239,7 +246,7 @@ __global__ void __launch_bounds__(kFlatThreads, 1) tc_flat_kernel(const __grid_c
       if (bcount >= 2) mbar_wait(&acc_empty[buf], ((bcount >> 1) - 1) & 1);
       return buf;
     };
-    for (int b = 0; b < nblk; ++b) {
+    for (int b = 0; b < nblk1; ++b) {
       const bool ps = piece_start(b), pe = piece_end(b);
       const uint32_t x0 = wait_tile(tcount), x1 = wait_tile(tcount + 1);
       if (Tr::p1_img && ps) mbar_wait(m_ready, iv++ & 1);
@@ -265,7 +272,7 @@ __global__ void __launch_bounds__(kFlatThreads, 1) tc_flat_kernel(const __grid_c
       if (pe) ++pc;
     }
     int cur = -1;
-    for (uint32_t b = 0;; ++b) {
+    for (uint32_t b = 0; run2; ++b) {
       const uint32_t x0 = wait_tile(tcount);
       const int f = (int)(uint32_t)ld_shared_u64(recs + b % kRecs);
       if (f < 0) break;
@@ -348,12 +355,12 @@ __global__ void __launch_bounds__(kFlatThreads, 1) tc_flat_kernel(const __grid_c
     };
 
     // ---- phase 1 (static range) ----
-    if (Tr::p1_img && nblk > 0) {
+    if (Tr::p1_img && nblk1 > 0) {
       load_state(a.m_in, slot0);
       build_image();
       if (slot0 + 1 < a.slots && (f1 - 1) / nb > slot0) load_state(a.m_in, slot0 + 1);
     }
-    for (int b = 0; b < nblk; ++b) {
+    for (int b = 0; b < nblk1; ++b) {
       const bool pe = piece_end(b);
       if (Tr::p1_nout) {
         const int buf = bcount & 1;
@@ -411,9 +418,9 @@ __global__ void __launch_bounds__(kFlatThreads, 1) tc_flat_kernel(const __grid_c
 
     // ---- slot totals: ordered sum of the partials over the whole grid ----
     trace(1);
-    grid_barrier(a.gbar, gridDim.x, et);
+    if (run1) grid_barrier(a.gbar, gridDim.x, et);
     trace(2);
-    {
+    if (run1) {
       // slot s = flat blocks [s*nb, (s+1)*nb) is covered by CTAs c_lo..c_hi (every CTA owns
       // >= 1 block since grid <= F); c_lo's piece index is s - slot0(c_lo), later CTAs' is 0.
       // float4 units, ~2 per thread; all partial loads of a unit are issued before the adds.
@@ -470,13 +477,15 @@ __global__ void __launch_bounds__(kFlatThreads, 1) tc_flat_kernel(const __grid_c
       }
     }
     trace(3);
-    grid_barrier(a.gbar, 2 * gridDim.x, et);
-    grid_barrier_rearm(a.gbar, gridDim.x, et);
+    if (run1) {
+      grid_barrier(a.gbar, 2 * gridDim.x, et);
+      grid_barrier_rearm(a.gbar, gridDim.x, et);
+    }
     trace(4);
 
     // ---- phase 2 (dynamic blocks, in the producer's record order) ----
     int cur = -1;
-    for (uint32_t b = 0;; ++b) {
+    for (uint32_t b = 0; run2; ++b) {
       uint64_t r;
       while ((uint32_t)((r = ld_shared_u64(recs + b % kRecs)) >> 32) != b) __nanosleep(20);
       const int f = (int)(uint32_t)r;
@@ -569,13 +578,13 @@ cudaError_t launch_flat(const tc::FlatMaps& tm, const tc::FlatArgs& a, int grid,
 int64_t flat_header(int64_t slots) { return 256 + ((slots * 4 + 255) / 256) * 256; }
 
 tc::FlatArgs flat_args(void* workspace, const float* m_in, float* total, int64_t slots, int64_t tokens, int dim,
-                       int grid) {
+                       int grid, int phases = 3) {
   uint8_t* ws = (uint8_t*)workspace;
   const int kmax = flat_kmax(slots, tokens, grid);
   float* part = (float*)(ws + flat_header(slots));
   if (total == nullptr) total = part + (int64_t)grid * kmax * dim * dim;
   return tc::FlatArgs{m_in, total, part, (unsigned*)ws, (unsigned*)ws + 2, (unsigned*)(ws + 256),
-                      tokens, dim, (int)slots, kmax};
+                      tokens, dim, (int)slots, kmax, phases};
 }
 
 }  // namespace
@@ -589,10 +598,20 @@ int64_t tc_flat_workspace_bytes(int64_t slots, int64_t tokens, int dim, int sm_c
 }
 
 // Unmasked forward of one rank of a world of one: m_full = K^T V, O = Q m_full.
+// phases 1 / 2 split it around a state all_gather (T > 1): phase 1 writes this
+// rank's chunk state K^T V to m_full; phase 2 computes O = Q m_full from the
+// folded state the caller put there.
 cudaError_t tc_flat_forward(const void* q, const void* k, const void* v, void* out, float* m_full, void* workspace,
-                            int64_t slots, int64_t tokens, int dim, int sm_count, cudaStream_t s) {
+                            int64_t slots, int64_t tokens, int dim, int sm_count, cudaStream_t s, int phases) {
   tc::FlatMaps tm;
   cudaError_t e;
+  // a phase-only call leaves the other phase's tensors null: their maps are never used,
+  // so they alias a tensor that is present
+  const void* any = k ? k : q;
+  if (!k) k = any;
+  if (!v) v = any;
+  if (!q) q = any;
+  if (!out) out = const_cast<void*>(any);
   if ((e = make_tmap_3d(&tm.p1_in0, k, slots, tokens, dim)) != cudaSuccess) return e;
   if ((e = make_tmap_3d(&tm.p1_in1, v, slots, tokens, dim)) != cudaSuccess) return e;
   tm.p1_out0 = tm.p1_in0;  // unused
@@ -601,16 +620,26 @@ cudaError_t tc_flat_forward(const void* q, const void* k, const void* v, void* o
   if ((e = make_tmap_3d(&tm.p2_out0, out, slots, tokens, dim)) != cudaSuccess) return e;
   tm.p2_out1 = tm.p2_out0;  // unused
   const int grid = flat_grid(slots, tokens, sm_count);
-  return launch_flat<0>(tm, flat_args(workspace, nullptr, m_full, slots, tokens, dim, grid), grid, s);
+  return launch_flat<0>(tm, flat_args(workspace, nullptr, m_full, slots, tokens, dim, grid, phases), grid, s);
 }
 
 // Unmasked backward of one rank of a world of one:
-// dM = Q^T dO, dQ = dO M^T, dK = V dM^T, dV = K dM (dM kept in the workspace).
+// dM = Q^T dO, dQ = dO M^T, dK = V dM^T, dV = K dM (dM kept in the workspace, or in
+// dm when given). phases 1 / 2 split it around the dM all_gather: phase 1 writes dQ
+// and this rank's Q^T dO to dm; phase 2 computes dK, dV from the folded dm.
 cudaError_t tc_flat_backward(const void* q, const void* k, const void* v, const void* d_out, const float* m_full,
                              void* dq, void* dk, void* dv, void* workspace, int64_t slots, int64_t tokens, int dim,
-                             int sm_count, cudaStream_t s) {
+                             int sm_count, cudaStream_t s, float* dm, int phases) {
   tc::FlatMaps tm;
   cudaError_t e;
+  const void* any = q ? q : v;  // phase-only calls: see tc_flat_forward
+  if (!q) q = any;
+  if (!d_out) d_out = any;
+  if (!dq) dq = const_cast<void*>(any);
+  if (!v) v = any;
+  if (!k) k = any;
+  if (!dk) dk = const_cast<void*>(any);
+  if (!dv) dv = const_cast<void*>(any);
   if ((e = make_tmap_3d(&tm.p1_in0, q, slots, tokens, dim)) != cudaSuccess) return e;
   if ((e = make_tmap_3d(&tm.p1_in1, d_out, slots, tokens, dim)) != cudaSuccess) return e;
   if ((e = make_tmap_3d(&tm.p1_out0, dq, slots, tokens, dim)) != cudaSuccess) return e;
@@ -619,7 +648,7 @@ cudaError_t tc_flat_backward(const void* q, const void* k, const void* v, const 
   if ((e = make_tmap_3d(&tm.p2_out0, dk, slots, tokens, dim)) != cudaSuccess) return e;
   if ((e = make_tmap_3d(&tm.p2_out1, dv, slots, tokens, dim)) != cudaSuccess) return e;
   const int grid = flat_grid(slots, tokens, sm_count);
-  return launch_flat<1>(tm, flat_args(workspace, m_full, nullptr, slots, tokens, dim, grid), grid, s);
+  return launch_flat<1>(tm, flat_args(workspace, m_full, dm, slots, tokens, dim, grid, phases), grid, s);
 }
 
 }  // namespace lasp

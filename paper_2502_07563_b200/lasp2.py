@@ -223,6 +223,19 @@ def _forward_nomask_rank(ctx, qc: torch.Tensor, kc: torch.Tensor,
         out, m_full = ops.nomask_forward_local(qc, kc, vc)
         _gather_states(ctx, m_full, "state")
         return out, ActivationCache(q=qc, k=kc, v=vc, masked=False, m_full=m_full, state_folds=1)
+    if FLAT_PHASES:
+        # M_t from the persistent phase-1 launch (in-kernel ordered reduction), then the
+        # exchange, then O = Q M_{1:T} as the dynamically scheduled phase-2 launch
+        m_t = ops.nomask_forward_phase(qc, kc, vc, _state_like(kc), 1)
+        ex = _peer(ctx, "state", m_t)
+        if ex is not None:  # one-segment scan_put: a copy of M_t into every peer's buffer
+            ops.scan_put(m_t.unsqueeze(2), False, kc.dtype, ex)
+            ctx.account_exchange(ex, "state")
+            m_full = ops.exchange_fold(ex, ops.FOLD_FULL)
+        else:
+            m_full = ops.sum_states(_unpack_gathered(_gather_states(ctx, m_t, "state"), m_t))
+        out = ops.nomask_forward_phase(qc, kc, vc, m_full, 2)
+        return out, ActivationCache(q=qc, k=kc, v=vc, masked=False, m_full=m_full, state_folds=1)
     nseg = ops.num_segments(kc)
     m_t, ex = _share_total(ctx, ops.segment_states(kc, vc, nseg), False, kc.dtype, "state")
     if ex is not None:
@@ -233,6 +246,11 @@ def _forward_nomask_rank(ctx, qc: torch.Tensor, kc: torch.Tensor,
     m_full = ops.sum_states(gathered)
     out = ops.apply_state(qc, m_full)
     return out, ActivationCache(q=qc, k=kc, v=vc, masked=False, m_full=m_full, state_folds=1)
+
+
+def _state_like(x: torch.Tensor) -> torch.Tensor:
+    d = x.shape[-1]
+    return torch.empty((*x.shape[:2], d, d), dtype=ops.state_dtype(x.dtype), device=x.device)
 
 
 def _forward_masked_rank(ctx, qc: torch.Tensor, kc: torch.Tensor, vc: torch.Tensor,
@@ -316,6 +334,18 @@ def _backward_nomask_rank(ctx, cache: ActivationCache, d_out: torch.Tensor) -> G
         dq, dk, dv = ops.nomask_backward_local(q, cache.k, cache.v, do, cache.m_full)
         _gather_states(ctx, cache.m_full, "state_grad")  # accounting only: identity at T = 1
         return GradientBundle(dq=dq, dk=dk, dv=dv)
+    if FLAT_PHASES:
+        # dQ and dM_t from the persistent phase-1 launch, the exchange, then dK, dV as phase 2
+        dq, g_t = ops.nomask_backward_phase1(q, do, cache.m_full)
+        ex = _peer(ctx, "state_grad", g_t)
+        if ex is not None:
+            ops.scan_put(g_t.unsqueeze(2), False, q.dtype, ex)
+            ctx.account_exchange(ex, "state_grad")
+            dm_full = ops.exchange_fold(ex, ops.FOLD_FULL)
+        else:
+            dm_full = ops.sum_states(_unpack_gathered(_gather_states(ctx, g_t, "state_grad"), g_t))
+        dk, dv = ops.nomask_backward_phase2(cache.v, cache.k, dm_full)
+        return GradientBundle(dq=dq, dk=dk, dv=dv)
     unit_bytes = q.numel() * q.element_size()
     if ctx.sp_size == 1 or unit_bytes >= _FUSE_DQ_MIN_BYTES or STATE_EXCHANGE == "peer":
         nseg = ops.num_segments(q)
@@ -339,6 +369,11 @@ def _backward_nomask_rank(ctx, cache: ActivationCache, d_out: torch.Tensor) -> G
 # world of one rank: run the unmasked layer as one persistent launch per direction
 # (lasp2_nomask_forward_local / _backward_local); False keeps the per-step kernels
 LOCAL_FUSED = True
+
+# T > 1 unmasked: the same persistent kernels split around the exchange (phase 1 ->
+# M_t / dM_t, phase 2 after the fold; lasp2_nomask_*_phase); False keeps segment
+# states + scan, apply_state / state_apply / apply_state2
+FLAT_PHASES = True
 
 # a bf16 chunk tensor of >= 256 MB takes >= ~40 us to stream, more than a
 # state all_gather costs, so fusing dQ into the dM pass wins even with T > 1

@@ -283,6 +283,48 @@ def nomask_backward_local(q, k, v, d_out, m_full) -> tuple[torch.Tensor, torch.T
     return dq, dk, dv
 
 
+def nomask_forward_phase(q, k, v, m: torch.Tensor, phase: int, out: torch.Tensor | None = None):
+    """Phase 1: m <- k^T v (this rank's chunk state); phase 2: out = q m with m the folded
+    state (header: lasp2_nomask_forward_phase). Returns out (phase 2) or m (phase 1)."""
+    require_cuda(k if phase == 1 else q, m)
+    x = k if phase == 1 else q
+    slots, n, d = _slots(x)
+    if m.shape != (*x.shape[:2], d, d) or m.dtype != state_dtype(x.dtype) or not m.is_contiguous():
+        raise ValueError(f"state {tuple(m.shape)} {m.dtype} does not match data {tuple(x.shape)}")
+    if phase == 2 and out is None:
+        out = torch.empty_like(q)
+    ws = local_workspace(x)
+    call("lasp2_nomask_forward_phase", dtype_code(x.dtype), ptr(q) if phase == 2 else 0, ptr(k) if phase == 1 else 0,
+         ptr(v) if phase == 1 else 0, ptr(out) if phase == 2 else 0, ptr(m), ptr(ws), ws.numel(), slots, n, d, phase,
+         stream_ptr())
+    return out if phase == 2 else m
+
+
+def nomask_backward_phase1(q, d_out, m_full) -> tuple[torch.Tensor, torch.Tensor]:
+    """(dq = d_out m_full^T, dm_t = q^T d_out) in one launch (header: lasp2_nomask_backward_phase)."""
+    require_cuda(q, d_out, m_full)
+    slots, n, d = _slots(q)
+    dq = torch.empty_like(d_out)
+    dm = torch.empty_like(m_full)
+    ws = local_workspace(q)
+    call("lasp2_nomask_backward_phase", dtype_code(q.dtype), ptr(q), 0, 0, ptr(d_out), ptr(m_full), ptr(dm), ptr(dq),
+         0, 0, ptr(ws), ws.numel(), slots, n, d, 1, stream_ptr())
+    return dq, dm
+
+
+def nomask_backward_phase2(v, k, dm) -> tuple[torch.Tensor, torch.Tensor]:
+    """(dk = v dm^T, dv = k dm) with dm the folded dM (header: lasp2_nomask_backward_phase)."""
+    require_cuda(v, k, dm)
+    slots, n, d = _slots(v)
+    if not dm.is_contiguous():
+        dm = dm.contiguous()
+    dk, dv = torch.empty_like(v), torch.empty_like(k)
+    ws = local_workspace(v)
+    call("lasp2_nomask_backward_phase", dtype_code(v.dtype), 0, ptr(k), ptr(v), 0, 0, ptr(dm), 0, ptr(dk), ptr(dv),
+         ptr(ws), ws.numel(), slots, n, d, 2, stream_ptr())
+    return dk, dv
+
+
 def softmax_forward(q: torch.Tensor, k_full: torch.Tensor, v_full: torch.Tensor, causal: bool, row_offset: int,
                     kv_tokens: int, kv_chunk: int, kv_rank_stride: int) -> tuple[torch.Tensor, torch.Tensor]:
     """Softmax attention of a query chunk against (possibly rank-major) full K/V (oracle.py:136-139)."""

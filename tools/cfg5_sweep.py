@@ -20,7 +20,8 @@ from paper_2502_07563_b200 import comm, lasp2  # noqa: E402
 from paper_2502_07563_b200.datagen import gen_slots_device  # noqa: E402
 
 W, H, D = 8, 16, 128
-SIZES = [int(a) for a in sys.argv[1:]] or [65536, 131072, 262144, 524288, 1048576, 2097152]
+MASKED = "--unmasked" not in sys.argv  # --unmasked: cfg2's layer at its W = 8 chunk (N = 128K -> C = 16K)
+SIZES = [int(a) for a in sys.argv[1:] if not a.startswith("--")] or [65536, 131072, 262144, 524288, 1048576, 2097152]
 
 
 class ProbeCtx(comm.LocalRankContext):
@@ -64,9 +65,12 @@ def run(n: int, t: int, overlap: bool, iters: int = 5):
     def step():
         ctx.events.clear()
         ctx.mark("start")
-        out, cache = lasp2._forward_masked_rank(ctx, q, k, v, overlap=overlap)
+        if MASKED:
+            out, cache = lasp2._forward_masked_rank(ctx, q, k, v, overlap=overlap)
+        else:
+            out, cache = lasp2._forward_nomask_rank(ctx, q, k, v)
         ctx.mark("fwd_end")
-        lasp2._backward_masked_rank(ctx, cache, do)
+        (lasp2._backward_masked_rank if MASKED else lasp2._backward_nomask_rank)(ctx, cache, do)
         ctx.mark("bwd_end")
         return out
 
@@ -108,16 +112,18 @@ def run(n: int, t: int, overlap: bool, iters: int = 5):
 
 
 def main() -> None:
-    print(f"cfg5 per-rank sweep, W={W} H={H} d={D} bf16 masked; exchange = local copy (0 cost)")
+    print(f"per-rank sweep, W={W} H={H} d={D} bf16 {'masked' if MASKED else 'unmasked'}; "
+          "exchange = local copy (0 cost)")
     for n in SIZES:
-        for overlap in (False, True):
+        for overlap in ((False, True) if MASKED else (False,)):
             for t in (0, W - 1):
                 c, ev = run(n, t, overlap)
                 fwd, step = ev["fwd_end#0"], ev["bwd_end#0"]
                 ag1 = ev["ag_issue:state#0"]
                 ag2 = ev.get("ag_issue:state_grad#0", float("nan"))
                 intra = ev.get("intra_end#0", float("nan")) - ev.get("intra_start#0", float("nan"))
-                flops = (12 * D * D + 7 * D * 257) * H * c  # BASELINE.md §3, per rank
+                ag2 = ag2 if MASKED else ev.get("ag_issue:state_grad#0", float("nan"))
+                flops = (12 * D * D + (7 * D * 257 if MASKED else 0)) * H * c  # BASELINE.md §3, per rank
                 print(f"N={n:>8} C={c:>7} {'overlap   ' if overlap else 'sequential'} t={t}: "
                       f"fwd {fwd:7.3f} ms (compute before AG {ag1:6.3f}, intra {intra:6.3f}) "
                       f"bwd {step - fwd:7.3f} ms (before dM AG {ag2 - fwd:6.3f}) step {step:7.3f} ms  "
