@@ -19,7 +19,12 @@ sys.path.insert(0, ".")
 from paper_2502_07563_b200 import comm, lasp2  # noqa: E402
 from paper_2502_07563_b200.datagen import gen_slots_device  # noqa: E402
 
+import os  # noqa: E402
+
 W, H, D = 8, 16, 128
+if os.environ.get("NSEG"):  # A/B: segments per slot of the masked passes
+    from paper_2502_07563_b200 import ops  # noqa: E402
+    ops.num_segments = lambda x, _n=int(os.environ["NSEG"]): _n
 MASKED = "--unmasked" not in sys.argv  # --unmasked: cfg2's layer at its W = 8 chunk (N = 128K -> C = 16K)
 SIZES = [int(a) for a in sys.argv[1:] if not a.startswith("--")] or [65536, 131072, 262144, 524288, 1048576, 2097152]
 
