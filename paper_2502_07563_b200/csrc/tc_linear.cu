@@ -224,6 +224,18 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
   unsigned long long t_begin = 0;  // per-CTA globaltimer span when the debug buffer is set (tools/cta_span_probe.py)
   if (g_trace != nullptr && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
 #endif
+#ifdef LASP2_SPAN  // A/B diagnostic build: 8 globaltimer stamps per CTA (tools/cta_phase_probe.py)
+  auto span = [&](int i) {
+    if (g_trace != nullptr) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      g_trace[8 * (blockIdx.y * gridDim.x + blockIdx.x) + i] = t;
+    }
+  };
+  if (threadIdx.x == 0) span(0);
+#else
+  auto span = [](int) {};
+#endif
   const uint32_t role_id = kMode == 1 ? cluster_ctarank() : kMode == 2 ? blockIdx.x % 3 : 0u;
   const int seg = kMode == 1 ? (int)(blockIdx.x >> 1) : kMode == 2 ? (int)(blockIdx.x / 3) : (int)blockIdx.x;
   const Role R = causal_role<kMode>(role_id, a);
@@ -247,6 +259,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
   if constexpr (kMode == 1) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) span(1);
   pdl_wait();
   pdl_launch_dependents();
   // TMEM: S [0,128), O[0] [128,256), running state [256,384), O[1] (kMode 3: G) [384,512)
@@ -431,33 +444,69 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       const float* xb = a.xrecv + (int64_t)slot * dd;
       float* bo = (a.base_out != nullptr && seg == 0 && (kMode != 1 || R.mcast == 1)) ? a.base_out + (int64_t)slot * dd
                                                                                         : nullptr;
+      // every load of a 32-column chunk is issued before any store (base_out), so the
+      // chunk costs one memory latency, not one per element (the stores may alias as
+      // far as the compiler knows)
+      const bool rowok = (int)row < dim;
+      int c0_cur = cb;
+      auto load32 = [&](const float* base, float* dst) {  // dst[i] = element (row, c0 + i) of base
+        if (!R.transpose && rowok && c0_cur + 32 <= dim) {
+          const float4* p4 = reinterpret_cast<const float4*>(base + (int64_t)row * dim + c0_cur);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const float4 f = __ldcg(p4 + u);
+            dst[4 * u] = f.x;
+            dst[4 * u + 1] = f.y;
+            dst[4 * u + 2] = f.z;
+            dst[4 * u + 3] = f.w;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int c = c0_cur + i;
+            dst[i] = (rowok && c < dim)
+                         ? __ldcg(base + (R.transpose ? (int64_t)c * dim + row : (int64_t)row * dim + c))
+                         : 0.f;
+          }
+        }
+      };
 #pragma unroll 1
       for (int c0 = cb; c0 < cb + 64; c0 += 32) {
-        float v[32];
+        c0_cur = c0;
+        float v[32], t[32];
+        if (fold) {  // first term copied, the rest in rank order (numerics.py:71-116)
+          const int first = a.xdesc ? a.xhi - 1 : a.xlo;
+          load32(xb + first * xstride, v);
+          if (a.xdesc) {
+            for (int j = a.xhi - 2; j >= a.xlo; --j) {
+              load32(xb + j * xstride, t);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int c = c0 + i;
-          float x = 0.f;
-          if ((int)row < dim && c < dim) {
-            const int64_t src = R.transpose ? (int64_t)c * dim + row : (int64_t)row * dim + c;
-            if (fold) {  // first term copied, the rest in rank order (numerics.py:71-116)
-              float b = 0.f;
-              if (a.xdesc) {
-                b = __ldcg(xb + (a.xhi - 1) * xstride + src);
-                for (int j = a.xhi - 2; j >= a.xlo; --j) b += __ldcg(xb + j * xstride + src);
-              } else {
-                b = __ldcg(xb + a.xlo * xstride + src);
-                for (int j = a.xlo + 1; j < a.xhi; ++j) b += __ldcg(xb + j * xstride + src);
-              }
-              if (bo != nullptr) bo[src] = b;
-              x += b;
-            } else {
-              if (bs) x += bs[src];
-              if (bo != nullptr) bo[src] = 0.f;
+              for (int i = 0; i < 32; ++i) v[i] += t[i];
             }
-            if (st) x += st[src];
+          } else {
+            for (int j = a.xlo + 1; j < a.xhi; ++j) {
+              load32(xb + j * xstride, t);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] += t[i];
+            }
           }
-          v[i] = x;
+        } else if (bs) {
+          load32(bs, v);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0.f;
+        }
+        if (bo != nullptr) {  // the folded base alone (M_{1:t-1} for the cache), zeros when nothing was folded
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int c = c0 + i;
+            if (rowok && c < dim) bo[R.transpose ? (int64_t)c * dim + row : (int64_t)row * dim + c] = fold ? v[i] : 0.f;
+          }
+        }
+        if (st) {
+          load32(st, t);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] += t[i];
         }
         uint32_t r[32];
 #pragma unroll
@@ -470,6 +519,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       tc_fence_before();
       named_bar_sync(1, kEpi);
       if (et == 0) mbar_arrive(sst_ready);  // forward form: image of block 0; subtract form: seed landed
+      if (et == 0) span(2);
     }
     for (int jj = 0; jj < nblk; ++jj) {
       const int j = R.reverse ? nblk - 1 - jj : jj;
@@ -507,6 +557,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       named_bar_sync(1, kEpi);
       if (et == 0) mbar_arrive(p_ready);
       if (et == 0) tr(23, jj);
+      if (et == 0 && jj == 0) span(3);
       // ---- forward form: next block's state image
       if (!R.subtract && jj < nblk - 1) {
         mbar_wait(st_full, jj & 1);
@@ -537,8 +588,10 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
         for (int bx = 0; bx < nbox; ++bx) tma_store_3d(tm_o, pimg + bx * kBoxBytes, 64 * bx, orow, slot);
         tma_store_commit();
         tr(27, jj);
+        if (jj == 0) span(4);
       }
     }
+    if (et == 0) span(5);
     if constexpr (kMode == 3) {  // segment state G -> fp32 [slot][seg][dim][dim]
       if (nblk > 0) {
         mbar_wait(g_full, 0);
@@ -566,11 +619,13 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
     }
     if (et == 0) tma_store_wait_all<0>();
     if (et == 0) tr.flush(1);
+    if (et == 0) span(6);
   }
   tc_fence_before();
   if constexpr (kMode == 1) cluster_sync(); else __syncthreads();
   if (warp == 1) tmem_dealloc<512>(tmem);
-#ifndef LASP2_TRACE
+  if (threadIdx.x == 0) span(7);
+#if !defined(LASP2_TRACE) && !defined(LASP2_SPAN)
   if (g_trace != nullptr && threadIdx.x == 0) {
     unsigned long long t_end;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
