@@ -449,12 +449,14 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       // far as the compiler knows)
       const bool rowok = (int)row < dim;
       int c0_cur = cb;
-      auto load32 = [&](const float* base, float* dst) {  // dst[i] = element (row, c0 + i) of base
+      // nc: states written by earlier launches (read-only here): L1-cached loads, so a
+      // thread's 8 float4 of one row cost one L2 request, not eight. Peer buffers use .cg.
+      auto load32 = [&](const float* base, float* dst, bool nc) {  // dst[i] = element (row, c0 + i) of base
         if (!R.transpose && rowok && c0_cur + 32 <= dim) {
           const float4* p4 = reinterpret_cast<const float4*>(base + (int64_t)row * dim + c0_cur);
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
-            const float4 f = __ldcg(p4 + u);
+            const float4 f = nc ? __ldg(p4 + u) : __ldcg(p4 + u);
             dst[4 * u] = f.x;
             dst[4 * u + 1] = f.y;
             dst[4 * u + 2] = f.z;
@@ -464,9 +466,8 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const int c = c0_cur + i;
-            dst[i] = (rowok && c < dim)
-                         ? __ldcg(base + (R.transpose ? (int64_t)c * dim + row : (int64_t)row * dim + c))
-                         : 0.f;
+            const float* e = base + (R.transpose ? (int64_t)c * dim + row : (int64_t)row * dim + c);
+            dst[i] = (rowok && c < dim) ? (nc ? __ldg(e) : __ldcg(e)) : 0.f;
           }
         }
       };
@@ -476,22 +477,22 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
         float v[32], t[32];
         if (fold) {  // first term copied, the rest in rank order (numerics.py:71-116)
           const int first = a.xdesc ? a.xhi - 1 : a.xlo;
-          load32(xb + first * xstride, v);
+          load32(xb + first * xstride, v, false);
           if (a.xdesc) {
             for (int j = a.xhi - 2; j >= a.xlo; --j) {
-              load32(xb + j * xstride, t);
+              load32(xb + j * xstride, t, false);
 #pragma unroll
               for (int i = 0; i < 32; ++i) v[i] += t[i];
             }
           } else {
             for (int j = a.xlo + 1; j < a.xhi; ++j) {
-              load32(xb + j * xstride, t);
+              load32(xb + j * xstride, t, false);
 #pragma unroll
               for (int i = 0; i < 32; ++i) v[i] += t[i];
             }
           }
         } else if (bs) {
-          load32(bs, v);
+          load32(bs, v, true);
         } else {
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = 0.f;
@@ -504,7 +505,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
           }
         }
         if (st) {
-          load32(st, t);
+          load32(st, t, true);
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] += t[i];
         }
