@@ -107,9 +107,17 @@ __global__ void __launch_bounds__(192, 1)
       tmem_ld_32x32b_x32(tmem + ((qd * 32) << 16) + c0, r);
       tmem_ld_wait();
       if ((int)row < dim) {
+        float* orow = ob + (int64_t)row * dim + c0;
+        if (c0 + 32 <= dim && (dim & 3) == 0) {  // 16-byte stores: 8 per 32 columns instead of 32
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (c0 + i < dim) ob[(int64_t)row * dim + c0 + i] = __uint_as_float(r[i]);
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(orow + i) = make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]),
+                                                               __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (c0 + i < dim) orow[i] = __uint_as_float(r[i]);
+        }
       }
     }
   }
@@ -972,9 +980,17 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         tmem_ld_32x32b_x32(tmem + lane_off + c0, r);
         tmem_ld_wait();
         if ((int)row < dim) {
+          float* orow = ob + (int64_t)row * dim + c0;
+          if (c0 + 32 <= dim && (dim & 3) == 0) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (c0 + i < dim) ob[(int64_t)row * dim + c0 + i] = __uint_as_float(r[i]);
+            for (int i = 0; i < 32; i += 4)
+              *reinterpret_cast<float4*>(orow + i) = make_float4(
+                  __uint_as_float(r[i]), __uint_as_float(r[i + 1]), __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (c0 + i < dim) orow[i] = __uint_as_float(r[i]);
+          }
         }
       }
     }
