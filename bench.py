@@ -444,7 +444,8 @@ def run_gpu_arm(args) -> None:
         else:
             dist.init_process_group(args.dist_backend)
         peer = args.state_exchange == "peer"
-        ctx = comm.DistRankContext(peer_exchange=peer)
+        ctx = comm.DistRankContext(peer_exchange=peer,
+                                   native_collectives=args.state_exchange == "native" and args.dist_backend == "nccl")
         if peer:  # fused state exchange over NVLink peer memory
             from paper_2502_07563_b200 import lasp2 as _l2
             _l2.STATE_EXCHANGE = "peer"
@@ -502,8 +503,9 @@ def main() -> None:
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--balanced", action="store_true",
                     help="cfg4 (LASP-2H): causal load balance across ranks (standard_sp.BALANCED)")
-    ap.add_argument("--state-exchange", default="collective", choices=["collective", "peer"],
-                    help="N>1: NCCL all_gather of the states, or the fused put into symmetric-memory peers")
+    ap.add_argument("--state-exchange", default="collective", choices=["collective", "peer", "native"],
+                    help="N>1: torch.distributed NCCL all_gather of the states, the fused put into "
+                         "symmetric-memory peers, or NCCL through the C ABI's wrappers (native)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--eager", action="store_true", help="time eager launches instead of CUDA-graph replay")

@@ -32,7 +32,8 @@ extern "C" {
 #endif
 
 enum lasp2_dtype { LASP2_F32 = 0, LASP2_F64 = 1, LASP2_BF16 = 2 };
-enum lasp2_status { LASP2_OK = 0, LASP2_ERR_INVALID = 1, LASP2_ERR_CUDA = 2, LASP2_ERR_UNSUPPORTED = 3 };
+enum lasp2_status { LASP2_OK = 0, LASP2_ERR_INVALID = 1, LASP2_ERR_CUDA = 2, LASP2_ERR_UNSUPPORTED = 3,
+                    LASP2_ERR_COMM = 4 };
 enum lasp2_fold_mode { LASP2_FOLD_PREFIX = 0, LASP2_FOLD_SUFFIX = 1, LASP2_FOLD_FULL = 2 };
 
 /* ABI version (major*100 + minor). */
@@ -261,6 +262,34 @@ int lasp2_debug_probe_gemm(const void* a, const void* b, void* d, int a_mn, int 
 /* Test hook: record a clock64() timeline of CTA (0,0) of the causal kernels into
  * `buffer` (4096 x {event, block, clock} uint64; NULL disables). */
 int lasp2_debug_trace(void* buffer);
+
+/* ---- collectives on the caller's stream ----
+ * NCCL over NVLink; libnccl.so.2 is resolved at run time (the instance
+ * torch.distributed loaded, if any), so `comm` may be an ncclComm_t created
+ * here or by the host framework. LASP2_ERR_COMM + lasp2_last_error() on an
+ * NCCL failure; LASP2_ERR_INVALID if the library is absent. */
+/* ncclGetUniqueId into 128 bytes at id_out (rank 0 shares them out of band). */
+int lasp2_nccl_unique_id(void* id_out);
+/* ncclCommInitRank: *comm_out = communicator of `nranks` ranks, this one `rank`. */
+int lasp2_nccl_comm_init(void** comm_out, int nranks, const void* id, int rank);
+int lasp2_nccl_comm_destroy(void* comm);
+/* The state AllGather of every LASP-2 pass (RankContext.all_gather,
+ * comm.py:367-412, as called at lasp2.py:211/226/232/260/276): `count`
+ * elements of this rank's chunk state (pack_slots payload, shards.py:24-29)
+ * -> gathered [nranks][count], rank-major (what lasp2_fold_states reads).
+ * dtype = the element type moved (LASP2_F32 states for bf16/f32 data). */
+int lasp2_state_allgather(void* comm, int dtype, const void* state, void* gathered, int64_t count, void* stream);
+/* LASP-2H K and V AllGathers (standard_sp.py:40-41, two launches as in the
+ * reference ledger): `count` = slots*chunk*dim elements per rank -> the
+ * rank-major [nranks][slots][chunk][dim] layout the softmax kernels read. */
+int lasp2h_kv_allgather(void* comm, int dtype, const void* k_chunk, const void* v_chunk, void* k_full, void* v_full,
+                        int64_t count, void* stream);
+/* LASP-2H dK/dV exchange: ReduceScatter (sum) of the rank-major
+ * [nranks][2][slots][chunk][dim] contributions -> this rank's
+ * [2][slots][chunk][dim] (replaces the stacked all_gather + ascending sum of
+ * standard_sp.py:69-75; recv_count = 2*slots*chunk*dim). */
+int lasp2h_grad_reduce_scatter(void* comm, int dtype, const void* contrib, void* out, int64_t recv_count,
+                               void* stream);
 
 #ifdef __cplusplus
 }

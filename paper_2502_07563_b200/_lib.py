@@ -50,6 +50,12 @@ SIGNATURES = {
     "lasp2_nomask_forward_local": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _vp]),
     "lasp2_nomask_backward_local": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64,
                                            _int, _vp]),
+    "lasp2_nccl_unique_id": (_int, [_vp]),
+    "lasp2_nccl_comm_init": (_int, [_vp, _int, _vp, _int]),
+    "lasp2_nccl_comm_destroy": (_int, [_vp]),
+    "lasp2_state_allgather": (_int, [_vp, _int, _vp, _vp, _i64, _vp]),
+    "lasp2h_kv_allgather": (_int, [_vp, _int, _vp, _vp, _vp, _vp, _i64, _vp]),
+    "lasp2h_grad_reduce_scatter": (_int, [_vp, _int, _vp, _vp, _i64, _vp]),
     "lasp2_nomask_forward_phase": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp]),
     "lasp2_nomask_backward_phase": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64,
                                            _i64, _int, _int, _vp]),
@@ -125,7 +131,10 @@ KERNELS_PER_CALL = {"lasp2h_softmax_backward": 4,  # bf16 tc path: delta, memset
                     "lasp2h_softmax_backward_range": 4}
 _NO_LAUNCH = {"lasp2_version", "lasp2_last_error", "lasp2_num_segments", "lasp2h_softmax_scratch_bytes",
               "lasp2_local_workspace_bytes",
-              "lasp2_debug_trace"}
+              "lasp2_debug_trace",
+              # NCCL's kernels, not this library's
+              "lasp2_nccl_unique_id", "lasp2_nccl_comm_init", "lasp2_nccl_comm_destroy", "lasp2_state_allgather",
+              "lasp2h_kv_allgather", "lasp2h_grad_reduce_scatter"}
 
 
 def call(name: str, *args) -> int:

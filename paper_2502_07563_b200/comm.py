@@ -21,6 +21,7 @@ NCCL P2P under torchrun), ``mark(kind)``, ``stats`` (CommStats) and ``trace``.
 """
 from __future__ import annotations
 
+import ctypes
 import threading
 import time
 from collections import deque
@@ -639,6 +640,74 @@ class DistPending:
         return self._out
 
 
+class NcclComm:
+    """An NCCL communicator driven through the C ABI's collective wrappers
+    (lasp2_state_allgather, lasp2h_kv_allgather, lasp2h_grad_reduce_scatter;
+    SURVEY §8b). Every call is enqueued on the given (default: current) stream."""
+
+    def __init__(self, nranks: int, rank: int, unique_id: bytes) -> None:
+        from . import _lib
+
+        if len(unique_id) != 128:
+            raise ValueError("an NCCL unique id is 128 bytes")
+        self._lib = _lib
+        self.nranks, self.rank = nranks, rank
+        handle = ctypes.c_void_p()
+        uid = ctypes.create_string_buffer(bytes(unique_id), 128)
+        _lib.call("lasp2_nccl_comm_init", ctypes.addressof(handle), nranks, ctypes.addressof(uid), rank)
+        self.handle = handle.value
+
+    @staticmethod
+    def unique_id() -> bytes:
+        from . import _lib
+
+        buf = ctypes.create_string_buffer(128)
+        _lib.call("lasp2_nccl_unique_id", ctypes.addressof(buf))
+        return buf.raw
+
+    def _stream(self, stream) -> int:
+        return self._lib.stream_ptr(stream)
+
+    def all_gather(self, payload: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """[nranks, *payload.shape], rank-major (the state AllGather)."""
+        payload = payload.contiguous()
+        if out is None:
+            out = torch.empty((self.nranks, *payload.shape), dtype=payload.dtype, device=payload.device)
+        self._lib.call("lasp2_state_allgather", self.handle, self._lib.dtype_code(payload.dtype), payload.data_ptr(),
+                       out.data_ptr(), payload.numel(), self._stream(stream))
+        return out
+
+    def all_gather_kv(self, k: torch.Tensor, v: torch.Tensor, stream=None) -> tuple[torch.Tensor, torch.Tensor]:
+        """LASP-2H K and V gathers (two launches), each [nranks, *chunk.shape]."""
+        k, v = k.contiguous(), v.contiguous()
+        kf = torch.empty((self.nranks, *k.shape), dtype=k.dtype, device=k.device)
+        vf = torch.empty_like(kf)
+        self._lib.call("lasp2h_kv_allgather", self.handle, self._lib.dtype_code(k.dtype), k.data_ptr(), v.data_ptr(),
+                       kf.data_ptr(), vf.data_ptr(), k.numel(), self._stream(stream))
+        return kf, vf
+
+    def reduce_scatter(self, stacked: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """Sum over ranks of stacked[my rank] (stacked: [nranks, ...])."""
+        if stacked.shape[0] != self.nranks:
+            raise ValueError(f"reduce_scatter expects a leading axis of {self.nranks}, got {tuple(stacked.shape)}")
+        stacked = stacked.contiguous()
+        if out is None:
+            out = torch.empty(stacked.shape[1:], dtype=stacked.dtype, device=stacked.device)
+        self._lib.call("lasp2h_grad_reduce_scatter", self.handle, self._lib.dtype_code(stacked.dtype),
+                       stacked.data_ptr(), out.data_ptr(), out.numel(), self._stream(stream))
+        return out
+
+    def close(self) -> None:
+        if self.handle:
+            self._lib.call("lasp2_nccl_comm_destroy", self.handle)
+            self.handle = None
+
+
+class _Done:
+    def wait(self) -> None:
+        return None
+
+
 class DistRankContext(_ContextBase):
     """Rank context over an initialised torch.distributed default group.
 
@@ -648,7 +717,8 @@ class DistRankContext(_ContextBase):
 
     one_gpu_per_rank = True  # consumers may wait for peers inside their kernels
 
-    def __init__(self, sp_size: int | None = None, peer_exchange: bool = False) -> None:
+    def __init__(self, sp_size: int | None = None, peer_exchange: bool = False,
+                 native_collectives: bool = False) -> None:
         import torch.distributed as dist
 
         self._init_common()
@@ -672,6 +742,14 @@ class DistRankContext(_ContextBase):
                     self._group = pg
         self.trace: list[TraceEvent] = []
         self.comm_stream = torch.cuda.Stream() if torch.cuda.is_available() else None
+        # native_collectives: the state / K,V gathers and the dK,dV reduce-scatter go through
+        # the C ABI's NCCL wrappers on this context's own communicator (one per SP group)
+        self.nccl: NcclComm | None = None
+        if native_collectives:
+            leader = self.rank - self.rank % sp
+            uid = [NcclComm.unique_id() if self.rank == leader else None]
+            dist.broadcast_object_list(uid, src=leader, group=self._group)
+            self.nccl = NcclComm(sp, self.rank % sp, uid[0])
 
     @property
     def sp_position(self) -> int:
@@ -706,7 +784,11 @@ class DistRankContext(_ContextBase):
             self.comm_stream.wait_stream(cur)
             with torch.cuda.stream(self.comm_stream):
                 self._device_mark("all_gather_issue", self.comm_stream)
-                work = self.dist.all_gather_into_tensor(flat, payload, group=self._group, async_op=True)
+                if self.nccl is not None:
+                    self.nccl.all_gather(payload, out=out, stream=self.comm_stream)
+                    work = _Done()
+                else:
+                    work = self.dist.all_gather_into_tensor(flat, payload, group=self._group, async_op=True)
             if not torch.cuda.is_current_stream_capturing():
                 payload.record_stream(self.comm_stream)
                 flat.record_stream(self.comm_stream)
@@ -723,6 +805,8 @@ class DistRankContext(_ContextBase):
         stacked = stacked.contiguous()
         out = torch.empty(stacked.shape[1:], dtype=stacked.dtype, device=stacked.device)
         self._account("reduce_scatter", stacked)
+        if self.nccl is not None and stacked.is_cuda:
+            return self.nccl.reduce_scatter(stacked, out=out)
         flat_in = stacked.view(-1)
         self.dist.reduce_scatter_tensor(out.view(-1), flat_in, group=self._group)
         return out

@@ -3,6 +3,8 @@
 // Validation and dtype dispatch only: argument errors return
 // LASP2_ERR_INVALID, CUDA failures LASP2_ERR_CUDA, and lasp2_last_error()
 // carries the message. No exception crosses this boundary.
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the library is dlopen'd (below)
 #include <stdio.h>
 #include <string.h>
 
@@ -522,3 +524,124 @@ int lasp2_debug_probe_gemm(const void* a, const void* b, void* d, int a_mn, int 
 }
 
 }  // extern "C"
+
+// ---- collectives on a caller-provided stream ---------------------
+// NCCL is resolved at run time from libnccl.so.2 — the instance torch.distributed
+// already loaded when there is one, so a communicator can be shared with it —
+// and the library links no NCCL at build time.
+namespace {
+struct Nccl {
+  decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+  decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+  decltype(&ncclCommDestroy) comm_destroy = nullptr;
+  decltype(&ncclAllGather) all_gather = nullptr;
+  decltype(&ncclReduceScatter) reduce_scatter = nullptr;
+  decltype(&ncclGroupStart) group_start = nullptr;
+  decltype(&ncclGroupEnd) group_end = nullptr;
+  decltype(&ncclGetErrorString) error_string = nullptr;
+  bool ok = false;
+};
+
+const Nccl& nccl() {
+  static Nccl n = [] {
+    Nccl x;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (h == nullptr) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h == nullptr) return x;
+    x.get_unique_id = (decltype(x.get_unique_id))dlsym(h, "ncclGetUniqueId");
+    x.comm_init_rank = (decltype(x.comm_init_rank))dlsym(h, "ncclCommInitRank");
+    x.comm_destroy = (decltype(x.comm_destroy))dlsym(h, "ncclCommDestroy");
+    x.all_gather = (decltype(x.all_gather))dlsym(h, "ncclAllGather");
+    x.reduce_scatter = (decltype(x.reduce_scatter))dlsym(h, "ncclReduceScatter");
+    x.group_start = (decltype(x.group_start))dlsym(h, "ncclGroupStart");
+    x.group_end = (decltype(x.group_end))dlsym(h, "ncclGroupEnd");
+    x.error_string = (decltype(x.error_string))dlsym(h, "ncclGetErrorString");
+    x.ok = x.get_unique_id && x.comm_init_rank && x.comm_destroy && x.all_gather && x.reduce_scatter &&
+           x.group_start && x.group_end && x.error_string;
+    return x;
+  }();
+  return n;
+}
+
+int nccl_status(ncclResult_t r, const char* where) {
+  if (r == ncclSuccess) {
+    g_err.clear();
+    return LASP2_OK;
+  }
+  char buf[256];
+  snprintf(buf, sizeof(buf), "%s: %s", where, nccl().error_string(r));
+  g_err = buf;
+  return LASP2_ERR_COMM;
+}
+
+bool nccl_type(int dtype, ncclDataType_t* t) {
+  switch (dtype) {
+    case LASP2_F32: *t = ncclFloat32; return true;
+    case LASP2_F64: *t = ncclFloat64; return true;
+    case LASP2_BF16: *t = ncclBfloat16; return true;
+    default: return false;
+  }
+}
+}  // namespace
+
+#define NCCL_READY(name) CHECK(nccl().ok, name ": libnccl.so.2 not found")
+
+int lasp2_nccl_unique_id(void* id_out) {
+  NCCL_READY("nccl_unique_id");
+  CHECK(id_out, "nccl_unique_id: null pointer");
+  return nccl_status(nccl().get_unique_id(reinterpret_cast<ncclUniqueId*>(id_out)), "nccl_unique_id");
+}
+
+int lasp2_nccl_comm_init(void** comm_out, int nranks, const void* id, int rank) {
+  NCCL_READY("nccl_comm_init");
+  CHECK(comm_out && id, "nccl_comm_init: null pointer");
+  CHECK(nranks >= 1 && rank >= 0 && rank < nranks, "nccl_comm_init: bad rank / nranks");
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof(uid));
+  ncclComm_t c = nullptr;
+  const int st = nccl_status(nccl().comm_init_rank(&c, nranks, uid, rank), "nccl_comm_init");
+  *comm_out = c;
+  return st;
+}
+
+int lasp2_nccl_comm_destroy(void* comm) {
+  NCCL_READY("nccl_comm_destroy");
+  CHECK(comm, "nccl_comm_destroy: null communicator");
+  return nccl_status(nccl().comm_destroy((ncclComm_t)comm), "nccl_comm_destroy");
+}
+
+int lasp2_state_allgather(void* comm, int dtype, const void* state, void* gathered, int64_t count, void* stream) {
+  NCCL_READY("state_allgather");
+  ncclDataType_t t;
+  CHECK(nccl_type(dtype, &t), "state_allgather: unknown dtype");
+  CHECK(comm && state && gathered, "state_allgather: null pointer");
+  CHECK(count >= 1, "state_allgather: count must be positive");
+  return nccl_status(nccl().all_gather(state, gathered, (size_t)count, t, (ncclComm_t)comm, S(stream)),
+                     "state_allgather");
+}
+
+int lasp2h_kv_allgather(void* comm, int dtype, const void* k_chunk, const void* v_chunk, void* k_full, void* v_full,
+                        int64_t count, void* stream) {
+  NCCL_READY("kv_allgather");
+  ncclDataType_t t;
+  CHECK(nccl_type(dtype, &t), "kv_allgather: unknown dtype");
+  CHECK(comm && k_chunk && v_chunk && k_full && v_full, "kv_allgather: null pointer");
+  CHECK(count >= 1, "kv_allgather: count must be positive");
+  int st = nccl_status(nccl().all_gather(k_chunk, k_full, (size_t)count, t, (ncclComm_t)comm, S(stream)),
+                       "kv_allgather (K)");
+  if (st != LASP2_OK) return st;
+  return nccl_status(nccl().all_gather(v_chunk, v_full, (size_t)count, t, (ncclComm_t)comm, S(stream)),
+                     "kv_allgather (V)");
+}
+
+int lasp2h_grad_reduce_scatter(void* comm, int dtype, const void* contrib, void* out, int64_t recv_count,
+                               void* stream) {
+  NCCL_READY("grad_reduce_scatter");
+  ncclDataType_t t;
+  CHECK(nccl_type(dtype, &t), "grad_reduce_scatter: unknown dtype");
+  CHECK(comm && contrib && out, "grad_reduce_scatter: null pointer");
+  CHECK(recv_count >= 1, "grad_reduce_scatter: count must be positive");
+  return nccl_status(
+      nccl().reduce_scatter(contrib, out, (size_t)recv_count, t, ncclSum, (ncclComm_t)comm, S(stream)),
+      "grad_reduce_scatter");
+}
