@@ -339,8 +339,8 @@ def measure_workload(workload: str, ctx, rank: int, world: int, steps: int, warm
         ev = lambda: torch.cuda.Event()  # noqa: E731
         h2d_done, comp_done, d2h_done = [ev(), ev()], [ev(), ev()], [ev(), ev()]
         # the pipeline fills once and drains once per measurement (one H2D and one D2H not
-        # overlapped): 16 steps keep that to ~1/16 of the steady-state PCIe-bound period
-        e2e_steps = max(4, min(2 * steps, 16))
+        # overlapped): 32 steps keep that to ~1/32 of the steady-state PCIe-bound period
+        e2e_steps = max(4, min(2 * steps, 32))
         sync_all()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(h2d_s)
