@@ -109,7 +109,10 @@ int lasp2_causal_chunk(int dtype, const void* q, const void* k, const void* v, c
  * and seeds its state with it. base_out (causal_chunk_x, may be NULL)
  * receives the folded base ([slots][dim][dim], the cache's M_{1:t-1}). The
  * caller acknowledges the epoch afterwards (lasp2_exchange_ack). This removes
- * the wait and fold launches between the collective and its consumer. */
+ * the wait and fold launches between the collective and its consumer.
+ * xflags = NULL: no wait — `xrecv` is a complete rank-major all_gather result
+ * already ordered before `stream` (the NCCL path: the prefix / suffix fold of
+ * the gathered states fused into the consumer's prologue, no fold launch). */
 int lasp2_causal_chunk_x(const void* q, const void* k, const void* v, const void* seg_states, const void* xrecv,
                          const void* xflags, int lo, int hi, int descending, uint64_t epoch, void* base_out, void* out,
                          int64_t slots, int64_t tokens, int dim, int nseg, int reverse, int transpose_state,

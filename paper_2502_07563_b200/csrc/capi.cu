@@ -165,7 +165,7 @@ int lasp2_causal_chunk_x(const void* q, const void* k, const void* v, const void
                          const void* xflags, int lo, int hi, int descending, uint64_t epoch, void* base_out, void* out,
                          int64_t slots, int64_t tokens, int dim, int nseg, int reverse, int transpose_state,
                          void* stream) {
-  CHECK(q && k && v && out && xrecv && xflags, "causal_chunk_x: null pointer");
+  CHECK(q && k && v && out && xrecv, "causal_chunk_x: null pointer");
   CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128, "causal_chunk_x: bad shape (1 <= dim <= 128)");
   CHECK(nseg >= 1 && nseg <= (tokens + LASP_BLOCK_TOKENS - 1) / LASP_BLOCK_TOKENS, "causal_chunk_x: bad nseg");
   CHECK(nseg == 1 || seg_states, "causal_chunk_x: nseg > 1 needs segment states");
@@ -181,7 +181,7 @@ int lasp2_causal_chunk_x(const void* q, const void* k, const void* v, const void
 int lasp2_dkdv_chunk_x(const void* q, const void* k, const void* v, const void* d_out, const void* seg_states,
                        const void* xrecv, const void* xflags, int lo, int hi, uint64_t epoch, void* dk, void* dv,
                        int64_t slots, int64_t tokens, int dim, int nseg, void* stream) {
-  CHECK(q && k && v && d_out && dk && dv && xrecv && xflags, "dkdv_chunk_x: null pointer");
+  CHECK(q && k && v && d_out && dk && dv && xrecv, "dkdv_chunk_x: null pointer");
   CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128, "dkdv_chunk_x: bad shape (1 <= dim <= 128)");
   CHECK(nseg >= 1 && nseg <= (tokens + LASP_BLOCK_TOKENS - 1) / LASP_BLOCK_TOKENS, "dkdv_chunk_x: bad nseg");
   CHECK(nseg == 1 || seg_states, "dkdv_chunk_x: nseg > 1 needs segment states");

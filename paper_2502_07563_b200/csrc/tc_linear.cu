@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
         bs = a.base ? a.base + (int64_t)slot * dd : nullptr;
       }
       const bool fold = a.xrecv != nullptr && a.xhi > a.xlo;
-      if (a.xrecv != nullptr) {  // wait for the ranks this fold needs (the TMA / MMA warps run ahead)
+      if (a.xrecv != nullptr && a.xflags != nullptr) {  // wait for the ranks this fold needs (TMA / MMA run ahead)
         if (et == 0) {
           for (int j = a.xlo; j < a.xhi; ++j) {
             const long long t0 = clock64();

@@ -202,6 +202,21 @@ def _fused_consumer(ctx, x: torch.Tensor) -> bool:
             and 8 <= d <= 128 and d % 8 == 0)
 
 
+# True: with the all_gather (NCCL) path too, the bf16 chunk / dK-dV kernels fold the
+# prefix / suffix of the gathered states in their prologue (lasp2_causal_chunk_x /
+# lasp2_dkdv_chunk_x with no flags), so no fold launch sits between the collective and
+# its consumer. Off by default: every CTA of a slot then re-reads all T states of that
+# slot (9-18x the fold kernel's L2 traffic, a few serial L2 latencies per CTA), which
+# cost more than the fold launch it saves (cfg5 C = 8K per-rank step 0.170 -> 0.202 ms).
+# The peer exchange keeps its fused consumers: there the prologue wait hides the exchange.
+GATHERED_FUSED_CONSUMER = False
+
+
+def _gathered_consumer(x: torch.Tensor) -> bool:
+    d = x.shape[-1]
+    return GATHERED_FUSED_CONSUMER and x.dtype == torch.bfloat16 and 8 <= d <= 128 and d % 8 == 0
+
+
 def _share_total(ctx, seg: torch.Tensor, reverse: bool, data_dtype: torch.dtype, tag: str):
     """Scan the segment states; returns (chunk total, exchange handle or None)."""
     ex = _peer(ctx, tag, seg[:, :, 0])
@@ -298,9 +313,14 @@ def _forward_masked_rank(ctx, qc: torch.Tensor, kc: torch.Tensor, vc: torch.Tens
             ops.apply_state(qc, m_prefix, out=out, accumulate=True)
     else:
         gathered = _unpack_gathered(_gather_states(ctx, m_t, "state"), m_t)
-        m_prefix = ops.prefix_states(gathered, t)
-        ctx.mark("intra_start", f"chunk={t}")
-        out = ops.causal_chunk(qc, kc, vc, seg, m_prefix if t > 0 else None, nseg)
+        if _gathered_consumer(qc):  # the chunk kernel folds M_{1:t-1} from the gathered states itself
+            m_prefix = torch.empty_like(m_t)
+            ctx.mark("intra_start", f"chunk={t}")
+            out = ops.causal_chunk_gathered(qc, kc, vc, seg, gathered, t, nseg, base_out=m_prefix)
+        else:
+            m_prefix = ops.prefix_states(gathered, t)
+            ctx.mark("intra_start", f"chunk={t}")
+            out = ops.causal_chunk(qc, kc, vc, seg, m_prefix if t > 0 else None, nseg)
         ctx.mark("intra_end", f"chunk={t}")
     cache = ActivationCache(q=qc, k=kc, v=vc, masked=True, m_prefix=m_prefix, state_folds=1, seg_prefix=seg,
                             seg_total=m_t, nseg=nseg)
@@ -408,6 +428,9 @@ def _backward_masked_rank(ctx, cache: ActivationCache, d_out: torch.Tensor) -> G
             r = r if t < world - 1 else None
         else:
             gathered = _unpack_gathered(_gather_states(ctx, g_t, "state_grad"), g_t)
+            if _gathered_consumer(q):  # the dK/dV kernel folds the suffix of ranks > t itself
+                dk, dv = ops.dkdv_chunk_gathered(q, k, v, do, gseg, gathered, t + 1, nseg)
+                return GradientBundle(dq=dq, dk=dk, dv=dv)
             r = ops.suffix_states(gathered, t + 1) if t < world - 1 else None
         dk, dv = ops.dkdv_chunk(q, k, v, do, gseg, r, nseg)
         return GradientBundle(dq=dq, dk=dk, dv=dv)

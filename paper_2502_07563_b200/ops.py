@@ -110,6 +110,30 @@ def causal_chunk_x(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, seg_states
     return out
 
 
+def causal_chunk_gathered(q, k, v, seg_states, gathered: torch.Tensor, upto: int, nseg: int,
+                          base_out: torch.Tensor | None = None) -> torch.Tensor:
+    """causal_chunk whose base M_{1:upto} (ascending, copy-first) is folded in-kernel from
+    a complete rank-major all_gather result [T, ...] (lasp2_causal_chunk_x, xflags NULL)."""
+    require_cuda(q, k, v, seg_states, gathered, base_out)
+    slots, n, d = _slots(q)
+    out = torch.empty_like(q)
+    call("lasp2_causal_chunk_x", ptr(q), ptr(k), ptr(v), ptr(seg_states), ptr(gathered), None, 0, upto, 0, 0,
+         ptr(base_out), ptr(out), slots, n, d, nseg, 0, 0, stream_ptr())
+    return out
+
+
+def dkdv_chunk_gathered(q, k, v, d_out, seg_states, gathered: torch.Tensor, start: int,
+                        nseg: int) -> tuple[torch.Tensor, torch.Tensor]:
+    """dkdv_chunk whose base (suffix of ranks >= start, descending) is folded in-kernel from
+    a complete rank-major all_gather result (lasp2_dkdv_chunk_x, xflags NULL)."""
+    require_cuda(q, k, v, d_out, seg_states, gathered)
+    slots, n, d = _slots(q)
+    dk, dv = torch.empty_like(k), torch.empty_like(v)
+    call("lasp2_dkdv_chunk_x", ptr(q), ptr(k), ptr(v), ptr(d_out), ptr(seg_states), ptr(gathered), None, start,
+         gathered.shape[0], 0, ptr(dk), ptr(dv), slots, n, d, nseg, stream_ptr())
+    return dk, dv
+
+
 def dkdv_chunk_x(q, k, v, d_out, seg_states, ex, start: int, nseg: int) -> tuple[torch.Tensor, torch.Tensor]:
     """dkdv_chunk whose base (suffix of ranks >= start, descending) is folded in-kernel
     from the peer exchange (header: lasp2_dkdv_chunk_x); acknowledges the epoch."""

@@ -302,3 +302,22 @@ def test_unmasked_flat_phases_match_per_step_kernels(t, n, d, h, monkeypatch):
     refs = O.lasp2_full(*(to_np(x) for x in xs), t, False)  # f64 on the same bf16-rounded inputs
     for got, ref in zip(res[True], refs):
         assert O.normalized_error(to_np(got), ref) <= 1e-2
+
+
+@pytest.mark.parametrize("t", [2, 4])
+def test_gathered_fused_consumer_matches_fold_then_kernel(t, monkeypatch):
+    """bf16 masked, all_gather path: the chunk / dK-dV kernels folding the gathered
+    states in their prologue == fold launch + seeded kernel, bit for bit (same
+    copy-first order), with the same M_{1:t-1} in the cache."""
+    from paper_2502_07563_b200 import lasp2 as L
+    q, k, v, do = O.inputs(4096, 128, 1, 4, 31)
+    xs = [dev(x, torch.bfloat16) for x in (q, k, v, do)]
+    res = {}
+    for fused in (True, False):
+        monkeypatch.setattr(L, "GATHERED_FUSED_CONSUMER", fused)
+        it = lasp2_iteration(ChunkedSequence(*xs[:3], t), xs[3], True)
+        res[fused] = ([cat(it.outputs)] + [cat(getattr(g, n_) for g in it.grads) for n_ in ("dq", "dk", "dv")]
+                      + [c.m_prefix for c in it.caches])
+        assert it.run.stats.allgather_launches == 2
+    for a, b in zip(res[True], res[False]):
+        assert torch.equal(a, b)
