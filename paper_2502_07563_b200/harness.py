@@ -42,7 +42,7 @@ from dataclasses import asdict, dataclass
 
 import torch
 
-from . import comm, costmodel
+from . import __version__, comm, costmodel
 from .datagen import gen_slots_device
 from .hybrid import ModelSpec, hybrid_iteration, layer_weights
 from .lasp1 import lasp1_iteration
@@ -569,7 +569,7 @@ def cmd_verify(args) -> int:
     if args.out:
         try:
             with open(args.out, "w", encoding="utf-8") as fh:
-                json.dump({"runs": records}, fh, indent=2)
+                json.dump({"version": __version__, "runs": records}, fh, indent=2)
                 fh.write("\n")
         except OSError as exc:
             raise UsageError(f"cannot write {args.out}: {exc}") from exc
@@ -609,6 +609,7 @@ def _run_flags(p: argparse.ArgumentParser) -> None:
 def build_parser() -> argparse.ArgumentParser:
     parser = argparse.ArgumentParser(prog="paper_2502_07563_b200.harness",
                                      description="LASP-2 / LASP-2H on B200: verify, bench and cost tables.")
+    parser.add_argument("--version", action="version", version=f"%(prog)s {__version__}")
     sub = parser.add_subparsers(dest="command", required=True)
     p = sub.add_parser("verify", help="correctness checks; JSON report with --out")
     _run_flags(p)
