@@ -346,6 +346,8 @@ def _backward_nomask_rank(ctx, cache: ActivationCache, d_out: torch.Tensor) -> G
     When the all_gather is free (one rank) or cheap next to a pass over the
     chunk, dQ = dO M^T is fused into the dM segment pass (Q and dO read once);
     otherwise dQ runs while the collective is in flight. dK and dV share one pass.
+    With FLAT_PHASES (default) both passes are the persistent flat kernels split
+    around the exchange (lasp2_nomask_backward_phase).
     """
     _require_cache(cache, masked=False)
     (do,) = _contig(d_out)
