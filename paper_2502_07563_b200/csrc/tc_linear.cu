@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
     if (g_trace != nullptr) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      g_trace[8 * (blockIdx.y * gridDim.x + blockIdx.x) + i] = t;
+      g_trace[16 * (blockIdx.y * gridDim.x + blockIdx.x) + i] = t;
     }
   };
   if (threadIdx.x == 0) span(0);
@@ -436,6 +436,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
         bs = a.base ? a.base + (int64_t)slot * dd : nullptr;
       }
       const bool fold = a.xrecv != nullptr && a.xhi > a.xlo;
+      if (et == 0) span(12);  // epilogue start
       if (a.xrecv != nullptr && a.xflags != nullptr) {  // wait for the ranks this fold needs (TMA / MMA run ahead)
         if (et == 0) {
           for (int j = a.xlo; j < a.xhi; ++j) {
@@ -517,11 +518,13 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] += t[i];
         }
+        if (et == 0) span(8 + (c0 - cb) / 16);  // 8 / 10: chunk loaded
         uint32_t r[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(R.subtract ? -v[i] : v[i]);
         tmem_st_32x32b_x32(t_st + lane_off + c0, r);
         if (!R.subtract) st_row32_bf16(simg, row, c0, v);
+        if (et == 0) span(9 + (c0 - cb) / 16);  // 9 / 11: chunk stored
       }
       tmem_st_wait();
       fence_proxy_async_smem();

@@ -22,7 +22,7 @@ seg = ops.segment_states(k, v, nseg)
 ops.scan_segments(seg, False, k.dtype)
 dq, gseg = ops.dq_chunk(q, k, v, do, seg, None, nseg)
 ops.scan_segments(gseg, True, q.dtype)
-buf = torch.zeros(8 * 2 * nseg * h + 64, dtype=torch.int64, device="cuda")
+buf = torch.zeros(16 * 2 * nseg * h + 64, dtype=torch.int64, device="cuda")
 NAMES = ["prologue", "seed", "first P", "first O store", "rest of blocks", "store drain", "exit"]
 runs = {"causal_chunk": lambda: ops.causal_chunk(q, k, v, seg, None, nseg),
         "dq_chunk": lambda: ops.dq_chunk(q, k, v, do, seg, None, nseg),
@@ -35,10 +35,14 @@ for name, fn in runs.items():
     fn()
     torch.cuda.synchronize()
     _lib.call("lasp2_debug_trace", None)
-    t = buf.view(-1, 8).cpu().double()
+    t = buf.view(-1, 16).cpu().double()
     t = t[t[:, 0] > 0]
-    dt = (t[:, 1:] - t[:, :-1]) / 1e3
+    dt = (t[:, 1:8] - t[:, 0:7]) / 1e3
     med = dt.median(dim=0).values.tolist()
     tot = ((t[:, 7] - t[:, 0]) / 1e3).median().item()
     print(f"n={n} {name:13s} ctas={len(t)} median CTA {tot:.1f} us: " +
           "  ".join(f"{nm} {x:.1f}" for nm, x in zip(NAMES, med)))
+    # inside the seed: epilogue start, chunk 0 loaded / stored, chunk 1 loaded / stored (from span 1)
+    sub = [((t[:, i] - t[:, 1]) / 1e3).median().item() for i in (12, 8, 9, 10, 11, 2)]
+    print("      seed detail (us after prologue): epi start %.1f  c0 loaded %.1f  c0 stored %.1f  "
+          "c1 loaded %.1f  c1 stored %.1f  seed done %.1f" % tuple(sub))
