@@ -75,3 +75,41 @@ def test_dist_native_collectives_match_torch_and_local():
         native.nccl.close()
     finally:
         dist.destroy_process_group()
+
+
+def test_integration_stub_unmasked_rank_through_the_c_abi():
+    """INTEGRATION.md's T-rank unmasked forward through raw C-ABI calls (phase 1, the
+    NCCL state AllGather wrapper, the full fold, phase 2) on a one-rank world equals
+    the world-of-one persistent launch bit for bit."""
+    import ctypes
+
+    from paper_2502_07563_b200 import _lib, ops
+
+    lib = _lib.load()
+    stream = torch.cuda.current_stream().cuda_stream
+    q, k, v = (gen_slots_device(0, 1, 4, 4096, 128, t) for t in ("q", "k", "v"))
+    b, h, c, d = q.shape
+    ws = ops.local_workspace(q)
+    uid = ctypes.create_string_buffer(128)
+    assert lib.lasp2_nccl_unique_id(ctypes.addressof(uid)) == 0
+    handle = ctypes.c_void_p()
+    assert lib.lasp2_nccl_comm_init(ctypes.addressof(handle), 1, ctypes.addressof(uid), 0) == 0
+    try:
+        m_t = torch.empty((b, h, d, d), dtype=torch.float32, device="cuda")
+        assert lib.lasp2_nomask_forward_phase(_lib.BF16, None, k.data_ptr(), v.data_ptr(), None, m_t.data_ptr(),
+                                              ws.data_ptr(), ws.numel(), b * h, c, d, 1, stream) == 0
+        gathered = torch.empty((1, b, h, d, d), dtype=torch.float32, device="cuda")
+        assert lib.lasp2_state_allgather(handle.value, _lib.F32, m_t.data_ptr(), gathered.data_ptr(), m_t.numel(),
+                                         stream) == 0
+        m_full = torch.empty_like(m_t)
+        assert lib.lasp2_fold_states(_lib.F32, gathered.data_ptr(), m_full.data_ptr(), 1, m_full.numel(), 2, 0,
+                                     stream) == 0
+        out = torch.empty_like(q)
+        assert lib.lasp2_nomask_forward_phase(_lib.BF16, q.data_ptr(), None, None, out.data_ptr(),
+                                              m_full.data_ptr(), ws.data_ptr(), ws.numel(), b * h, c, d, 2,
+                                              stream) == 0
+        ref_out, ref_m = ops.nomask_forward_local(q, k, v)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref_out) and torch.equal(m_full, ref_m)
+    finally:
+        lib.lasp2_nccl_comm_destroy(handle.value)
