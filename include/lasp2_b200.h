@@ -223,6 +223,15 @@ int lasp2_nomask_backward_phase(int dtype, const void* q, const void* k, const v
 int lasp2h_softmax_forward(int dtype, const void* q, const void* k_full, const void* v_full, void* out, void* lse,
                            int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim, int causal, int64_t row_offset,
                            int64_t kv_chunk, int64_t kv_rank_stride, void* stream);
+/* The same over the key range [kv_start, kv_start + kv_tokens) of the
+ * rank-major layout (k_full / v_full still point at rank 0; kv_tokens need not
+ * be a multiple of kv_chunk; row_offset is relative to kv_start; the bf16 path
+ * needs kv_start % 128 == 0). The balanced LASP-2H schedule's half-chunk
+ * splits; no reference counterpart. */
+int lasp2h_softmax_forward_range(int dtype, const void* q, const void* k_full, const void* v_full, void* out,
+                                 void* lse, int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim, int causal,
+                                 int64_t row_offset, int64_t kv_chunk, int64_t kv_rank_stride, int64_t kv_start,
+                                 void* stream);
 
 /* Gradients of <d_out, softmax_chunk_forward(...)>: dq for the chunk and this
  * chunk's full-length dk/dv contributions (accumulate dtype: f32 for bf16/f32,
@@ -241,12 +250,14 @@ int lasp2h_softmax_backward(int dtype, const void* q, const void* k_full, const 
  * final O, so partial dQ and dK/dV contributions of disjoint ranges add up
  * to the full gradients. Identical to lasp2h_softmax_backward on the bf16
  * tensor-core path; the f32/f64 path would otherwise renormalise over its
- * range. lse must be given (states dtype). */
+ * range. lse must be given (states dtype). The keys are [kv_start, kv_start +
+ * kv_tokens) of the rank-major layout as in lasp2h_softmax_forward_range (dk /
+ * dv land at the absolute key index). */
 int lasp2h_softmax_backward_range(int dtype, const void* q, const void* k_full, const void* v_full, const void* out,
                                   const void* lse, const void* d_out, void* dq, void* dk_full, void* dv_full,
                                   void* scratch, int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim,
                                   int causal, int64_t row_offset, int64_t kv_chunk, int64_t kv_rank_stride,
-                                  int64_t grad_rank_stride, void* stream);
+                                  int64_t grad_rank_stride, int64_t kv_start, void* stream);
 int64_t lasp2h_softmax_scratch_bytes(int dtype, int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim);
 
 /* Deterministic inputs: out[slot] = rows [row_offset, row_offset+rows) of

@@ -59,12 +59,14 @@ SIGNATURES = {
     "lasp2_nomask_forward_phase": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _vp]),
     "lasp2_nomask_backward_phase": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64,
                                            _i64, _int, _int, _vp]),
+    "lasp2h_softmax_forward_range": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _i64,
+                                            _i64, _i64, _i64, _vp]),
     "lasp2h_softmax_forward": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _int, _i64, _i64, _i64,
                                       _vp]),
     "lasp2h_softmax_backward": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int,
                                        _int, _i64, _i64, _i64, _i64, _vp]),
     "lasp2h_softmax_backward_range": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64,
-                                             _i64, _int, _int, _i64, _i64, _i64, _i64, _vp]),
+                                             _i64, _int, _int, _i64, _i64, _i64, _i64, _i64, _vp]),
     "lasp2h_softmax_scratch_bytes": (_i64, [_int, _i64, _i64, _i64, _int]),
     "lasp2_gen_slots": (_int, [_int, _u64, _vp, _vp, _i64, _i64, _i64, _i64, _vp]),
     "lasp2_debug_probe_gemm": (_int, [_vp, _vp, _vp, _int, _int, _vp]),

@@ -404,29 +404,47 @@ int lasp2_nomask_backward_phase(int dtype, const void* q, const void* k, const v
   return st;
 }
 
-int lasp2h_softmax_forward(int dtype, const void* q, const void* k_full, const void* v_full, void* out, void* lse,
-                           int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim, int causal, int64_t row_offset,
-                           int64_t kv_chunk, int64_t kv_rank_stride, void* stream) {
+static int softmax_forward_impl(int dtype, const void* q, const void* k_full, const void* v_full, void* out,
+                                void* lse, int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim, int causal,
+                                int64_t row_offset, int64_t kv_chunk, int64_t kv_rank_stride, int64_t kv_start,
+                                void* stream) {
   CHECK(valid_dtype(dtype), "softmax_forward: unknown dtype");
   CHECK(q && k_full && v_full && out && lse, "softmax_forward: null pointer");
   CHECK(slots >= 1 && q_tokens >= 1 && kv_tokens >= 1 && dim >= 1 && dim <= 128, "softmax_forward: bad shape");
   CHECK(row_offset >= 0 && (!causal || row_offset < kv_tokens), "softmax_forward: bad row_offset");
-  CHECK(kv_chunk >= 1 && kv_tokens % kv_chunk == 0, "softmax_forward: kv_chunk must divide kv_tokens");
+  CHECK(kv_chunk >= 1 && kv_start >= 0, "softmax_forward: bad kv_chunk / kv_start");
+  const bool tc = dtype == LASP2_BF16 && lasp::tc_softmax_supported(dim, kv_chunk);
+  CHECK(!tc || kv_start % 128 == 0, "softmax_forward: the bf16 path needs kv_start % 128 == 0");
   cudaError_t e;
-  if (dtype == LASP2_BF16 && lasp::tc_softmax_supported(dim, kv_chunk))
+  if (tc)
     e = lasp::tc_softmax_forward(q, k_full, v_full, out, (float*)lse, slots, q_tokens, kv_tokens, dim, causal,
-                                 row_offset, kv_chunk, kv_rank_stride, S(stream));
+                                 row_offset, kv_chunk, kv_rank_stride, S(stream), kv_start);
   else if (dtype == LASP2_F32)
     e = lasp::simt_softmax_forward<float, float>(q, k_full, v_full, out, lse, slots, q_tokens, kv_tokens, dim,
-                                                 causal, row_offset, kv_chunk, kv_rank_stride, S(stream));
+                                                 causal, row_offset, kv_chunk, kv_rank_stride, S(stream), kv_start);
   else if (dtype == LASP2_F64)
-    e = lasp::simt_softmax_forward<double, double>(q, k_full, v_full, out, lse, slots, q_tokens, kv_tokens,
-                                                   dim, causal, row_offset, kv_chunk, kv_rank_stride, S(stream));
+    e = lasp::simt_softmax_forward<double, double>(q, k_full, v_full, out, lse, slots, q_tokens, kv_tokens, dim,
+                                                   causal, row_offset, kv_chunk, kv_rank_stride, S(stream), kv_start);
   else
-    e = lasp::simt_softmax_forward<__nv_bfloat16, float>(q, k_full, v_full, out, lse, slots, q_tokens,
-                                                         kv_tokens, dim, causal, row_offset, kv_chunk, kv_rank_stride,
-                                                         S(stream));
+    e = lasp::simt_softmax_forward<__nv_bfloat16, float>(q, k_full, v_full, out, lse, slots, q_tokens, kv_tokens,
+                                                         dim, causal, row_offset, kv_chunk, kv_rank_stride, S(stream),
+                                                         kv_start);
   return cuda_status(e, "softmax_forward");
+}
+
+int lasp2h_softmax_forward(int dtype, const void* q, const void* k_full, const void* v_full, void* out, void* lse,
+                           int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim, int causal, int64_t row_offset,
+                           int64_t kv_chunk, int64_t kv_rank_stride, void* stream) {
+  return softmax_forward_impl(dtype, q, k_full, v_full, out, lse, slots, q_tokens, kv_tokens, dim, causal, row_offset,
+                              kv_chunk, kv_rank_stride, 0, stream);
+}
+
+int lasp2h_softmax_forward_range(int dtype, const void* q, const void* k_full, const void* v_full, void* out,
+                                 void* lse, int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim, int causal,
+                                 int64_t row_offset, int64_t kv_chunk, int64_t kv_rank_stride, int64_t kv_start,
+                                 void* stream) {
+  return softmax_forward_impl(dtype, q, k_full, v_full, out, lse, slots, q_tokens, kv_tokens, dim, causal, row_offset,
+                              kv_chunk, kv_rank_stride, kv_start, stream);
 }
 
 int64_t lasp2h_softmax_scratch_bytes(int dtype, int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim) {
@@ -444,7 +462,7 @@ static int softmax_backward_impl(bool range, int dtype, const void* q, const voi
                             const void* lse, const void* d_out, void* dq, void* dk_full, void* dv_full, void* scratch,
                             int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim, int causal,
                             int64_t row_offset, int64_t kv_chunk, int64_t kv_rank_stride, int64_t grad_rank_stride,
-                            void* stream) {
+                            int64_t kv_start, void* stream) {
   CHECK(!range || lse, "softmax_backward_range: needs the forward's lse of the whole key set");
   const void* lse_range = range ? lse : nullptr;
   CHECK(valid_dtype(dtype), "softmax_backward: unknown dtype");
@@ -452,27 +470,30 @@ static int softmax_backward_impl(bool range, int dtype, const void* q, const voi
         "softmax_backward: null pointer");
   CHECK(slots >= 1 && q_tokens >= 1 && kv_tokens >= 1 && dim >= 1 && dim <= 128, "softmax_backward: bad shape");
   CHECK(row_offset >= 0 && (!causal || row_offset < kv_tokens), "softmax_backward: bad row_offset");
-  CHECK(kv_chunk >= 1 && kv_tokens % kv_chunk == 0, "softmax_backward: kv_chunk must divide kv_tokens");
+  CHECK(kv_chunk >= 1 && kv_start >= 0, "softmax_backward: bad kv_chunk / kv_start");
+  const bool tc = dtype == LASP2_BF16 && lasp::tc_softmax_supported(dim, kv_chunk);
+  CHECK(!tc || kv_start % 128 == 0, "softmax_backward: the bf16 path needs kv_start % 128 == 0");
   cudaError_t e;
-  if (dtype == LASP2_BF16 && lasp::tc_softmax_supported(dim, kv_chunk)) {
+  if (tc) {
     CHECK(lse, "softmax_backward: the bf16 path needs the forward's lse");
     e = lasp::tc_softmax_backward(q, k_full, v_full, out, (const float*)lse, d_out, dq, (float*)dk_full,
                                   (float*)dv_full, scratch, slots, q_tokens, kv_tokens, dim, causal, row_offset,
-                                  kv_chunk, kv_rank_stride, grad_rank_stride, S(stream));
+                                  kv_chunk, kv_rank_stride, grad_rank_stride, S(stream), kv_start);
   } else if (dtype == LASP2_F32)
     e = lasp::simt_softmax_backward<float, float, float>(q, k_full, v_full, out, d_out, dq, dk_full, dv_full, scratch,
                                                          slots, q_tokens, kv_tokens, dim, causal, row_offset,
-                                                         kv_chunk, kv_rank_stride, grad_rank_stride, S(stream), lse_range);
+                                                         kv_chunk, kv_rank_stride, grad_rank_stride, S(stream), lse_range,
+                                                         kv_start);
   else if (dtype == LASP2_F64)
     e = lasp::simt_softmax_backward<double, double, double>(q, k_full, v_full, out, d_out, dq, dk_full, dv_full,
                                                             scratch, slots, q_tokens, kv_tokens, dim, causal,
                                                             row_offset, kv_chunk, kv_rank_stride, grad_rank_stride,
-                                                            S(stream), lse_range);
+                                                            S(stream), lse_range, kv_start);
   else
     e = lasp::simt_softmax_backward<__nv_bfloat16, float, float>(q, k_full, v_full, out, d_out, dq, dk_full, dv_full,
                                                                  scratch, slots, q_tokens, kv_tokens, dim, causal,
                                                                  row_offset, kv_chunk, kv_rank_stride, grad_rank_stride,
-                                                                 S(stream), lse_range);
+                                                                 S(stream), lse_range, kv_start);
   return cuda_status(e, "softmax_backward");
 }
 int lasp2h_softmax_backward(int dtype, const void* q, const void* k_full, const void* v_full, const void* out,
@@ -482,17 +503,17 @@ int lasp2h_softmax_backward(int dtype, const void* q, const void* k_full, const 
                             void* stream) {
   return softmax_backward_impl(false, dtype, q, k_full, v_full, out, lse, d_out, dq, dk_full, dv_full, scratch, slots,
                                q_tokens, kv_tokens, dim, causal, row_offset, kv_chunk, kv_rank_stride,
-                               grad_rank_stride, stream);
+                               grad_rank_stride, 0, stream);
 }
 
 int lasp2h_softmax_backward_range(int dtype, const void* q, const void* k_full, const void* v_full, const void* out,
                                   const void* lse, const void* d_out, void* dq, void* dk_full, void* dv_full,
                                   void* scratch, int64_t slots, int64_t q_tokens, int64_t kv_tokens, int dim,
                                   int causal, int64_t row_offset, int64_t kv_chunk, int64_t kv_rank_stride,
-                                  int64_t grad_rank_stride, void* stream) {
+                                  int64_t grad_rank_stride, int64_t kv_start, void* stream) {
   return softmax_backward_impl(true, dtype, q, k_full, v_full, out, lse, d_out, dq, dk_full, dv_full, scratch, slots,
                                q_tokens, kv_tokens, dim, causal, row_offset, kv_chunk, kv_rank_stride,
-                               grad_rank_stride, stream);
+                               grad_rank_stride, kv_start, stream);
 }
 
 

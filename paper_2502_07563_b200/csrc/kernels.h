@@ -19,13 +19,13 @@ cudaError_t simt_apply_state(const void* x, const void* m, void* out, int64_t sl
 template <typename T, typename A>
 cudaError_t simt_softmax_forward(const void* q, const void* kf, const void* vf, void* out, void* lse, int64_t slots,
                                  int64_t qtok, int64_t kvtok, int dim, int causal, int64_t row_offset, int64_t kv_chunk,
-                                 int64_t kv_rank_stride, cudaStream_t s);
+                                 int64_t kv_rank_stride, cudaStream_t s, int64_t kv_start = 0);
 template <typename T, typename A, typename G>
 cudaError_t simt_softmax_backward(const void* q, const void* kf, const void* vf, const void* o, const void* d_out,
                                   void* dq, void* dk_full, void* dv_full, void* scratch, int64_t slots, int64_t qtok,
                                   int64_t kvtok, int dim, int causal, int64_t row_offset, int64_t kv_chunk,
                                   int64_t kv_rank_stride, int64_t grad_rank_stride, cudaStream_t s,
-                                  const void* lse = nullptr);
+                                  const void* lse = nullptr, int64_t kv_start = 0);
 
 // shared state reductions / datagen
 template <typename A>
@@ -72,12 +72,13 @@ cudaError_t tc_apply_state(const void* x, const float* m, void* out, int64_t slo
 bool tc_softmax_supported(int dim, int64_t kv_chunk);
 cudaError_t tc_softmax_forward(const void* q, const void* kf, const void* vf, void* out, float* lse, int64_t slots,
                                int64_t qtok, int64_t kvtok, int dim, int causal, int64_t row_offset, int64_t kv_chunk,
-                               int64_t kv_rank_stride, cudaStream_t s);
+                               int64_t kv_rank_stride, cudaStream_t s, int64_t kv_start = 0);
 int64_t tc_softmax_bwd_scratch(int64_t slots, int64_t qtok, int dim);
 cudaError_t tc_softmax_backward(const void* q, const void* kf, const void* vf, const void* o, const float* lse,
                                 const void* d_out, void* dq, float* dk_full, float* dv_full, void* scratch,
                                 int64_t slots, int64_t qtok, int64_t kvtok, int dim, int causal, int64_t row_offset,
-                                int64_t kv_chunk, int64_t kv_rank_stride, int64_t grad_rank_stride, cudaStream_t s);
+                                int64_t kv_chunk, int64_t kv_rank_stride, int64_t grad_rank_stride, cudaStream_t s,
+                                int64_t kv_start = 0);
 cudaError_t softmax_delta_bf16(const void* o, const void* d_out, float* delta, int64_t rows, int dim,
                                cudaStream_t s);
 cudaError_t tc_backward_triple(const void* q, const void* k, const void* v, const void* d_out, const float* fwd_seg,

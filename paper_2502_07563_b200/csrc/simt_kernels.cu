@@ -241,11 +241,14 @@ __device__ __forceinline__ A block_reduce_max(A v, A* red) {
 // collectives produce them: key j of slot lives at
 //   (j / chunk) * rank_stride + slot * chunk * dim + (j % chunk) * dim.
 // chunk == kvtok with rank_stride == 0 is the plain [slots][kvtok][dim] layout.
+// `start` offsets a key range inside that layout: the call's key j is key start + j.
 struct KvLayout {
   int64_t chunk;
   int64_t rank_stride;
+  int64_t start;
   __device__ __forceinline__ int64_t row(int64_t slot, int64_t j, int dim) const {
-    return (j / chunk) * rank_stride + (slot * chunk + (j % chunk)) * dim;
+    const int64_t a = j + start;
+    return (a / chunk) * rank_stride + (slot * chunk + (a % chunk)) * dim;
   }
 };
 
@@ -554,8 +557,8 @@ cudaError_t simt_apply_state(const void* x, const void* m, void* out, int64_t sl
 template <typename T, typename A>
 cudaError_t simt_softmax_forward(const void* q, const void* kf, const void* vf, void* out, void* lse, int64_t slots,
                                  int64_t qtok, int64_t kvtok, int dim, int causal, int64_t row_offset, int64_t kv_chunk,
-                                 int64_t kv_rank_stride, cudaStream_t s) {
-  const KvLayout kl{kv_chunk, kv_rank_stride};
+                                 int64_t kv_rank_stride, cudaStream_t s, int64_t kv_start) {
+  const KvLayout kl{kv_chunk, kv_rank_stride, kv_start};
   const size_t smem = (size_t)(dim + kSmKeys + 32) * sizeof(A);
   dim3 grid((unsigned)qtok, (unsigned)slots);
   simt_softmax_fwd_kernel<T, A><<<grid, kSmThreads, smem, s>>>((const T*)q, (const T*)kf, (const T*)vf, (T*)out,
@@ -567,8 +570,9 @@ template <typename T, typename A, typename G>
 cudaError_t simt_softmax_backward(const void* q, const void* kf, const void* vf, const void* o, const void* d_out,
                                   void* dq, void* dk_full, void* dv_full, void* scratch, int64_t slots, int64_t qtok,
                                   int64_t kvtok, int dim, int causal, int64_t row_offset, int64_t kv_chunk,
-                                  int64_t kv_rank_stride, int64_t grad_rank_stride, cudaStream_t s, const void* lse) {
-  const KvLayout kl{kv_chunk, kv_rank_stride}, gl{kv_chunk, grad_rank_stride};
+                                  int64_t kv_rank_stride, int64_t grad_rank_stride, cudaStream_t s, const void* lse,
+                                  int64_t kv_start) {
+  const KvLayout kl{kv_chunk, kv_rank_stride, kv_start}, gl{kv_chunk, grad_rank_stride, kv_start};
   A* delta = reinterpret_cast<A*>(scratch);
   A* mx = delta + slots * qtok;
   A* sm = mx + slots * qtok;
@@ -615,23 +619,23 @@ cudaError_t softmax_delta_bf16(const void* o, const void* d_out, float* delta, i
                                               cudaStream_t);                                                    \
   template cudaError_t simt_softmax_forward<T, A>(const void*, const void*, const void*, void*, void*, int64_t, \
                                                   int64_t, int64_t, int, int, int64_t, int64_t, int64_t,         \
-                                                  cudaStream_t);
+                                                  cudaStream_t, int64_t);
 LASP_INST(float, float)
 LASP_INST(double, double)
 LASP_INST(__nv_bfloat16, float)
 template cudaError_t simt_softmax_backward<float, float, float>(const void*, const void*, const void*, const void*,
                                                                 const void*, void*, void*, void*, void*, int64_t,
                                                                 int64_t, int64_t, int, int, int64_t, int64_t, int64_t,
-                                                                int64_t, cudaStream_t, const void*);
+                                                                int64_t, cudaStream_t, const void*, int64_t);
 template cudaError_t simt_softmax_backward<double, double, double>(const void*, const void*, const void*,
                                                                    const void*, const void*, void*, void*, void*,
                                                                    void*, int64_t, int64_t, int64_t, int, int,
                                                                    int64_t, int64_t, int64_t, int64_t, cudaStream_t,
-                                                                   const void*);
+                                                                   const void*, int64_t);
 template cudaError_t simt_softmax_backward<__nv_bfloat16, float, float>(const void*, const void*, const void*,
                                                                         const void*, const void*, void*, void*,
                                                                         void*, void*, int64_t, int64_t, int64_t,
                                                                         int, int, int64_t, int64_t, int64_t, int64_t,
-                                                                        cudaStream_t, const void*);
+                                                                        cudaStream_t, const void*, int64_t);
 
 }  // namespace lasp

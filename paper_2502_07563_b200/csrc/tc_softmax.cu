@@ -35,6 +35,7 @@ struct SmFwdArgs {
   int dim;
   int causal;
   float scale_log2;  // log2(e) / sqrt(d)
+  int64_t kv_start;  // the call's key j is key kv_start + j of the rank-major layout (multiple of 128)
 };
 
 __device__ __forceinline__ void kv_coords(int64_t key0, int64_t chunk, int* row, int* rank) {
@@ -93,7 +94,7 @@ __global__ void __launch_bounds__(kSmFwdThreads, 1)
       for (int bx = 0; bx < nbox; ++bx) tma_load_3d(qimg + bx * kBoxBytes, &tm_q, q_full, 64 * bx, (int)q0, slot);
       for (int j = 0; j < nkb; ++j) {
         int row, rank;
-        kv_coords((int64_t)j * kTile, a.chunk, &row, &rank);
+        kv_coords((int64_t)j * kTile + a.kv_start, a.chunk, &row, &rank);
         for (int w = 0; w < 2; ++w) {
           const int t = 2 * j + w, s = t % kKvRing, u = t / kKvRing;
           if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
@@ -352,7 +353,7 @@ __global__ void __launch_bounds__(kSmFwdThreads, 1)
           tma_load_3d(qimg + t * kTileBytes + bx * kBoxBytes, &tm_q, q_full, 64 * bx, (2 * pair + t) * kTile, slot);
       for (int j = 0; j < nkb; ++j) {
         int row, rank;
-        kv_coords((int64_t)j * kTile, a.chunk, &row, &rank);
+        kv_coords((int64_t)j * kTile + a.kv_start, a.chunk, &row, &rank);
         for (int w = 0; w < 2; ++w) {
           const int t = 2 * j + w, s = t % kF2Ring, u = t / kF2Ring;
           if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
@@ -565,6 +566,7 @@ struct SmBwdArgs {
   int causal;
   float scale;       // 1/sqrt(d)
   float scale_log2;  // log2(e)/sqrt(d)
+  int64_t kv_start;  // as SmFwdArgs::kv_start (dk/dv land at the absolute key)
 };
 
 // P and dS of this thread's row (64 columns from c0) as packed bf16 pairs -> SW128 image
@@ -635,7 +637,7 @@ __global__ void __launch_bounds__(kSmBwdThreads, 1)
       prefetch_tmap(&tm_q);
       prefetch_tmap(&tm_do);
       int row, rank;
-      kv_coords(k0, a.chunk, &row, &rank);
+      kv_coords(k0 + a.kv_start, a.chunk, &row, &rank);
       mbar_arrive_expect_tx(kv_full, 2 * nbox * kBoxBytes);
       for (int bx = 0; bx < nbox; ++bx) {
         tma_load_4d(kimg + bx * kBoxBytes, &tm_k, kv_full, 64 * bx, row, slot, rank);
@@ -838,7 +840,8 @@ __global__ void __launch_bounds__(kSmBwdThreads, 1)
     tc_fence_after();
     const int64_t key = k0 + row;
     if (key < a.kvtok) {
-      const int64_t off = (key / a.chunk) * a.grad_rank_stride + ((int64_t)slot * a.chunk + key % a.chunk) * a.dim;
+      const int64_t ka = key + a.kv_start;
+      const int64_t off = (ka / a.chunk) * a.grad_rank_stride + ((int64_t)slot * a.chunk + ka % a.chunk) * a.dim;
       float* dkr = a.dk_full + off;
       float* dvr = a.dv_full + off;
       if (nq == 0) {
@@ -890,15 +893,16 @@ bool tc_softmax_supported(int dim, int64_t kv_chunk) {
 
 cudaError_t tc_softmax_forward(const void* q, const void* kf, const void* vf, void* out, float* lse, int64_t slots,
                                int64_t qtok, int64_t kvtok, int dim, int causal, int64_t row_offset, int64_t kv_chunk,
-                               int64_t kv_rank_stride, cudaStream_t s) {
+                               int64_t kv_rank_stride, cudaStream_t s, int64_t kv_start) {
   CUtensorMap mq, mk, mv, mo;
   cudaError_t e;
-  const int64_t ranks = kvtok / kv_chunk;
+  const int64_t ranks = (kv_start + kvtok + kv_chunk - 1) / kv_chunk;
   if ((e = make_tmap_3d(&mq, q, slots, qtok, dim)) != cudaSuccess) return e;
   if ((e = make_tmap_4d(&mk, kf, ranks, slots, kv_chunk, dim, kv_rank_stride)) != cudaSuccess) return e;
   if ((e = make_tmap_4d(&mv, vf, ranks, slots, kv_chunk, dim, kv_rank_stride)) != cudaSuccess) return e;
   if ((e = make_tmap_3d(&mo, out, slots, qtok, dim)) != cudaSuccess) return e;
-  tc::SmFwdArgs a{lse, qtok, kvtok, kv_chunk, row_offset, dim, causal, 1.4426950408889634f / sqrtf((float)dim)};
+  tc::SmFwdArgs a{lse, qtok, kvtok, kv_chunk, row_offset, dim, causal, 1.4426950408889634f / sqrtf((float)dim),
+                  kv_start};
   static const bool one_tile = std::getenv("LASP2_SOFTMAX_FWD1") != nullptr;  // previous kernel, for comparison
   if (one_tile) {
     if ((e = set_smem_once((const void*)tc::tc_softmax_fwd_kernel, tc::kSmFwdSmem)) != cudaSuccess) return e;
@@ -920,13 +924,14 @@ int64_t tc_softmax_bwd_scratch(int64_t slots, int64_t qtok, int dim) {
 cudaError_t tc_softmax_backward(const void* q, const void* kf, const void* vf, const void* o, const float* lse,
                                 const void* d_out, void* dq, float* dk_full, float* dv_full, void* scratch,
                                 int64_t slots, int64_t qtok, int64_t kvtok, int dim, int causal, int64_t row_offset,
-                                int64_t kv_chunk, int64_t kv_rank_stride, int64_t grad_rank_stride, cudaStream_t s) {
+                                int64_t kv_chunk, int64_t kv_rank_stride, int64_t grad_rank_stride, cudaStream_t s,
+                                int64_t kv_start) {
   float* delta = reinterpret_cast<float*>(scratch);
   float* dq_acc = delta + ((slots * qtok + 63) / 64) * 64;
   cudaError_t e = softmax_delta_bf16(o, d_out, delta, slots * qtok, dim, s);
   if (e != cudaSuccess) return e;
   CUtensorMap mq, mdo, mk, mv;
-  const int64_t ranks = kvtok / kv_chunk;
+  const int64_t ranks = (kv_start + kvtok + kv_chunk - 1) / kv_chunk;
   if ((e = make_tmap_3d(&mq, q, slots, qtok, dim)) != cudaSuccess) return e;
   if ((e = make_tmap_3d(&mdo, d_out, slots, qtok, dim)) != cudaSuccess) return e;
   if ((e = make_tmap_4d(&mk, kf, ranks, slots, kv_chunk, dim, kv_rank_stride)) != cudaSuccess) return e;
@@ -936,7 +941,7 @@ cudaError_t tc_softmax_backward(const void* q, const void* kf, const void* vf, c
   if ((e = make_tmap_3d_f32(&mdq, dq_acc, slots, qtok, dim)) != cudaSuccess) return e;
   if ((e = set_smem_once((const void*)tc::tc_softmax_bwd_kernel, tc::kSmBwdSmem)) != cudaSuccess) return e;
   tc::SmBwdArgs a{lse, delta, dq_acc, dk_full, dv_full, qtok, kvtok, kv_chunk, grad_rank_stride, row_offset, dim,
-                  causal, 1.f / sqrtf((float)dim), 1.4426950408889634f / sqrtf((float)dim)};
+                  causal, 1.f / sqrtf((float)dim), 1.4426950408889634f / sqrtf((float)dim), kv_start};
   dim3 grid((unsigned)((kvtok + 127) / 128), (unsigned)slots);
   tc::tc_softmax_bwd_kernel<<<grid, tc::kSmBwdThreads, tc::kSmBwdSmem, s>>>(mq, mdo, mk, mv, mdq, a);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;

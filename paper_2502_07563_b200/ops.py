@@ -350,14 +350,22 @@ def nomask_backward_phase2(v, k, dm) -> tuple[torch.Tensor, torch.Tensor]:
 
 
 def softmax_forward(q: torch.Tensor, k_full: torch.Tensor, v_full: torch.Tensor, causal: bool, row_offset: int,
-                    kv_tokens: int, kv_chunk: int, kv_rank_stride: int) -> tuple[torch.Tensor, torch.Tensor]:
-    """Softmax attention of a query chunk against (possibly rank-major) full K/V (oracle.py:136-139)."""
+                    kv_tokens: int, kv_chunk: int, kv_rank_stride: int,
+                    kv_start: int = 0) -> tuple[torch.Tensor, torch.Tensor]:
+    """Softmax attention of a query chunk against (possibly rank-major) full K/V (oracle.py:136-139).
+    kv_start > 0: the keys are [kv_start, kv_start + kv_tokens) of that layout (row_offset relative
+    to kv_start; lasp2h_softmax_forward_range)."""
     require_cuda(q, k_full, v_full)
     slots, qn, d = _slots(q)
     out = torch.empty_like(q)
     lse = torch.empty(q.shape[:3], dtype=state_dtype(q.dtype), device=q.device)  # f64 data: f64 lse
-    call("lasp2h_softmax_forward", dtype_code(q.dtype), ptr(q), ptr(k_full), ptr(v_full), ptr(out), ptr(lse), slots,
-         qn, kv_tokens, d, int(causal), row_offset, kv_chunk, kv_rank_stride, stream_ptr())
+    if kv_start or kv_tokens % kv_chunk:
+        call("lasp2h_softmax_forward_range", dtype_code(q.dtype), ptr(q), ptr(k_full), ptr(v_full), ptr(out),
+             ptr(lse), slots, qn, kv_tokens, d, int(causal), row_offset, kv_chunk, kv_rank_stride, kv_start,
+             stream_ptr())
+    else:
+        call("lasp2h_softmax_forward", dtype_code(q.dtype), ptr(q), ptr(k_full), ptr(v_full), ptr(out), ptr(lse),
+             slots, qn, kv_tokens, d, int(causal), row_offset, kv_chunk, kv_rank_stride, stream_ptr())
     return out, lse
 
 
@@ -375,7 +383,8 @@ def softmax_backward(q, k_full, v_full, out, lse, d_out, causal: bool, row_offse
 
 def softmax_backward_acc(q, k_full, v_full, out, lse, d_out, causal: bool, row_offset: int, kv_tokens: int,
                          kv_chunk: int, kv_rank_stride: int, grads: torch.Tensor, grad_rank_stride: int,
-                         dv_offset: int, key_range: bool = False) -> tuple[torch.Tensor, torch.Tensor | None]:
+                         dv_offset: int, key_range: bool = False,
+                         kv_start: int = 0) -> tuple[torch.Tensor, torch.Tensor | None]:
     """softmax_backward that also returns the fp32 dQ accumulator the bf16 tensor-core
     path reduces into (None on the other paths, whose dq is already exact): partial
     dQs of one query chunk from several key ranges then add with one rounding.
@@ -387,10 +396,13 @@ def softmax_backward_acc(q, k_full, v_full, out, lse, d_out, causal: bool, row_o
     nbytes = int(_lib.load().lasp2h_softmax_scratch_bytes(code, slots, qn, kv_tokens, d))
     scratch = torch.empty(nbytes, dtype=torch.uint8, device=q.device)
     flat = grads.view(-1)
-    entry = "lasp2h_softmax_backward_range" if key_range else "lasp2h_softmax_backward"
-    call(entry, code, ptr(q), ptr(k_full), ptr(v_full), ptr(out), ptr(lse), ptr(d_out), ptr(dq),
-         flat.data_ptr(), flat.data_ptr() + dv_offset * flat.element_size(), ptr(scratch), slots, qn, kv_tokens, d,
-         int(causal), row_offset, kv_chunk, kv_rank_stride, grad_rank_stride, stream_ptr())
+    args = (code, ptr(q), ptr(k_full), ptr(v_full), ptr(out), ptr(lse), ptr(d_out), ptr(dq), flat.data_ptr(),
+            flat.data_ptr() + dv_offset * flat.element_size(), ptr(scratch), slots, qn, kv_tokens, d, int(causal),
+            row_offset, kv_chunk, kv_rank_stride, grad_rank_stride)
+    if key_range or kv_start:
+        call("lasp2h_softmax_backward_range", *args, kv_start, stream_ptr())
+    else:
+        call("lasp2h_softmax_backward", *args, stream_ptr())
     acc = None
     if q.dtype == torch.bfloat16 and 8 <= d <= 128 and d % 8 == 0 and kv_chunk % 128 == 0:
         # tc_softmax_backward's scratch: delta [slots*qtok] (padded to 64) then dq_acc [slots][qtok][d] fp32

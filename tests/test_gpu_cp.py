@@ -105,15 +105,17 @@ def test_balanced_schedule_f64_matches_oracle(t, monkeypatch):
     assert np.max(np.abs(to_np(cat(it.outputs)) - out)) <= 1e-12
     for name, ref in (("dq", dq), ("dk", dk), ("dv", dv)):
         assert O.relative_error(to_np(cat(getattr(g, name) for g in it.grads)), ref) <= 1e-10, name
-    pairs = sum(1 for r in range(t) if sp._pairing(r, t)[0] >= 0)
+    pairs = sum(1 for r in range(t) if sp._pairing(r, t, n // t, 1)[0] >= 0)
     assert it.run.stats.p2p_sends == 7 * pairs  # fwd: Q, O, lse; bwd: O, lse, dO, dQ
     assert it.run.stats.allgather_launches == 2 and it.run.stats.reduce_scatter_launches == 1
 
 
-@pytest.mark.parametrize("t", [4, 8])
-def test_balanced_schedule_bf16_matches_unbalanced(t, monkeypatch):
+@pytest.mark.parametrize("t,c", [(4, 256), (8, 256), (4, 384)])
+def test_balanced_schedule_bf16_matches_unbalanced(t, c, monkeypatch):
+    """bf16: half-chunk offloads (c = 256) and offloads rounded down to 128-key blocks that
+    start inside a chunk (c = 384: kv_start = 128) against the contiguous schedule."""
     import paper_2502_07563_b200.standard_sp as sp
-    n, d, b, h = 256 * t, 128, 1, 2
+    n, d, b, h = c * t, 128, 1, 2
     q, k, v, do = (O.bf16_round(x) for x in O.inputs(n, d, b, h, 5))
     seq = ChunkedSequence(*(torch.from_numpy(x).to("cuda", torch.bfloat16) for x in (q, k, v)), t)
     dod = torch.from_numpy(do).to("cuda", torch.bfloat16)
@@ -126,3 +128,17 @@ def test_balanced_schedule_bf16_matches_unbalanced(t, monkeypatch):
                                                     for nm in ("dq", "dk", "dv")], ref):
         assert O.normalized_error(to_np(got), r) <= 1e-2
         assert O.normalized_error(to_np(got), to_np(want)) <= 1e-2
+
+
+def test_pairing_balances_to_half_the_world():
+    """Offloaded keys give every paired rank T/2 chunk-squares of causal work at even T."""
+    import paper_2502_07563_b200.standard_sp as sp
+    for world in (2, 4, 8):
+        c = 1024
+        cost = [(r + 0.5) * c * c for r in range(world)]
+        for r in range(world):
+            helper, guest, u = sp._pairing(r, world, c, 128)
+            if helper >= 0:
+                cost[r] -= u * c
+                cost[helper] += u * c
+        assert max(cost) == pytest.approx(world / 2 * c * c), (world, cost)

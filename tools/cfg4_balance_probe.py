@@ -36,29 +36,29 @@ grads = torch.empty((W, 2, 1, H, C, D), dtype=torch.float32, device="cuda")
 
 
 def unit(t, lo, hi, causal):
-    """fwd + bwd of rank t's queries against key chunks [lo, hi)."""
+    """fwd + bwd of rank t's queries against keys [lo, hi) (key indices, rank-major layout)."""
     q, do = qs[t], dos[t]
-    off = t * C - lo * C
-    out, lse = ops.softmax_forward(q, kf[lo:hi], vf[lo:hi], causal, off if causal else 0, kv_tokens=(hi - lo) * C,
-                                   kv_chunk=C, kv_rank_stride=per)
+    off = t * C - lo
+    out, lse = ops.softmax_forward(q, kf, vf, causal, off if causal else 0, kv_tokens=hi - lo, kv_chunk=C,
+                                   kv_rank_stride=per, kv_start=lo)
 
     def run():
-        o, l_ = ops.softmax_forward(q, kf[lo:hi], vf[lo:hi], causal, off if causal else 0, kv_tokens=(hi - lo) * C,
-                                    kv_chunk=C, kv_rank_stride=per)
-        ops.softmax_backward_acc(q, kf[lo:hi], vf[lo:hi], out, lse, do, causal, off if causal else 0,
-                                 kv_tokens=(hi - lo) * C, kv_chunk=C, kv_rank_stride=per, grads=grads[lo:hi],
-                                 grad_rank_stride=2 * per, dv_offset=per, key_range=True)
+        ops.softmax_forward(q, kf, vf, causal, off if causal else 0, kv_tokens=hi - lo, kv_chunk=C,
+                            kv_rank_stride=per, kv_start=lo)
+        ops.softmax_backward_acc(q, kf, vf, out, lse, do, causal, off if causal else 0, kv_tokens=hi - lo,
+                                 kv_chunk=C, kv_rank_stride=per, grads=grads, grad_rank_stride=2 * per,
+                                 dv_offset=per, key_range=True, kv_start=lo)
     return timeit(run)
 
 
-plain = [unit(t, 0, t + 1, True) for t in range(W)]
+plain = [unit(t, 0, (t + 1) * C, True) for t in range(W)]
 bal = []
 for t in range(W):
-    helper, guest, u = _pairing(t, W)
+    helper, guest, u = _pairing(t, W, C, 128)  # u in keys (half chunks at even W)
     u = u if helper >= 0 else 0
-    ms = unit(t, u, t + 1, True)
+    ms = unit(t, u, (t + 1) * C, True)
     if guest >= 0:
-        ms += unit(guest, 0, _pairing(guest, W)[2], False)
+        ms += unit(guest, 0, _pairing(guest, W, C, 128)[2], False)
     bal.append(ms)
 print("contiguous per-rank fwd+bwd ms:", [round(x, 1) for x in plain], f"-> max {max(plain):.1f}")
 print("balanced   per-rank fwd+bwd ms:", [round(x, 1) for x in bal], f"-> max {max(bal):.1f}")
