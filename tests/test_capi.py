@@ -30,8 +30,12 @@ def test_host_side_validation_returns_status_not_exception():
     assert st == 1 and b"bound" in lib.lasp2_last_error()
     st = lib.lasp2_causal_chunk(7, 1, 1, 1, None, None, 1, 1, 128, 128, 1, 0, 0, None)
     assert st == 1 and b"dtype" in lib.lasp2_last_error()
-    st = lib.lasp2h_softmax_forward(_lib.F32, 1, 1, 1, 1, 1, 1, 8, 12, 4, 1, 0, 5, 0, None)
+    st = lib.lasp2h_softmax_forward(_lib.F32, 1, 1, 1, 1, 1, 1, 8, 12, 4, 1, 0, 0, 0, None)
     assert st == 1 and b"kv_chunk" in lib.lasp2_last_error()
+    st = lib.lasp2h_softmax_forward_range(_lib.F32, 1, 1, 1, 1, 1, 1, 8, 12, 4, 1, 0, 4, 0, -4, None)
+    assert st == 1 and b"kv_start" in lib.lasp2_last_error()
+    st = lib.lasp2h_softmax_forward_range(_lib.BF16, 1, 1, 1, 1, 1, 1, 8, 256, 64, 1, 0, 128, 0, 64, None)
+    assert st == 1 and b"kv_start % 128" in lib.lasp2_last_error()
     with pytest.raises(ValueError, match="nseg"):
         _lib.call("lasp2_segment_states", _lib.F32, 16, 16, 16, 1, 128, 64, 5, None)
 
