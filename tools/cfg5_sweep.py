@@ -22,6 +22,8 @@ from paper_2502_07563_b200.datagen import gen_slots_device  # noqa: E402
 import os  # noqa: E402
 
 W, H, D = 8, 16, 128
+if os.environ.get("GATHERED_FUSED"):  # A/B: consumers fold the gathered states in their prologue
+    lasp2.GATHERED_FUSED_CONSUMER = True
 if os.environ.get("NSEG"):  # A/B: segments per slot of the masked passes
     from paper_2502_07563_b200 import ops  # noqa: E402
     ops.num_segments = lambda x, _n=int(os.environ["NSEG"]): _n
