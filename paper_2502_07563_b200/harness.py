@@ -75,41 +75,38 @@ class UsageError(Exception):
     """Bad flags, config keys or parameter combinations; exit code 2 (cli.py:66-67)."""
 
 
-def _to_int(s: str) -> int:
-    try:
-        return int(s)
-    except ValueError as exc:
-        raise UsageError(f"expected an integer, got {s!r}") from exc
+_TRUE, _FALSE = frozenset({"true", "1", "yes"}), frozenset({"false", "0", "no"})
 
 
-def _to_float(s: str) -> float:
-    try:
-        return float(s)
-    except ValueError as exc:
-        raise UsageError(f"expected a number, got {s!r}") from exc
+def _parse_bool(text: str) -> bool:
+    word = text.strip().lower()
+    if word in _TRUE or word in _FALSE:
+        return word in _TRUE
+    raise ValueError(text)
 
 
-def _to_bool(s: str) -> bool:
-    low = s.strip().lower()
-    if low in ("true", "1", "yes"):
-        return True
-    if low in ("false", "0", "no"):
-        return False
-    raise UsageError(f"expected true or false, got {s!r}")
-
-
-_CONVERTERS = {"method": str, "seq_len": _to_int, "chunks": _to_int, "world": _to_int, "dim": _to_int,
-               "heads": _to_int, "batch": _to_int, "masked": _to_bool, "pattern": str, "precision": str,
-               "seed": _to_int, "latency_per_launch": _to_float, "latency_per_byte": _to_float,
-               "element_bytes": _to_int, "iterations": _to_int}
+# key -> (parser, what the value must look like); keys accept '-' or '_' and leading dashes
+_KEY_TYPES = {
+    **{k: (int, "an integer") for k in ("seq_len", "chunks", "world", "dim", "heads", "batch", "seed",
+                                        "element_bytes", "iterations")},
+    **{k: (float, "a number") for k in ("latency_per_launch", "latency_per_byte")},
+    **{k: (str, "a string") for k in ("method", "pattern", "precision")},
+    "masked": (_parse_bool, "true or false"),
+}
 
 
 def _coerce(key: str, value):
-    norm = key.strip().lstrip("-").replace("-", "_")
-    conv = _CONVERTERS.get(norm)
-    if conv is None:
+    """(normalised key, typed value) of one flag or config-file entry (cli.py:70-117)."""
+    name = key.strip().lstrip("-").replace("-", "_")
+    if name not in _KEY_TYPES:
         raise UsageError(f"unknown configuration key {key.strip()!r}")
-    return norm, (conv(value) if isinstance(value, str) else value)
+    parse, expected = _KEY_TYPES[name]
+    if not isinstance(value, str):
+        return name, value
+    try:
+        return name, parse(value)
+    except ValueError:
+        raise UsageError(f"expected {expected}, got {value!r}") from None
 
 
 @dataclass(frozen=True)
@@ -470,47 +467,43 @@ _RUN_KEYS = ("method", "seq_len", "chunks", "world", "dim", "heads", "batch", "m
 _COST_KEYS = ("method", "world", "chunks", "batch", "heads", "dim", "element_bytes", "iterations")
 
 
-def _kv_lines(path: str) -> list[tuple[str, str]]:
-    pairs = []
+def _entries(path: str, allowed) -> list[tuple[str, str, str]]:
+    """(key as written, normalised key, raw value) of every 'key = value' line, comments
+    and blank lines skipped, keys checked against `allowed` (cli.py:552-596)."""
     try:
-        with open(path, encoding="utf-8") as fh:
-            for lineno, raw in enumerate(fh, 1):
-                line = raw.strip()
-                if not line or line.startswith("#"):
-                    continue
-                if "=" not in line:
-                    raise UsageError(f"{path}:{lineno}: expected key = value")
-                key, _, value = line.partition("=")
-                pairs.append((key.strip(), value.strip()))
+        text = open(path, encoding="utf-8").read()
     except OSError as exc:
         raise UsageError(f"cannot read {path}: {exc}") from exc
-    return pairs
-
-
-def _config_file(path: str, allowed) -> dict:
-    out = {}
-    for key, value in _kv_lines(path):
-        norm, val = _coerce(key, value)
-        if norm not in allowed:
-            raise UsageError(f"{path}: key {key!r} not valid here")
-        out[norm] = val
+    out = []
+    for n, line in enumerate(text.splitlines(), 1):
+        line = line.strip()
+        if line and not line.startswith("#"):
+            key, eq, value = (part.strip() for part in line.partition("="))
+            if not eq:
+                raise UsageError(f"{path}:{n}: expected key = value")
+            name = key.strip().lstrip("-").replace("-", "_")
+            if name not in _KEY_TYPES:
+                raise UsageError(f"unknown configuration key {key!r}")
+            if name not in allowed:
+                raise UsageError(f"{path}: key {key!r} not valid here")
+            out.append((key, name, value))
     return out
 
 
+def _config_file(path: str, allowed) -> dict:
+    return {name: _coerce(key, value)[1] for key, name, value in _entries(path, allowed)}
+
+
 def _grid_file(path: str, allowed) -> list[dict]:
-    keys, columns = [], []
-    for key, value in _kv_lines(path):
-        coerced = [_coerce(key, piece.strip()) for piece in value.split(",")]
-        norm = coerced[0][0]
-        if norm not in allowed:
-            raise UsageError(f"{path}: key {key!r} not valid here")
-        if norm in keys:
+    """Cartesian product of comma-separated values, one axis per key."""
+    axes: dict[str, list] = {}
+    for key, name, value in _entries(path, allowed):
+        if name in axes:
             raise UsageError(f"{path}: duplicate key {key!r}")
-        keys.append(norm)
-        columns.append([v for _, v in coerced])
-    if not keys:
+        axes[name] = [_coerce(key, piece.strip())[1] for piece in value.split(",")]
+    if not axes:
         raise UsageError(f"{path}: grid file is empty")
-    return [dict(zip(keys, combo)) for combo in itertools.product(*columns)]
+    return [dict(zip(axes, combo)) for combo in itertools.product(*axes.values())]
 
 
 def _expand(args, allowed, default_grid) -> list[dict]:
