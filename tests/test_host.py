@@ -54,3 +54,20 @@ def test_world_spawn_requires_cuda_when_absent():
         pytest.skip("CUDA present")
     with pytest.raises(RuntimeError, match="CUDA"):
         comm.world_spawn(comm.WorldConfig(2), lambda ctx: None)
+
+
+def test_package_datagen_matches_pinned_oracle_generator():
+    """The package's host generator (used for f64 reference data and weights) equals
+    the oracle's, which test_oracle.py pins to the reference's golden values."""
+    import numpy as np
+
+    from oracle import lasp_oracle as O
+    from paper_2502_07563_b200 import datagen
+
+    for seed, tag in ((0, "q"), (1, "x/b0/h1"), (-3, ""), (2**70 + 5, "do")):
+        for dt in (np.float64, np.float32):
+            assert np.array_equal(datagen.gen_data(seed, 7, 5, tag, dt), O.gen_data(seed, 7, 5, tag, dt))
+    assert np.array_equal(datagen.gen_slots(0, 2, 3, 9, 4, "k"), O.gen_slots(0, 2, 3, 9, 4, "k"))
+    assert all(np.array_equal(a, b) for a, b in zip(datagen.qkv_slots(4, 1, 2, 8, 4), O.qkv_slots(4, 1, 2, 8, 4)))
+    assert np.array_equal(datagen.projection_weight(7, 0, "q", 4), O.projection_weight(7, 0, "q", 4))
+    assert datagen.projection_weight(7, 0, "q", 4)[0, 0] == 0.3980089845330995  # test_datagen.py:82
