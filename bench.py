@@ -452,10 +452,12 @@ def run_gpu_arm(args) -> None:
     else:
         ctx = comm.LocalRankContext()
     peaks = load_peaks()
-    main = measure_workload(args.workload, ctx, rank, world, args.steps, args.warmup, device, not args.eager)
+    # the peer exchange's epochs are host counters: it cannot be replayed from a CUDA graph
+    use_graph = not args.eager and not (world > 1 and args.state_exchange == "peer")
+    main = measure_workload(args.workload, ctx, rank, world, args.steps, args.warmup, device, use_graph)
     sec_name = "cfg3" if args.workload == "cfg2" else "cfg2"
     secondary = None if args.no_secondary else measure_workload(sec_name, ctx, rank, world, args.steps, args.warmup,
-                                                                device, not args.eager)
+                                                                device, use_graph)
     if rank == 0:
         s = summarize(main, world, peaks)
         line = {"metric": METRIC, "value": s["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -466,7 +468,9 @@ def run_gpu_arm(args) -> None:
                            "seq_len": main["n"], "chunk_per_gpu": main["c"], "heads": H, "dim": D,
                            "parallelism": f"sp{world}", "masked": main["masked"],
                            "l2": "inputs >= 2 GiB per step >> 126 MB L2; no flush needed",
-                           "state_exchange": args.state_exchange if world > 1 else "none (one rank)",
+                           "state_exchange": (args.state_exchange if world > 1 else "none (one rank)") + (
+                               f" (fell back to collective: {ctx.peer_fallback})"
+                               if getattr(ctx, "peer_fallback", None) else ""),
                            "lasp2h_schedule": "balanced" if args.balanced else "contiguous"},
                 "tensor_frac_of_peak": s["tensor_frac_of_peak"], "tensor_tflops_per_gpu": s["tensor_tflops_per_gpu"],
                 "hbm_frac_of_peak_min_bytes": s["hbm_frac_of_peak"], "roofline": s["roofline"],

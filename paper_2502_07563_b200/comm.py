@@ -22,6 +22,7 @@ NCCL P2P under torchrun), ``mark(kind)``, ``stats`` (CommStats) and ``trace``.
 from __future__ import annotations
 
 import ctypes
+import sys
 import threading
 import time
 from collections import deque
@@ -723,6 +724,7 @@ class DistRankContext(_ContextBase):
 
         self._init_common()
         self._peer = peer_exchange
+        self.peer_fallback: str | None = None  # why a requested peer exchange is not in use
         self._exchanges: dict[tuple, PeerExchange] = {}
         self.dist = dist
         self.rank = dist.get_rank()
@@ -825,25 +827,41 @@ class DistRankContext(_ContextBase):
         key = (tag, tuple(like.shape), like.dtype)
         ex = self._exchanges.get(key)
         if ex is None:
-            import torch.distributed._symmetric_memory as symm_mem
-
-            t, dev = self._sp_size, like.device
-            group_name = self._group.group_name
-            bufs = [symm_mem.empty((2, t, *like.shape), dtype=like.dtype, device=dev),
-                    symm_mem.empty((t,), dtype=torch.int64, device=dev),
-                    symm_mem.empty((t,), dtype=torch.int64, device=dev)]
-            tables = []
-            for buf in bufs:
-                buf.zero_()
-                hdl = symm_mem.rendezvous(buf, group_name)
-                if hdl.buffer_ptrs[hdl.rank] != buf.data_ptr():
-                    raise RuntimeError("symmetric-memory buffer is not at the start of its allocation")
-                tables.append(torch.tensor(list(hdl.buffer_ptrs), dtype=torch.int64, device=dev))
-            torch.cuda.synchronize(dev)
-            self.dist.barrier(group=self._group)  # every rank's zero-fill precedes any put
-            ex = PeerExchange(self.sp_position, t, *bufs, torch.zeros(1, dtype=torch.int32, device=dev), *tables)
+            err = None
+            try:
+                ex = self._rendezvous_exchange(like)
+            except Exception as exc:  # noqa: BLE001 - reported, then the all_gather path runs
+                err = f"{type(exc).__name__}: {exc}"
+            # the group agrees (MIN over ranks) so that all ranks keep one exchange protocol
+            ok = torch.tensor([0 if err else 1], dtype=torch.int32, device=like.device)
+            self.dist.all_reduce(ok, op=self.dist.ReduceOp.MIN, group=self._group)
+            if not int(ok.item()):
+                self._peer = False
+                self.peer_fallback = err or "another rank of the group failed the rendezvous"
+                print(f"[lasp2] rank {self.rank}: peer state exchange unavailable ({self.peer_fallback}); "
+                      f"falling back to the NCCL all_gather", file=sys.stderr, flush=True)
+                return None
             self._exchanges[key] = ex
         return ex
+
+    def _rendezvous_exchange(self, like: torch.Tensor) -> PeerExchange:
+        import torch.distributed._symmetric_memory as symm_mem
+
+        t, dev = self._sp_size, like.device
+        group_name = self._group.group_name
+        bufs = [symm_mem.empty((2, t, *like.shape), dtype=like.dtype, device=dev),
+                symm_mem.empty((t,), dtype=torch.int64, device=dev),
+                symm_mem.empty((t,), dtype=torch.int64, device=dev)]
+        tables = []
+        for buf in bufs:
+            buf.zero_()
+            hdl = symm_mem.rendezvous(buf, group_name)
+            if hdl.buffer_ptrs[hdl.rank] != buf.data_ptr():
+                raise RuntimeError("symmetric-memory buffer is not at the start of its allocation")
+            tables.append(torch.tensor(list(hdl.buffer_ptrs), dtype=torch.int64, device=dev))
+        torch.cuda.synchronize(dev)
+        self.dist.barrier(group=self._group)  # every rank's zero-fill precedes any put
+        return PeerExchange(self.sp_position, t, *bufs, torch.zeros(1, dtype=torch.int32, device=dev), *tables)
 
     def account_exchange(self, ex: PeerExchange, tag: str = "") -> None:
         nbytes = ex.recv[0, 0].numel() * ex.recv.element_size()

@@ -39,6 +39,10 @@ int sm_count_current() {
 }
 bool valid_dtype(int dt) { return dt == LASP2_F32 || dt == LASP2_F64 || dt == LASP2_BF16; }
 bool use_tc(int dtype, int dim, int64_t tokens) { return dtype == LASP2_BF16 && lasp::tc_supported(dim, tokens); }
+// bfloat16 runs on the tcgen05 kernels only; there is no second bf16 backend.
+bool bf16_ok(int dtype, int dim, int64_t tokens) { return dtype != LASP2_BF16 || use_tc(dtype, dim, tokens); }
+#define BF16_ENVELOPE "bfloat16 needs the tcgen05 envelope: 8 <= dim <= 128 and dim % 8 == 0 (float32 / float64 run any shape)"
+
 cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 #define CHECK(cond, msg) \
@@ -73,6 +77,7 @@ int lasp2_segment_states(int dtype, const void* x, const void* y, void* seg_stat
   CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128, "segment_states: bad shape (1 <= dim <= 128)");
   CHECK(nseg >= 1 && nseg <= (tokens + LASP_BLOCK_TOKENS - 1) / LASP_BLOCK_TOKENS, "segment_states: bad nseg");
   cudaError_t e;
+  CHECK(bf16_ok(dtype, dim, tokens), BF16_ENVELOPE);
   if (use_tc(dtype, dim, tokens))
     e = lasp::tc_segment_states(x, y, (float*)seg_states, slots, tokens, dim, nseg, S(stream));
   else if (dtype == LASP2_F32)
@@ -80,7 +85,7 @@ int lasp2_segment_states(int dtype, const void* x, const void* y, void* seg_stat
   else if (dtype == LASP2_F64)
     e = lasp::simt_segment_states<double, double>(x, y, seg_states, slots, tokens, dim, nseg, S(stream));
   else
-    e = lasp::simt_segment_states<__nv_bfloat16, float>(x, y, seg_states, slots, tokens, dim, nseg, S(stream));
+    e = cudaErrorInvalidValue;  // unreachable: bf16_ok() above
   return cuda_status(e, "segment_states");
 }
 
@@ -146,6 +151,7 @@ int lasp2_causal_chunk(int dtype, const void* q, const void* k, const void* v, c
   CHECK(nseg >= 1 && nseg <= (tokens + LASP_BLOCK_TOKENS - 1) / LASP_BLOCK_TOKENS, "causal_chunk: bad nseg");
   CHECK(nseg == 1 || seg_states, "causal_chunk: nseg > 1 needs segment states");
   cudaError_t e;
+  CHECK(bf16_ok(dtype, dim, tokens), BF16_ENVELOPE);
   if (use_tc(dtype, dim, tokens))
     e = lasp::tc_causal_chunk(q, k, v, (const float*)seg_states, (const float*)base, out, slots, tokens, dim, nseg,
                               reverse, transpose_state, S(stream));
@@ -156,8 +162,7 @@ int lasp2_causal_chunk(int dtype, const void* q, const void* k, const void* v, c
     e = lasp::simt_causal_chunk<double, double>(q, k, v, seg_states, base, out, slots, tokens, dim, nseg, reverse,
                                                 transpose_state, S(stream));
   else
-    e = lasp::simt_causal_chunk<__nv_bfloat16, float>(q, k, v, seg_states, base, out, slots, tokens, dim, nseg,
-                                                      reverse, transpose_state, S(stream));
+    e = cudaErrorInvalidValue;  // unreachable: bf16_ok() above
   return cuda_status(e, "causal_chunk");
 }
 
@@ -201,6 +206,7 @@ int lasp2_dq_chunk(int dtype, const void* q, const void* k, const void* v, const
   CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128, "dq_chunk: bad shape (1 <= dim <= 128)");
   CHECK(nseg >= 1 && nseg <= (tokens + LASP_BLOCK_TOKENS - 1) / LASP_BLOCK_TOKENS, "dq_chunk: bad nseg");
   CHECK(nseg == 1 || fwd_seg, "dq_chunk: nseg > 1 needs segment states");
+  CHECK(bf16_ok(dtype, dim, tokens), BF16_ENVELOPE);
   if (use_tc(dtype, dim, tokens))
     return cuda_status(lasp::tc_dq_chunk(q, k, v, d_out, (const float*)fwd_seg, (const float*)fwd_base,
                                          (float*)g_seg, dq, slots, tokens, dim, nseg, S(stream)),
@@ -218,6 +224,7 @@ int lasp2_dkdv_chunk(int dtype, const void* q, const void* k, const void* v, con
   CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128, "dkdv_chunk: bad shape (1 <= dim <= 128)");
   CHECK(nseg >= 1 && nseg <= (tokens + LASP_BLOCK_TOKENS - 1) / LASP_BLOCK_TOKENS, "dkdv_chunk: bad nseg");
   CHECK(nseg == 1 || seg_states, "dkdv_chunk: nseg > 1 needs segment states");
+  CHECK(bf16_ok(dtype, dim, tokens), BF16_ENVELOPE);
   if (use_tc(dtype, dim, tokens))
     return cuda_status(lasp::tc_dkdv_pair(q, k, v, d_out, (const float*)seg_states, (const float*)base, dk, dv, slots,
                                           tokens, dim, nseg, S(stream)),
@@ -236,6 +243,7 @@ int lasp2_backward_chunk(int dtype, const void* q, const void* k, const void* v,
   CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128, "backward_chunk: bad shape (1 <= dim <= 128)");
   CHECK(nseg >= 1 && nseg <= (tokens + LASP_BLOCK_TOKENS - 1) / LASP_BLOCK_TOKENS, "backward_chunk: bad nseg");
   CHECK(nseg == 1 || (fwd_seg && bwd_seg), "backward_chunk: nseg > 1 needs segment states");
+  CHECK(bf16_ok(dtype, dim, tokens), BF16_ENVELOPE);
   if (use_tc(dtype, dim, tokens))
     return cuda_status(lasp::tc_backward_triple(q, k, v, d_out, (const float*)fwd_seg, (const float*)fwd_total,
                                                 (const float*)fwd_base, (const float*)bwd_seg, (const float*)bwd_base,
@@ -252,6 +260,7 @@ int lasp2_apply_state(int dtype, const void* x, const void* m, void* out, int64_
   CHECK(x && m && out, "apply_state: null pointer");
   CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128, "apply_state: bad shape (1 <= dim <= 128)");
   cudaError_t e;
+  CHECK(bf16_ok(dtype, dim, tokens), BF16_ENVELOPE);
   if (use_tc(dtype, dim, tokens))
     e = lasp::tc_apply_state(x, (const float*)m, out, slots, tokens, dim, transpose, accumulate, sm_count_current(),
                              S(stream));
@@ -260,8 +269,7 @@ int lasp2_apply_state(int dtype, const void* x, const void* m, void* out, int64_
   else if (dtype == LASP2_F64)
     e = lasp::simt_apply_state<double, double>(x, m, out, slots, tokens, dim, transpose, accumulate, S(stream));
   else
-    e = lasp::simt_apply_state<__nv_bfloat16, float>(x, m, out, slots, tokens, dim, transpose, accumulate,
-                                                     S(stream));
+    e = cudaErrorInvalidValue;  // unreachable: bf16_ok() above
   return cuda_status(e, "apply_state");
 }
 
@@ -271,6 +279,7 @@ int lasp2_state_apply(int dtype, const void* q, const void* d_out, const void* m
   CHECK(q && d_out && m && seg_states && dq, "state_apply: null pointer");
   CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128, "state_apply: bad shape (1 <= dim <= 128)");
   CHECK(nseg >= 1 && nseg <= (tokens + LASP_BLOCK_TOKENS - 1) / LASP_BLOCK_TOKENS, "state_apply: bad nseg");
+  CHECK(bf16_ok(dtype, dim, tokens), BF16_ENVELOPE);
   if (use_tc(dtype, dim, tokens))
     return cuda_status(lasp::tc_state_apply(q, d_out, (const float*)m, (float*)seg_states, dq, slots, tokens, dim, nseg,
                                             S(stream)),
@@ -285,6 +294,7 @@ int lasp2_apply_state2(int dtype, const void* v, const void* k, const void* dm, 
   CHECK(valid_dtype(dtype), "apply_state2: unknown dtype");
   CHECK(v && k && dm && dk && dv, "apply_state2: null pointer");
   CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128, "apply_state2: bad shape (1 <= dim <= 128)");
+  CHECK(bf16_ok(dtype, dim, tokens), BF16_ENVELOPE);
   if (use_tc(dtype, dim, tokens))
     return cuda_status(lasp::tc_apply2(v, k, (const float*)dm, dk, dv, slots, tokens, dim, sm_count_current(),
                                        S(stream)),
@@ -319,6 +329,7 @@ int lasp2_nomask_forward_local(int dtype, const void* q, const void* k, const vo
   const int sms = sm_count_current();
   CHECK(workspace_bytes >= lasp2_local_workspace_bytes(dtype, slots, tokens, dim, sms),
         "nomask_forward_local: workspace too small (lasp2_local_workspace_bytes)");
+  CHECK(bf16_ok(dtype, dim, tokens), BF16_ENVELOPE);
   if (use_tc(dtype, dim, tokens))
     return cuda_status(lasp::tc_flat_forward(q, k, v, out, (float*)m_full, workspace, slots, tokens, dim, sms,
                                              S(stream)),
@@ -339,6 +350,7 @@ int lasp2_nomask_backward_local(int dtype, const void* q, const void* k, const v
   const int sms = sm_count_current();
   CHECK(workspace_bytes >= lasp2_local_workspace_bytes(dtype, slots, tokens, dim, sms),
         "nomask_backward_local: workspace too small (lasp2_local_workspace_bytes)");
+  CHECK(bf16_ok(dtype, dim, tokens), BF16_ENVELOPE);
   if (use_tc(dtype, dim, tokens))
     return cuda_status(lasp::tc_flat_backward(q, k, v, d_out, (const float*)m_full, dq, dk, dv, workspace, slots,
                                               tokens, dim, sms, S(stream)),
@@ -363,6 +375,7 @@ int lasp2_nomask_forward_phase(int dtype, const void* q, const void* k, const vo
   const int sms = sm_count_current();
   CHECK(workspace_bytes >= lasp2_local_workspace_bytes(dtype, slots, tokens, dim, sms),
         "nomask_forward_phase: workspace too small (lasp2_local_workspace_bytes)");
+  CHECK(bf16_ok(dtype, dim, tokens), BF16_ENVELOPE);
   if (use_tc(dtype, dim, tokens))
     return cuda_status(lasp::tc_flat_forward(q, k, v, out, (float*)m, workspace, slots, tokens, dim, sms, S(stream),
                                              phase),
@@ -390,6 +403,7 @@ int lasp2_nomask_backward_phase(int dtype, const void* q, const void* k, const v
   const int sms = sm_count_current();
   CHECK(workspace_bytes >= lasp2_local_workspace_bytes(dtype, slots, tokens, dim, sms),
         "nomask_backward_phase: workspace too small (lasp2_local_workspace_bytes)");
+  CHECK(bf16_ok(dtype, dim, tokens), BF16_ENVELOPE);
   if (use_tc(dtype, dim, tokens))
     return cuda_status(lasp::tc_flat_backward(q, k, v, d_out, (const float*)m_full, dq, dk, dv, workspace, slots,
                                               tokens, dim, sms, S(stream), (float*)dm, phase),
@@ -414,6 +428,9 @@ static int softmax_forward_impl(int dtype, const void* q, const void* k_full, co
   CHECK(row_offset >= 0 && (!causal || row_offset < kv_tokens), "softmax_forward: bad row_offset");
   CHECK(kv_chunk >= 1 && kv_start >= 0, "softmax_forward: bad kv_chunk / kv_start");
   const bool tc = dtype == LASP2_BF16 && lasp::tc_softmax_supported(dim, kv_chunk);
+  CHECK(dtype != LASP2_BF16 || tc,
+        "softmax_forward: bfloat16 needs the tcgen05 envelope: 8 <= dim <= 128, dim % 8 == 0 and kv_chunk % 128 == 0 "
+        "(float32 / float64 run any shape)");
   CHECK(!tc || kv_start % 128 == 0, "softmax_forward: the bf16 path needs kv_start % 128 == 0");
   cudaError_t e;
   if (tc)
@@ -426,9 +443,7 @@ static int softmax_forward_impl(int dtype, const void* q, const void* k_full, co
     e = lasp::simt_softmax_forward<double, double>(q, k_full, v_full, out, lse, slots, q_tokens, kv_tokens, dim,
                                                    causal, row_offset, kv_chunk, kv_rank_stride, S(stream), kv_start);
   else
-    e = lasp::simt_softmax_forward<__nv_bfloat16, float>(q, k_full, v_full, out, lse, slots, q_tokens, kv_tokens,
-                                                         dim, causal, row_offset, kv_chunk, kv_rank_stride, S(stream),
-                                                         kv_start);
+    e = cudaErrorInvalidValue;  // unreachable: bf16_ok() above
   return cuda_status(e, "softmax_forward");
 }
 
@@ -472,6 +487,9 @@ static int softmax_backward_impl(bool range, int dtype, const void* q, const voi
   CHECK(row_offset >= 0 && (!causal || row_offset < kv_tokens), "softmax_backward: bad row_offset");
   CHECK(kv_chunk >= 1 && kv_start >= 0, "softmax_backward: bad kv_chunk / kv_start");
   const bool tc = dtype == LASP2_BF16 && lasp::tc_softmax_supported(dim, kv_chunk);
+  CHECK(dtype != LASP2_BF16 || tc,
+        "softmax_backward: bfloat16 needs the tcgen05 envelope: 8 <= dim <= 128, dim % 8 == 0 and kv_chunk % 128 == 0 "
+        "(float32 / float64 run any shape)");
   CHECK(!tc || kv_start % 128 == 0, "softmax_backward: the bf16 path needs kv_start % 128 == 0");
   cudaError_t e;
   if (tc) {
@@ -490,10 +508,7 @@ static int softmax_backward_impl(bool range, int dtype, const void* q, const voi
                                                             row_offset, kv_chunk, kv_rank_stride, grad_rank_stride,
                                                             S(stream), lse_range, kv_start);
   else
-    e = lasp::simt_softmax_backward<__nv_bfloat16, float, float>(q, k_full, v_full, out, d_out, dq, dk_full, dv_full,
-                                                                 scratch, slots, q_tokens, kv_tokens, dim, causal,
-                                                                 row_offset, kv_chunk, kv_rank_stride, grad_rank_stride,
-                                                                 S(stream), lse_range, kv_start);
+    e = cudaErrorInvalidValue;  // unreachable: bf16_ok() above
   return cuda_status(e, "softmax_backward");
 }
 int lasp2h_softmax_backward(int dtype, const void* q, const void* k_full, const void* v_full, const void* out,

@@ -609,7 +609,8 @@ cudaError_t softmax_delta_bf16(const void* o, const void* d_out, float* delta, i
   return cudaGetLastError();
 }
 
-// explicit instantiations: (io, accumulate) = (f32,f32), (f64,f64), (bf16,f32)
+// explicit instantiations: (io, accumulate) = (f32,f32), (f64,f64) -- the validation modes;
+// bfloat16 runs on the tcgen05 kernels only
 #define LASP_INST(T, A)                                                                                         \
   template cudaError_t simt_segment_states<T, A>(const void*, const void*, void*, int64_t, int64_t, int, int,   \
                                                  cudaStream_t);                                                 \
@@ -622,7 +623,6 @@ cudaError_t softmax_delta_bf16(const void* o, const void* d_out, float* delta, i
                                                   cudaStream_t, int64_t);
 LASP_INST(float, float)
 LASP_INST(double, double)
-LASP_INST(__nv_bfloat16, float)
 template cudaError_t simt_softmax_backward<float, float, float>(const void*, const void*, const void*, const void*,
                                                                 const void*, void*, void*, void*, void*, int64_t,
                                                                 int64_t, int64_t, int, int, int64_t, int64_t, int64_t,
@@ -632,10 +632,5 @@ template cudaError_t simt_softmax_backward<double, double, double>(const void*, 
                                                                    void*, int64_t, int64_t, int64_t, int, int,
                                                                    int64_t, int64_t, int64_t, int64_t, cudaStream_t,
                                                                    const void*, int64_t);
-template cudaError_t simt_softmax_backward<__nv_bfloat16, float, float>(const void*, const void*, const void*,
-                                                                        const void*, const void*, void*, void*,
-                                                                        void*, void*, int64_t, int64_t, int64_t,
-                                                                        int, int, int64_t, int64_t, int64_t, int64_t,
-                                                                        cudaStream_t, const void*, int64_t);
 
 }  // namespace lasp

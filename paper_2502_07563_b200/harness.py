@@ -471,7 +471,8 @@ def _entries(path: str, allowed) -> list[tuple[str, str, str]]:
     """(key as written, normalised key, raw value) of every 'key = value' line, comments
     and blank lines skipped, keys checked against `allowed` (cli.py:552-596)."""
     try:
-        text = open(path, encoding="utf-8").read()
+        with open(path, encoding="utf-8") as fh:
+            text = fh.read()
     except OSError as exc:
         raise UsageError(f"cannot read {path}: {exc}") from exc
     out = []

@@ -184,8 +184,16 @@ STATE_EXCHANGE = "collective"
 def _peer(ctx, tag: str, like: torch.Tensor):
     if STATE_EXCHANGE != "peer" or ctx.sp_size == 1:
         return None
+    if torch.cuda.is_current_stream_capturing():
+        # the exchange epoch is a host counter passed to the kernels by value: a captured
+        # graph would replay one epoch forever and every flag / ack wait after the first
+        # replay would pass without synchronising with the peers
+        raise RuntimeError("the peer state exchange cannot be captured in a CUDA graph "
+                           "(host-side epochs); run it eagerly")
     fn = getattr(ctx, "peer_exchange", None)
-    return fn(tag, like) if fn is not None else None
+    if fn is None:
+        raise RuntimeError(f"STATE_EXCHANGE='peer' but {type(ctx).__name__} has no peer exchange")
+    return fn(tag, like)  # None: this context keeps the all_gather (reported by the context)
 
 
 # with the peer exchange, the bf16 chunk / dK-dV kernels wait for the ranks they need and

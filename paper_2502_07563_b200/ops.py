@@ -6,6 +6,8 @@ stream and returns new tensors; the library itself never allocates.
 """
 from __future__ import annotations
 
+from collections import OrderedDict
+
 import torch
 
 from . import _lib
@@ -260,14 +262,18 @@ def apply_state2(v: torch.Tensor, k: torch.Tensor, dm: torch.Tensor) -> tuple[to
     return dk, dv
 
 
-_LOCAL_WS: dict[tuple[int, int], torch.Tensor] = {}
+_LOCAL_WS: OrderedDict[tuple[int, int], torch.Tensor] = OrderedDict()
+_LOCAL_WS_MAX = 8  # streams with a cached workspace (least recently used dropped first)
 
 
 def local_workspace(x: torch.Tensor) -> torch.Tensor:
     """Zero-initialised workspace of the world-of-one kernels, one per (device, stream).
 
     The kernels leave their grid-barrier words at zero, so the buffer is reused
-    across calls on the same stream (the header's contract)."""
+    across calls on the same stream (the header's contract). At most
+    _LOCAL_WS_MAX streams keep one: a dropped workspace was allocated on, and
+    last used by, its own stream, so the caching allocator recycles it only
+    behind that stream's queued kernels."""
     slots, n, d = _slots(x)
     need = int(_lib.load().lasp2_local_workspace_bytes(dtype_code(x.dtype), slots, n, d, sm_count(x.device)))
     if need < 0:
@@ -277,6 +283,9 @@ def local_workspace(x: torch.Tensor) -> torch.Tensor:
     if ws is None or ws.numel() < need:
         ws = torch.zeros(max(need, 256), dtype=torch.uint8, device=x.device)
         _LOCAL_WS[key] = ws
+    _LOCAL_WS.move_to_end(key)
+    while len(_LOCAL_WS) > _LOCAL_WS_MAX:
+        _LOCAL_WS.popitem(last=False)
     return ws
 
 

@@ -36,6 +36,11 @@ def test_host_side_validation_returns_status_not_exception():
     assert st == 1 and b"kv_start" in lib.lasp2_last_error()
     st = lib.lasp2h_softmax_forward_range(_lib.BF16, 1, 1, 1, 1, 1, 1, 8, 256, 64, 1, 0, 128, 0, 64, None)
     assert st == 1 and b"kv_start % 128" in lib.lasp2_last_error()
+    # bfloat16 outside the tcgen05 envelope is refused (no second bf16 backend)
+    st = lib.lasp2_apply_state(_lib.BF16, 16, 16, 16, 1, 256, 12, 0, 0, None)
+    assert st == 1 and b"tcgen05 envelope" in lib.lasp2_last_error()
+    st = lib.lasp2h_softmax_forward(_lib.BF16, 1, 1, 1, 1, 1, 1, 64, 256, 64, 1, 0, 64, 0, None)
+    assert st == 1 and b"kv_chunk % 128" in lib.lasp2_last_error()
     with pytest.raises(ValueError, match="nseg"):
         _lib.call("lasp2_segment_states", _lib.F32, 16, 16, 16, 1, 128, 64, 5, None)
 

@@ -69,6 +69,11 @@ def test_lowp_stack_matches_oracle(case, shift, dtype, tol):
     x, dy, xd, dyd = xy(case, dtype)
     x, xd = x * 2.0 ** -shift, xd * 2.0 ** -shift
     bf = dtype == torch.bfloat16
+    if bf and (n // t) % 128:
+        # bf16 softmax layers run on tcgen05 only, which needs 128-key chunks (C-ABI refuses others)
+        with pytest.raises(ValueError, match="tcgen05 envelope"):
+            hybrid_iteration(ModelSpec(pattern, dim=d, heads=h, batch=b, seed=seed), xd, dyd, t, causal=causal)
+        t = n // 128
     if bf:
         x, dy = O.bf16_round(x), O.bf16_round(dy)
     ws = O.stack_weights(pattern.replace(" ", ""), d, seed, round_bf16=bf)
