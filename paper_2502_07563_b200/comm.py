@@ -744,6 +744,9 @@ class DistRankContext(_ContextBase):
                     self._group = pg
         self.trace: list[TraceEvent] = []
         self.comm_stream = torch.cuda.Stream() if torch.cuda.is_available() else None
+        # gloo moves host memory: device payloads are staged through the host (synchronous;
+        # the multi-process tests run several ranks on one GPU this way, NCCL refuses that)
+        self._stage = dist.get_backend(self._group) == "gloo"
         # native_collectives: the state / K,V gathers and the dK,dV reduce-scatter go through
         # the C ABI's NCCL wrappers on this context's own communicator (one per SP group)
         self.nccl: NcclComm | None = None
@@ -781,7 +784,12 @@ class DistRankContext(_ContextBase):
                            device=payload.device)
         out = flat.view(self._sp_size, *payload.shape)
         self._account("all_gather", payload)
-        if payload.is_cuda:
+        if payload.is_cuda and self._stage:
+            host = torch.empty(flat.shape, dtype=flat.dtype)
+            self.dist.all_gather_into_tensor(host, payload.cpu(), group=self._group)
+            flat.copy_(host)
+            work = _Done()
+        elif payload.is_cuda:
             cur = torch.cuda.current_stream()
             self.comm_stream.wait_stream(cur)
             with torch.cuda.stream(self.comm_stream):
@@ -809,6 +817,10 @@ class DistRankContext(_ContextBase):
         self._account("reduce_scatter", stacked)
         if self.nccl is not None and stacked.is_cuda:
             return self.nccl.reduce_scatter(stacked, out=out)
+        if stacked.is_cuda and self._stage:
+            host = torch.empty(out.shape, dtype=out.dtype)
+            self.dist.reduce_scatter_tensor(host.view(-1), stacked.view(-1).cpu(), group=self._group)
+            return out.copy_(host)
         flat_in = stacked.view(-1)
         self.dist.reduce_scatter_tensor(out.view(-1), flat_in, group=self._group)
         return out
@@ -880,7 +892,7 @@ class DistRankContext(_ContextBase):
         self.stats._account("send", nbytes)
         self.trace.append(TraceEvent(len(self.trace), self.rank, time.perf_counter(), "send",
                                      f"dst={dst} tag={tag} bytes={nbytes}"))
-        self.dist.send(payload, dst)
+        self.dist.send(payload.cpu() if payload.is_cuda and self._stage else payload, dst)
 
     def recv(self, src: int, tag: str = "", like: torch.Tensor | None = None) -> torch.Tensor:
         """Receive into a fresh tensor shaped like ``like`` (the ring's payloads
@@ -888,7 +900,12 @@ class DistRankContext(_ContextBase):
         if like is None:
             raise ValueError("DistRankContext.recv needs a template tensor (like=)")
         out = torch.empty_like(like)
-        self.dist.recv(out, src)
+        if out.is_cuda and self._stage:
+            host = torch.empty(out.shape, dtype=out.dtype)
+            self.dist.recv(host, src)
+            out.copy_(host)
+        else:
+            self.dist.recv(out, src)
         self.stats.p2p_recvs += 1
         self.trace.append(TraceEvent(len(self.trace), self.rank, time.perf_counter(), "recv", f"src={src} tag={tag}"))
         return out

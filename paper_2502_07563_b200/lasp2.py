@@ -276,6 +276,17 @@ def _state_like(x: torch.Tensor) -> torch.Tensor:
     return torch.empty((*x.shape[:2], d, d), dtype=ops.state_dtype(x.dtype), device=x.device)
 
 
+def _separate_inter(x: torch.Tensor) -> bool:
+    """Validation modes (float32 / float64) keep the reference's grouping on every schedule:
+    the intra-chunk term from a zero rank-level state, then `+= Q M_{1:t-1}` (and in the
+    backward `+= dO M^T`, `+= V dM^T`, `+= K dM`) as separate passes (lasp2.py:236-240,
+    :277-283). The sequential, overlap, LASP-1 ring and peer schedules then compute the
+    same expression in the same order and agree bitwise (reference acceptance criteria 3
+    and 8). bfloat16 folds the rank-level state into the chunk kernel's seed instead
+    (one pass over the chunk, one rounding)."""
+    return x.dtype != torch.bfloat16
+
+
 def _forward_masked_rank(ctx, qc: torch.Tensor, kc: torch.Tensor, vc: torch.Tensor,
                          overlap: bool = False) -> tuple[torch.Tensor, ActivationCache]:
     """O_t = intra(Q_t, K_t, V_t) + Q_t M_{1:t-1} (lasp2.py:219-243).
@@ -306,8 +317,10 @@ def _forward_masked_rank(ctx, qc: torch.Tensor, kc: torch.Tensor, vc: torch.Tens
         else:
             m_prefix = ops.exchange_fold(ex, ops.FOLD_PREFIX, t)
             ctx.mark("intra_start", f"chunk={t}")
-            out = ops.causal_chunk(qc, kc, vc, seg, m_prefix if t > 0 else None, nseg)
+            out = ops.causal_chunk(qc, kc, vc, seg, m_prefix if t > 0 and not _separate_inter(qc) else None, nseg)
             ctx.mark("intra_end", f"chunk={t}")
+            if t > 0 and _separate_inter(qc):
+                ops.apply_state(qc, m_prefix, out=out, accumulate=True)
         return out, ActivationCache(q=qc, k=kc, v=vc, masked=True, m_prefix=m_prefix, state_folds=1,
                                     seg_prefix=seg, seg_total=m_t, nseg=nseg)
     if overlap:
@@ -328,7 +341,9 @@ def _forward_masked_rank(ctx, qc: torch.Tensor, kc: torch.Tensor, vc: torch.Tens
         else:
             m_prefix = ops.prefix_states(gathered, t)
             ctx.mark("intra_start", f"chunk={t}")
-            out = ops.causal_chunk(qc, kc, vc, seg, m_prefix if t > 0 else None, nseg)
+            out = ops.causal_chunk(qc, kc, vc, seg, m_prefix if t > 0 and not _separate_inter(qc) else None, nseg)
+            if t > 0 and _separate_inter(qc):
+                ops.apply_state(qc, m_prefix, out=out, accumulate=True)
         ctx.mark("intra_end", f"chunk={t}")
     cache = ActivationCache(q=qc, k=kc, v=vc, masked=True, m_prefix=m_prefix, state_folds=1, seg_prefix=seg,
                             seg_total=m_t, nseg=nseg)
@@ -428,7 +443,10 @@ def _backward_masked_rank(ctx, cache: ActivationCache, d_out: torch.Tensor) -> G
     if MASKED_DQ_WITH_STATES and not MASKED_BWD_FUSED:
         # dq_s = sum_{i<=s}(do_s.v_i) k_i + do_s (M_{1:t-1} + local prefix)^T, and in the same
         # pass over (dO, V, K, Q) the dM segment states Q_g^T dO_g (lasp2.py:273-279)
-        dq, gseg = ops.dq_chunk(q, k, v, do, cache.seg_prefix, cache.m_prefix if t > 0 else None, nseg)
+        sep = _separate_inter(q)
+        dq, gseg = ops.dq_chunk(q, k, v, do, cache.seg_prefix, cache.m_prefix if t > 0 and not sep else None, nseg)
+        if t > 0 and sep:
+            ops.apply_state(do, cache.m_prefix, transpose=True, out=dq, accumulate=True)
         g_t, ex = _share_total(ctx, gseg, True, q.dtype, "state_grad")
         if ex is not None and _fused_consumer(ctx, q):  # dK/dV kernel waits for ranks > t, folds their dM itself
             dk, dv = ops.dkdv_chunk_x(q, k, v, do, gseg, ex, t + 1, nseg)
@@ -442,7 +460,10 @@ def _backward_masked_rank(ctx, cache: ActivationCache, d_out: torch.Tensor) -> G
                 dk, dv = ops.dkdv_chunk_gathered(q, k, v, do, gseg, gathered, t + 1, nseg)
                 return GradientBundle(dq=dq, dk=dk, dv=dv)
             r = ops.suffix_states(gathered, t + 1) if t < world - 1 else None
-        dk, dv = ops.dkdv_chunk(q, k, v, do, gseg, r, nseg)
+        dk, dv = ops.dkdv_chunk(q, k, v, do, gseg, None if sep else r, nseg)
+        if sep and r is not None:
+            ops.apply_state(v, r, transpose=True, out=dk, accumulate=True)
+            ops.apply_state(k, r, out=dv, accumulate=True)
         return GradientBundle(dq=dq, dk=dk, dv=dv)
     gseg = ops.segment_states(q, do, nseg)
     g_t = ops.scan_segments(gseg, reverse=True, data_dtype=q.dtype)

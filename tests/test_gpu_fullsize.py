@@ -1,5 +1,6 @@
-"""Parity at the BASELINE.json bench sizes (cfg2: unmasked N=128K, cfg3: masked
-N=512K; B=1 H=16 d=128, bf16, one rank) through an N-independent property:
+"""Parity at the BASELINE.json sizes (cfg2: unmasked N=128K at T=1 and 8; cfg3:
+masked N=512K at T=1, 2, 4, 8; cfg5: masked N=2M at T=8; B=1 H=16 d=128, bf16,
+all 16 heads) through the multi-rank path and an N-independent property:
 at sampled token positions s, the layer's outputs must equal the closed forms
     O_s  = q_s S_s,   dQ_s = dO_s S_s^T,   dK_s = v_s G_s^T,   dV_s = k_s G_s
 with S_s = sum_{i<=s} k_i^T v_i and G_s = sum_{i>=s} q_i^T dO_i (masked;
@@ -17,41 +18,73 @@ from paper_2502_07563_b200.lasp2 import ChunkedSequence, lasp2_iteration
 pytestmark = pytest.mark.gpu
 
 H, D = 16, 128
-HEADS = (0, 7, 15)
 
 
-def sample_rows(n: int) -> torch.Tensor:
-    edges = [0, 1, 127, 128, 129, n // 2 - 1, n // 2, n - 129, n - 128, n - 2, n - 1]
-    g = torch.Generator().manual_seed(n)
-    return torch.unique(torch.cat([torch.tensor(edges), torch.randint(0, n, (37,), generator=g)])).cuda()
+def sample_rows(n: int, chunks: int, ranks) -> torch.Tensor:
+    """Chunk and block edges of every checked rank plus random rows inside its chunk."""
+    c = n // chunks
+    g = torch.Generator().manual_seed(n + chunks)
+    rows = []
+    for t in ranks:
+        lo = t * c
+        rows += [lo, lo + 1, lo + 127, lo + 128, lo + 129, lo + c // 2, lo + c - 129, lo + c - 128, lo + c - 2,
+                 lo + c - 1]
+        rows += (lo + torch.randint(0, c, (24,), generator=g)).tolist()
+    return torch.unique(torch.tensor(rows)).cuda()
 
 
 def inclusive_states(x: torch.Tensor, y: torch.Tensor, rows: torch.Tensor, masked: bool, suffix: bool,
                      blk: int = 4096) -> torch.Tensor:
-    """[len(rows), d, d] f64: sum over i<=s (suffix: i>=s; unmasked: all i) of x_i^T y_i."""
+    """[len(rows), d, d] f64: sum over i<=s (suffix: i>=s; unmasked: all i) of x_i^T y_i.
+    Whole blocks come from a cumulative sum of per-block partials, so every earlier
+    rank's chunk state M_j and the rank's own in-chunk prefix enter in f64."""
     n, d = x.shape
     nb = (n + blk - 1) // blk
     parts = torch.stack([x[b * blk:(b + 1) * blk].T @ y[b * blk:(b + 1) * blk] for b in range(nb)])
     if not masked:
         return parts.sum(0).expand(len(rows), d, d)
+    zero = torch.zeros((1, d, d), dtype=parts.dtype, device=parts.device)
+    before = torch.cat([zero, parts.cumsum(0)])  # before[b] = sum of blocks < b
+    total = before[-1]
     out = []
     for s in rows.tolist():
         b = s // blk
         if not suffix:
-            acc = parts[:b].sum(0) + x[b * blk:s + 1].T @ y[b * blk:s + 1]
+            acc = before[b] + x[b * blk:s + 1].T @ y[b * blk:s + 1]
         else:
-            acc = parts[b + 1:].sum(0) + x[s:(b + 1) * blk].T @ y[s:(b + 1) * blk]
+            acc = (total - before[b + 1]) + x[s:(b + 1) * blk].T @ y[s:(b + 1) * blk]
         out.append(acc)
     return torch.stack(out)
 
 
-@pytest.mark.parametrize("n,masked", [(131072, False), (524288, True)])
-def test_bench_size_sampled_rows_match_closed_form(n, masked):
+# (N, masked, T, ranks checked): the BASELINE.json configs through the multi-rank
+# per-rank programs (threads-as-ranks world: every rank's product path, gathered
+# fp32 states, prefix / suffix folds), at their full sizes
+CASES = [
+    (131072, False, 1, (0,)),          # cfg2, one GPU (persistent world-of-one kernels)
+    (131072, False, 8, (0, 3, 7)),     # cfg2 on 8 GPUs: flat-phase kernels at C = 16K
+    (524288, True, 1, (0,)),           # cfg3, one GPU
+    (524288, True, 2, (0, 1)),         # cfg3 W = 2, 4, 8
+    (524288, True, 4, (0, 1, 3)),
+    (524288, True, 8, (0, 3, 7)),
+    (2097152, True, 8, (0, 3, 7)),     # cfg5 at its largest N: rank 7 folds 7 fp32 states
+]
+
+
+@pytest.mark.parametrize("n,masked,chunks,ranks", CASES, ids=lambda c: str(c))
+def test_config_sampled_rows_match_closed_form(n, masked, chunks, ranks):
     q, k, v, do = (gen_slots_device(0, 1, H, n, D, t) for t in ("q", "k", "v", "do"))
-    it = lasp2_iteration(ChunkedSequence(q, k, v, 1), do, masked)
-    got = {"out": it.outputs[0], "dq": it.grads[0].dq, "dk": it.grads[0].dk, "dv": it.grads[0].dv}
-    rows = sample_rows(n)
-    for h in HEADS:
+    it = lasp2_iteration(ChunkedSequence(q, k, v, chunks), do, masked)
+    assert it.run.stats.allgather_launches == 2
+    c = n // chunks
+    rows = sample_rows(n, chunks, ranks)
+    # this rank's outputs at the sampled global rows
+    def pick(per_rank):
+        return torch.stack([per_rank[r // c][0, :, r % c] for r in rows.tolist()], 1)  # [H, rows, d]
+    got = {"out": pick(it.outputs), "dq": pick([g.dq for g in it.grads]),
+           "dk": pick([g.dk for g in it.grads]), "dv": pick([g.dv for g in it.grads])}
+    worst = {}
+    for h in range(H):
         qh, kh, vh, dh = (x[0, h].double() for x in (q, k, v, do))
         s_fw = inclusive_states(kh, vh, rows, masked, suffix=False)
         g_bw = inclusive_states(qh, dh, rows, masked, suffix=True)
@@ -61,8 +94,11 @@ def test_bench_size_sampled_rows_match_closed_form(n, masked):
             "dk": torch.einsum("rd,red->re", vh[rows], g_bw),
             "dv": torch.einsum("rd,rde->re", kh[rows], g_bw),
         }
+        del qh, kh, vh, dh
         for name, ref in want.items():
-            g = got[name][0, h][rows].double()
+            g = got[name][h].double()
             assert torch.isfinite(g).all(), name
             err = ((g - ref).abs().max() / ref.abs().max()).item()
+            worst[name] = max(worst.get(name, 0.0), err)
             assert err <= 1e-2, (h, name, err)
+    print(f"N={n} masked={masked} T={chunks} ranks={ranks} rows={len(rows)} worst normalised error {worst}")

@@ -202,8 +202,8 @@ def test_overlap_schedule_agrees_and_trace_order():
     plain = lasp2_forward_masked(seq)
     overlap = lasp2_overlap_schedule(seq)
     for a, b in zip(plain.outputs, overlap.outputs):
-        # sequential fuses the inter term into the chunk kernel; overlap adds it after the wait
-        assert O.relative_error(to_np(a), to_np(b)) <= 1e-12
+        # f64: both schedules add the inter term after the intra pass -> bitwise equal
+        assert torch.equal(a, b)
 
     def kinds(run):
         order = {r: [] for r in range(4)}
