@@ -16,8 +16,10 @@ reference datagen, generated on device) are 2 GiB+ per step, far above the
 stream between barrier+synchronize brackets, max over ranks.
 
 --impl reference times the reference algorithm's CPU implementation (the
-numpy oracle port under oracle/, f32, all host cores) on a bounded sample of
-the same workload; rank 0 only.
+numpy oracle port under oracle/, f32, all host cores) on the same config: cfg2
+at its full N with T = --gpus chunks (same `config` object as this arm), the
+masked / LASP-2H workloads at the largest N the port runs in seconds
+(labelled, never extrapolated); rank 0 only.
 """
 from __future__ import annotations
 
@@ -100,7 +102,7 @@ class ClockSampler:
     def __init__(self, index: int, period: float = 0.005) -> None:
         self.index = index
         self.period = period
-        self.samples: list[tuple[float, float, int]] = []
+        self.samples: list[tuple[float, float, int, float]] = []
         self.max_mhz = None
         self._stop = threading.Event()
         self._thread = None
@@ -121,11 +123,19 @@ class ClockSampler:
 
     def _run(self):
         nv, h = self._nv, self._h
+        try:
+            self.power_limit_w = nv.nvmlDeviceGetEnforcedPowerLimit(h) / 1e3
+        except Exception:  # noqa: BLE001
+            self.power_limit_w = None
         while not self._stop.is_set():
             try:
                 sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
                 rs = int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))
-                self.samples.append((time.time(), sm, rs))
+                try:
+                    pw = nv.nvmlDeviceGetPowerUsage(h) / 1e3
+                except Exception:  # noqa: BLE001
+                    pw = float("nan")
+                self.samples.append((time.time(), sm, rs, pw))
             except Exception:  # noqa: BLE001
                 pass
             time.sleep(self.period)
@@ -139,73 +149,154 @@ class ClockSampler:
         rows = [r for r in self.samples if (t0 is None or r[0] >= t0) and (t1 is None or r[0] <= t1)]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "samples": 0}
-        reasons = sorted({n for _, _, rs in rows for n, bit in self.REASONS.items() if rs & bit} - {"gpu_idle"})
+        reasons = sorted({n for *_, rs, _ in rows for n, bit in self.REASONS.items() if rs & bit} - {"gpu_idle"})
+        bits = 0
+        for r in rows:
+            bits |= r[2]
+        pw = [r[3] for r in rows if r[3] == r[3]]
         return {"sm_mhz": statistics.median(r[1] for r in rows), "sm_max_mhz": self.max_mhz,
-                "sm_min_mhz": min(r[1] for r in rows), "reasons": reasons, "samples": len(rows)}
+                "sm_min_mhz": min(r[1] for r in rows), "reasons": reasons, "samples": len(rows),
+                "reason_bits_or": hex(bits),
+                "reason_samples": {n: sum(1 for r in rows if r[2] & bit) for n, bit in self.REASONS.items()
+                                   if any(r[2] & bit for r in rows)},
+                "power_w_median": statistics.median(pw) if pw else None, "power_w_max": max(pw) if pw else None,
+                "power_limit_w": getattr(self, "power_limit_w", None)}
 
 
 # ---------------------------------------------------------------------------
 # CPU reference arm / cpu_baseline: the oracle port on a bounded sample
 # ---------------------------------------------------------------------------
 
-def cpu_reference(workload: str, budget_s: float = 20.0) -> dict:
+def _oracle_inputs(workload: str, n: int, dtype):
+    import numpy as np  # noqa: F401
+
+    from oracle import lasp_oracle as O
+
+    return tuple(O.gen_slots(0, B, H, n, D, t, dtype) for t in ("q", "k", "v", "do"))
+
+
+def _oracle_iteration(workload: str, n: int, world: int, inputs):
+    """One fwd+bwd iteration of the reference algorithm (the numpy oracle port restating
+    lasp2.py:390-409 / standard_sp.py:112-127) on a world of `world` chunks."""
+    from oracle import lasp_oracle as O
+
+    wl = WORKLOADS[workload]
+    q, k, v, do = inputs
+    if wl.get("softmax"):
+        return O.cp_full(q, k, v, do, world, True)
+    return O.lasp2_full(q, k, v, do, world, wl["masked"], bc=BC)
+
+
+# largest N the CPU port runs per workload (masked: the blocked intra pass is ~1.3 K tok/s per
+# core-second; LASP-2H: the full softmax rows are O(N^2)); cfg2 runs at its full N
+CPU_MAX_N = {"cfg2": 131072, "cfg3": 16384, "cfg4": 4096}
+
+
+def _time_oracle(workload: str, n: int, world: int, dtype, iters: int, warmup: int = 1) -> dict:
+    import numpy as np
+
+    inputs = _oracle_inputs(workload, n, dtype)
+    for _ in range(warmup):
+        _oracle_iteration(workload, n, world, inputs)
+    times = []
+    for _ in range(max(1, iters)):
+        t0 = time.perf_counter()
+        _oracle_iteration(workload, n, world, inputs)
+        times.append(time.perf_counter() - t0)
+    med = statistics.median(times)
+    return {"tokens_per_s": n / med, "ms_per_iteration": med * 1e3, "iterations": len(times),
+            "dtype": np.dtype(dtype).name, "seq_len": n, "chunks": world}
+
+
+def cpu_reference(workload: str, world: int = 1) -> dict:
+    """cpu_baseline of the GPU line: the oracle port (f32, all host cores) on the same
+    workload at its full N when the port can run it (cfg2), else at the largest N it runs
+    in seconds (same B, H, d, T; labelled, not extrapolated). Adds the f64 number of the
+    same sample and the cfg1 config exactly (B=1 H=4 d=64 N=4096 T=2 masked) in f32 / f64."""
     import numpy as np
 
     from oracle import lasp_oracle as O
 
-    wl = WORKLOADS[workload]
     cores = len(os.sched_getaffinity(0))
-    softmax = wl.get("softmax", False)
-    n = 1024 if softmax else (2048 if wl["masked"] else 8192)
-    q, k, v, do = (O.gen_slots(0, B, H, n, D, t, np.float32) for t in ("q", "k", "v", "do"))
-
-    def run():
-        if softmax:
-            O.cp_full(q, k, v, do, 1, True)
-        else:
-            O.lasp2_full(q, k, v, do, 1, wl["masked"], bc=BC)
-
-    # warm-up once, then as many full fwd+bwd iterations of the sample as fit the budget
-    run()
-    times = []
-    t_end = time.perf_counter() + budget_s
-    while time.perf_counter() < t_end or len(times) < 2:
-        t0 = time.perf_counter()
-        run()
-        times.append(time.perf_counter() - t0)
-        if len(times) >= 50:
-            break
-    med = statistics.median(times)
-    return {"value": n / med, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"numpy f32 oracle (oracle/lasp_oracle.py, restating "
-                      f"{'standard_sp.py:37-76' if softmax else f'lasp2.py:208-285 blocked at Bc={BC}'}) "
-                      f"on N={n} tokens of the same B=1 H=16 d=128 layer, T=1, median of {len(times)} "
-                      f"iterations, OpenBLAS threads={os.environ.get('OPENBLAS_NUM_THREADS', 'default')}"}
+    n = min(WORKLOADS[workload]["n"], CPU_MAX_N[workload])
+    t0 = time.perf_counter()
+    main = _time_oracle(workload, n, world, np.float32, iters=3)
+    f64 = _time_oracle(workload, n, world, np.float64, iters=1, warmup=0)
+    # cfg1 exactly (BASELINE.json configs[0]): the reference's own CPU-runnable case
+    q, k, v, do = (O.gen_slots(0, 1, 4, 4096, 64, t) for t in ("q", "k", "v", "do"))
+    cfg1 = {}
+    for nm, dt in (("f32", np.float32), ("f64", np.float64)):
+        xs = [x.astype(dt) for x in (q, k, v, do)]
+        O.lasp2_full(*xs, 2, True, bc=BC)
+        ts = []
+        while len(ts) < 3:
+            a = time.perf_counter()
+            O.lasp2_full(*xs, 2, True, bc=BC)
+            ts.append(time.perf_counter() - a)
+        cfg1[nm] = {"tokens_per_s": 4096 / statistics.median(ts), "ms_per_iteration": statistics.median(ts) * 1e3}
+    full = n == WORKLOADS[workload]["n"]
+    return {"value": main["tokens_per_s"], "unit": UNIT, "cores": cores, "kind": "port",
+            "same_config": full, "ms_per_iteration": main["ms_per_iteration"],
+            "sample": (f"numpy oracle port (oracle/lasp_oracle.py restating "
+                       f"{'standard_sp.py:37-76' if WORKLOADS[workload].get('softmax') else 'lasp2.py:208-285'}), "
+                       f"f32, {'full' if full else 'reduced'} N={n} of the same B=1 H=16 d=128 layer, T={world}, "
+                       f"median of {main['iterations']} timed fwd+bwd iterations (not extrapolated), "
+                       f"OpenBLAS threads={os.environ.get('OPENBLAS_NUM_THREADS', 'all cores')}"),
+            "f64": {"value": f64["tokens_per_s"], "ms_per_iteration": f64["ms_per_iteration"], "seq_len": n},
+            "cfg1_exact": {"config": "B=1 H=4 d=64 N=4096 T=2 masked (BASELINE.json configs[0])", **cfg1},
+            "wall_s": time.perf_counter() - t0}
 
 
 def run_reference_arm(args) -> None:
+    """--impl reference: the reference algorithm's CPU implementation (oracle port, all host
+    threads) on this arm's exact config (cfg2: full N, T = --gpus chunks); rank 0 only."""
+    import numpy as np
+
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cfg = dict(workload=WORKLOADS[args.workload]["name"], global_batch=B, seq_len=WORKLOADS[args.workload]["n"],
-               heads=H, dim=D)
-    vals = []
+    wl = WORKLOADS[args.workload]
+    n_full = seq_override.get(args.workload, wl["n"])
+    n = min(n_full, CPU_MAX_N[args.workload])
+    world = args.gpus
+    cores = len(os.sched_getaffinity(0))
+    inputs = _oracle_inputs(args.workload, n, np.float32)
     for _ in range(args.warmup):
-        cpu_reference(args.workload, budget_s=0.5)
+        _oracle_iteration(args.workload, n, world, inputs)
     t0 = time.perf_counter()
+    times = []
     for _ in range(args.steps):
-        vals.append(cpu_reference(args.workload, budget_s=max(0.5, min(5.0, 120.0 / max(1, args.steps)))))
+        a = time.perf_counter()
+        _oracle_iteration(args.workload, n, world, inputs)
+        times.append(time.perf_counter() - a)
     wall = time.perf_counter() - t0
-    v = statistics.median(x["value"] for x in vals)
-    base = dict(vals[0])
-    base["value"] = v
+    ms = statistics.mean(times) * 1e3
+    v = n / (ms / 1e3)
+    full = n == n_full
+    sample = (f"numpy oracle port (oracle/lasp_oracle.py), f32, {'full' if full else 'reduced'} N={n}, "
+              f"T={world} chunks, {args.steps} timed fwd+bwd iterations after {args.warmup} warm-up, "
+              f"host threads={cores}")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": WORKLOADS[args.workload]["n"] / v * 1e3,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (reference datagen SplitMix64 counter-hash)", "config": cfg,
-            "cpu_baseline": base, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "data": "synthetic (reference datagen SplitMix64 counter-hash)",
+            "config": bench_config(args.workload, n, world, args.state_exchange, args.balanced),
+            "same_config": full,
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "wall_s": wall}
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
+
+
+def bench_config(workload: str, n: int, world: int, state_exchange: str, balanced: bool, fallback: str = "") -> dict:
+    """The `config` object of both arms (identical keys and values for the same run)."""
+    wl = WORKLOADS[workload]
+    return {"workload": wl["name"], "global_batch": B, "seq_len": n, "chunk_per_gpu": n // world, "heads": H,
+            "dim": D, "parallelism": f"sp{world}", "masked": wl["masked"],
+            "l2": "inputs >= 2 GiB per step >> 126 MB L2; no flush needed",
+            "state_exchange": (state_exchange if world > 1 else "none (one rank)") + (
+                f" (fell back to collective: {fallback})" if fallback else ""),
+            "lasp2h_schedule": "balanced" if balanced else "contiguous"}
 
 
 # ---------------------------------------------------------------------------
@@ -213,6 +304,19 @@ def run_reference_arm(args) -> None:
 # ---------------------------------------------------------------------------
 
 seq_override: dict[str, int] = {}
+
+
+# algorithmic HBM traffic per launch in units of one bf16 (B, H, C, d) tensor
+ALGO_UNITS = {"lasp2_causal_chunk": 4, "lasp2_apply_state": 2, "lasp2_segment_states": 2, "lasp2_dkdv_chunk": 6,
+              "lasp2_state_apply": 3, "lasp2_apply_state2": 4, "lasp2_backward_chunk": 7,
+              "lasp2_dq_chunk": 5,  # dO, V, K, Q in, dQ out
+              # world-of-one persistent kernels: K,V in + Q in, O out | Q,dO in, dQ out + V,K in, dK,dV out
+              "lasp2_nomask_forward_local": 4, "lasp2_nomask_backward_local": 7,
+              # T > 1: the same kernels split around the exchange (profiler labels per phase)
+              "lasp2_nomask_forward_phase1": 2,   # K, V in -> M_t
+              "lasp2_nomask_forward_phase2": 2,   # Q in, O out
+              "lasp2_nomask_backward_phase1": 3,  # Q, dO in, dQ out (+ dM_t)
+              "lasp2_nomask_backward_phase2": 4}  # V, K in, dK, dV out
 
 
 def measure_workload(workload: str, ctx, rank: int, world: int, steps: int, warmup: int, device,
@@ -267,13 +371,35 @@ def measure_workload(workload: str, ctx, rank: int, world: int, steps: int, warm
         #     CUDA-event bracket measures the kernel alone (no host gaps)
         prof_steps = max(1, min(steps, 10))
         _lib.PROFILER.reset(enabled=True)
+        dev_events = getattr(ctx, "device_events", None)
+        if dev_events is not None:
+            dev_events.clear()
         torch.cuda._sleep(int(6e8))
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
         for _ in range(prof_steps):
             step()
+        p1.record(stream)
         sync_all()
         durations = _lib.PROFILER.durations_ms()
         launches_per_step = _lib.PROFILER.launches / prof_steps
         _lib.PROFILER.reset(enabled=False)
+        prof_step_ms = p0.elapsed_time(p1) / prof_steps
+        # collectives on the side stream (DistRankContext marks issue / completion there):
+        # device duration of each, and how much of the step the compute stream spent not
+        # running this library's kernels (the exposed exchange + launch gaps)
+        comm = None
+        if world > 1 and dev_events is not None:
+            issues = [ev for kind, ev in dev_events if kind == "all_gather_issue"]
+            dones = [ev for kind, ev in dev_events if kind == "all_gather_complete"]
+            ag = [a.elapsed_time(b) for a, b in zip(issues, dones)]
+            comm = {"allgathers_per_step": len(ag) / prof_steps,
+                    "allgather_device_ms_mean": statistics.mean(ag) if ag else None,
+                    "allgather_device_ms_max": max(ag) if ag else None,
+                    "profiled_step_ms": prof_step_ms,
+                    "kernel_sum_ms": sum(sum(v2) for v2 in durations.values()) / prof_steps}
+            comm["exposed_ms_per_step"] = max(0.0, prof_step_ms - comm["kernel_sum_ms"])
+            dev_events.clear()
 
         # (2) capture one step as a CUDA graph (host launch overhead removed)
         graph = None
@@ -286,7 +412,8 @@ def measure_workload(workload: str, ctx, rank: int, world: int, steps: int, warm
                 stream.wait_stream(s2)
                 sync_all()
                 graph = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(graph):
+                # thread-local capture: NCCL's watchdog thread may query events meanwhile
+                with torch.cuda.graph(graph, capture_error_mode="thread_local" if world > 1 else "global"):
                     outs = step()
                 for _ in range(3):
                     graph.replay()
@@ -328,7 +455,7 @@ def measure_workload(workload: str, ctx, rank: int, world: int, steps: int, warm
                         make()
                     stream.wait_stream(s3)
                     sync_all()
-                    with torch.cuda.graph(g2):
+                    with torch.cuda.graph(g2, capture_error_mode="thread_local" if world > 1 else "global"):
                         outs2 = make()
                     runners.append((g2.replay, outs2))
             else:
@@ -375,14 +502,7 @@ def measure_workload(workload: str, ctx, rank: int, world: int, steps: int, warm
     dom = max(per_kernel, key=per_kernel.get)
     dom_launch_ms = statistics.mean(durations[dom])
     unit_bytes = B * H * c * D * 2  # one bf16 (B,H,C,d) tensor
-    algo_bytes = {"lasp2_causal_chunk": 4 * unit_bytes, "lasp2_apply_state": 2 * unit_bytes,
-                  "lasp2_segment_states": 2 * unit_bytes, "lasp2_dkdv_chunk": 6 * unit_bytes,
-                  "lasp2_state_apply": 3 * unit_bytes, "lasp2_apply_state2": 4 * unit_bytes,
-                  "lasp2_backward_chunk": 7 * unit_bytes,
-                  "lasp2_dq_chunk": 5 * unit_bytes,  # dO, V, K, Q in, dQ out
-                  # world-of-one persistent kernels: K,V in + Q in, O out | Q,dO in, dQ out + V,K in, dK,dV out
-                  "lasp2_nomask_forward_local": 4 * unit_bytes,
-                  "lasp2_nomask_backward_local": 7 * unit_bytes}.get(dom, 0)
+    algo_bytes = ALGO_UNITS.get(dom, 0) * unit_bytes
     # causal softmax useful FLOPs of one rank: queries [rC, (r+1)C) see keys <= position
     pairs = H * (c * rank * c + c * (c + 1) / 2)
     algo_flops = {"lasp2h_softmax_forward": 4 * D * pairs, "lasp2h_softmax_backward": 10 * D * pairs}.get(dom, 0)
@@ -390,7 +510,7 @@ def measure_workload(workload: str, ctx, rank: int, world: int, steps: int, warm
                 dom_launch_ms=dom_launch_ms, dom_algo_bytes=algo_bytes, dom_algo_flops=algo_flops, launches_per_step=launches_per_step,
                 h2d=4 * q.numel() * q.element_size() * world, d2h=4 * q.numel() * q.element_size() * world,
                 clocks=clk, e2e_steps=e2e_steps, graph=graph is not None,
-                kernel_sum_ms=sum(per_kernel.values()))
+                kernel_sum_ms=sum(per_kernel.values()), comm=comm)
 
 
 def summarize(r: dict, world: int, peaks: dict) -> dict:
@@ -398,8 +518,14 @@ def summarize(r: dict, world: int, peaks: dict) -> dict:
     flop_s = flops_per_token(r["masked"], r.get("softmax", False), r["n"]) * tok_s
     byte_s = min_bytes_per_token() * tok_s
     achieved = r["dom_algo_bytes"] / (r["dom_launch_ms"] / 1e3) / 1e9
+    tensor_peak, peak_kind = peaks["tensor"], "burst"
     if r.get("softmax"):  # tensor-bound: useful FLOPs of the dominant kernel per launch
         achieved = r["dom_algo_flops"] / (r["dom_launch_ms"] / 1e3) / 1e12
+        if r["dom_launch_ms"] >= 50.0 and peaks.get("tensor_sustained"):
+            # a launch this long runs at the board's sustained (power-limited) clock
+            tensor_peak, peak_kind = peaks["tensor_sustained"], "sustained"
+    peak = tensor_peak if r.get("softmax") else peaks["hbm"]
+    traffic_key = r["workload"] if world == 1 else f"{r['workload']}@C={r['c']}"
     return dict(
         value=tok_s, ms_per_step=r["ms"],
         tensor_tflops_per_gpu=flop_s / world / 1e12,
@@ -408,15 +534,14 @@ def summarize(r: dict, world: int, peaks: dict) -> dict:
         hbm_frac_of_peak=byte_s / world / (peaks["hbm"] * 1e9),
         per_kernel_ms_per_step=r["per_kernel_ms"],
         roofline={"kernel": r["dominant"], "bound": "tensor" if r.get("softmax") else "hbm", "achieved": achieved,
-                  "peak": peaks["tensor"] if r.get("softmax") else peaks["hbm"],
-                  "unit": "TFLOP/s" if r.get("softmax") else "GB/s",
-                  "frac": achieved / (peaks["tensor"] if r.get("softmax") else peaks["hbm"]), "traffic": ncu_traffic(r["workload"], r["dominant"]) if world == 1 else None,
-                  "peak_source": peaks["source"],
+                  "peak": peak, "unit": "TFLOP/s" if r.get("softmax") else "GB/s",
+                  "frac": achieved / peak, "traffic": ncu_traffic(traffic_key, r["dominant"]),
+                  "peak_source": peaks["source"] + (f", {peak_kind} bf16 figure" if r.get("softmax") else ""),
                   "algorithmic_bytes_per_launch": r["dom_algo_bytes"], "avg_launch_ms": r["dom_launch_ms"]},
         e2e={"value": r["n"] / (r["e2e_ms"] / 1e3), "unit": UNIT, "h2d_bytes_per_step": r["h2d"],
              "d2h_bytes_per_step": r["d2h"], "ms_per_step": r["e2e_ms"], "steps": r["e2e_steps"]},
         gpu_launches_per_step=r["launches_per_step"], clocks=r["clocks"], graph=r["graph"],
-        kernel_sum_ms=r["kernel_sum_ms"])
+        kernel_sum_ms=r["kernel_sum_ms"], comm=r.get("comm"))
 
 
 def run_gpu_arm(args) -> None:
@@ -440,6 +565,11 @@ def run_gpu_arm(args) -> None:
         import torch.distributed as dist
 
         if args.dist_backend == "nccl":
+            # communicator-init lines (rank / nranks / transport) to stderr, so the JSON line
+            # stays alone on stdout
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group("nccl", device_id=device)
         else:
             dist.init_process_group(args.dist_backend)
@@ -464,19 +594,15 @@ def run_gpu_arm(args) -> None:
                 "warmup": args.warmup, "ms_per_step": s["ms_per_step"], "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic: reference datagen (SplitMix64 counter-hash) generated on device, bf16",
-                "config": {"workload": WORKLOADS[args.workload]["name"], "global_batch": B,
-                           "seq_len": main["n"], "chunk_per_gpu": main["c"], "heads": H, "dim": D,
-                           "parallelism": f"sp{world}", "masked": main["masked"],
-                           "l2": "inputs >= 2 GiB per step >> 126 MB L2; no flush needed",
-                           "state_exchange": (args.state_exchange if world > 1 else "none (one rank)") + (
-                               f" (fell back to collective: {ctx.peer_fallback})"
-                               if getattr(ctx, "peer_fallback", None) else ""),
-                           "lasp2h_schedule": "balanced" if args.balanced else "contiguous"},
+                "config": bench_config(args.workload, main["n"], world, args.state_exchange, args.balanced,
+                                       getattr(ctx, "peer_fallback", None) or ""),
                 "tensor_frac_of_peak": s["tensor_frac_of_peak"], "tensor_tflops_per_gpu": s["tensor_tflops_per_gpu"],
                 "hbm_frac_of_peak_min_bytes": s["hbm_frac_of_peak"], "roofline": s["roofline"],
                 "e2e": s["e2e"], "gpu_launches": int(round(s["gpu_launches_per_step"] * args.steps)),
                 "clocks": s["clocks"], "per_kernel_ms_per_step": s["per_kernel_ms_per_step"],
                 "kernel_sum_ms_per_step": s["kernel_sum_ms"], "cuda_graph": s["graph"]}
+        if s["comm"] is not None:
+            line["comm"] = s["comm"]
         if secondary is not None:
             ss = summarize(secondary, world, peaks)
             line["secondary"] = {"workload": WORKLOADS[sec_name]["name"], "value": ss["value"], "unit": UNIT,
@@ -486,10 +612,10 @@ def run_gpu_arm(args) -> None:
                                  "hbm_frac_of_peak_min_bytes": ss["hbm_frac_of_peak"], "roofline": ss["roofline"],
                                  "e2e": ss["e2e"], "per_kernel_ms_per_step": ss["per_kernel_ms_per_step"],
                                  "kernel_sum_ms_per_step": ss["kernel_sum_ms"], "clocks": ss["clocks"],
-                                 "gpu_launches_per_step": ss["gpu_launches_per_step"]}
+                                 "gpu_launches_per_step": ss["gpu_launches_per_step"], "comm": ss["comm"]}
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_reference(args.workload, budget_s=args.cpu_budget)
-        print(json.dumps(line))
+            line["cpu_baseline"] = cpu_reference(args.workload, world)
+        print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
 
@@ -511,7 +637,6 @@ def main() -> None:
                     help="N>1: torch.distributed NCCL all_gather of the states, the fused put into "
                          "symmetric-memory peers, or NCCL through the C ABI's wrappers (native)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--eager", action="store_true", help="time eager launches instead of CUDA-graph replay")
     ap.add_argument("--seq-len", type=int, default=0, help="override N of the selected workload")
     ap.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo for multi-rank smoke runs on one GPU")

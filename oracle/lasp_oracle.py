@@ -44,10 +44,40 @@ def _tag_word(tag: str):
     return _U64(int.from_bytes(hashlib.blake2b(tag.encode("utf-8"), digest_size=8).digest(), "little"))
 
 
+_CGEN = []
+
+
+def _c_datagen():
+    """oracle/liboracle_datagen.so (oracle/datagen.c, the same formula in C with OpenMP) if built."""
+    if not _CGEN:
+        import ctypes
+        from pathlib import Path
+
+        lib = None
+        path = Path(__file__).resolve().parent / "liboracle_datagen.so"
+        if path.exists():
+            try:
+                lib = ctypes.CDLL(str(path))
+                for nm in ("oracle_gen_data_f64", "oracle_gen_data_f32"):
+                    getattr(lib, nm).argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p]
+            except OSError:
+                lib = None
+        _CGEN.append(lib)
+    return _CGEN[0]
+
+
 def gen_data(seed: int, rows: int, cols: int, tag: str = "", dtype=np.float64) -> np.ndarray:
     """datagen.py:35-57."""
     with np.errstate(over="ignore"):
         h0 = _mix64(_U64(seed % (1 << 64)) ^ _tag_word(tag))
+    lib = _c_datagen()
+    dt = np.dtype(dtype)
+    if lib is not None and dt in (np.dtype(np.float64), np.dtype(np.float32)) and rows * cols >= 1 << 16:
+        out = np.empty((rows, cols), dtype=dt)
+        fn = lib.oracle_gen_data_f64 if dt == np.float64 else lib.oracle_gen_data_f32
+        fn(int(h0), rows, cols, out.ctypes.data)
+        return out
+    with np.errstate(over="ignore"):
         r = np.arange(rows, dtype=np.uint64)[:, None]
         c = np.arange(cols, dtype=np.uint64)[None, :]
         h = _mix64(_mix64(h0 ^ r) ^ c)

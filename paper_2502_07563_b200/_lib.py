@@ -139,7 +139,10 @@ _NO_LAUNCH = {"lasp2_version", "lasp2_last_error", "lasp2_num_segments", "lasp2h
               "lasp2h_kv_allgather", "lasp2h_grad_reduce_scatter"}
 
 
-def call(name: str, *args) -> int:
+def call(name: str, *args, label: str | None = None) -> int:
+    """Call a C-ABI entry point; raise on a non-zero status. `label` names the call in
+    the profiler when one entry point launches different kernels (e.g. the two phases
+    of lasp2_nomask_*_phase)."""
     lib = load()
     prof = PROFILER
     if prof.enabled and name not in _NO_LAUNCH:
@@ -148,7 +151,7 @@ def call(name: str, *args) -> int:
         a.record()
         status = getattr(lib, name)(*args)
         b.record()
-        prof.events.setdefault(name, []).append((a, b))
+        prof.events.setdefault(label or name, []).append((a, b))
         prof.launches += KERNELS_PER_CALL.get(name, 1)
     else:
         status = getattr(lib, name)(*args)

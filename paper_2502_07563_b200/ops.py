@@ -329,7 +329,7 @@ def nomask_forward_phase(q, k, v, m: torch.Tensor, phase: int, out: torch.Tensor
     ws = local_workspace(x)
     call("lasp2_nomask_forward_phase", dtype_code(x.dtype), ptr(q) if phase == 2 else 0, ptr(k) if phase == 1 else 0,
          ptr(v) if phase == 1 else 0, ptr(out) if phase == 2 else 0, ptr(m), ptr(ws), ws.numel(), slots, n, d, phase,
-         stream_ptr())
+         stream_ptr(), label=f"lasp2_nomask_forward_phase{phase}")
     return out if phase == 2 else m
 
 
@@ -341,7 +341,7 @@ def nomask_backward_phase1(q, d_out, m_full) -> tuple[torch.Tensor, torch.Tensor
     dm = torch.empty_like(m_full)
     ws = local_workspace(q)
     call("lasp2_nomask_backward_phase", dtype_code(q.dtype), ptr(q), 0, 0, ptr(d_out), ptr(m_full), ptr(dm), ptr(dq),
-         0, 0, ptr(ws), ws.numel(), slots, n, d, 1, stream_ptr())
+         0, 0, ptr(ws), ws.numel(), slots, n, d, 1, stream_ptr(), label="lasp2_nomask_backward_phase1")
     return dq, dm
 
 
@@ -354,7 +354,7 @@ def nomask_backward_phase2(v, k, dm) -> tuple[torch.Tensor, torch.Tensor]:
     dk, dv = torch.empty_like(v), torch.empty_like(k)
     ws = local_workspace(v)
     call("lasp2_nomask_backward_phase", dtype_code(v.dtype), 0, ptr(k), ptr(v), 0, 0, ptr(dm), 0, ptr(dk), ptr(dv),
-         ptr(ws), ws.numel(), slots, n, d, 2, stream_ptr())
+         ptr(ws), ws.numel(), slots, n, d, 2, stream_ptr(), label="lasp2_nomask_backward_phase2")
     return dk, dv
 
 

@@ -105,3 +105,20 @@ def test_bf16_round_matches_torch():
     x = O.gen_data(11, 64, 64) * 300.0
     want = torch.from_numpy(x).float().bfloat16().double().numpy()
     assert np.array_equal(O.bf16_round(x), want)
+
+
+def test_c_datagen_matches_numpy_restatement():
+    """oracle/datagen.c (bench.py's full-size CPU inputs) is bit-exact with gen_data."""
+    import numpy as np
+
+    lib = O._c_datagen()
+    if lib is None:
+        pytest.skip("oracle/liboracle_datagen.so not built (make -C oracle)")
+    saved = list(O._CGEN)
+    for dt in (np.float64, np.float32):
+        O._CGEN[:] = [lib]
+        fast = O.gen_data(7, 1024, 96, "v/b0/h3", dt)
+        O._CGEN[:] = [None]
+        slow = O.gen_data(7, 1024, 96, "v/b0/h3", dt)
+        O._CGEN[:] = saved
+        assert fast.dtype == slow.dtype and np.array_equal(fast, slow)
