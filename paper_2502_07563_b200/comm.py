@@ -414,6 +414,18 @@ class RankContext(_ContextBase):
         self._device_mark("reduce_scatter_complete")
         return acc
 
+    def reduce_to_owners(self, contrib: torch.Tensor, counts: Sequence[int], tag: str = "") -> torch.Tensor:
+        """LASP-2H dK/dV exchange with per-rank contribution counts (rank t holds
+        contributions to owners [0, counts[t])): in this world a zero-padded
+        reduce_scatter, so ledger, bytes and simulated clock stay the reference's
+        (standard_sp.py:69-75)."""
+        t, pos = self.sp_size, self.sp_position
+        if len(counts) != t or contrib.shape[0] != counts[pos]:
+            raise ValueError(f"reduce_to_owners: contribution {tuple(contrib.shape)} does not match counts {counts}")
+        padded = torch.zeros((t, *contrib.shape[1:]), dtype=contrib.dtype, device=contrib.device)
+        padded[:counts[pos]] = contrib
+        return self.reduce_scatter(padded, tag)
+
     def peer_exchange(self, tag: str, like: torch.Tensor) -> PeerExchange:
         """This rank's handle on the fused state exchange for states shaped like
         ``like`` (allocated once per group, tag, shape and dtype; every rank of
@@ -825,6 +837,52 @@ class DistRankContext(_ContextBase):
         self.dist.reduce_scatter_tensor(out.view(-1), flat_in, group=self._group)
         return out
 
+    def reduce_to_owners(self, contrib: torch.Tensor, counts: Sequence[int], tag: str = "") -> torch.Tensor:
+        """The LASP-2H dK/dV reduction without the causal zeros: rank t holds contributions
+        to owners (key chunks) [0, counts[t]); owner r receives them from every rank with
+        counts[t] > r over point-to-point transfers (one NCCL group) and folds them in
+        ascending rank order, copy-first, as the reference's sum over ranks
+        (standard_sp.py:69-75). With contiguous causal chunks counts[t] = t + 1, so a rank
+        sends t chunks instead of the reduce_scatter's T - 1. Ledger: one reduce_scatter
+        launch with the bytes this rank actually sends."""
+        t_world, pos = self._sp_size, self.sp_position
+        if len(counts) != t_world or contrib.shape[0] != counts[pos]:
+            raise ValueError(f"reduce_to_owners: contribution {tuple(contrib.shape)} does not match counts {counts}")
+        contrib = contrib.contiguous()
+        peers = self.sp_peers
+        senders = [r for r in range(t_world) if r != pos and counts[r] > pos]
+        targets = [r for r in range(counts[pos]) if r != pos]
+        esize = contrib[0].numel() * contrib.element_size()
+        nbytes = esize * len(targets)
+        self.stats.reduce_scatter_launches += 1
+        self.stats.communication_steps += 1
+        self.stats._account("reduce_scatter", nbytes)
+        self.trace.append(TraceEvent(len(self.trace), self.rank, time.perf_counter(), "reduce_scatter_issue",
+                                     f"bytes={nbytes} owners tag={tag}"))
+        stage = self._stage and contrib.is_cuda
+        src = contrib.cpu() if stage else contrib
+        recv = {r: torch.empty(contrib.shape[1:], dtype=contrib.dtype, device=src.device) for r in senders}
+        ops = [self.dist.P2POp(self.dist.irecv, recv[r], peers[r]) for r in senders]
+        ops += [self.dist.P2POp(self.dist.isend, src[r], peers[r]) for r in targets]
+        if ops:
+            for work in self.dist.batch_isend_irecv(ops):
+                work.wait()
+        acc = None
+        for r in range(t_world):
+            if r == pos and pos < counts[pos]:
+                part = contrib[pos]
+            elif r in recv:
+                part = recv[r].to(contrib.device, non_blocking=True) if stage else recv[r]
+            else:
+                continue
+            if acc is None:
+                acc = part.clone()
+            else:
+                acc += part
+        if acc is None:
+            acc = torch.zeros(contrib.shape[1:], dtype=contrib.dtype, device=contrib.device)
+        return acc
+
     @property
     def sp_peers(self) -> tuple[int, ...]:
         g = self.rank // self._sp_size
@@ -954,6 +1012,9 @@ class LocalRankContext(_ContextBase):
     def reduce_scatter(self, stacked: torch.Tensor, tag: str = "") -> torch.Tensor:
         self._account("reduce_scatter", stacked)
         return stacked[0]
+
+    def reduce_to_owners(self, contrib: torch.Tensor, counts: Sequence[int], tag: str = "") -> torch.Tensor:
+        return self.reduce_scatter(contrib[:1], tag)
 
     sp_peers = (0,)
 

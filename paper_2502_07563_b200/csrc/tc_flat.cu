@@ -569,7 +569,9 @@ cudaError_t launch_flat(const tc::FlatMaps& tm, const tc::FlatArgs& a, int grid,
   attr[1].id = cudaLaunchAttributeCooperative;  // grid barrier: every CTA must be resident
   attr[1].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 2;
+  // phase 2 alone has no grid barrier (dynamic counters, re-armed by the last grabber):
+  // a plain launch starts 2-3 us sooner than a cooperative one (C = 16K: 29.4 -> 27.4 us)
+  cfg.numAttrs = a.phases == 2 ? 1 : 2;
   return cudaLaunchKernelEx(&cfg, kernel, tm, a);
 }
 

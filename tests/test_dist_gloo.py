@@ -144,3 +144,37 @@ def test_three_rank_gloo_ring_send_recv():
         want = (r < world - 1) + (r > 0)  # one hop each way except at the ends
         assert sends == recvs == want and nbytes == want * 8 * 4 * 8
     assert np.allclose(results[world - 1]["through"], O.sum_states(states), rtol=0, atol=1e-12)
+
+
+def _owners_worker(rank, world, port, counts, results):
+    """LASP-2H dK/dV reduction without causal zeros (DistRankContext.reduce_to_owners)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ctx = DistRankContext()
+        # rank t's contribution to owner r: 10**t + r (exact in f64), shape (2, 3)
+        contrib = torch.stack([torch.full((2, 3), 10.0 ** rank + r, dtype=torch.float64)
+                               for r in range(counts[rank])])
+        mine = ctx.reduce_to_owners(contrib, counts, tag="dkv")
+        results[rank] = dict(mine=mine.numpy(), stats=(ctx.stats.reduce_scatter_launches, ctx.stats.bytes_sent,
+                                                       ctx.stats.p2p_sends))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("counts", [[1, 2, 3], [1, 3, 3], [3, 3, 3]])
+def test_three_rank_gloo_reduce_to_owners(counts):
+    """Causal counts (t + 1), a balanced helper holding a later chunk, and the full
+    (non-causal) case: owner r gets the ascending-rank sum of every rank with counts[t] > r,
+    one reduce_scatter launch in the ledger with the bytes actually sent."""
+    world = 3
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_owners_worker, args=(world, _free_port(), counts, results), nprocs=world, join=True)
+    for r in range(world):
+        want = sum(10.0 ** t + r for t in range(world) if counts[t] > r)
+        assert np.array_equal(results[r]["mine"], np.full((2, 3), want))
+        rs, nbytes, p2p = results[r]["stats"]
+        sent = sum(1 for o in range(counts[r]) if o != r)
+        assert rs == 1 and p2p == 0 and nbytes == sent * 6 * 8
