@@ -41,10 +41,19 @@ def main():
     traffic = json.loads(traffic_path.read_text()) if traffic_path.exists() else {}
     workload = sys.argv[2]
     traffic.setdefault(workload, {})
+    # per-rank captures of T > 1 (workload "cfgN@C=..."): the flat kernels run as two phase
+    # launches each, labelled in launch order like bench.py's profiler
+    phased = "@C=" in workload
+    seen: dict[str, int] = {}
     for rep in sys.argv[3:]:
         launches, units = raw(rep)
         for rec in launches:
             name = rec.get("Kernel Name", "?")
+            phase_entry = None
+            if phased and "tc_flat_kernel<" in name:
+                kind = "forward" if "tc_flat_kernel<0>" in name else "backward"
+                seen[kind] = seen.get(kind, 0) + 1
+                phase_entry = f"lasp2_nomask_{kind}_phase{2 - seen[kind] % 2}"
             lines.append(f"== {Path(rep).name}: {name[:100]}")
             for k in KEYS:
                 if k in rec:
@@ -60,7 +69,10 @@ def main():
             try:
                 rd = float(rec["dram__bytes_read.sum"]) * (1e9 if units["dram__bytes_read.sum"] == "Gbyte" else 1e6 if units["dram__bytes_read.sum"] == "Mbyte" else 1)
                 wr = float(rec["dram__bytes_write.sum"]) * (1e9 if units["dram__bytes_write.sum"] == "Gbyte" else 1e6 if units["dram__bytes_write.sum"] == "Mbyte" else 1)
-                for key, entry in ENTRY.items():
+                if phase_entry is not None:
+                    traffic[workload][phase_entry] = {"bytes_per_launch": rd + wr, "read": rd, "write": wr,
+                                                      "source": str(prefix.name), "kernel": name[:80]}
+                for key, entry in (() if phase_entry is not None else ENTRY.items()):
                     if key in name:
                         traffic[workload][entry] = {"bytes_per_launch": rd + wr, "read": rd, "write": wr,
                                           "source": str(prefix.name), "kernel": name[:80]}
