@@ -77,9 +77,9 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
 
 // Grid-wide barriers among the epilogue warps of every CTA (all CTAs are
 // co-resident: one per SM, cooperative launch). gbar[0] counts arrivals over
-// the launch's two barriers (targets n and 2n: one red.add and an acquire
-// spin each); gbar[1] counts CTAs past the second one, and the last of those
-// re-arms both words for the next launch, off the critical path.
+// the launch's barriers (targets n and 2n: one red.add and an acquire spin
+// each); gbar[1] counts CTAs past the last barrier of the launch, and the last
+// of those re-arms both words for the next launch, off the critical path.
 __device__ __forceinline__ void grid_barrier(unsigned* gbar, unsigned target, int et) {
   named_bar_sync(1, kFlatEpi);
   if (et == 0) {
@@ -477,10 +477,10 @@ __global__ void __launch_bounds__(kFlatThreads, 1) tc_flat_kernel(const __grid_c
       }
     }
     trace(3);
-    if (run1) {
-      grid_barrier(a.gbar, 2 * gridDim.x, et);
-      grid_barrier_rearm(a.gbar, gridDim.x, et);
-    }
+    if (run1 && run2) grid_barrier(a.gbar, 2 * gridDim.x, et);  // every slot total is complete
+    // re-arm: each CTA counts itself past barrier 1 (and 2), the last resets both words; a
+    // phase-1-only launch needs no second barrier (its totals are read by later launches)
+    if (run1) grid_barrier_rearm(a.gbar, gridDim.x, et);
     trace(4);
 
     // ---- phase 2 (dynamic blocks, in the producer's record order) ----
