@@ -47,6 +47,42 @@ __global__ void scan_states_kernel(A* __restrict__ seg, A* __restrict__ total, i
   if (total) total[slot * dd + el] = run;
 }
 
+// fp32 scan, four consecutive elements per thread (16-byte loads / stores), same order
+__global__ void scan_states_f4_kernel(float4* __restrict__ seg, float4* __restrict__ total, int64_t slots, int nseg,
+                                      int64_t dd4, int reverse) {
+  ptx::pdl_wait();
+  ptx::pdl_launch_dependents();
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= slots * dd4) return;
+  const int64_t slot = idx / dd4, el = idx % dd4;
+  float4* base = seg + slot * nseg * dd4 + el;
+  float4 run = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int i0 = 0; i0 < nseg; i0 += 8) {
+    float4 vals[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u;
+      if (i < nseg) vals[u] = __ldcg(base + (int64_t)(reverse ? nseg - 1 - i : i) * dd4);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u;
+      if (i < nseg) {
+        base[(int64_t)(reverse ? nseg - 1 - i : i) * dd4] = run;
+        if (i == 0) {
+          run = vals[u];
+        } else {
+          run.x += vals[u].x;
+          run.y += vals[u].y;
+          run.z += vals[u].z;
+          run.w += vals[u].w;
+        }
+      }
+    }
+  }
+  if (total) total[slot * dd4 + el] = run;
+}
+
 // ---- fused state exchange over peer memory -------------------
 // scan_put: the scan above, and the chunk total (this rank's M_t / dM_t, the
 // all_gather payload) is stored straight into slot `rank` of every rank's
@@ -270,6 +306,12 @@ template <typename A>
 cudaError_t scan_states(void* seg, void* total, int64_t slots, int nseg, int dim, int reverse, cudaStream_t s) {
   const int64_t dd = (int64_t)dim * dim;
   const int64_t n = slots * dd;
+  if (std::is_same<A, float>::value && dd % 4 == 0 &&
+      ((reinterpret_cast<uintptr_t>(seg) | reinterpret_cast<uintptr_t>(total)) & 15) == 0) {
+    const int64_t n4 = n / 4;
+    return launch_pdl(scan_states_f4_kernel, dim3((unsigned)((n4 + 127) / 128)), dim3(128), 0, s, 1, (float4*)seg,
+                      (float4*)total, slots, nseg, dd / 4, reverse);
+  }
   return launch_pdl(scan_states_kernel<A>, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, 1, (A*)seg, (A*)total,
                     slots, nseg, dd, reverse);
 }
