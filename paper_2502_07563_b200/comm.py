@@ -172,7 +172,10 @@ class _ContextBase:
         self.device_events: list[tuple[str, torch.cuda.Event]] = []
 
     def _device_mark(self, kind: str, stream=None) -> None:
-        if torch.cuda.is_available() and torch.cuda.is_initialized():
+        # timing events are for eager runs (bench.py's profiled pass); a captured graph
+        # replays without them
+        if torch.cuda.is_available() and torch.cuda.is_initialized() and \
+                not torch.cuda.is_current_stream_capturing():
             ev = torch.cuda.Event(enable_timing=True)
             ev.record(stream if stream is not None else torch.cuda.current_stream())
             self.device_events.append((kind, ev))
