@@ -539,7 +539,12 @@ def summarize(r: dict, world: int, peaks: dict) -> dict:
                   "peak_source": peaks["source"] + (f", {peak_kind} bf16 figure" if r.get("softmax") else ""),
                   "algorithmic_bytes_per_launch": r["dom_algo_bytes"], "avg_launch_ms": r["dom_launch_ms"]},
         e2e={"value": r["n"] / (r["e2e_ms"] / 1e3), "unit": UNIT, "h2d_bytes_per_step": r["h2d"],
-             "d2h_bytes_per_step": r["d2h"], "ms_per_step": r["e2e_ms"], "steps": r["e2e_steps"]},
+             "d2h_bytes_per_step": r["d2h"], "ms_per_step": r["e2e_ms"], "steps": r["e2e_steps"],
+             "path": ("pinned host inputs -> HBM, rank_forward + rank_backward (the per-rank public API) "
+                      "replayed from a CUDA graph captured once (Python call overhead outside the timed "
+                      "region), outputs and all three gradients -> pinned host; H2D / compute / D2H "
+                      "pipelined over three streams with two buffer sets") if r["graph"] else
+                     "pinned host inputs -> HBM, eager rank_forward + rank_backward, outputs + gradients -> host"},
         gpu_launches_per_step=r["launches_per_step"], clocks=r["clocks"], graph=r["graph"],
         kernel_sum_ms=r["kernel_sum_ms"], comm=r.get("comm"))
 

@@ -740,6 +740,7 @@ class DistRankContext(_ContextBase):
         self._init_common()
         self._peer = peer_exchange
         self.peer_fallback: str | None = None  # why a requested peer exchange is not in use
+        self.peer_method: str | None = None    # "symmetric_memory" or "cuda_ipc" once rendezvoused
         self._exchanges: dict[tuple, PeerExchange] = {}
         self.dist = dist
         self.rank = dist.get_rank()
@@ -900,22 +901,67 @@ class DistRankContext(_ContextBase):
         key = (tag, tuple(like.shape), like.dtype)
         ex = self._exchanges.get(key)
         if ex is None:
-            err = None
-            try:
-                ex = self._rendezvous_exchange(like)
-            except Exception as exc:  # noqa: BLE001 - reported, then the all_gather path runs
-                err = f"{type(exc).__name__}: {exc}"
-            # the group agrees (MIN over ranks) so that all ranks keep one exchange protocol
-            ok = torch.tensor([0 if err else 1], dtype=torch.int32, device=like.device)
-            self.dist.all_reduce(ok, op=self.dist.ReduceOp.MIN, group=self._group)
-            if not int(ok.item()):
+            errors = []
+            for method in ("symmetric_memory", "cuda_ipc"):
+                err = None
+                try:
+                    ex = (self._rendezvous_exchange if method == "symmetric_memory" else
+                          self._rendezvous_exchange_ipc)(like)
+                except Exception as exc:  # noqa: BLE001 - reported, then the next method runs
+                    err, ex = f"{method}: {type(exc).__name__}: {exc}", None
+                # the group agrees (MIN over ranks) so that all ranks keep one exchange protocol
+                ok = torch.tensor([0 if err else 1], dtype=torch.int32,
+                                  device="cpu" if self._stage else like.device)  # gloo reduces host tensors
+                self.dist.all_reduce(ok, op=self.dist.ReduceOp.MIN, group=self._group)
+                if int(ok.item()):
+                    self.peer_method = method
+                    break
+                errors.append(err or f"{method}: another rank of the group failed the rendezvous")
+                ex = None
+            if ex is None:
                 self._peer = False
-                self.peer_fallback = err or "another rank of the group failed the rendezvous"
+                self.peer_fallback = "; ".join(errors)
                 print(f"[lasp2] rank {self.rank}: peer state exchange unavailable ({self.peer_fallback}); "
                       f"falling back to the NCCL all_gather", file=sys.stderr, flush=True)
                 return None
+            if errors:
+                print(f"[lasp2] rank {self.rank}: peer state exchange over {self.peer_method} "
+                      f"({'; '.join(errors)})", file=sys.stderr, flush=True)
             self._exchanges[key] = ex
         return ex
+
+    def _rendezvous_exchange_ipc(self, like: torch.Tensor) -> PeerExchange:
+        """The same buffers mapped into every rank of the group with CUDA IPC handles
+        (torch's own tensor-sharing reductions, exchanged with all_gather_object): works
+        where symmetric memory refuses, e.g. several ranks on one device, and for peer
+        devices with P2P access (the mapping enables it lazily)."""
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        t, dev = self._sp_size, like.device
+        bufs = [torch.zeros((2, t, *like.shape), dtype=like.dtype, device=dev),
+                torch.zeros((t,), dtype=torch.int64, device=dev),
+                torch.zeros((t,), dtype=torch.int64, device=dev)]
+        torch.cuda.synchronize(dev)
+        mine = [reduce_tensor(b) for b in bufs]
+        everyone: list = [None] * t
+        self.dist.all_gather_object(everyone, mine, group=self._group)
+        self._ipc_keep = getattr(self, "_ipc_keep", [])  # peers' mappings live as long as the context
+        tables = []
+        for i, buf in enumerate(bufs):
+            ptrs = []
+            for r in range(t):
+                if r == self.sp_position:
+                    ptrs.append(buf.data_ptr())
+                else:
+                    fn, args = everyone[r][i]
+                    peer = fn(*args)
+                    self._ipc_keep.append(peer)
+                    ptrs.append(peer.data_ptr())
+            tables.append(torch.tensor(ptrs, dtype=torch.int64, device=dev))
+        self._ipc_keep.extend(bufs)
+        torch.cuda.synchronize(dev)
+        self.dist.barrier(group=self._group)  # every rank's zero-fill and mapping precede any put
+        return PeerExchange(self.sp_position, t, *bufs, torch.zeros(1, dtype=torch.int32, device=dev), *tables)
 
     def _rendezvous_exchange(self, like: torch.Tensor) -> PeerExchange:
         import torch.distributed._symmetric_memory as symm_mem

@@ -11,7 +11,12 @@ exactly what bench.py and a model run per rank:
 * ``standard_sp._cp_forward_rank`` / ``_cp_backward_rank`` (LASP-2H, reference
   standard_sp.py:37-76) with contiguous chunks and with the balanced schedule
   (P2P send / recv between paired ranks), one reduce_scatter of dK / dV;
-* ``lasp1.rank_forward`` / ``rank_backward`` (the ring, P2P).
+* ``lasp1.rank_forward`` / ``rank_backward`` (the ring, P2P);
+* the fused peer state exchange (``lasp2.STATE_EXCHANGE = "peer"``)
+  across processes: receive buffers, flags and acks mapped into every rank with
+  CUDA IPC (torch symmetric memory refuses ranks sharing one device), the scan
+  kernel's stores and the bf16 consumers' in-kernel flag waits crossing process
+  boundaries — bitwise equal to the all_gather path.
 
 The gathered results are compared with the oracle (reference tolerances in f64;
 normalised <= 1e-2 for bf16 on the same bf16-rounded inputs, SURVEY §8a note P)
@@ -76,6 +81,19 @@ def _worker(rank, world, port, results):
                 torch.cuda.synchronize()
                 out[f"lasp2_{name}_{masked}"] = [_np(x) for x in (o, g.dq, g.dk, g.dv)]
                 out[f"lasp2_{name}_{masked}_ledger"] = (ctx.stats.allgather_launches, ctx.stats.p2p_sends)
+                # the fused state exchange: the scan kernel stores M_t into every
+                # rank's receive buffer through CUDA IPC mappings (symmetric memory refuses ranks
+                # sharing a device) and the bf16 consumers wait for the flags inside their kernels
+                lasp2.STATE_EXCHANGE = "peer"
+                try:
+                    ctx = DistRankContext(peer_exchange=True)
+                    o, cache = lasp2.rank_forward(ctx, qc, kc, vc, masked=masked)
+                    g = lasp2.rank_backward(ctx, cache, dc)
+                    torch.cuda.synchronize()
+                finally:
+                    lasp2.STATE_EXCHANGE = "collective"
+                out[f"peer_{name}_{masked}"] = [_np(x) for x in (o, g.dq, g.dk, g.dv)]
+                out[f"peer_{name}_{masked}_info"] = (ctx.peer_method, ctx.peer_fallback, ctx.stats.allgather_launches)
             for balanced in (False, True):
                 standard_sp.BALANCED = balanced
                 ctx = DistRankContext()
@@ -171,3 +189,17 @@ def test_lasp1_ring_rank_programs_match_oracle(world_results, name):
     _check(name, _cat(res, world, f"lasp1_{name}"), ref)
     # 2(W-1) P2P steps over the whole world (lasp1.py:43-107)
     assert sum(res[r][f"lasp1_{name}_ledger"][0] for r in range(world)) == 2 * (world - 1)
+
+
+@pytest.mark.parametrize("name", list(CASES))
+@pytest.mark.parametrize("masked", [True, False])
+def test_peer_exchange_across_processes_matches_collective_bitwise(world_results, name, masked):
+    """Same scan, same copy-first fold order: the fused peer exchange gives the all_gather
+    path's bits, with one all_gather launch per exchange in the ledger."""
+    world, res = world_results
+    for r in range(world):
+        method, fallback, launches = res[r][f"peer_{name}_{masked}_info"]
+        assert fallback is None and method in ("symmetric_memory", "cuda_ipc"), (method, fallback)
+        assert launches == 2
+        for a, b in zip(res[r][f"peer_{name}_{masked}"], res[r][f"lasp2_{name}_{masked}"]):
+            assert np.array_equal(a, b)
