@@ -160,6 +160,15 @@ int lasp2_backward_chunk(int dtype, const void* q, const void* k, const void* v,
 int lasp2_apply_state(int dtype, const void* x, const void* m, void* out, int64_t slots, int64_t tokens, int dim,
                       int transpose, int accumulate, void* stream);
 
+/* Hybrid-stack projections (replaces the W_Q/K/V GEMMs of hybrid.py:136-151):
+ * out (+)= sum_{i<nx} xs[i] op(ws[i]) per (batch, head) slot, op = W (transpose 0)
+ * or W^T (transpose 1), every ws[i] one [dim][dim] weight in the states dtype
+ * (f32 for bf16 data) shared by all slots; xs[i] / out [slots][tokens][dim].
+ * nx = 1 (accumulate allowed) or 3 (the chain-rule dX = dQ W_Q^T + dK W_K^T +
+ * dV W_V^T with one rounding). bf16: tcgen05 kernels. */
+int lasp2_project(int dtype, const void* const* xs, const void* const* ws, int nx, void* out, int64_t slots,
+                  int64_t tokens, int dim, int transpose, int accumulate, void* stream);
+
 /* Unmasked backward, fused (lasp2.py:256-267): seg_states[slot][g] = Q_g^T dO_g
  * (the dM segments, scanned by lasp2_scan_segments) and dq = dO M^T, reading Q and
  * dO once. `m` = the forward's M_{1:T} (states dtype). */

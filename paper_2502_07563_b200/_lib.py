@@ -41,6 +41,7 @@ SIGNATURES = {
                                   _int, _vp]),
     "lasp2_dq_chunk": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _int, _int, _vp]),
     "lasp2_dkdv_chunk": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _int, _int, _vp]),
+    "lasp2_project": (_int, [_int, _vp, _vp, _int, _vp, _i64, _i64, _int, _int, _int, _vp]),
     "lasp2_state_apply": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _int, _int, _vp]),
     "lasp2_apply_state2": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _int, _vp]),
     "lasp2_backward_chunk": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64,

@@ -273,6 +273,33 @@ int lasp2_apply_state(int dtype, const void* x, const void* m, void* out, int64_
   return cuda_status(e, "apply_state");
 }
 
+int lasp2_project(int dtype, const void* const* xs, const void* const* ws, int nx, void* out, int64_t slots,
+                  int64_t tokens, int dim, int transpose, int accumulate, void* stream) {
+  CHECK(valid_dtype(dtype), "project: unknown dtype");
+  CHECK(xs && ws && out, "project: null pointer");
+  CHECK(nx == 1 || nx == 3, "project: nx must be 1 or 3");
+  for (int i = 0; i < nx; ++i) CHECK(xs[i] && ws[i], "project: null input or weight");
+  CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128, "project: bad shape (1 <= dim <= 128)");
+  CHECK(nx == 1 || !accumulate, "project: accumulate needs nx == 1");
+  CHECK(bf16_ok(dtype, dim, tokens), BF16_ENVELOPE);
+  cudaError_t e = cudaSuccess;
+  if (use_tc(dtype, dim, tokens)) {
+    e = lasp::tc_apply_multi(xs, reinterpret_cast<const float* const*>(ws), nx, 0, out, slots, tokens, dim, transpose,
+                             accumulate, sm_count_current(), S(stream));
+  } else {
+    // validation dtypes: one pass per input, the later ones accumulating in the data dtype
+    for (int i = 0; i < nx && e == cudaSuccess; ++i) {
+      const int acc = i > 0 ? 1 : accumulate;
+      e = dtype == LASP2_F64
+              ? lasp::simt_apply_state<double, double>(xs[i], ws[i], out, slots, tokens, dim, transpose, acc,
+                                                       S(stream), 0)
+              : lasp::simt_apply_state<float, float>(xs[i], ws[i], out, slots, tokens, dim, transpose, acc, S(stream),
+                                                     0);
+    }
+  }
+  return cuda_status(e, "project");
+}
+
 int lasp2_state_apply(int dtype, const void* q, const void* d_out, const void* m, void* seg_states, void* dq,
                       int64_t slots, int64_t tokens, int dim, int nseg, void* stream) {
   CHECK(valid_dtype(dtype), "state_apply: unknown dtype");

@@ -15,7 +15,7 @@ cudaError_t simt_causal_chunk(const void* q, const void* k, const void* v, const
                               int transpose_state, cudaStream_t s);
 template <typename T, typename A>
 cudaError_t simt_apply_state(const void* x, const void* m, void* out, int64_t slots, int64_t tokens, int dim,
-                             int transpose, int accumulate, cudaStream_t s);
+                             int transpose, int accumulate, cudaStream_t s, int64_t m_stride = -1);
 template <typename T, typename A>
 cudaError_t simt_softmax_forward(const void* q, const void* kf, const void* vf, void* out, void* lse, int64_t slots,
                                  int64_t qtok, int64_t kvtok, int dim, int causal, int64_t row_offset, int64_t kv_chunk,
@@ -69,6 +69,11 @@ cudaError_t tc_dkdv_pair(const void* q, const void* k, const void* v, const void
                          cudaStream_t s, const XFold* xfold = nullptr);
 cudaError_t tc_apply_state(const void* x, const float* m, void* out, int64_t slots, int64_t tokens, int dim,
                            int transpose, int accumulate, int sm_count, cudaStream_t s);
+// out (+)= sum_i xs[i] op(ms[i]) for nx in {1, 3} (accumulate only with nx = 1); m_stride =
+// dim^2 for per-slot states, 0 for one weight shared by every slot
+cudaError_t tc_apply_multi(const void* const* xs, const float* const* ms, int nx, int64_t m_stride, void* out,
+                           int64_t slots, int64_t tokens, int dim, int transpose, int accumulate, int sm_count,
+                           cudaStream_t s);
 bool tc_softmax_supported(int dim, int64_t kv_chunk);
 cudaError_t tc_softmax_forward(const void* q, const void* kf, const void* vf, void* out, float* lse, int64_t slots,
                                int64_t qtok, int64_t kvtok, int dim, int causal, int64_t row_offset, int64_t kv_chunk,

@@ -154,13 +154,13 @@ template <typename T, typename A>
 __global__ void __launch_bounds__(kSimtThreads) simt_apply_state_kernel(const T* __restrict__ x,
                                                                         const A* __restrict__ m, T* out,
                                                                         int64_t tokens, int dim, int transpose,
-                                                                        int accumulate) {
+                                                                        int accumulate, int64_t m_stride) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   A* M = reinterpret_cast<A*>(smem_raw);  // [dim][dim] as used: M[a][c]
   A* xs = M + dim * dim;                  // [BT][dim]
   const int64_t slot = blockIdx.y;
   const int dd = dim * dim;
-  const A* mb = m + slot * (int64_t)dd;
+  const A* mb = m + slot * m_stride;  // m_stride 0: one weight shared by every slot
   for (int el = threadIdx.x; el < dd; el += blockDim.x) {
     const int a = el / dim, c = el % dim;
     M[el] = transpose ? mb[c * dim + a] : mb[el];
@@ -543,14 +543,16 @@ cudaError_t simt_causal_chunk(const void* q, const void* k, const void* v, const
 
 template <typename T, typename A>
 cudaError_t simt_apply_state(const void* x, const void* m, void* out, int64_t slots, int64_t tokens, int dim,
-                             int transpose, int accumulate, cudaStream_t s) {
+                             int transpose, int accumulate, cudaStream_t s, int64_t m_stride) {
+  if (m_stride < 0) m_stride = (int64_t)dim * dim;
   const size_t smem = (size_t)(dim * dim + kSimtBT * dim) * sizeof(A);
   auto kern = simt_apply_state_kernel<T, A>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int64_t per_cta = kSimtBT * 8;
   dim3 grid((unsigned)((tokens + per_cta - 1) / per_cta), (unsigned)slots);
-  kern<<<grid, kSimtThreads, smem, s>>>((const T*)x, (const A*)m, (T*)out, tokens, dim, transpose, accumulate);
+  kern<<<grid, kSimtThreads, smem, s>>>((const T*)x, (const A*)m, (T*)out, tokens, dim, transpose, accumulate,
+                                         m_stride);
   return cudaGetLastError();
 }
 
@@ -617,7 +619,7 @@ cudaError_t softmax_delta_bf16(const void* o, const void* d_out, float* delta, i
   template cudaError_t simt_causal_chunk<T, A>(const void*, const void*, const void*, const void*, const void*, \
                                                void*, int64_t, int64_t, int, int, int, int, cudaStream_t);      \
   template cudaError_t simt_apply_state<T, A>(const void*, const void*, void*, int64_t, int64_t, int, int, int, \
-                                              cudaStream_t);                                                    \
+                                              cudaStream_t, int64_t);                                           \
   template cudaError_t simt_softmax_forward<T, A>(const void*, const void*, const void*, void*, void*, int64_t, \
                                                   int64_t, int64_t, int, int, int64_t, int64_t, int64_t,         \
                                                   cudaStream_t, int64_t);

@@ -649,28 +649,43 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
 }
 
 // ============================================================================
-// apply_state: O (+)= X M  (transpose=0) or X M^T (transpose=1)
+// apply_state: O (+)= X M  (transpose=0) or X M^T (transpose=1); with NX = 3 the
+// sum of three such products into one accumulator (one rounding): the hybrid
+// stack's dX = dQ W_Q^T + dK W_K^T + dV W_V^T. M is per slot (m_stride = dim^2)
+// or one weight shared by every slot (m_stride = 0).
 // ============================================================================
-constexpr int kApplyRing = 4;
-constexpr uint32_t kApplySmem = (kApplyRing + 3) * kTileBytes + 1024 + 256;
+template <int NX>
+struct ApplyCfg {
+  static constexpr int kRing = NX == 1 ? 4 : 3;
+  static constexpr int kStages = NX == 1 ? 2 : 1;
+  static constexpr uint32_t kSmem = (kRing + NX + kStages) * kTileBytes + 1024 + 256;
+};
+constexpr uint32_t kApplySmem = ApplyCfg<1>::kSmem;
 
+struct ApplyMaps {
+  CUtensorMap x[3];
+};
+
+template <int NX>
 __global__ void __launch_bounds__(192, 1)
-    tc_apply_state_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_o,
-                          const float* __restrict__ m, __nv_bfloat16* out, int64_t tokens, int dim, int transpose,
-                          int accumulate, int blocks_per_cta) {
+    tc_apply_state_kernel(const __grid_constant__ ApplyMaps tmx, const __grid_constant__ CUtensorMap tm_o,
+                          const float* m0, const float* m1, const float* m2, int64_t m_stride,
+                          __nv_bfloat16* out, int64_t tokens, int dim, int transpose, int accumulate,
+                          int blocks_per_cta) {
+  using C = ApplyCfg<NX>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* ring = smem;
-  uint8_t* mimg = ring + kApplyRing * kTileBytes;
-  uint8_t* stage = mimg + kTileBytes;  // 2 x 32 KB
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stage + 2 * kTileBytes);
+  uint8_t* mimg = ring + C::kRing * kTileBytes;  // [NX]
+  uint8_t* stage = mimg + NX * kTileBytes;       // [kStages] x 32 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stage + C::kStages * kTileBytes);
   uint64_t* full = bars;
-  uint64_t* empty = bars + kApplyRing;
-  uint64_t* acc_full = bars + 2 * kApplyRing;       // [2]
-  uint64_t* acc_empty = bars + 2 * kApplyRing + 2;  // [2]
-  uint64_t* m_ready = bars + 2 * kApplyRing + 4;
-  uint64_t* o_full = bars + 2 * kApplyRing + 5;  // [2] accumulate: the old O tile landed in stage[buf]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kApplyRing + 7);
+  uint64_t* empty = bars + C::kRing;
+  uint64_t* acc_full = bars + 2 * C::kRing;       // [2]
+  uint64_t* acc_empty = bars + 2 * C::kRing + 2;  // [2]
+  uint64_t* m_ready = bars + 2 * C::kRing + 4;
+  uint64_t* o_full = bars + 2 * C::kRing + 5;  // [2] accumulate: the old O tile landed in stage[buf]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::kRing + 7);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slot = blockIdx.y;
@@ -682,7 +697,7 @@ __global__ void __launch_bounds__(192, 1)
   const int kfeat = (dim + 15) / 16;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kApplyRing; ++i) {
+    for (int i = 0; i < C::kRing; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
@@ -699,37 +714,40 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0) {
     if (elect_one()) {
-      prefetch_tmap(&tm_x);
+      for (int i = 0; i < NX; ++i) prefetch_tmap(&tmx.x[i]);
       prefetch_tmap(&tm_o);
       for (int b = 0; b < nblk; ++b) {
-        const int s = b % kApplyRing, u = b / kApplyRing;
-        if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
-        uint8_t* dst = ring + s * kTileBytes;
-        mbar_arrive_expect_tx(&full[s], nbox * kBoxBytes);
         const int row = (int)((b0 + b) * kTile);
-        for (int bx = 0; bx < nbox; ++bx) tma_load_3d(dst + bx * kBoxBytes, &tm_x, &full[s], 64 * bx, row, slot);
+        for (int i = 0; i < NX; ++i) {
+          const int t = NX * b + i, s = t % C::kRing, u = t / C::kRing;
+          if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+          uint8_t* dst = ring + s * kTileBytes;
+          mbar_arrive_expect_tx(&full[s], nbox * kBoxBytes);
+          for (int bx = 0; bx < nbox; ++bx) tma_load_3d(dst + bx * kBoxBytes, &tmx.x[i], &full[s], 64 * bx, row, slot);
+        }
       }
     }
   } else if (warp == 1) {
     const uint32_t idesc = idesc_bf16_f32(128, 128, 0, transpose ? 0 : 1);
-    const uint32_t ma = smem_u32(mimg);
     mbar_wait(m_ready, 0);
     for (int b = 0; b < nblk; ++b) {
-      const int s = b % kApplyRing, u = b / kApplyRing;
       const int buf = b & 1;
-      mbar_wait(&full[s], u & 1);
       if (b >= 2) mbar_wait(&acc_empty[buf], ((b >> 1) - 1) & 1);
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t xa = smem_u32(ring + s * kTileBytes);
-        for (int kk = 0; kk < kfeat; ++kk) {
-          const uint64_t bdesc = transpose ? desc_kmajor(ma, kk) : desc_mnmajor(ma, kk);
-          mma_bf16_ss(tmem + buf * 128, desc_kmajor(xa, kk), bdesc, idesc, kk > 0);
+      for (int i = 0; i < NX; ++i) {
+        const int t = NX * b + i, s = t % C::kRing, u = t / C::kRing;
+        mbar_wait(&full[s], u & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t xa = smem_u32(ring + s * kTileBytes), ma = smem_u32(mimg + i * kTileBytes);
+          for (int kk = 0; kk < kfeat; ++kk) {
+            const uint64_t bdesc = transpose ? desc_kmajor(ma, kk) : desc_mnmajor(ma, kk);
+            mma_bf16_ss(tmem + buf * 128, desc_kmajor(xa, kk), bdesc, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&empty[s]);
+          if (i == NX - 1) mma_commit(&acc_full[buf]);
         }
-        mma_commit(&empty[s]);
-        mma_commit(&acc_full[buf]);
+        __syncwarp();
       }
-      __syncwarp();
     }
   } else {
     const int qd = warp & 3;
@@ -737,23 +755,28 @@ __global__ void __launch_bounds__(192, 1)
     const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
     const int et = threadIdx.x - 64;
     const int64_t dd = (int64_t)dim * dim;
-    const float* mb = m + (int64_t)slot * dd;
-    // state image: rows = first index of M, contiguous = second index
+    // state / weight images: rows = first index of M, contiguous = second index
+    const float* ms[3] = {m0, m1, m2};
 #pragma unroll 1
-    for (int c0 = 0; c0 < 128; c0 += 32) {
-      float v[32];
+    for (int i = 0; i < NX; ++i) {
+      const float* mb = ms[i] + (int64_t)slot * m_stride;
+#pragma unroll 1
+      for (int c0 = 0; c0 < 128; c0 += 32) {
+        float v[32];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int c = c0 + i;
-        v[i] = ((int)row < dim && c < dim) ? mb[(int64_t)row * dim + c] : 0.f;
+        for (int k = 0; k < 32; ++k) {
+          const int c = c0 + k;
+          v[k] = ((int)row < dim && c < dim) ? mb[(int64_t)row * dim + c] : 0.f;
+        }
+        st_row32_bf16(mimg + i * kTileBytes, row, c0, v);
       }
-      st_row32_bf16(mimg, row, c0, v);
     }
+    (void)dd;
     fence_proxy_async_smem();
     named_bar_sync(1, 128);
     if (et == 0) mbar_arrive(m_ready);
-    // accumulate: the old O tile of block b is TMA-loaded into stage[buf] (once the store
-    // of block b-2 has read it) and added from shared memory, coalesced like the stores
+    // accumulate (NX = 1): the old O tile of block b is TMA-loaded into stage[buf] (once the
+    // store of block b-2 has read it) and added from shared memory, coalesced like the stores
     auto load_old = [&](int b) {
       const int buf = b & 1;
       if (b >= 2) tma_store_wait_read<0>();  // the store of block b-2 (the latest group) has read stage[buf]
@@ -762,16 +785,20 @@ __global__ void __launch_bounds__(192, 1)
       for (int bx = 0; bx < nbox; ++bx)
         tma_load_3d(stage + buf * kTileBytes + bx * kBoxBytes, &tm_o, &o_full[buf], 64 * bx, orow, slot);
     };
-    if (accumulate && et == 0 && nblk > 0) load_old(0);
+    const bool acc_old = NX == 1 && accumulate;
+    if (acc_old && et == 0 && nblk > 0) load_old(0);
     for (int b = 0; b < nblk; ++b) {
-      const int buf = b & 1;
-      if (accumulate && et == 0 && b + 1 < nblk) load_old(b + 1);
+      const int buf = b & 1, sbuf = C::kStages == 2 ? buf : 0;
+      if (acc_old && et == 0 && b + 1 < nblk) load_old(b + 1);
       mbar_wait(&acc_full[buf], (b >> 1) & 1);
       tc_fence_after();
-      if (accumulate) mbar_wait(&o_full[buf], (b >> 1) & 1);
-      else if (b >= 2 && et == 0) tma_store_wait_read<1>();
+      if (acc_old) mbar_wait(&o_full[buf], (b >> 1) & 1);
+      else if (et == 0) {
+        if (C::kStages == 2 && b >= 2) tma_store_wait_read<1>();
+        if (C::kStages == 1 && b >= 1) tma_store_wait_read<0>();
+      }
       named_bar_sync(1, 128);
-      uint8_t* st = stage + buf * kTileBytes;
+      uint8_t* st = stage + sbuf * kTileBytes;
 #pragma unroll 1
       for (int c0 = 0; c0 < 128; c0 += 32) {
         uint32_t r[32];
@@ -779,8 +806,8 @@ __global__ void __launch_bounds__(192, 1)
         tmem_ld_wait();
         float v[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        if (accumulate) ld_row32_add_bf16(st, row, c0, v);
+        for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(r[k]);
+        if (acc_old) ld_row32_add_bf16(st, row, c0, v);
         st_row32_bf16(st, row, c0, v);
       }
       fence_proxy_async_smem();
@@ -1175,13 +1202,16 @@ cudaError_t tc_backward_triple(const void* q, const void* k, const void* v, cons
   return launch_pdl(tc::tc_causal_chunk_kernel<2>, grid, dim3(tc::kCausalThreads), tc::kCausalSmem, s, 1, tm, a);
 }
 
-cudaError_t tc_apply_state(const void* x, const float* m, void* out, int64_t slots, int64_t tokens, int dim,
-                           int transpose, int accumulate, int sm_count, cudaStream_t s) {
-  CUtensorMap mx, mo;
+cudaError_t tc_apply_multi(const void* const* xs, const float* const* ms, int nx, int64_t m_stride, void* out,
+                           int64_t slots, int64_t tokens, int dim, int transpose, int accumulate, int sm_count,
+                           cudaStream_t s) {
+  tc::ApplyMaps tm;
+  CUtensorMap mo;
   cudaError_t e;
-  if ((e = make_tmap_3d(&mx, x, slots, tokens, dim)) != cudaSuccess) return e;
+  for (int i = 0; i < nx; ++i)
+    if ((e = make_tmap_3d(&tm.x[i], xs[i], slots, tokens, dim)) != cudaSuccess) return e;
+  for (int i = nx; i < 3; ++i) tm.x[i] = tm.x[0];
   if ((e = make_tmap_3d(&mo, out, slots, tokens, dim)) != cudaSuccess) return e;
-  if ((e = set_smem_once((const void*)tc::tc_apply_state_kernel, tc::kApplySmem)) != cudaSuccess) return e;
   const int64_t nblk = (tokens + tc::kTile - 1) / tc::kTile;
   // exactly one wave (one CTA per SM): ctas_per_slot * slots <= sm_count
   int64_t ctas = sm_count / slots;
@@ -1190,8 +1220,24 @@ cudaError_t tc_apply_state(const void* x, const float* m, void* out, int64_t slo
   const int bpc = (int)((nblk + ctas - 1) / ctas);
   ctas = (nblk + bpc - 1) / bpc;
   dim3 grid((unsigned)ctas, (unsigned)slots);
-  return launch_pdl(tc::tc_apply_state_kernel, grid, dim3(192), tc::kApplySmem, s, 1, mx, mo, m,
-                    (__nv_bfloat16*)out, tokens, dim, transpose, accumulate, bpc);
+  const float* m1 = nx > 1 ? ms[1] : ms[0];
+  const float* m2 = nx > 2 ? ms[2] : ms[0];
+  if (nx == 1) {
+    if ((e = set_smem_once((const void*)tc::tc_apply_state_kernel<1>, tc::ApplyCfg<1>::kSmem)) != cudaSuccess)
+      return e;
+    return launch_pdl(tc::tc_apply_state_kernel<1>, grid, dim3(192), tc::ApplyCfg<1>::kSmem, s, 1, tm, mo, ms[0],
+                      m1, m2, m_stride, (__nv_bfloat16*)out, tokens, dim, transpose, accumulate, bpc);
+  }
+  if ((e = set_smem_once((const void*)tc::tc_apply_state_kernel<3>, tc::ApplyCfg<3>::kSmem)) != cudaSuccess) return e;
+  return launch_pdl(tc::tc_apply_state_kernel<3>, grid, dim3(192), tc::ApplyCfg<3>::kSmem, s, 1, tm, mo, ms[0], m1,
+                    m2, m_stride, (__nv_bfloat16*)out, tokens, dim, transpose, 0, bpc);
+}
+
+cudaError_t tc_apply_state(const void* x, const float* m, void* out, int64_t slots, int64_t tokens, int dim,
+                           int transpose, int accumulate, int sm_count, cudaStream_t s) {
+  const void* xs[1] = {x};
+  const float* ms[1] = {m};
+  return tc_apply_multi(xs, ms, 1, (int64_t)dim * dim, out, slots, tokens, dim, transpose, accumulate, sm_count, s);
 }
 
 // Unmasked backward, fused: dM segment states (Q^T dO) and dQ = dO M^T in one pass.

@@ -240,6 +240,34 @@ def apply_state(x: torch.Tensor, m: torch.Tensor, transpose: bool = False,
     return out
 
 
+def project(xs: list[torch.Tensor], ws: list[torch.Tensor], transpose: bool = False,
+            out: torch.Tensor | None = None, accumulate: bool = False) -> torch.Tensor:
+    """out (+)= sum_i xs[i] op(ws[i]) per slot, op(W) = W or W^T, every W one [d, d] weight
+    shared by all slots (header: lasp2_project; hybrid.py:136-151). len(xs) is 1 or 3."""
+    import ctypes
+
+    require_cuda(*xs, *ws)
+    x0 = xs[0]
+    slots, n, d = _slots(x0)
+    if len(xs) != len(ws) or len(xs) not in (1, 3):
+        raise ValueError("project takes one or three (input, weight) pairs")
+    sd = state_dtype(x0.dtype)
+    for x, w in zip(xs, ws):
+        if x.shape != x0.shape or x.dtype != x0.dtype or not x.is_contiguous():
+            raise ValueError(f"projection inputs differ: {tuple(x.shape)} {x.dtype}")
+        if tuple(w.shape) != (d, d) or w.dtype != sd or not w.is_contiguous():
+            raise ValueError(f"weight {tuple(w.shape)} {w.dtype} is not a contiguous ({d}, {d}) {sd} matrix")
+    if out is None:
+        if accumulate:
+            raise ValueError("accumulate needs an output tensor")
+        out = torch.empty_like(x0)
+    xp = (ctypes.c_void_p * 3)(*[x.data_ptr() for x in xs])
+    wp = (ctypes.c_void_p * 3)(*[w.data_ptr() for w in ws])
+    call("lasp2_project", dtype_code(x0.dtype), ctypes.addressof(xp), ctypes.addressof(wp), len(xs), ptr(out), slots,
+         n, d, int(transpose), int(accumulate), stream_ptr())
+    return out
+
+
 def state_apply(q: torch.Tensor, d_out: torch.Tensor, m: torch.Tensor, nseg: int) -> tuple[torch.Tensor, torch.Tensor]:
     """(dM segment states Q^T dO, dq = dO M^T) in one pass (header: lasp2_state_apply)."""
     require_cuda(q, d_out, m)

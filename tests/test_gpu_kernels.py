@@ -314,3 +314,32 @@ def test_nomask_local_workspace_validation():
     with pytest.raises(ValueError, match="workspace too small"):
         ops.call("lasp2_nomask_forward_local", _lib.BF16, ops.ptr(x), ops.ptr(x), ops.ptr(x), ops.ptr(x),
                  ops.ptr(m), ops.ptr(small), small.numel(), 2, 256, 128, ops.stream_ptr())
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32, torch.float64])
+@pytest.mark.parametrize("shape", [(1, 4, 640, 128), (2, 2, 300, 64)])
+def test_project_shared_weights(dtype, shape):
+    """lasp2_project (hybrid.py:136-151): X W and X W^T with one weight for every slot, the
+    accumulate form, and the three-term chain-rule sum dQ W_Q^T + dK W_K^T + dV W_V^T
+    (one accumulator) against an f64 torch reference of the same rounded operands."""
+    d = shape[-1]
+    sd = torch.float64 if dtype == torch.float64 else torch.float32
+    xs = [rand(shape, dtype, 70 + i) for i in range(3)]
+    ws = [rand((d, d), dtype, 80 + i).to(sd) for i in range(3)]  # weights rounded to the data dtype
+    tol = {torch.bfloat16: 1e-2, torch.float32: 1e-5, torch.float64: 1e-12}[dtype]
+
+    def ref(terms):
+        return sum(x.double() @ w.double() for x, w in terms)
+
+    def err(got, want):
+        return ((got.double() - want).abs().max() / want.abs().max()).item()
+
+    assert err(ops.project([xs[0]], [ws[0]]), ref([(xs[0], ws[0])])) <= tol
+    assert err(ops.project([xs[0]], [ws[0]], transpose=True), ref([(xs[0], ws[0].t())])) <= tol
+    out = ops.project([xs[0]], [ws[0]])
+    ops.project([xs[1]], [ws[1]], out=out, accumulate=True)
+    assert err(out, ref([(xs[0], ws[0]), (xs[1], ws[1])])) <= 2 * tol
+    three = ops.project(xs, ws, transpose=True)
+    assert err(three, ref([(x, w.t()) for x, w in zip(xs, ws)])) <= tol
+    with pytest.raises(ValueError):
+        ops.project(xs[:2], ws[:2])
