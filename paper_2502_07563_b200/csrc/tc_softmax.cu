@@ -1121,28 +1121,41 @@ __global__ void __launch_bounds__(kSmBwdThreads, 1)
       tmem_ld_32x32b_x32(t_r0 + lane_off + cb + 32, rt);
       tmem_ld_wait();
       named_bar_sync(bar_id, 128);  // publishes this block's stats (written last iteration)
-      // ---- P^T = exp2(S^T * scale*log2e - lse*log2e), this half's 64 query columns
+      // ---- P^T = exp2(S^T * scale*log2e - lse*log2e), this half's 64 query columns; the
+      // causal / ragged mask is resolved per warp: rows entirely inside or outside the
+      // visible columns skip the per-element tests (only diagonal and tail blocks pay them)
       uint32_t ppk[32];
+      const bool all_in = __all_sync(0xffffffffu, cmin <= cb && cmax >= cb + 64);
+      const bool all_out = __all_sync(0xffffffffu, cmin >= cb + 64 || cmax <= cb);
+      if (all_out) {
 #pragma unroll
-      for (int c = 0; c < 64; c += 4) {
-        const int col = cb + c;
-        const float4 l4 = *reinterpret_cast<const float4*>(my_stats + c);  // smem broadcast
-        const uint32_t* src = c < 32 ? rs + c : rt + (c - 32);
-        float p[4];
-        const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+        for (int e = 0; e < 32; ++e) ppk[e] = 0u;
+      } else if (all_in) {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const bool ok = col + e >= cmin && col + e < cmax;
-          const float x = fmaf(__uint_as_float(src[e]), a.scale_log2, -lv[e]);
-#ifdef LASP2_BWD_POLY  // every LASP2_BWD_POLY-th group on the FMA pipe: measured no gain (4: same, 2: -1.5 %)
-          const float y = ((c >> 2) % LASP2_BWD_POLY == LASP2_BWD_POLY - 1) ? ex2_poly(x) : ex2_approx(x);
-#else
-          const float y = ex2_approx(x);
-#endif
-          p[e] = ok ? y : 0.f;
+        for (int c = 0; c < 64; c += 4) {
+          const float4 l4 = *reinterpret_cast<const float4*>(my_stats + c);  // smem broadcast
+          const uint32_t* src = c < 32 ? rs + c : rt + (c - 32);
+          ppk[c >> 1] = pack_bf16x2(ex2_approx(fmaf(__uint_as_float(src[0]), a.scale_log2, -l4.x)),
+                                    ex2_approx(fmaf(__uint_as_float(src[1]), a.scale_log2, -l4.y)));
+          ppk[(c >> 1) + 1] = pack_bf16x2(ex2_approx(fmaf(__uint_as_float(src[2]), a.scale_log2, -l4.z)),
+                                          ex2_approx(fmaf(__uint_as_float(src[3]), a.scale_log2, -l4.w)));
         }
-        ppk[c >> 1] = pack_bf16x2(p[0], p[1]);
-        ppk[(c >> 1) + 1] = pack_bf16x2(p[2], p[3]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 64; c += 4) {
+          const int col = cb + c;
+          const float4 l4 = *reinterpret_cast<const float4*>(my_stats + c);
+          const uint32_t* src = c < 32 ? rs + c : rt + (c - 32);
+          float p[4];
+          const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const bool ok = col + e >= cmin && col + e < cmax;
+            p[e] = ok ? ex2_approx(fmaf(__uint_as_float(src[e]), a.scale_log2, -lv[e])) : 0.f;
+          }
+          ppk[c >> 1] = pack_bf16x2(p[0], p[1]);
+          ppk[(c >> 1) + 1] = pack_bf16x2(p[2], p[3]);
+        }
       }
       tmem_st_32x32b_x32(t_r0 + lane_off + cb, ppk);  // P^T packed over this half's S^T columns
       if (eh == 0 && h == 0) tr(21, i);
