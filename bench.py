@@ -587,8 +587,7 @@ def run_gpu_arm(args) -> None:
     else:
         ctx = comm.LocalRankContext()
     peaks = load_peaks()
-    # the peer exchange's epochs are host counters: it cannot be replayed from a CUDA graph
-    use_graph = not args.eager and not (world > 1 and args.state_exchange == "peer")
+    use_graph = not args.eager
     main = measure_workload(args.workload, ctx, rank, world, args.steps, args.warmup, device, use_graph)
     sec_name = "cfg3" if args.workload == "cfg2" else "cfg2"
     secondary = None if args.no_secondary else measure_workload(sec_name, ctx, rank, world, args.steps, args.warmup,

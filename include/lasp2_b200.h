@@ -74,12 +74,23 @@ int lasp2_scan_segments(int dtype, void* seg_states, void* chunk_total, int64_t 
  * lasp2_exchange_ack then sets acks[rank] = epoch on every rank (`peer_acks`,
  * device array of nranks pointers to uint64[nranks]). Before a put of epoch
  * e > 2 the caller waits on its own acks[0..nranks) for e - 2, so no reader
- * still needs the half being overwritten. */
+ * still needs the half being overwritten.
+ * Device-resident epoch (`epoch_dev`, a zeroed uint64 per rank and exchange; NULL =
+ * the host `epoch` above): lasp2_scan_put uses *epoch_dev + 1 and stores it back,
+ * the other calls use *epoch_dev + (int64_t)epoch (an offset: 0 for this
+ * exchange's flags and acks, -1 for the back-pressure wait before the next put),
+ * and lasp2_exchange_fold folds half (*epoch_dev & 1). Every value is read on the
+ * device, so a captured CUDA graph advances the exchange on each replay. */
 int lasp2_scan_put(int dtype, void* seg_states, void* chunk_total, int64_t slots, int nseg, int dim, int reverse,
                    const void* peer_recv, const void* peer_flags, int rank, int nranks, uint64_t epoch, void* done,
-                   void* stream);
-int lasp2_exchange_wait(const void* flags, int lo, int hi, uint64_t epoch, void* stream);
-int lasp2_exchange_ack(const void* peer_acks, int rank, int nranks, uint64_t epoch, void* stream);
+                   void* epoch_dev, void* stream);
+int lasp2_exchange_wait(const void* flags, int lo, int hi, uint64_t epoch, const void* epoch_dev, void* stream);
+int lasp2_exchange_ack(const void* peer_acks, int rank, int nranks, uint64_t epoch, const void* epoch_dev,
+                       void* stream);
+/* lasp2_fold_states over half (*epoch_dev & 1) of a receive buffer whose halves are
+ * half_elems apart. */
+int lasp2_exchange_fold(int dtype, const void* recv, int64_t half_elems, const void* epoch_dev, void* out,
+                        int nstates, int64_t elems, int mode, int bound, void* stream);
 
 /* out = ordered fold of `nstates` gathered states, each `elems` elements,
  * stored rank-major ([nstates][elems], the all_gather layout):
@@ -112,14 +123,17 @@ int lasp2_causal_chunk(int dtype, const void* q, const void* k, const void* v, c
  * the wait and fold launches between the collective and its consumer.
  * xflags = NULL: no wait — `xrecv` is a complete rank-major all_gather result
  * already ordered before `stream` (the NCCL path: the prefix / suffix fold of
- * the gathered states fused into the consumer's prologue, no fold launch). */
+ * the gathered states fused into the consumer's prologue, no fold launch).
+ * epoch_dev != NULL: the epoch is *epoch_dev (device-resident, see lasp2_scan_put)
+ * and `xrecv` is the whole receive buffer, the half (epoch & 1) half_elems apart. */
 int lasp2_causal_chunk_x(const void* q, const void* k, const void* v, const void* seg_states, const void* xrecv,
-                         const void* xflags, int lo, int hi, int descending, uint64_t epoch, void* base_out, void* out,
-                         int64_t slots, int64_t tokens, int dim, int nseg, int reverse, int transpose_state,
-                         void* stream);
+                         const void* xflags, int lo, int hi, int descending, uint64_t epoch, const void* epoch_dev,
+                         int64_t half_elems, void* base_out, void* out, int64_t slots, int64_t tokens, int dim,
+                         int nseg, int reverse, int transpose_state, void* stream);
 int lasp2_dkdv_chunk_x(const void* q, const void* k, const void* v, const void* d_out, const void* seg_states,
-                       const void* xrecv, const void* xflags, int lo, int hi, uint64_t epoch, void* dk, void* dv,
-                       int64_t slots, int64_t tokens, int dim, int nseg, void* stream);
+                       const void* xrecv, const void* xflags, int lo, int hi, uint64_t epoch, const void* epoch_dev,
+                       int64_t half_elems, void* dk, void* dv, int64_t slots, int64_t tokens, int dim, int nseg,
+                       void* stream);
 
 /* Masked backward dQ of one rank's chunk plus the dM segment states, one pass:
  *   dq_s = sum_{i<=s} (do_s.v_i) k_i + do_s S_s^T,  S_s = fwd_base + fwd_seg[seg(s)]

@@ -32,13 +32,14 @@ SIGNATURES = {
     "lasp2_scan_segments": (_int, [_int, _vp, _vp, _i64, _int, _int, _int, _vp]),
     "lasp2_fold_states": (_int, [_int, _vp, _vp, _int, _i64, _int, _int, _vp]),
     "lasp2_causal_chunk": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _int, _int, _int, _int, _vp]),
-    "lasp2_scan_put": (_int, [_int, _vp, _vp, _i64, _int, _int, _int, _vp, _vp, _int, _int, _u64, _vp, _vp]),
-    "lasp2_exchange_wait": (_int, [_vp, _int, _int, _u64, _vp]),
-    "lasp2_exchange_ack": (_int, [_vp, _int, _int, _u64, _vp]),
-    "lasp2_causal_chunk_x": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _int, _int, _int, _u64, _vp, _vp, _i64, _i64, _int,
-                                    _int, _int, _int, _vp]),
-    "lasp2_dkdv_chunk_x": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _int, _int, _u64, _vp, _vp, _i64, _i64, _int,
-                                  _int, _vp]),
+    "lasp2_scan_put": (_int, [_int, _vp, _vp, _i64, _int, _int, _int, _vp, _vp, _int, _int, _u64, _vp, _vp, _vp]),
+    "lasp2_exchange_wait": (_int, [_vp, _int, _int, _u64, _vp, _vp]),
+    "lasp2_exchange_ack": (_int, [_vp, _int, _int, _u64, _vp, _vp]),
+    "lasp2_exchange_fold": (_int, [_int, _vp, _i64, _vp, _vp, _int, _i64, _int, _int, _vp]),
+    "lasp2_causal_chunk_x": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _int, _int, _int, _u64, _vp, _i64, _vp, _vp, _i64,
+                                    _i64, _int, _int, _int, _int, _vp]),
+    "lasp2_dkdv_chunk_x": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _int, _int, _u64, _vp, _i64, _vp, _vp, _i64,
+                                  _i64, _int, _int, _vp]),
     "lasp2_dq_chunk": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _int, _int, _vp]),
     "lasp2_dkdv_chunk": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _int, _int, _vp]),
     "lasp2_project": (_int, [_int, _vp, _vp, _int, _vp, _i64, _i64, _int, _int, _int, _vp]),

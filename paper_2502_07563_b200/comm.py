@@ -129,7 +129,9 @@ class PeerExchange:
     finished folding (back-pressure for this rank's puts), ``*_table`` device
     arrays of every rank's buffer / flag / ack addresses (peer addresses over
     NVLink with symmetric memory; same-device addresses in the threads-as-ranks
-    world), ``done`` the put kernel's completion counter. ``ops.scan_put``
+    world), ``done`` the put kernel's completion counter, ``ep`` this rank's
+    device-resident epoch (advanced by the put kernel itself, so a captured
+    CUDA graph advances the exchange on every replay). ``ops.scan_put``
     writes, ``ops.exchange_fold`` waits, folds and acknowledges.
     """
 
@@ -139,7 +141,8 @@ class PeerExchange:
         self.rank, self.nranks = rank, nranks
         self.recv, self.flags, self.acks, self.done = recv, flags, acks, done
         self.recv_table, self.flag_table, self.ack_table = recv_table, flag_table, ack_table
-        self.epoch = 0
+        self.ep = torch.zeros(1, dtype=torch.int64, device=recv.device)
+        self.epoch = 0  # host count of exchanges issued (eager runs; a graph replay does not advance it)
 
     def next_epoch(self) -> int:
         self.epoch += 1

@@ -103,30 +103,46 @@ int lasp2_scan_segments(int dtype, void* seg_states, void* chunk_total, int64_t 
 
 int lasp2_scan_put(int dtype, void* seg_states, void* chunk_total, int64_t slots, int nseg, int dim, int reverse,
                    const void* peer_recv, const void* peer_flags, int rank, int nranks, uint64_t epoch, void* done,
-                   void* stream) {
+                   void* epoch_dev, void* stream) {
   CHECK(valid_dtype(dtype), "scan_put: unknown dtype");
   CHECK(seg_states && peer_recv && peer_flags && done, "scan_put: null pointer");
   CHECK(slots >= 1 && nseg >= 1 && dim >= 1, "scan_put: bad shape");
   CHECK(nranks >= 1 && rank >= 0 && rank < nranks, "scan_put: rank outside [0, nranks)");
-  CHECK(epoch >= 1, "scan_put: epochs start at 1");
+  CHECK(epoch >= 1 || epoch_dev, "scan_put: epochs start at 1");
   cudaError_t e = dtype == LASP2_F64
                       ? lasp::scan_put<double>(seg_states, chunk_total, slots, nseg, dim, reverse, peer_recv,
-                                               peer_flags, rank, nranks, epoch, (unsigned*)done, S(stream))
+                                               peer_flags, rank, nranks, epoch, (unsigned*)done, S(stream), epoch_dev)
                       : lasp::scan_put<float>(seg_states, chunk_total, slots, nseg, dim, reverse, peer_recv,
-                                              peer_flags, rank, nranks, epoch, (unsigned*)done, S(stream));
+                                              peer_flags, rank, nranks, epoch, (unsigned*)done, S(stream), epoch_dev);
   return cuda_status(e, "scan_put");
 }
 
-int lasp2_exchange_wait(const void* flags, int lo, int hi, uint64_t epoch, void* stream) {
+int lasp2_exchange_wait(const void* flags, int lo, int hi, uint64_t epoch, const void* epoch_dev, void* stream) {
   CHECK(flags, "exchange_wait: null pointer");
   CHECK(lo >= 0 && hi >= lo, "exchange_wait: bad range");
-  return cuda_status(lasp::exchange_wait(flags, lo, hi, epoch, S(stream)), "exchange_wait");
+  return cuda_status(lasp::exchange_wait(flags, lo, hi, epoch, S(stream), epoch_dev), "exchange_wait");
 }
 
-int lasp2_exchange_ack(const void* peer_acks, int rank, int nranks, uint64_t epoch, void* stream) {
+int lasp2_exchange_ack(const void* peer_acks, int rank, int nranks, uint64_t epoch, const void* epoch_dev,
+                       void* stream) {
   CHECK(peer_acks, "exchange_ack: null pointer");
   CHECK(nranks >= 1 && rank >= 0 && rank < nranks, "exchange_ack: rank outside [0, nranks)");
-  return cuda_status(lasp::exchange_ack(peer_acks, rank, nranks, epoch, S(stream)), "exchange_ack");
+  return cuda_status(lasp::exchange_ack(peer_acks, rank, nranks, epoch, S(stream), epoch_dev), "exchange_ack");
+}
+
+int lasp2_exchange_fold(int dtype, const void* recv, int64_t half_elems, const void* epoch_dev, void* out,
+                        int nstates, int64_t elems, int mode, int bound, void* stream) {
+  CHECK(valid_dtype(dtype), "exchange_fold: unknown dtype");
+  CHECK(recv && epoch_dev && out, "exchange_fold: null pointer");
+  CHECK(nstates >= 1 && elems >= 1 && half_elems >= (int64_t)nstates * elems, "exchange_fold: bad shape");
+  CHECK(mode >= 0 && mode <= 2, "exchange_fold: bad mode");
+  CHECK(mode == LASP2_FOLD_FULL || (bound >= 0 && bound <= nstates), "exchange_fold: bound outside [0, nstates]");
+  cudaError_t e = dtype == LASP2_F64
+                      ? lasp::exchange_fold<double>(recv, half_elems, epoch_dev, out, nstates, elems, mode, bound,
+                                                    S(stream))
+                      : lasp::exchange_fold<float>(recv, half_elems, epoch_dev, out, nstates, elems, mode, bound,
+                                                   S(stream));
+  return cuda_status(e, "exchange_fold");
 }
 
 int lasp2_fold_states(int dtype, const void* gathered, void* out, int nstates, int64_t elems, int mode, int bound,
@@ -167,9 +183,9 @@ int lasp2_causal_chunk(int dtype, const void* q, const void* k, const void* v, c
 }
 
 int lasp2_causal_chunk_x(const void* q, const void* k, const void* v, const void* seg_states, const void* xrecv,
-                         const void* xflags, int lo, int hi, int descending, uint64_t epoch, void* base_out, void* out,
-                         int64_t slots, int64_t tokens, int dim, int nseg, int reverse, int transpose_state,
-                         void* stream) {
+                         const void* xflags, int lo, int hi, int descending, uint64_t epoch, const void* epoch_dev,
+                         int64_t half_elems, void* base_out, void* out, int64_t slots, int64_t tokens, int dim,
+                         int nseg, int reverse, int transpose_state, void* stream) {
   CHECK(q && k && v && out && xrecv, "causal_chunk_x: null pointer");
   CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128, "causal_chunk_x: bad shape (1 <= dim <= 128)");
   CHECK(nseg >= 1 && nseg <= (tokens + LASP_BLOCK_TOKENS - 1) / LASP_BLOCK_TOKENS, "causal_chunk_x: bad nseg");
@@ -177,22 +193,24 @@ int lasp2_causal_chunk_x(const void* q, const void* k, const void* v, const void
   CHECK(lo >= 0 && hi >= lo, "causal_chunk_x: bad rank range");
   CHECK(use_tc(LASP2_BF16, dim, tokens), "causal_chunk_x: bf16 tensor-core path only (fold, then lasp2_causal_chunk)");
   const lasp::XFold x{(const float*)xrecv, (const unsigned long long*)xflags, lo, hi, descending, epoch,
-                      (float*)base_out};
+                      (float*)base_out, (const unsigned long long*)epoch_dev, half_elems};
   return cuda_status(lasp::tc_causal_chunk(q, k, v, (const float*)seg_states, nullptr, out, slots, tokens, dim, nseg,
                                            reverse, transpose_state, S(stream), &x),
                      "causal_chunk_x");
 }
 
 int lasp2_dkdv_chunk_x(const void* q, const void* k, const void* v, const void* d_out, const void* seg_states,
-                       const void* xrecv, const void* xflags, int lo, int hi, uint64_t epoch, void* dk, void* dv,
-                       int64_t slots, int64_t tokens, int dim, int nseg, void* stream) {
+                       const void* xrecv, const void* xflags, int lo, int hi, uint64_t epoch, const void* epoch_dev,
+                       int64_t half_elems, void* dk, void* dv, int64_t slots, int64_t tokens, int dim, int nseg,
+                       void* stream) {
   CHECK(q && k && v && d_out && dk && dv && xrecv, "dkdv_chunk_x: null pointer");
   CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128, "dkdv_chunk_x: bad shape (1 <= dim <= 128)");
   CHECK(nseg >= 1 && nseg <= (tokens + LASP_BLOCK_TOKENS - 1) / LASP_BLOCK_TOKENS, "dkdv_chunk_x: bad nseg");
   CHECK(nseg == 1 || seg_states, "dkdv_chunk_x: nseg > 1 needs segment states");
   CHECK(lo >= 0 && hi >= lo, "dkdv_chunk_x: bad rank range");
   CHECK(use_tc(LASP2_BF16, dim, tokens), "dkdv_chunk_x: bf16 tensor-core path only (fold, then lasp2_dkdv_chunk)");
-  const lasp::XFold x{(const float*)xrecv, (const unsigned long long*)xflags, lo, hi, 1, epoch, nullptr};
+  const lasp::XFold x{(const float*)xrecv, (const unsigned long long*)xflags, lo, hi, 1, epoch, nullptr,
+                      (const unsigned long long*)epoch_dev, half_elems};
   return cuda_status(lasp::tc_dkdv_pair(q, k, v, d_out, (const float*)seg_states, nullptr, dk, dv, slots, tokens, dim,
                                         nseg, S(stream), &x),
                      "dkdv_chunk_x");

@@ -33,9 +33,15 @@ cudaError_t scan_states(void* seg, void* total, int64_t slots, int nseg, int dim
 template <typename A>
 cudaError_t scan_put(void* seg, void* total, int64_t slots, int nseg, int dim, int reverse, const void* peer_recv,
                      const void* peer_flags, int rank, int nranks, unsigned long long epoch, unsigned* done,
-                     cudaStream_t s);
-cudaError_t exchange_wait(const void* flags, int lo, int hi, unsigned long long epoch, cudaStream_t s);
-cudaError_t exchange_ack(const void* peer_acks, int rank, int nranks, unsigned long long epoch, cudaStream_t s);
+                     cudaStream_t s, void* epoch_dev = nullptr);
+// epoch_dev != null: the epoch is *epoch_dev + (signed) epoch, read on the device
+cudaError_t exchange_wait(const void* flags, int lo, int hi, unsigned long long epoch, cudaStream_t s,
+                          const void* epoch_dev = nullptr);
+cudaError_t exchange_ack(const void* peer_acks, int rank, int nranks, unsigned long long epoch, cudaStream_t s,
+                         const void* epoch_dev = nullptr);
+template <typename A>
+cudaError_t exchange_fold(const void* recv, int64_t half_elems, const void* epoch_dev, void* out, int nstates,
+                          int64_t elems, int mode, int bound, cudaStream_t s);
 template <typename A>
 cudaError_t fold_states(const void* gathered, void* out, int nstates, int64_t elems, int mode, int bound,
                         cudaStream_t s);
@@ -51,11 +57,13 @@ cudaError_t tc_segment_states(const void* x, const void* y, float* out, int64_t 
 // rank-level base is folded from this epoch's receive half once the flags of
 // ranks [lo, hi) carry `epoch` (see CausalArgs in tc_linear.cu).
 struct XFold {
-  const float* recv;                // [T][slots][dim][dim]
+  const float* recv;                // [T][slots][dim][dim] (with epoch_dev: [2][T][...], half by epoch parity)
   const unsigned long long* flags;  // [T]
   int lo, hi, descending;
   unsigned long long epoch;
   float* base_out;                  // folded base per slot, or null
+  const unsigned long long* epoch_dev = nullptr;  // device-resident epoch (graph-capturable exchange)
+  int64_t half_elems = 0;           // elements of one receive half
 };
 cudaError_t tc_causal_chunk(const void* q, const void* k, const void* v, const float* seg_states, const float* base,
                             void* out, int64_t slots, int64_t tokens, int dim, int nseg, int reverse,

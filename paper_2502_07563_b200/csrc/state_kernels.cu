@@ -121,9 +121,13 @@ template <typename A>
 __global__ void scan_put_kernel(A* __restrict__ seg, A* __restrict__ total, int64_t slots, int nseg, int64_t dd,
                                 int reverse, A* const* __restrict__ peer_recv,
                                 unsigned long long* const* __restrict__ peer_flags, int rank, int nranks,
-                                unsigned long long epoch, unsigned* __restrict__ done) {
+                                unsigned long long epoch, unsigned* __restrict__ done,
+                                unsigned long long* __restrict__ epoch_dev) {
   ptx::pdl_wait();
   ptx::pdl_launch_dependents();
+  // device-resident epoch (graph replays advance it): this exchange is *epoch_dev + 1, stored
+  // back by the last block, after every block has read the old value
+  if (epoch_dev != nullptr) epoch = *(volatile unsigned long long*)epoch_dev + 1;
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = slots * dd;
   const int64_t off = ((int64_t)(epoch & 1) * nranks + rank) * n;
@@ -154,23 +158,55 @@ __global__ void scan_put_kernel(A* __restrict__ seg, A* __restrict__ total, int6
   __syncthreads();
   if (threadIdx.x == 0 && atomicAdd(done, 1u) == gridDim.x - 1) {
     *done = 0;  // every block has stored and fenced: re-arm for the next exchange
+    if (epoch_dev != nullptr) *epoch_dev = epoch;
     __threadfence_system();
     for (int r = 0; r < nranks; ++r) st_release_sys_u64(peer_flags[r] + rank, epoch);
   }
 }
 
+// the epoch a peer kernel works on: the host value, or *epoch_dev + offset (signed)
+__device__ __forceinline__ long long effective_epoch(unsigned long long epoch, const unsigned long long* epoch_dev) {
+  return epoch_dev != nullptr ? (long long)*(volatile const unsigned long long*)epoch_dev + (long long)epoch
+                              : (long long)epoch;
+}
+
 // Block until flags[lo..hi) all carry `epoch` (or a later one). One thread; a
 // peer that never arrives traps after ~2^36 cycles instead of hanging the GPU.
 __global__ void exchange_wait_kernel(const unsigned long long* __restrict__ flags, int lo, int hi,
-                                     unsigned long long epoch) {
-  wait_epochs(flags, lo, hi, epoch);
+                                     unsigned long long epoch, const unsigned long long* __restrict__ epoch_dev) {
+  const long long e = effective_epoch(epoch, epoch_dev);
+  if (e > 0) wait_epochs(flags, lo, hi, (unsigned long long)e);
 }
 
 // After this rank's fold of `epoch` (stream order): acks[rank] = epoch on every rank.
 __global__ void exchange_ack_kernel(unsigned long long* const* __restrict__ peer_acks, int rank, int nranks,
-                                    unsigned long long epoch) {
+                                    unsigned long long epoch, const unsigned long long* __restrict__ epoch_dev) {
+  const unsigned long long e = (unsigned long long)effective_epoch(epoch, epoch_dev);
   __threadfence_system();
-  for (int r = 0; r < nranks; ++r) st_release_sys_u64(peer_acks[r] + rank, epoch);
+  for (int r = 0; r < nranks; ++r) st_release_sys_u64(peer_acks[r] + rank, e);
+}
+
+// fold of the receive half of the current device epoch: recv + (e & 1) * half_elems
+template <typename A>
+__global__ void exchange_fold_kernel(const A* __restrict__ recv, int64_t half_elems,
+                                     const unsigned long long* __restrict__ epoch_dev, A* __restrict__ out,
+                                     int nstates, int64_t elems, int mode, int bound) {
+  const unsigned long long e = *(volatile const unsigned long long*)epoch_dev;
+  const A* gathered = recv + (int64_t)(e & 1) * half_elems;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= elems) return;
+  A acc = A(0);
+  const int lo = mode == 1 ? bound : 0, hi = mode == 1 ? nstates : (mode == 2 ? nstates : bound);
+  if (hi > lo) {
+    if (mode == 1) {  // descending from the last (numerics.py:93-116)
+      acc = gathered[(int64_t)(hi - 1) * elems + idx];
+      for (int i = hi - 2; i >= lo; --i) acc += gathered[(int64_t)i * elems + idx];
+    } else {  // ascending from the first (numerics.py:71-90)
+      acc = gathered[idx];
+      for (int i = 1; i < hi; ++i) acc += gathered[(int64_t)i * elems + idx];
+    }
+  }
+  out[idx] = acc;
 }
 
 // gathered: [nstates][elems]. mode 0 = prefix(bound), 1 = suffix(bound), 2 = full.
@@ -319,24 +355,40 @@ cudaError_t scan_states(void* seg, void* total, int64_t slots, int nseg, int dim
 template <typename A>
 cudaError_t scan_put(void* seg, void* total, int64_t slots, int nseg, int dim, int reverse, const void* peer_recv,
                      const void* peer_flags, int rank, int nranks, unsigned long long epoch, unsigned* done,
-                     cudaStream_t s) {
+                     cudaStream_t s, void* epoch_dev) {
   const int64_t dd = (int64_t)dim * dim;
   const int64_t n = slots * dd;
   return launch_pdl(scan_put_kernel<A>, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, 1, (A*)seg, (A*)total,
                     slots, nseg, dd, reverse, (A* const*)peer_recv, (unsigned long long* const*)peer_flags, rank,
-                    nranks, epoch, done);
+                    nranks, epoch, done, (unsigned long long*)epoch_dev);
 }
 
-cudaError_t exchange_wait(const void* flags, int lo, int hi, unsigned long long epoch, cudaStream_t s) {
+cudaError_t exchange_wait(const void* flags, int lo, int hi, unsigned long long epoch, cudaStream_t s,
+                          const void* epoch_dev) {
   if (hi <= lo) return cudaSuccess;
-  exchange_wait_kernel<<<1, 1, 0, s>>>((const unsigned long long*)flags, lo, hi, epoch);
+  exchange_wait_kernel<<<1, 1, 0, s>>>((const unsigned long long*)flags, lo, hi, epoch,
+                                       (const unsigned long long*)epoch_dev);
   return cudaGetLastError();
 }
 
-cudaError_t exchange_ack(const void* peer_acks, int rank, int nranks, unsigned long long epoch, cudaStream_t s) {
-  exchange_ack_kernel<<<1, 1, 0, s>>>((unsigned long long* const*)peer_acks, rank, nranks, epoch);
+cudaError_t exchange_ack(const void* peer_acks, int rank, int nranks, unsigned long long epoch, cudaStream_t s,
+                         const void* epoch_dev) {
+  exchange_ack_kernel<<<1, 1, 0, s>>>((unsigned long long* const*)peer_acks, rank, nranks, epoch,
+                                      (const unsigned long long*)epoch_dev);
   return cudaGetLastError();
 }
+
+template <typename A>
+cudaError_t exchange_fold(const void* recv, int64_t half_elems, const void* epoch_dev, void* out, int nstates,
+                          int64_t elems, int mode, int bound, cudaStream_t s) {
+  exchange_fold_kernel<A><<<(unsigned)((elems + 255) / 256), 256, 0, s>>>(
+      (const A*)recv, half_elems, (const unsigned long long*)epoch_dev, (A*)out, nstates, elems, mode, bound);
+  return cudaGetLastError();
+}
+template cudaError_t exchange_fold<float>(const void*, int64_t, const void*, void*, int, int64_t, int, int,
+                                          cudaStream_t);
+template cudaError_t exchange_fold<double>(const void*, int64_t, const void*, void*, int, int64_t, int, int,
+                                           cudaStream_t);
 
 template <typename A>
 cudaError_t fold_states(const void* gathered, void* out, int nstates, int64_t elems, int mode, int bound,
@@ -364,9 +416,9 @@ cudaError_t gen_slots(uint64_t seed, const uint64_t* tag_words, void* out, int64
 template cudaError_t scan_states<float>(void*, void*, int64_t, int, int, int, cudaStream_t);
 template cudaError_t scan_states<double>(void*, void*, int64_t, int, int, int, cudaStream_t);
 template cudaError_t scan_put<float>(void*, void*, int64_t, int, int, int, const void*, const void*, int, int,
-                                     unsigned long long, unsigned*, cudaStream_t);
+                                     unsigned long long, unsigned*, cudaStream_t, void*);
 template cudaError_t scan_put<double>(void*, void*, int64_t, int, int, int, const void*, const void*, int, int,
-                                      unsigned long long, unsigned*, cudaStream_t);
+                                      unsigned long long, unsigned*, cudaStream_t, void*);
 template cudaError_t fold_states<float>(const void*, void*, int, int64_t, int, int, cudaStream_t);
 template cudaError_t fold_states<double>(const void*, void*, int, int64_t, int, int, cudaStream_t);
 template cudaError_t gen_slots<float>(uint64_t, const uint64_t*, void*, int64_t, int64_t, int64_t, int64_t, cudaStream_t);

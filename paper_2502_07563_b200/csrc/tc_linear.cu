@@ -152,6 +152,8 @@ struct CausalArgs {
   const unsigned long long* xflags = nullptr;
   int xlo = 0, xhi = 0, xdesc = 0;
   unsigned long long xepoch = 0;
+  const unsigned long long* xepoch_dev = nullptr;  // device epoch: recv half (e & 1) * xhalf, flags >= e
+  int64_t xhalf = 0;
   float* base_out = nullptr;  // the folded base of each slot (written by its segment-0 CTA), or null
 };
 
@@ -437,11 +439,15 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       }
       const bool fold = a.xrecv != nullptr && a.xhi > a.xlo;
       if (et == 0) span(12);  // epilogue start
+      // device-resident epoch (graph replays): the producer's scan_put, earlier on this stream, set it
+      const unsigned long long xep =
+          a.xepoch_dev != nullptr ? *(volatile const unsigned long long*)a.xepoch_dev : a.xepoch;
+      const float* xrecv = a.xepoch_dev != nullptr ? a.xrecv + (int64_t)(xep & 1) * a.xhalf : a.xrecv;
       if (a.xrecv != nullptr && a.xflags != nullptr) {  // wait for the ranks this fold needs (TMA / MMA run ahead)
         if (et == 0) {
           for (int j = a.xlo; j < a.xhi; ++j) {
             const long long t0 = clock64();
-            while (ld_acquire_sys_u64(a.xflags + j) < a.xepoch) {
+            while (ld_acquire_sys_u64(a.xflags + j) < xep) {
               __nanosleep(64);
               if (clock64() - t0 > (1ll << 36)) __trap();  // a peer never arrived: fail loudly
             }
@@ -450,7 +456,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
         named_bar_sync(1, kEpi);
       }
       const int64_t xstride = (int64_t)gridDim.y * dd;  // one rank's [slots][dim][dim] in the receive half
-      const float* xb = a.xrecv + (int64_t)slot * dd;
+      const float* xb = xrecv + (int64_t)slot * dd;
       float* bo = (a.base_out != nullptr && seg == 0 && (kMode != 1 || R.mcast == 1)) ? a.base_out + (int64_t)slot * dd
                                                                                         : nullptr;
       // every load of a 32-column chunk is issued before any store (base_out), so the
@@ -1137,6 +1143,8 @@ void set_xfold(tc::CausalArgs* a, const XFold* x) {
   a->xdesc = x->descending;
   a->xepoch = x->epoch;
   a->base_out = x->base_out;
+  a->xepoch_dev = x->epoch_dev;
+  a->xhalf = x->half_elems;
 }
 }  // namespace
 

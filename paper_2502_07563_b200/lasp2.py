@@ -177,19 +177,14 @@ def _unpack_gathered(gathered: torch.Tensor, like: torch.Tensor) -> torch.Tensor
 # kernel that produces M_t stores it straight into every rank's receive buffer
 # (symmetric-memory peer addresses over NVLink) and releases a flag per rank;
 # the fold waits on the flags it needs (lasp2_scan_put / lasp2_exchange_wait,
-# SURVEY §8f.2). Both count one all_gather launch per exchange, same bytes.
+# SURVEY §8f.2). Both count one all_gather launch per exchange, same bytes. The
+# exchange epoch lives on the device, so both are CUDA-graph capturable.
 STATE_EXCHANGE = "collective"
 
 
 def _peer(ctx, tag: str, like: torch.Tensor):
     if STATE_EXCHANGE != "peer" or ctx.sp_size == 1:
         return None
-    if torch.cuda.is_current_stream_capturing():
-        # the exchange epoch is a host counter passed to the kernels by value: a captured
-        # graph would replay one epoch forever and every flag / ack wait after the first
-        # replay would pass without synchronising with the peers
-        raise RuntimeError("the peer state exchange cannot be captured in a CUDA graph "
-                           "(host-side epochs); run it eagerly")
     fn = getattr(ctx, "peer_exchange", None)
     if fn is None:
         raise RuntimeError(f"STATE_EXCHANGE='peer' but {type(ctx).__name__} has no peer exchange")

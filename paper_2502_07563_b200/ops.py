@@ -6,6 +6,7 @@ stream and returns new tensors; the library itself never allocates.
 """
 from __future__ import annotations
 
+import ctypes
 from collections import OrderedDict
 
 import torch
@@ -67,47 +68,56 @@ def chunk_states(x: torch.Tensor, y: torch.Tensor, reverse: bool = False) -> tup
 
 def scan_put(seg: torch.Tensor, reverse: bool, data_dtype: torch.dtype, ex) -> torch.Tensor:
     """scan_segments that also stores the chunk total into slot ex.rank of every
-    rank's receive buffer and releases the flags (header: lasp2_scan_put)."""
+    rank's receive buffer and releases the flags (header: lasp2_scan_put). The
+    epoch lives on the device (ex.ep): the put advances it, so this is safe to
+    capture in a CUDA graph."""
     require_cuda(seg)
     b, h, nseg, d, _ = seg.shape
     total = torch.empty((b, h, d, d), dtype=seg.dtype, device=seg.device)
     if tuple(ex.recv.shape[2:]) != tuple(total.shape) or ex.recv.dtype != seg.dtype:
         raise ValueError(f"exchange buffer {tuple(ex.recv.shape)} {ex.recv.dtype} does not fit state "
                          f"{tuple(total.shape)} {seg.dtype}")
-    epoch = ex.next_epoch()
-    if epoch > 2:  # every reader has folded the half this put overwrites
-        call("lasp2_exchange_wait", ptr(ex.acks), 0, ex.nranks, epoch - 2, stream_ptr())
+    ex.next_epoch()
+    # back-pressure: every reader has acknowledged epoch e - 2 (= *ep - 1) before the put of e
+    call("lasp2_exchange_wait", ptr(ex.acks), 0, ex.nranks, (1 << 64) - 1,
+         ptr(ex.ep), stream_ptr())
     call("lasp2_scan_put", dtype_code(data_dtype), ptr(seg), ptr(total), b * h, nseg, d, int(reverse),
-         ptr(ex.recv_table), ptr(ex.flag_table), ex.rank, ex.nranks, epoch, ptr(ex.done), stream_ptr())
+         ptr(ex.recv_table), ptr(ex.flag_table), ex.rank, ex.nranks, 0, ptr(ex.done), ptr(ex.ep), stream_ptr())
     return total
 
 
 def exchange_fold(ex, mode: int, bound: int = 0) -> torch.Tensor:
     """Wait for the ranks a fold needs (header: lasp2_exchange_wait), fold this
     epoch's half of the rank-major receive buffer exactly like an all_gather
-    result, then acknowledge the epoch to every writer (lasp2_exchange_ack).
-    Every rank must call it once per exchange, also when it needs no state."""
+    result (lasp2_exchange_fold), then acknowledge the epoch to every writer
+    (lasp2_exchange_ack). Every rank must call it once per exchange, also when it
+    needs no state. All epoch values are read on the device."""
     lo, hi = {FOLD_PREFIX: (0, bound), FOLD_SUFFIX: (bound, ex.nranks), FOLD_FULL: (0, ex.nranks)}[mode]
-    call("lasp2_exchange_wait", ptr(ex.flags), lo, hi, ex.epoch, stream_ptr())
-    out = fold(ex.recv[ex.epoch & 1], mode, bound)
+    call("lasp2_exchange_wait", ptr(ex.flags), lo, hi, 0, ptr(ex.ep), stream_ptr())
+    half = ex.recv[0]
+    out = torch.empty(half.shape[1:], dtype=half.dtype, device=half.device)
+    code = _lib.F64 if half.dtype == torch.float64 else _lib.F32
+    call("lasp2_exchange_fold", code, ptr(ex.recv), half.numel(), ptr(ex.ep), ptr(out), ex.nranks, out.numel(), mode,
+         bound, stream_ptr())
     exchange_ack(ex)
     return out
 
 
 def exchange_ack(ex) -> None:
     """This rank is done with the current epoch's half (header: lasp2_exchange_ack)."""
-    call("lasp2_exchange_ack", ptr(ex.ack_table), ex.rank, ex.nranks, ex.epoch, stream_ptr())
+    call("lasp2_exchange_ack", ptr(ex.ack_table), ex.rank, ex.nranks, 0, ptr(ex.ep), stream_ptr())
 
 
 def causal_chunk_x(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, seg_states: torch.Tensor, ex, upto: int,
                    nseg: int, base_out: torch.Tensor | None = None) -> torch.Tensor:
     """causal_chunk whose base M_{1:upto} is folded in-kernel from the peer exchange
-    (header: lasp2_causal_chunk_x); acknowledges the epoch. bf16 only."""
+    (header: lasp2_causal_chunk_x, device epoch); acknowledges the epoch. bf16 only."""
     require_cuda(q, k, v, seg_states, base_out)
     slots, n, d = _slots(q)
     out = torch.empty_like(q)
-    call("lasp2_causal_chunk_x", ptr(q), ptr(k), ptr(v), ptr(seg_states), ptr(ex.recv[ex.epoch & 1]), ptr(ex.flags),
-         0, upto, 0, ex.epoch, ptr(base_out), ptr(out), slots, n, d, nseg, 0, 0, stream_ptr())
+    call("lasp2_causal_chunk_x", ptr(q), ptr(k), ptr(v), ptr(seg_states), ptr(ex.recv), ptr(ex.flags),
+         0, upto, 0, 0, ptr(ex.ep), ex.recv[0].numel(), ptr(base_out), ptr(out), slots, n, d, nseg, 0, 0,
+         stream_ptr())
     exchange_ack(ex)
     return out
 
@@ -119,7 +129,7 @@ def causal_chunk_gathered(q, k, v, seg_states, gathered: torch.Tensor, upto: int
     require_cuda(q, k, v, seg_states, gathered, base_out)
     slots, n, d = _slots(q)
     out = torch.empty_like(q)
-    call("lasp2_causal_chunk_x", ptr(q), ptr(k), ptr(v), ptr(seg_states), ptr(gathered), None, 0, upto, 0, 0,
+    call("lasp2_causal_chunk_x", ptr(q), ptr(k), ptr(v), ptr(seg_states), ptr(gathered), None, 0, upto, 0, 0, None, 0,
          ptr(base_out), ptr(out), slots, n, d, nseg, 0, 0, stream_ptr())
     return out
 
@@ -132,18 +142,18 @@ def dkdv_chunk_gathered(q, k, v, d_out, seg_states, gathered: torch.Tensor, star
     slots, n, d = _slots(q)
     dk, dv = torch.empty_like(k), torch.empty_like(v)
     call("lasp2_dkdv_chunk_x", ptr(q), ptr(k), ptr(v), ptr(d_out), ptr(seg_states), ptr(gathered), None, start,
-         gathered.shape[0], 0, ptr(dk), ptr(dv), slots, n, d, nseg, stream_ptr())
+         gathered.shape[0], 0, None, 0, ptr(dk), ptr(dv), slots, n, d, nseg, stream_ptr())
     return dk, dv
 
 
 def dkdv_chunk_x(q, k, v, d_out, seg_states, ex, start: int, nseg: int) -> tuple[torch.Tensor, torch.Tensor]:
     """dkdv_chunk whose base (suffix of ranks >= start, descending) is folded in-kernel
-    from the peer exchange (header: lasp2_dkdv_chunk_x); acknowledges the epoch."""
+    from the peer exchange (header: lasp2_dkdv_chunk_x, device epoch); acknowledges the epoch."""
     require_cuda(q, k, v, d_out, seg_states)
     slots, n, d = _slots(q)
     dk, dv = torch.empty_like(k), torch.empty_like(v)
-    call("lasp2_dkdv_chunk_x", ptr(q), ptr(k), ptr(v), ptr(d_out), ptr(seg_states), ptr(ex.recv[ex.epoch & 1]),
-         ptr(ex.flags), start, ex.nranks, ex.epoch, ptr(dk), ptr(dv), slots, n, d, nseg, stream_ptr())
+    call("lasp2_dkdv_chunk_x", ptr(q), ptr(k), ptr(v), ptr(d_out), ptr(seg_states), ptr(ex.recv), ptr(ex.flags),
+         start, ex.nranks, 0, ptr(ex.ep), ex.recv[0].numel(), ptr(dk), ptr(dv), slots, n, d, nseg, stream_ptr())
     exchange_ack(ex)
     return dk, dv
 

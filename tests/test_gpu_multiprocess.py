@@ -94,6 +94,27 @@ def _worker(rank, world, port, results):
                     lasp2.STATE_EXCHANGE = "collective"
                 out[f"peer_{name}_{masked}"] = [_np(x) for x in (o, g.dq, g.dk, g.dv)]
                 out[f"peer_{name}_{masked}_info"] = (ctx.peer_method, ctx.peer_fallback, ctx.stats.allgather_launches)
+                # the same program captured once in a CUDA graph and replayed: the epoch lives on
+                # the device, so every replay is a new exchange (flags, acks, receive halves)
+                lasp2.STATE_EXCHANGE = "peer"
+                try:
+                    side = torch.cuda.Stream()
+                    side.wait_stream(torch.cuda.current_stream())
+                    graph = torch.cuda.CUDAGraph()
+                    with torch.cuda.stream(side):
+                        with torch.cuda.graph(graph, stream=side):
+                            o, cache = lasp2.rank_forward(ctx, qc, kc, vc, masked=masked)
+                            g = lasp2.rank_backward(ctx, cache, dc)
+                    torch.cuda.current_stream().wait_stream(side)
+                    replays = []
+                    for _ in range(3):
+                        graph.replay()
+                        torch.cuda.synchronize()
+                        replays.append([_np(x) for x in (o, g.dq, g.dk, g.dv)])
+                finally:
+                    lasp2.STATE_EXCHANGE = "collective"
+                out[f"peer_graph_{name}_{masked}"] = replays
+                out[f"peer_graph_{name}_{masked}_epoch"] = [int(e.ep.item()) for e in ctx._exchanges.values()]
             for balanced in (False, True):
                 standard_sp.BALANCED = balanced
                 ctx = DistRankContext()
@@ -203,3 +224,17 @@ def test_peer_exchange_across_processes_matches_collective_bitwise(world_results
         assert launches == 2
         for a, b in zip(res[r][f"peer_{name}_{masked}"], res[r][f"lasp2_{name}_{masked}"]):
             assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("name", list(CASES))
+@pytest.mark.parametrize("masked", [True, False])
+def test_peer_exchange_graph_replays_match_collective_bitwise(world_results, name, masked):
+    """Three replays of a captured peer-exchange program: each replay is a fresh exchange
+    (device epochs advance: 1 eager + 3 replays per state), results bitwise equal to the
+    all_gather path every time."""
+    world, res = world_results
+    for r in range(world):
+        for rep in res[r][f"peer_graph_{name}_{masked}"]:
+            for a, b in zip(rep, res[r][f"lasp2_{name}_{masked}"]):
+                assert np.array_equal(a, b)
+        assert res[r][f"peer_graph_{name}_{masked}_epoch"] == [4, 4]  # state + state_grad exchanges
