@@ -44,6 +44,11 @@ WORKLOADS = {
                  n=131072, masked=False),
     "cfg3": dict(name="cfg3: LASP-2 masked layer fwd+bwd at Linear-Llama3-1B shape, B=1 H=16 d=128, N=524288 total",
                  n=524288, masked=True),
+    # BASELINE.json configs[4]: the masked sequence-length sweep at 8 GPUs (64K ... 2M; --seq-len
+    # picks the point, default the largest); N > 1 lines carry the comm / compute breakdown (`comm`)
+    "cfg5": dict(name="cfg5: LASP-2 masked layer fwd+bwd, sequence-length sweep point, B=1 H=16 d=128, "
+                      "N=2097152 total (64K-2M with --seq-len)",
+                 n=2097152, masked=True),
     # LASP-2H N layer (K/V all_gather + causal softmax); opt-in (compute-bound, seconds per step at full N)
     "cfg4": dict(name="cfg4: LASP-2H causal softmax layer fwd+bwd (K/V AllGather), B=1 H=16 d=128, N=262144 total",
                  n=262144, masked=True, softmax=True),
@@ -189,7 +194,7 @@ def _oracle_iteration(workload: str, n: int, world: int, inputs):
 
 # largest N the CPU port runs per workload (masked: the blocked intra pass is ~1.3 K tok/s per
 # core-second; LASP-2H: the full softmax rows are O(N^2)); cfg2 runs at its full N
-CPU_MAX_N = {"cfg2": 131072, "cfg3": 16384, "cfg4": 4096}
+CPU_MAX_N = {"cfg2": 131072, "cfg3": 16384, "cfg4": 4096, "cfg5": 16384}
 
 
 def _time_oracle(workload: str, n: int, world: int, dtype, iters: int, warmup: int = 1) -> dict:
