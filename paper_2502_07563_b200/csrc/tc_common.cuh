@@ -113,7 +113,10 @@ __device__ __forceinline__ void tmem_cols_to_image(uint32_t taddr_lane, uint8_t*
 // TS-mode MMA: column pair (c, c+1) of this thread's row packed into one 32-bit
 // column at taddr_dst_lane + c/2 (low half = column c). Caller: tcgen05.wait::st
 // + fence before signalling the MMA warp.
-template <int MASK>
+// INPLACE: the packed pairs of [c_begin, c_begin + ncols) land at [c_begin, c_begin + ncols / 2) of
+// taddr_dst (the caller passes the source), i.e. only over columns this thread has already read, so
+// two column halves owned by different warps can convert the same TMEM tile in place.
+template <int MASK, bool INPLACE = false>
 __device__ __forceinline__ void tmem_cols_to_tmem_bf16(uint32_t taddr_lane, uint32_t taddr_dst_lane, uint32_t row,
                                                        int c_begin, int ncols) {
   const int r_lo = (int)(row & ~31u), r_hi = r_lo + 31;
@@ -142,7 +145,7 @@ __device__ __forceinline__ void tmem_cols_to_tmem_bf16(uint32_t taddr_lane, uint
         }
       }
     }
-    tmem_st_32x32b_x16(taddr_dst_lane + (uint32_t)(c0 >> 1), pk);
+    tmem_st_32x32b_x16(taddr_dst_lane + (uint32_t)(INPLACE ? c_begin + ((c0 - c_begin) >> 1) : (c0 >> 1)), pk);
   }
 }
 

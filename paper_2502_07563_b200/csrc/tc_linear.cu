@@ -167,6 +167,15 @@ struct TileMaps {
   CUtensorMap m[7];
 };
 
+// The dK/dV pair (kMode 1) prefetches the tiles of block j + 1 into L2 while it loads block j: its
+// 5-slot ring holds only ~1.7 blocks and the MMA warp waited for tiles (cfg3: 2.31 -> 2.14 ms). The
+// HBM-bound kModes 0 / 3 got slower with any distance (1: +5 / +10 %), so they do not prefetch.
+#ifndef LASP2_L2PF
+#define LASP2_L2PF 1
+#endif
+template <int kMode>
+constexpr int kL2Prefetch = kMode == 1 ? LASP2_L2PF : 0;
+
 constexpr int kCausalThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
 
 // Per-CTA role: which maps feed q', k', v' and receive the output, how the
@@ -226,8 +235,17 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
   uint64_t* g_full = bars + 2 * kRing + 8;   // kMode 3
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kRing + 9);
   constexpr int kTPB = kMode == 3 ? 4 : 3;   // ring tiles per block: q', k', v' (+ X)
-  constexpr bool kPT = kMode == 1;           // P goes back to TMEM [384,448) (TS-mode P.v' MMA)
-  constexpr bool kOneO = kMode == 3 || kPT;  // TMEM [384,512) holds G or P, so O is single-buffered
+  // kMode 1: P goes back to TMEM as bf16 over the S columns it came from (each column half packs into
+  // the first half of its own columns: [0,32) and [64,96)) and feeds a TS-mode P.v' MMA; the next
+  // block's S MMA is issued after that P.v' MMA, and tcgen05 MMAs execute in issue order.
+  constexpr bool kPT = kMode == 1;
+#ifdef LASP2_PAIR_SINGLE_O  // A/B: P in TMEM [384,448) and a single O buffer (round-2 layout)
+  constexpr bool kPInPlace = false;
+  constexpr bool kOneO = kMode == 3 || kPT;
+#else
+  constexpr bool kPInPlace = kPT;
+  constexpr bool kOneO = kMode == 3;  // TMEM [384,512) holds G (kMode 3), else the second O buffer
+#endif
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifndef LASP2_TRACE
@@ -289,6 +307,13 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       for (int jj = 0; jj < nblk; ++jj) {
         const int j = R.reverse ? nblk - 1 - jj : jj;
         const int row = (int)(lo + (int64_t)j * kTile);
+        if (kL2Prefetch<kMode> > 0 && jj + kL2Prefetch<kMode> < nblk) {  // the tiles this CTA loads, blocks ahead
+          const int jp = R.reverse ? nblk - 1 - (jj + kL2Prefetch<kMode>) : jj + kL2Prefetch<kMode>;
+          const int prow = (int)(lo + (int64_t)jp * kTile);
+          for (int w = 0; w < kTPB; ++w)
+            if (kMode != 1 || w == 0 || R.mcast == w)
+              for (int bx = 0; bx < nbox; ++bx) tma_prefetch_3d(maps[w], 64 * bx, prow, slot);
+        }
         for (int w = 0; w < kTPB; ++w) {
           const int t = kTPB * jj + w, s = t % kRing, u = t / kRing;
           if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
@@ -402,7 +427,8 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           if constexpr (kPT)
-            mma_bf16_ts(t_o(ob), t_p + kk * 8, desc_mnmajor(va, kk), id_pv, 1u);
+            mma_bf16_ts(t_o(ob), kPInPlace ? t_s + kk * 8 + (kk >= 4 ? 32 : 0) : t_p + kk * 8, desc_mnmajor(va, kk),
+                        id_pv, 1u);
           else
             mma_bf16_ss(t_o(ob), desc_kmajor(pimg_a, kk), desc_mnmajor(va, kk), id_pv, 1u);
         }
@@ -559,7 +585,10 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       if (et == 0) tr(21, jj);
       if constexpr (kPT) {  // P -> TMEM (the previous block's P.v' MMA completed before its o_full)
         if (et == 0) tr(22, jj);
-        tmem_cols_to_tmem_bf16<2>(t_s + lane_off, t_p + lane_off, row, cb, 64);
+        if constexpr (kPInPlace)
+          tmem_cols_to_tmem_bf16<2, true>(t_s + lane_off, t_s + lane_off, row, cb, 64);
+        else
+          tmem_cols_to_tmem_bf16<2>(t_s + lane_off, t_p + lane_off, row, cb, 64);
         tmem_st_wait();
       } else {
         if (jj > 0 && et == 0) tma_store_wait_read<0>();
