@@ -169,12 +169,16 @@ struct TileMaps {
 
 // The dK/dV pair (kMode 1) prefetches the tiles of block j + 1 into L2 while it loads block j: its
 // 5-slot ring holds only ~1.7 blocks and the MMA warp waited for tiles (cfg3: 2.31 -> 2.14 ms). The
-// HBM-bound kModes 0 / 3 got slower with any distance (1: +5 / +10 %), so they do not prefetch.
+// HBM-bound kModes 0 / 3 got slower with any distance (1: +5 / +10 %), so they do not prefetch. The
+// opt-in single-launch backward (kMode 2, chain-bound like the pair) gains too (4.00 -> 3.89 ms).
 #ifndef LASP2_L2PF
 #define LASP2_L2PF 1
 #endif
+#ifndef LASP2_L2PF_TRIPLE
+#define LASP2_L2PF_TRIPLE 1
+#endif
 template <int kMode>
-constexpr int kL2Prefetch = kMode == 1 ? LASP2_L2PF : 0;
+constexpr int kL2Prefetch = kMode == 1 ? LASP2_L2PF : kMode == 2 ? LASP2_L2PF_TRIPLE : 0;
 
 constexpr int kCausalThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
 
