@@ -169,6 +169,20 @@ int lasp2_backward_chunk(int dtype, const void* q, const void* k, const void* v,
                          const void* bwd_base, void* dq, void* dk, void* dv, int64_t slots, int64_t tokens, int dim,
                          int nseg, void* stream);
 
+/* The same backward with every CTA walking its segment forwards (the bf16 path:
+ * three CTAs per segment streaming Q, K, V, dO in the same order, no subtract
+ * form): dK / dV use the suffix INCLUSIVE of the current block,
+ *   dk_j = v_j G_{>=j}^T - strict(V_j dO_j^T) Q_j,  dv_j = k_j G_{>=j} - strict(K_j Q_j^T) dO_j,
+ * seeded per segment with bwd_base + (seg > 0 ? bwd_seg[seg-1] : bwd_total), where
+ * bwd_seg is the exclusive suffix scan of the Q^T dO segment states (as
+ * lasp2_scan_segments(reverse=1) leaves it) and bwd_total its chunk total; dq as
+ * lasp2_backward_chunk (fwd_seg exclusive K^T V prefixes, fwd_base M_{1:t-1}).
+ * Replaces intra_backward + both inter terms (lasp2.py:270-285) in one launch. */
+int lasp2_backward_chunk_fwd(int dtype, const void* q, const void* k, const void* v, const void* d_out,
+                             const void* fwd_seg, const void* fwd_base, const void* bwd_seg, const void* bwd_total,
+                             const void* bwd_base, void* dq, void* dk, void* dv, int64_t slots, int64_t tokens,
+                             int dim, int nseg, void* stream);
+
 /* out (+)= x M (transpose=0) or x M^T (transpose=1) per slot.
  * Replaces apply_state / apply_state_t (lasp2.py:150-165). */
 int lasp2_apply_state(int dtype, const void* x, const void* m, void* out, int64_t slots, int64_t tokens, int dim,

@@ -272,6 +272,26 @@ int lasp2_backward_chunk(int dtype, const void* q, const void* k, const void* v,
   return lasp2_dkdv_chunk(dtype, q, k, v, d_out, bwd_seg, bwd_base, dk, dv, slots, tokens, dim, nseg, stream);
 }
 
+int lasp2_backward_chunk_fwd(int dtype, const void* q, const void* k, const void* v, const void* d_out,
+                             const void* fwd_seg, const void* fwd_base, const void* bwd_seg, const void* bwd_total,
+                             const void* bwd_base, void* dq, void* dk, void* dv, int64_t slots, int64_t tokens,
+                             int dim, int nseg, void* stream) {
+  CHECK(valid_dtype(dtype), "backward_chunk_fwd: unknown dtype");
+  CHECK(q && k && v && d_out && dq && dk && dv && bwd_total, "backward_chunk_fwd: null pointer");
+  CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128, "backward_chunk_fwd: bad shape (1 <= dim <= 128)");
+  CHECK(nseg >= 1 && nseg <= (tokens + LASP_BLOCK_TOKENS - 1) / LASP_BLOCK_TOKENS, "backward_chunk_fwd: bad nseg");
+  CHECK(nseg == 1 || (fwd_seg && bwd_seg), "backward_chunk_fwd: nseg > 1 needs segment states");
+  CHECK(bf16_ok(dtype, dim, tokens), BF16_ENVELOPE);
+  if (use_tc(dtype, dim, tokens))
+    return cuda_status(lasp::tc_backward_triple(q, k, v, d_out, (const float*)fwd_seg, nullptr, (const float*)fwd_base,
+                                                (const float*)bwd_seg, (const float*)bwd_base, dq, dk, dv, slots,
+                                                tokens, dim, nseg, S(stream), (const float*)bwd_total),
+                       "backward_chunk_fwd");
+  int st = lasp2_causal_chunk(dtype, d_out, v, k, fwd_seg, fwd_base, dq, slots, tokens, dim, nseg, 0, 1, stream);
+  if (st != LASP2_OK) return st;
+  return lasp2_dkdv_chunk(dtype, q, k, v, d_out, bwd_seg, bwd_base, dk, dv, slots, tokens, dim, nseg, stream);
+}
+
 int lasp2_apply_state(int dtype, const void* x, const void* m, void* out, int64_t slots, int64_t tokens, int dim,
                       int transpose, int accumulate, void* stream) {
   CHECK(valid_dtype(dtype), "apply_state: unknown dtype");

@@ -97,7 +97,7 @@ cudaError_t softmax_delta_bf16(const void* o, const void* d_out, float* delta, i
 cudaError_t tc_backward_triple(const void* q, const void* k, const void* v, const void* d_out, const float* fwd_seg,
                                const float* fwd_total, const float* fwd_base, const float* bwd_seg,
                                const float* bwd_base, void* dq, void* dk, void* dv, int64_t slots, int64_t tokens,
-                               int dim, int nseg, cudaStream_t s);
+                               int dim, int nseg, cudaStream_t s, const float* bwd_total = nullptr);
 cudaError_t tc_state_apply(const void* x0, const void* x1, const float* m, float* seg_out, void* out, int64_t slots,
                            int64_t tokens, int dim, int nseg, cudaStream_t s);
 cudaError_t tc_apply2(const void* x0, const void* x1, const float* m, void* out0, void* out1, int64_t slots,

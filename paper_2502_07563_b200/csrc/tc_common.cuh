@@ -123,7 +123,7 @@ __device__ __forceinline__ void tmem_cols_to_tmem_bf16(uint32_t taddr_lane, uint
 #pragma unroll 1
   for (int c0 = c_begin; c0 < c_begin + ncols; c0 += 32) {
     uint32_t pk[16];
-    const bool all_drop = (MASK == 1 && c0 > r_hi) || (MASK == 2 && c0 + 31 < r_lo);
+    const bool all_drop = (MASK == 1 && c0 > r_hi) || (MASK == 2 && c0 + 31 < r_lo) || (MASK == 3 && c0 >= r_hi);
     if (all_drop) {
 #pragma unroll
       for (int i = 0; i < 16; ++i) pk[i] = 0u;
@@ -131,7 +131,8 @@ __device__ __forceinline__ void tmem_cols_to_tmem_bf16(uint32_t taddr_lane, uint
       uint32_t r[32];
       tmem_ld_32x32b_x32(taddr_lane + c0, r);
       tmem_ld_wait();
-      const bool all_keep = MASK == 0 || (MASK == 1 && c0 + 31 <= r_lo) || (MASK == 2 && c0 >= r_hi);
+      const bool all_keep = MASK == 0 || (MASK == 1 && c0 + 31 <= r_lo) || (MASK == 2 && c0 >= r_hi) ||
+                            (MASK == 3 && c0 + 31 < r_lo);
       if (all_keep) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
@@ -140,7 +141,8 @@ __device__ __forceinline__ void tmem_cols_to_tmem_bf16(uint32_t taddr_lane, uint
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int a = 2 * i, b = 2 * i + 1;
-          const bool ka = MASK == 1 ? (a <= lim) : (a >= lim), kb = MASK == 1 ? (b <= lim) : (b >= lim);
+          const bool ka = MASK == 1 ? (a <= lim) : MASK == 3 ? (a < lim) : (a >= lim);
+          const bool kb = MASK == 1 ? (b <= lim) : MASK == 3 ? (b < lim) : (b >= lim);
           pk[i] = pack_bf16x2(ka ? __uint_as_float(r[a]) : 0.f, kb ? __uint_as_float(r[b]) : 0.f);
         }
       }

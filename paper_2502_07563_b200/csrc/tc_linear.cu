@@ -155,6 +155,7 @@ struct CausalArgs {
   const unsigned long long* xepoch_dev = nullptr;  // device epoch: recv half (e & 1) * xhalf, flags >= e
   int64_t xhalf = 0;
   float* base_out = nullptr;  // the folded base of each slot (written by its segment-0 CTA), or null
+  const float* seg_total = nullptr;  // kMode 4: [slots][dim][dim] chunk total of the (suffix-scanned) seg_states
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
@@ -178,7 +179,7 @@ struct TileMaps {
 #define LASP2_L2PF_TRIPLE 1
 #endif
 template <int kMode>
-constexpr int kL2Prefetch = kMode == 1 ? LASP2_L2PF : kMode == 2 ? LASP2_L2PF_TRIPLE : 0;
+constexpr int kL2Prefetch = kMode == 1 ? LASP2_L2PF : (kMode == 2 || kMode == 4) ? LASP2_L2PF_TRIPLE : 0;
 
 constexpr int kCausalThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
 
@@ -189,8 +190,9 @@ struct Role {
   int reverse;          // block order (1: last block first)
   int transpose;        // seed the state transposed
   int subtract;         // state -= k'^T v' before the block (dQ run in reverse)
-  int mask;             // 1 keep col <= row, 2 keep col >= row
+  int mask;             // 1 keep col <= row, 2 keep col >= row, 3 keep col < row
   int mcast;            // kMode 1: which ring position (1 or 2) this CTA multicasts
+  int neg;              // kMode 4 dK / dV: TMEM holds minus the state, the output is drained negated
 };
 
 // kMode 0: causal_chunk(q, k, v) -> o; maps [q, k, v, o].
@@ -204,19 +206,32 @@ struct Role {
 //          forward form run backwards: TMEM holds T = -S, seeded with minus the
 //          segment-END state; each block adds K^T V (so T becomes minus the
 //          block-start state) and the state image is written as -T.
+// kMode 4: kMode 2's three roles with every role walking its segment forwards, so the
+//          three stream the same tiles in the same order with no subtract-form chain.
+//          dK / dV use the suffix INCLUSIVE of the current block, G_{>=j} = G_{>j} + Q_j^T dO_j:
+//          dK_j = V_j G_{>=j}^T - strict(V_j dO_j^T) Q_j and dV_j = K_j G_{>=j} - strict(K_j Q_j^T) dO_j
+//          (strict: keep col < row), so with T = -G in TMEM (seeded with -(R + G_{>=seg}), then
+//          T += k'^T v' per block like the forward form) the output is minus the forward-form chain
+//          with mask 3, drained negated. Seeds: dQ fwd_base + fwd_seg[seg]; dK / dV base +
+//          (seg > 0 ? seg_states[seg - 1] : seg_total), seg_states the exclusive suffix scan.
 // kMode 3: kMode 0 plus one more tile per block, X (maps[4]), and the segment
 //          state G = X^T q' accumulated in TMEM [384,512) (O single-buffered):
 //          the masked backward's dQ pass (q' = dO, k' = V, v' = K) also yields
 //          the dM segment states (X = Q), so Q^T dO needs no pass of its own.
 template <int kMode>
 __device__ __forceinline__ Role causal_role(uint32_t role, const CausalArgs& a) {
-  if (kMode == 0 || kMode == 3) return Role{0, 1, 2, 3, a.reverse, a.transpose_state, 0, a.reverse ? 2 : 1, 0};
+  if (kMode == 0 || kMode == 3) return Role{0, 1, 2, 3, a.reverse, a.transpose_state, 0, a.reverse ? 2 : 1, 0, 0};
   if (kMode == 1)
     // ring positions are shared by both CTAs: 0 private (V | K), 1 = dO, 2 = Q; rank 1 swaps k'/v' at the MMA
-    return role == 0 ? Role{0, 2, 3, 4, 1, 1, 0, 2, 1} : Role{1, 2, 3, 5, 1, 0, 0, 2, 2};
-  if (role == 0) return Role{2, 3, 0, 5, 1, 1, 0, 2, 0};  // dK = anti-causal(V, dO, Q; G^T)
-  if (role == 1) return Role{1, 0, 3, 6, 1, 0, 0, 2, 0};  // dV = anti-causal(K, Q, dO; G)
-  return Role{3, 2, 1, 4, 1, 1, 1, 1, 0};                 // dQ = causal(dO, V, K; S^T), reversed
+    return role == 0 ? Role{0, 2, 3, 4, 1, 1, 0, 2, 1, 0} : Role{1, 2, 3, 5, 1, 0, 0, 2, 2, 0};
+  if (kMode == 4) {  // every role walks its segment forwards (see the kMode 4 note above)
+    if (role == 0) return Role{2, 3, 0, 5, 0, 1, 0, 3, 0, 1};  // dK = V G_{>=j}^T - strict(V dO^T) Q
+    if (role == 1) return Role{1, 0, 3, 6, 0, 0, 0, 3, 0, 1};  // dV = K G_{>=j} - strict(K Q^T) dO
+    return Role{3, 2, 1, 4, 0, 1, 0, 1, 0, 0};                 // dQ = causal(dO, V, K; S^T)
+  }
+  if (role == 0) return Role{2, 3, 0, 5, 1, 1, 0, 2, 0, 0};  // dK = anti-causal(V, dO, Q; G^T)
+  if (role == 1) return Role{1, 0, 3, 6, 1, 0, 0, 2, 0, 0};  // dV = anti-causal(K, Q, dO; G)
+  return Role{3, 2, 1, 4, 1, 1, 1, 1, 0, 0};                 // dQ = causal(dO, V, K; S^T), reversed
 }
 
 template <int kMode>
@@ -242,7 +257,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
   // kMode 1: P goes back to TMEM as bf16 over the S columns it came from (each column half packs into
   // the first half of its own columns: [0,32) and [64,96)) and feeds a TS-mode P.v' MMA; the next
   // block's S MMA is issued after that P.v' MMA, and tcgen05 MMAs execute in issue order.
-  constexpr bool kPT = kMode == 1;
+  constexpr bool kPT = kMode == 1 || kMode == 4;
 #ifdef LASP2_PAIR_SINGLE_O  // A/B: P in TMEM [384,448) and a single O buffer (round-2 layout)
   constexpr bool kPInPlace = false;
   constexpr bool kOneO = kMode == 3 || kPT;
@@ -268,8 +283,9 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
 #else
   auto span = [](int) {};
 #endif
-  const uint32_t role_id = kMode == 1 ? cluster_ctarank() : kMode == 2 ? blockIdx.x % 3 : 0u;
-  const int seg = kMode == 1 ? (int)(blockIdx.x >> 1) : kMode == 2 ? (int)(blockIdx.x / 3) : (int)blockIdx.x;
+  constexpr bool kTriple = kMode == 2 || kMode == 4;
+  const uint32_t role_id = kMode == 1 ? cluster_ctarank() : kTriple ? blockIdx.x % 3 : 0u;
+  const int seg = kMode == 1 ? (int)(blockIdx.x >> 1) : kTriple ? (int)(blockIdx.x / 3) : (int)blockIdx.x;
   const Role R = causal_role<kMode>(role_id, a);
   const int slot = blockIdx.y;
   int64_t lo, hi;
@@ -310,7 +326,11 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       const uint32_t bytes = nbox * kBoxBytes;
       for (int jj = 0; jj < nblk; ++jj) {
         const int j = R.reverse ? nblk - 1 - jj : jj;
+#ifdef LASP2_CHAIN_PROBE  // diagnostic: every block re-reads the segment's first tiles (L2-resident)
+        const int row = (int)lo + 0 * j;
+#else
         const int row = (int)(lo + (int64_t)j * kTile);
+#endif
         if (kL2Prefetch<kMode> > 0 && jj + kL2Prefetch<kMode> < nblk) {  // the tiles this CTA loads, blocks ahead
           const int jp = R.reverse ? nblk - 1 - (jj + kL2Prefetch<kMode>) : jj + kL2Prefetch<kMode>;
           const int prow = (int)(lo + (int64_t)jp * kTile);
@@ -463,6 +483,12 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       if (R.subtract) {
         st = seg + 1 < a.nseg ? a.fwd_seg + ((int64_t)slot * a.nseg + seg + 1) * dd : a.fwd_total + (int64_t)slot * dd;
         bs = a.fwd_base ? a.fwd_base + (int64_t)slot * dd : nullptr;
+      } else if (kMode == 4 && !R.neg) {  // dQ: forward prefix at the segment start
+        st = a.fwd_seg ? a.fwd_seg + ((int64_t)slot * a.nseg + seg) * dd : nullptr;
+        bs = a.fwd_base ? a.fwd_base + (int64_t)slot * dd : nullptr;
+      } else if (kMode == 4) {  // dK / dV: suffix inclusive of the segment (seg_states: exclusive suffix scan)
+        st = seg > 0 ? a.seg_states + ((int64_t)slot * a.nseg + seg - 1) * dd : a.seg_total + (int64_t)slot * dd;
+        bs = a.base ? a.base + (int64_t)slot * dd : nullptr;
       } else {
         st = a.seg_states ? a.seg_states + ((int64_t)slot * a.nseg + seg) * dd : nullptr;
         bs = a.base ? a.base + (int64_t)slot * dd : nullptr;
@@ -555,6 +581,10 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
           for (int i = 0; i < 32; ++i) v[i] += t[i];
         }
         if (et == 0) span(8 + (c0 - cb) / 16);  // 8 / 10: chunk loaded
+        if (R.neg) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = -v[i];
+        }
         uint32_t r[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(R.subtract ? -v[i] : v[i]);
@@ -589,10 +619,20 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       if (et == 0) tr(21, jj);
       if constexpr (kPT) {  // P -> TMEM (the previous block's P.v' MMA completed before its o_full)
         if (et == 0) tr(22, jj);
-        if constexpr (kPInPlace)
-          tmem_cols_to_tmem_bf16<2, true>(t_s + lane_off, t_s + lane_off, row, cb, 64);
-        else
+#ifdef LASP2_EPI_PROBE  // diagnostic: the epilogue only signals (garbage results; timing of the MMA / TMA chain)
+        if (false) {
+#else
+        if constexpr (kPInPlace) {
+#endif
+          if (R.mask == 2)
+            tmem_cols_to_tmem_bf16<2, true>(t_s + lane_off, t_s + lane_off, row, cb, 64);
+          else if (R.mask == 3)
+            tmem_cols_to_tmem_bf16<3, true>(t_s + lane_off, t_s + lane_off, row, cb, 64);
+          else
+            tmem_cols_to_tmem_bf16<1, true>(t_s + lane_off, t_s + lane_off, row, cb, 64);
+        } else if (!kPInPlace) {
           tmem_cols_to_tmem_bf16<2>(t_s + lane_off, t_p + lane_off, row, cb, 64);
+        }
         tmem_st_wait();
       } else {
         if (jj > 0 && et == 0) tma_store_wait_read<0>();
@@ -614,7 +654,9 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
         mbar_wait(st_full, jj & 1);
         tc_fence_after();
         if (et == 0) tr(24, jj);
+#ifndef LASP2_EPI_PROBE
         tmem_cols_to_image<0>(t_st + lane_off, simg, row, cb, 64);
+#endif
         fence_proxy_async_smem();
         tc_fence_before();
         named_bar_sync(1, kEpi);
@@ -629,13 +671,22 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
         if (et == 0) tma_store_wait_read<0>();
         named_bar_sync(1, kEpi);
       }
-      tmem_cols_to_image<0>(t_o(ob) + lane_off, pimg, row, cb, 64);
+#ifndef LASP2_EPI_PROBE
+      if (R.neg)
+        tmem_cols_to_image<0, true>(t_o(ob) + lane_off, pimg, row, cb, 64);
+      else
+        tmem_cols_to_image<0>(t_o(ob) + lane_off, pimg, row, cb, 64);
+#endif
       fence_proxy_async_smem();
       tc_fence_before();
       named_bar_sync(1, kEpi);
       if (et == 0) {
         mbar_arrive(&o_empty[ob]);
+#ifdef LASP2_CHAIN_PROBE
+        const int orow = (int)lo + 0 * j;
+#else
         const int orow = (int)(lo + (int64_t)j * kTile);
+#endif
         for (int bx = 0; bx < nbox; ++bx) tma_store_3d(tm_o, pimg + bx * kBoxBytes, 64 * bx, orow, slot);
         tma_store_commit();
         tr(27, jj);
@@ -1231,15 +1282,21 @@ cudaError_t tc_dkdv_pair(const void* q, const void* k, const void* v, const void
 cudaError_t tc_backward_triple(const void* q, const void* k, const void* v, const void* d_out, const float* fwd_seg,
                                const float* fwd_total, const float* fwd_base, const float* bwd_seg,
                                const float* bwd_base, void* dq, void* dk, void* dv, int64_t slots, int64_t tokens,
-                               int dim, int nseg, cudaStream_t s) {
+                               int dim, int nseg, cudaStream_t s, const float* bwd_total) {
   tc::TileMaps tm;
   cudaError_t e;
   const void* ptrs[7] = {q, k, v, d_out, dq, dk, dv};
   for (int i = 0; i < 7; ++i)
     if ((e = make_tmap_3d(&tm.m[i], ptrs[i], slots, tokens, dim)) != cudaSuccess) return e;
+  dim3 grid(3 * nseg, (unsigned)slots);
+  if (bwd_total != nullptr) {  // forward-order triple (kMode 4)
+    if ((e = set_smem_once((const void*)tc::tc_causal_chunk_kernel<4>, tc::kCausalSmem)) != cudaSuccess) return e;
+    tc::CausalArgs a{bwd_seg, bwd_base, fwd_seg, nullptr, fwd_base, nullptr, tokens, dim, nseg, 0, 0};
+    a.seg_total = bwd_total;
+    return launch_pdl(tc::tc_causal_chunk_kernel<4>, grid, dim3(tc::kCausalThreads), tc::kCausalSmem, s, 1, tm, a);
+  }
   if ((e = set_smem_once((const void*)tc::tc_causal_chunk_kernel<2>, tc::kCausalSmem)) != cudaSuccess) return e;
   tc::CausalArgs a{bwd_seg, bwd_base, fwd_seg, fwd_total, fwd_base, nullptr, tokens, dim, nseg, 1, 0};
-  dim3 grid(3 * nseg, (unsigned)slots);
   return launch_pdl(tc::tc_causal_chunk_kernel<2>, grid, dim3(tc::kCausalThreads), tc::kCausalSmem, s, 1, tm, a);
 }
 

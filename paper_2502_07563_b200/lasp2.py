@@ -19,7 +19,7 @@ Inside a GPU the chunk is split again into segments (one CTA per segment of a
     dQ = causal(dO, V, K; S^T)                            [... during dQ]
     R = suffix fold(gathered, t+1)
     dK = anti-causal(V, dO, Q; G^T), dV = anti-causal(K, Q, dO; G)  -> lasp2_dkdv_chunk
-    (or all three in one launch: lasp2_backward_chunk, MASKED_BWD_FUSED)
+    (or all three in one launch: lasp2_backward_chunk_fwd, MASKED_BWD_FUSED)
 
 Precision follows the data dtype: bfloat16 runs the tcgen05/TMEM/TMA kernels
 with fp32 states; float32 / float64 run the exact validation kernels.
@@ -429,7 +429,7 @@ def _backward_masked_rank(ctx, cache: ActivationCache, d_out: torch.Tensor) -> G
     computes dK and dV together (2-CTA clusters, Q/dO multicast).
     `MASKED_DQ_WITH_STATES = False` runs Q^T dO as its own pass with the gather
     in flight during dQ; `MASKED_BWD_FUSED = True` selects the single-launch
-    dQ/dK/dV kernel (lasp2_backward_chunk).
+    dQ/dK/dV kernel (lasp2_backward_chunk_fwd).
     """
     _require_cache(cache, masked=True)
     t, world = ctx.sp_position, ctx.sp_size
@@ -465,8 +465,8 @@ def _backward_masked_rank(ctx, cache: ActivationCache, d_out: torch.Tensor) -> G
     if MASKED_BWD_FUSED:
         gathered = _unpack_gathered(_gather_states(ctx, g_t, "state_grad"), g_t)
         r = ops.suffix_states(gathered, t + 1) if t < world - 1 else None
-        dq, dk, dv = ops.backward_chunk(q, k, v, do, cache.seg_prefix, cache.seg_total,
-                                        cache.m_prefix if t > 0 else None, gseg, r, nseg)
+        dq, dk, dv = ops.backward_chunk_fwd(q, k, v, do, cache.seg_prefix, cache.m_prefix if t > 0 else None,
+                                            gseg, g_t, r, nseg)
         return GradientBundle(dq=dq, dk=dk, dv=dv)
     pending = _gather_states(ctx, g_t, "state_grad", async_op=True)
     # dq_s = sum_{i<=s}(do_s.v_i) k_i + do_s (M_{1:t-1} + local prefix)^T   (overlaps the all_gather)
@@ -479,8 +479,10 @@ def _backward_masked_rank(ctx, cache: ActivationCache, d_out: torch.Tensor) -> G
     return GradientBundle(dq=dq, dk=dk, dv=dv)
 
 
-# single-launch dQ/dK/dV backward (three CTAs per segment sharing L2); off by
-# default while the per-CTA MMA/epilogue chain, not HBM, bounds both variants
+# single-launch dQ/dK/dV backward (lasp2_backward_chunk_fwd: three CTAs per segment
+# walking forwards and sharing tiles through L2, 9 HBM units with the Q^T dO state
+# pass instead of 11); off by default: its three 4-GEMM block chains per token block,
+# not HBM, bound it, and it measures 2-3 % behind the dQ pass + dK/dV pair at cfg3
 MASKED_BWD_FUSED = False
 
 # masked backward default: the dQ pass also accumulates the dM segment states

@@ -234,6 +234,18 @@ def backward_chunk(q, k, v, d_out, fwd_seg, fwd_total, fwd_base, bwd_seg, bwd_ba
     return dq, dk, dv
 
 
+def backward_chunk_fwd(q, k, v, d_out, fwd_seg, fwd_base, bwd_seg, bwd_total, bwd_base, nseg: int):
+    """(dq, dk, dv) of the masked chunk in one launch, every CTA walking forwards
+    (header: lasp2_backward_chunk_fwd); bwd_seg / bwd_total as the reverse scan leaves them."""
+    require_cuda(q, k, v, d_out, fwd_seg, fwd_base, bwd_seg, bwd_total, bwd_base)
+    slots, n, d = _slots(q)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    call("lasp2_backward_chunk_fwd", dtype_code(q.dtype), ptr(q), ptr(k), ptr(v), ptr(d_out), ptr(fwd_seg),
+         ptr(fwd_base), ptr(bwd_seg), ptr(bwd_total), ptr(bwd_base), ptr(dq), ptr(dk), ptr(dv), slots, n, d, nseg,
+         stream_ptr())
+    return dq, dk, dv
+
+
 def apply_state(x: torch.Tensor, m: torch.Tensor, transpose: bool = False,
                 out: torch.Tensor | None = None, accumulate: bool = False) -> torch.Tensor:
     """out (+)= x M or x M^T per slot (lasp2.py:150-165)."""

@@ -259,6 +259,31 @@ def test_backward_chunk_matches_separate_passes(dtype, shape, nseg):
     assert nerr(dv, rv) <= tol
 
 
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32, torch.float64])
+@pytest.mark.parametrize("shape,nseg", [((1, 2, 1024, 128), 3), ((2, 1, 1000, 64), 2), ((1, 3, 2048, 128), 9),
+                                        ((1, 1, 77, 128), 1)])
+def test_backward_chunk_fwd_matches_separate_passes(dtype, shape, nseg):
+    """Forward-walking single-launch backward: dK / dV from the suffix inclusive of each
+    block (seeded from the neighbouring segment's exclusive scan or the chunk total)."""
+    q, k, v, do = (rand(shape, dtype, s) for s in (51, 52, 53, 54))
+    b, h, n, d = shape
+    sd = _lib.state_dtype(dtype)
+    fseg = ops.segment_states(k, v, nseg)
+    ops.scan_segments(fseg, reverse=False, data_dtype=dtype)
+    fbase = rand((b, h, d, d), sd, 55, scale=30.0)
+    gseg = ops.segment_states(q, do, nseg)
+    gtot = ops.scan_segments(gseg, reverse=True, data_dtype=dtype)  # exclusive suffix scan + chunk total
+    gbase = rand((b, h, d, d), sd, 57, scale=30.0)
+    dq, dk, dv = ops.backward_chunk_fwd(q, k, v, do, fseg, fbase, gseg, gtot, gbase, nseg)
+    rq = ref_causal(do, v, k, fseg, fbase, nseg, False, True)
+    rk = ref_causal(v, do, q, gseg, gbase, nseg, True, True)
+    rv = ref_causal(k, q, do, gseg, gbase, nseg, True, False)
+    tol = {torch.bfloat16: 6e-3, torch.float32: F32_TOL, torch.float64: F64_TOL}[dtype]
+    assert nerr(dq, rq) <= tol
+    assert nerr(dk, rk) <= tol
+    assert nerr(dv, rv) <= tol
+
+
 def ref_nomask_local(q, k, v, do, m_in):
     qd, kd, vd, dod = (x.double() for x in (q, k, v, do))
     m = kd.transpose(-1, -2) @ vd

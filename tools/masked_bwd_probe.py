@@ -1,5 +1,6 @@
 """Masked backward variants at one rank's shape: per-kernel CUDA-event times (sleep-queued) of
-the default (dq_chunk + dkdv pair) and the single-launch kMode 2 (lasp2.MASKED_BWD_FUSED).
+the default (dq_chunk + dkdv pair) and the single-launch forward-walking triple
+(lasp2_backward_chunk_fwd, kMode 4; lasp2.MASKED_BWD_FUSED).
 
 usage: python tools/masked_bwd_probe.py [N] [T]   (rank t = T-1 of a T-rank world: both folds)"""
 import sys
