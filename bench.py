@@ -65,6 +65,17 @@ def flops_per_token(masked: bool, softmax: bool = False, n: int = 0) -> float:
     return float(per_head * H)
 
 
+def executed_flops_per_token(masked: bool, softmax: bool = False, n: int = 0) -> float:
+    """FLOPs the kernels actually issue per token (all heads), SURVEY §8d's secondary column: 128-token
+    blocks with full diagonal squares plus the recomputed products. Masked (default schedule):
+    forward segment states 2d^2 + chunk pass 4d^2 + 4*128*d, backward dQ pass 6d^2 + 4*128*d and
+    dK/dV pair 8d^2 + 8*128*d: 20d^2 + 2048d. Unmasked: 12d^2 (nothing recomputed). LASP-2H: the
+    diagonal 128 x 128 blocks in full, 7d(N + 128)."""
+    if softmax:
+        return float(7 * D * (n + 128) * H)
+    return float((20 * D * D + 16 * 128 * D if masked else 12 * D * D) * H)
+
+
 def min_bytes_per_token() -> float:
     """fwd reads q,k,v writes o; bwd reads q,k,v,dO writes dq,dk,dv: 22*d bytes/token/head (bf16)."""
     return 22.0 * D * H
@@ -538,6 +549,8 @@ def summarize(r: dict, world: int, peaks: dict) -> dict:
         value=tok_s, ms_per_step=r["ms"],
         tensor_tflops_per_gpu=flop_s / world / 1e12,
         tensor_frac_of_peak=flop_s / world / (peaks["tensor"] * 1e12),
+        executed_tflops_per_gpu=executed_flops_per_token(r["masked"], r.get("softmax", False), r["n"]) * tok_s
+        / world / 1e12,
         min_bytes_gbs_per_gpu=byte_s / world / 1e9,
         hbm_frac_of_peak=byte_s / world / (peaks["hbm"] * 1e9),
         per_kernel_ms_per_step=r["per_kernel_ms"],
@@ -609,6 +622,7 @@ def run_gpu_arm(args) -> None:
                 "config": bench_config(args.workload, main["n"], world, args.state_exchange, args.balanced,
                                        getattr(ctx, "peer_fallback", None) or ""),
                 "tensor_frac_of_peak": s["tensor_frac_of_peak"], "tensor_tflops_per_gpu": s["tensor_tflops_per_gpu"],
+                "executed_tflops_per_gpu": s["executed_tflops_per_gpu"],
                 "hbm_frac_of_peak_min_bytes": s["hbm_frac_of_peak"], "roofline": s["roofline"],
                 "e2e": s["e2e"], "gpu_launches": int(round(s["gpu_launches_per_step"] * args.steps)),
                 "clocks": s["clocks"], "per_kernel_ms_per_step": s["per_kernel_ms_per_step"],
@@ -621,6 +635,7 @@ def run_gpu_arm(args) -> None:
                                  "ms_per_step": ss["ms_per_step"], "chunk_per_gpu": secondary["c"],
                                  "tensor_frac_of_peak": ss["tensor_frac_of_peak"],
                                  "tensor_tflops_per_gpu": ss["tensor_tflops_per_gpu"],
+                                 "executed_tflops_per_gpu": ss["executed_tflops_per_gpu"],
                                  "hbm_frac_of_peak_min_bytes": ss["hbm_frac_of_peak"], "roofline": ss["roofline"],
                                  "e2e": ss["e2e"], "per_kernel_ms_per_step": ss["per_kernel_ms_per_step"],
                                  "kernel_sum_ms_per_step": ss["kernel_sum_ms"], "clocks": ss["clocks"],
