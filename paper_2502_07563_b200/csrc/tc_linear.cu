@@ -181,6 +181,12 @@ struct TileMaps {
 template <int kMode>
 constexpr int kL2Prefetch = kMode == 1 ? LASP2_L2PF : (kMode == 2 || kMode == 4) ? LASP2_L2PF_TRIPLE : 0;
 
+#ifdef LASP2_MMA_PROBE  // diagnostic: the MMA warp ignores the epilogue (TMA + MMA only; garbage results)
+constexpr bool kMmaProbe = true;
+#else
+constexpr bool kMmaProbe = false;
+#endif
+
 constexpr int kCausalThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
 
 // Per-CTA role: which maps feed q', k', v' and receive the output, how the
@@ -381,7 +387,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       mbar_wait(&full[sq], (t0 / kRing) & 1);
       mbar_wait(&full[sk], (tk / kRing) & 1);
       if (lane == 0) tr(11, jj);
-      if (jj > 0) mbar_wait(p_ready, (jj - 1) & 1);  // S tile drained by the epilogue
+      if (!kMmaProbe && jj > 0) mbar_wait(p_ready, (jj - 1) & 1);  // S tile drained by the epilogue
       tc_fence_after();
       if (lane == 0) tr(12, jj);
       if (elect_one()) {
@@ -403,9 +409,9 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
         }
         __syncwarp();
       }
-      mbar_wait(sst_ready, (jj + (R.subtract ? 1 : 0)) & 1);  // subtract form: arrival 0 is the seed
+      if (!kMmaProbe) mbar_wait(sst_ready, (jj + (R.subtract ? 1 : 0)) & 1);  // subtract form: arrival 0 is the seed
       if (lane == 0) tr(13, jj);
-      if (kOneO ? jj >= 1 : jj >= 2) mbar_wait(&o_empty[ob], (kOneO ? jj - 1 : (jj >> 1) - 1) & 1);
+      if (!kMmaProbe && (kOneO ? jj >= 1 : jj >= 2)) mbar_wait(&o_empty[ob], (kOneO ? jj - 1 : (jj >> 1) - 1) & 1);
       tc_fence_after();
       if (lane == 0) tr(14, jj);
       if (elect_one()) {
@@ -444,7 +450,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
         }
         __syncwarp();
       }
-      mbar_wait(p_ready, jj & 1);
+      if (!kMmaProbe) mbar_wait(p_ready, jj & 1);
       tc_fence_after();
       if (lane == 0) tr(16, jj);
       if (elect_one()) {
@@ -462,6 +468,11 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       __syncwarp();
     }
     if (lane == 0) tr.flush(0);
+    if (kMmaProbe) {  // every MMA complete before TMEM is released (no epilogue waits on them)
+      if (elect_one()) mma_commit(g_full);
+      __syncwarp();
+      mbar_wait(g_full, 0);
+    }
   } else {
     // -------- epilogue: 8 warps; warp w owns TMEM lanes 32*(w%4).. and columns [64*half, +64) --------
     const int qd = warp & 3;
@@ -599,7 +610,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       if (et == 0) mbar_arrive(sst_ready);  // forward form: image of block 0; subtract form: seed landed
       if (et == 0) span(2);
     }
-    for (int jj = 0; jj < nblk; ++jj) {
+    for (int jj = 0; jj < (kMmaProbe ? 0 : nblk); ++jj) {
       const int j = R.reverse ? nblk - 1 - jj : jj;
       const int ob = o_buf(jj);
       // ---- subtract form: this block's (post-subtraction) state image comes first
