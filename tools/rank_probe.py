@@ -2,7 +2,7 @@
 T-rank world, on one GPU: the state exchange is replaced by a local tensor of the right shape
 (same kernels, no collective). Also the CUDA-graph step time.
 
-usage: python tools/rank_probe.py C T masked(0/1) [rank]"""
+usage: python tools/rank_probe.py C T masked(0/1) [rank] [LASP2_SWITCH=0|1 ...]"""
 import sys
 
 import torch
@@ -14,6 +14,10 @@ from paper_2502_07563_b200.lasp2 import rank_backward, rank_forward  # noqa: E40
 
 c = int(sys.argv[1]); world = int(sys.argv[2]); masked = sys.argv[3] == "1"
 rank = int(sys.argv[4]) if len(sys.argv) > 4 else world - 1
+for kv in sys.argv[5:]:  # module switches for A/B, e.g. FLAT_FOLD_IN_PHASE2=0
+    key, val = kv.split("=")
+    import paper_2502_07563_b200.lasp2 as _l2  # noqa: E402
+    setattr(_l2, key, bool(int(val)))
 
 
 class FakeWorld(comm.LocalRankContext):
