@@ -68,13 +68,23 @@ CASES = [
     (524288, True, 4, (0, 1, 3)),
     (524288, True, 8, (0, 3, 7)),
     (2097152, True, 8, (0, 3, 7)),     # cfg5 at its largest N: rank 7 folds 7 fp32 states
+    # the opt-in single-launch masked backward (lasp2.MASKED_BWD_FUSED: forward-walking
+    # triple, suffix inclusive of each block) at cfg3 W = 2 and cfg5 N = 2M W = 8
+    (524288, True, 2, (0, 1), "fused"),
+    (2097152, True, 8, (0, 3, 7), "fused"),
 ]
 
 
-@pytest.mark.parametrize("n,masked,chunks,ranks", CASES, ids=lambda c: str(c))
-def test_config_sampled_rows_match_closed_form(n, masked, chunks, ranks):
+@pytest.mark.parametrize("case", CASES, ids=lambda c: str(c))
+def test_config_sampled_rows_match_closed_form(case):
+    import paper_2502_07563_b200.lasp2 as L
+    n, masked, chunks, ranks = case[:4]
     q, k, v, do = (gen_slots_device(0, 1, H, n, D, t) for t in ("q", "k", "v", "do"))
-    it = lasp2_iteration(ChunkedSequence(q, k, v, chunks), do, masked)
+    L.MASKED_BWD_FUSED = len(case) > 4
+    try:
+        it = lasp2_iteration(ChunkedSequence(q, k, v, chunks), do, masked)
+    finally:
+        L.MASKED_BWD_FUSED = False
     assert it.run.stats.allgather_launches == 2
     c = n // chunks
     rows = sample_rows(n, chunks, ranks)
@@ -101,4 +111,5 @@ def test_config_sampled_rows_match_closed_form(n, masked, chunks, ranks):
             err = ((g - ref).abs().max() / ref.abs().max()).item()
             worst[name] = max(worst.get(name, 0.0), err)
             assert err <= 1e-2, (h, name, err)
-    print(f"N={n} masked={masked} T={chunks} ranks={ranks} rows={len(rows)} worst normalised error {worst}")
+    print(f"N={n} masked={masked} T={chunks} ranks={ranks} fused={len(case) > 4} rows={len(rows)} "
+          f"worst normalised error {worst}")

