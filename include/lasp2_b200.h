@@ -244,6 +244,32 @@ int lasp2_nomask_backward_phase(int dtype, const void* q, const void* k, const v
                                 int64_t workspace_bytes, int64_t slots, int64_t tokens, int dim, int phase,
                                 void* stream);
 
+/* The unmasked layer of one rank of a T-rank world as ONE launch per direction,
+ * the state all_gather fused in (the peer exchange of
+ * lasp2_scan_put, bf16, one GPU per rank): phase 1 as lasp2_nomask_*_phase;
+ * the in-kernel reduction that produces this rank's chunk state stores it
+ * straight into slot `rank` of every rank's receive half (recv_table: T peer
+ * addresses of [2][T][slots][dim][dim] fp32, half = epoch parity) after every
+ * reader acknowledged the exchange two epochs back; the last CTA to have fenced
+ * its stores releases this rank's flag on every rank (flag_table), every CTA
+ * waits for all T flags, the full sum is folded in ascending rank order
+ * (numerics.py:119-121) into m / dm, and after a grid barrier the epoch is
+ * acknowledged to every writer (ack_table) and *epoch_dev advanced; then
+ * phase 2. Replaces
+ * chunk_state + all_gather + sum_states + apply_state of _forward_nomask_rank
+ * (lasp2.py:208-216) and its backward (lasp2.py:256-267). Every rank's kernel
+ * must be able to run concurrently (one GPU per rank, or time-sliced
+ * processes): a peer that never arrives traps after ~2^36 cycles. */
+int lasp2_nomask_forward_x(const void* q, const void* k, const void* v, void* out, void* m, void* workspace,
+                           int64_t workspace_bytes, int64_t slots, int64_t tokens, int dim, const void* recv,
+                           const void* recv_table, const void* flags, const void* flag_table, const void* acks,
+                           const void* ack_table, int rank, int nranks, void* epoch_dev, void* stream);
+int lasp2_nomask_backward_x(const void* q, const void* k, const void* v, const void* d_out, const void* m_full,
+                            void* dm, void* dq, void* dk, void* dv, void* workspace, int64_t workspace_bytes,
+                            int64_t slots, int64_t tokens, int dim, const void* recv, const void* recv_table,
+                            const void* flags, const void* flag_table, const void* acks, const void* ack_table,
+                            int rank, int nranks, void* epoch_dev, void* stream);
+
 /* LASP-2H softmax attention of one chunk of queries (global rows
  * [row_offset, row_offset+q_tokens)) against full-length keys/values.
  * Full-length tensors may be rank-major as the collectives produce them:

@@ -49,6 +49,10 @@ SIGNATURES = {
                                     _int, _int, _vp]),
     "lasp2_backward_chunk_fwd": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64,
                                         _i64, _int, _int, _vp]),
+    "lasp2_nomask_forward_x": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _vp, _vp, _vp, _vp,
+                                      _vp, _vp, _int, _int, _vp, _vp]),
+    "lasp2_nomask_backward_x": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int,
+                                       _vp, _vp, _vp, _vp, _vp, _vp, _int, _int, _vp, _vp]),
     "lasp2_apply_state": (_int, [_int, _vp, _vp, _vp, _i64, _i64, _int, _int, _int, _vp]),
     "lasp2_local_workspace_bytes": (_i64, [_int, _i64, _i64, _int, _int]),
     "lasp2_nomask_forward_local": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _vp]),

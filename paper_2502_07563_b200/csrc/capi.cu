@@ -455,6 +455,50 @@ int lasp2_nomask_forward_phase(int dtype, const void* q, const void* k, const vo
   return st;
 }
 
+static lasp::FlatXchg flat_xchg(const void* recv, const void* recv_table, const void* flags, const void* flag_table,
+                                const void* acks, const void* ack_table, int rank, int nranks, void* epoch_dev) {
+  return lasp::FlatXchg{(float* const*)recv_table, (unsigned long long* const*)flag_table,
+                        (unsigned long long* const*)ack_table, (const float*)recv, (const unsigned long long*)flags,
+                        (const unsigned long long*)acks, (unsigned long long*)epoch_dev, rank, nranks};
+}
+
+int lasp2_nomask_forward_x(const void* q, const void* k, const void* v, void* out, void* m, void* workspace,
+                           int64_t workspace_bytes, int64_t slots, int64_t tokens, int dim, const void* recv,
+                           const void* recv_table, const void* flags, const void* flag_table, const void* acks,
+                           const void* ack_table, int rank, int nranks, void* epoch_dev, void* stream) {
+  CHECK(q && k && v && out && m && workspace, "nomask_forward_x: null pointer");
+  CHECK(recv && recv_table && flags && flag_table && acks && ack_table && epoch_dev, "nomask_forward_x: null exchange");
+  CHECK(nranks >= 1 && rank >= 0 && rank < nranks, "nomask_forward_x: bad rank / nranks");
+  CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128 && dim % 4 == 0, "nomask_forward_x: bad shape");
+  CHECK(use_tc(LASP2_BF16, dim, tokens), "nomask_forward_x: bf16 tensor-core path only");
+  const int sms = sm_count_current();
+  CHECK(workspace_bytes >= lasp2_local_workspace_bytes(LASP2_BF16, slots, tokens, dim, sms),
+        "nomask_forward_x: workspace too small (lasp2_local_workspace_bytes)");
+  const lasp::FlatXchg x = flat_xchg(recv, recv_table, flags, flag_table, acks, ack_table, rank, nranks, epoch_dev);
+  return cuda_status(lasp::tc_flat_forward(q, k, v, out, (float*)m, workspace, slots, tokens, dim, sms, S(stream), 3,
+                                           &x),
+                     "nomask_forward_x");
+}
+
+int lasp2_nomask_backward_x(const void* q, const void* k, const void* v, const void* d_out, const void* m_full,
+                            void* dm, void* dq, void* dk, void* dv, void* workspace, int64_t workspace_bytes,
+                            int64_t slots, int64_t tokens, int dim, const void* recv, const void* recv_table,
+                            const void* flags, const void* flag_table, const void* acks, const void* ack_table,
+                            int rank, int nranks, void* epoch_dev, void* stream) {
+  CHECK(q && k && v && d_out && m_full && dm && dq && dk && dv && workspace, "nomask_backward_x: null pointer");
+  CHECK(recv && recv_table && flags && flag_table && acks && ack_table && epoch_dev, "nomask_backward_x: null exchange");
+  CHECK(nranks >= 1 && rank >= 0 && rank < nranks, "nomask_backward_x: bad rank / nranks");
+  CHECK(slots >= 1 && tokens >= 1 && dim >= 1 && dim <= 128 && dim % 4 == 0, "nomask_backward_x: bad shape");
+  CHECK(use_tc(LASP2_BF16, dim, tokens), "nomask_backward_x: bf16 tensor-core path only");
+  const int sms = sm_count_current();
+  CHECK(workspace_bytes >= lasp2_local_workspace_bytes(LASP2_BF16, slots, tokens, dim, sms),
+        "nomask_backward_x: workspace too small (lasp2_local_workspace_bytes)");
+  const lasp::FlatXchg x = flat_xchg(recv, recv_table, flags, flag_table, acks, ack_table, rank, nranks, epoch_dev);
+  return cuda_status(lasp::tc_flat_backward(q, k, v, d_out, (const float*)m_full, dq, dk, dv, workspace, slots, tokens,
+                                            dim, sms, S(stream), (float*)dm, 3, &x),
+                     "nomask_backward_x");
+}
+
 int lasp2_nomask_backward_phase(int dtype, const void* q, const void* k, const void* v, const void* d_out,
                                 const void* m_full, void* dm, void* dq, void* dk, void* dv, void* workspace,
                                 int64_t workspace_bytes, int64_t slots, int64_t tokens, int dim, int phase,

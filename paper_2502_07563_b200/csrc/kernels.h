@@ -103,11 +103,26 @@ cudaError_t tc_state_apply(const void* x0, const void* x1, const float* m, float
 cudaError_t tc_apply2(const void* x0, const void* x1, const float* m, void* out0, void* out1, int64_t slots,
                       int64_t tokens, int dim, int sm_count, cudaStream_t s);
 int64_t tc_flat_workspace_bytes(int64_t slots, int64_t tokens, int dim, int sm_count);
+// Fused state exchange of the unmasked world kernels (T > 1, one GPU per rank): the phase-1
+// reduction stores this rank's chunk state into every rank's receive buffer, the kernel waits
+// for every rank's flag, folds the full sum and runs phase 2 in the same launch.
+struct FlatXchg {
+  float* const* recv_peers;                // [T] receive buffers [2][T][slots][dim][dim]
+  unsigned long long* const* flag_peers;   // [T] flag arrays [T]
+  unsigned long long* const* ack_peers;    // [T] ack arrays [T]
+  const float* recv;                       // this rank's receive buffer
+  const unsigned long long* flags;         // this rank's flags
+  const unsigned long long* acks;          // this rank's acks (written by the readers)
+  unsigned long long* epoch_dev;           // device epoch: this exchange is *epoch_dev + 1
+  int rank, nranks;
+};
 cudaError_t tc_flat_forward(const void* q, const void* k, const void* v, void* out, float* m_full, void* workspace,
-                            int64_t slots, int64_t tokens, int dim, int sm_count, cudaStream_t s, int phases = 3);
+                            int64_t slots, int64_t tokens, int dim, int sm_count, cudaStream_t s, int phases = 3,
+                            const FlatXchg* x = nullptr);
 cudaError_t tc_flat_backward(const void* q, const void* k, const void* v, const void* d_out, const float* m_full,
                              void* dq, void* dk, void* dv, void* workspace, int64_t slots, int64_t tokens, int dim,
-                             int sm_count, cudaStream_t s, float* dm = nullptr, int phases = 3);
+                             int sm_count, cudaStream_t s, float* dm = nullptr, int phases = 3,
+                             const FlatXchg* x = nullptr);
 cudaError_t tc_set_trace(unsigned long long* buf);
 cudaError_t tc_set_trace_flat(unsigned long long* buf);
 cudaError_t tc_set_trace_softmax(unsigned long long* buf);

@@ -98,8 +98,10 @@ __global__ void scan_states_f4_kernel(float4* __restrict__ seg, float4* __restri
 // clobbers the half another rank has not folded yet. The wait is its own
 // one-thread kernel: spinning inside the put's grid could starve the other
 // ranks' kernels of SM slots when ranks share one GPU.
-__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// flag / ack words are stored relaxed after one fence.sc.sys by the storing thread (the fence
+// and the relaxed stores form the release pattern; st.release.sys would fence once per word)
+__device__ __forceinline__ void st_relaxed_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
   unsigned long long v;
@@ -160,7 +162,7 @@ __global__ void scan_put_kernel(A* __restrict__ seg, A* __restrict__ total, int6
     *done = 0;  // every block has stored and fenced: re-arm for the next exchange
     if (epoch_dev != nullptr) *epoch_dev = epoch;
     __threadfence_system();
-    for (int r = 0; r < nranks; ++r) st_release_sys_u64(peer_flags[r] + rank, epoch);
+    for (int r = 0; r < nranks; ++r) st_relaxed_sys_u64(peer_flags[r] + rank, epoch);
   }
 }
 
@@ -183,7 +185,7 @@ __global__ void exchange_ack_kernel(unsigned long long* const* __restrict__ peer
                                     unsigned long long epoch, const unsigned long long* __restrict__ epoch_dev) {
   const unsigned long long e = (unsigned long long)effective_epoch(epoch, epoch_dev);
   __threadfence_system();
-  for (int r = 0; r < nranks; ++r) st_release_sys_u64(peer_acks[r] + rank, e);
+  for (int r = 0; r < nranks; ++r) st_relaxed_sys_u64(peer_acks[r] + rank, e);
 }
 
 // fold of the receive half of the current device epoch: recv + (e & 1) * half_elems

@@ -48,6 +48,7 @@ struct FlatArgs {
   int slots;
   int kmax;
   int phases;  // bit 0: phase 1 + reduction (total = this rank's chunk state); bit 1: phase 2 (state = total)
+  FlatXchg x;  // x.nranks > 0 (phases 3): fused peer exchange between the phases, total = the full sum
 };
 
 template <int KIND>
@@ -91,6 +92,27 @@ __device__ __forceinline__ void grid_barrier(unsigned* gbar, unsigned target, in
     }
   }
   named_bar_sync(1, kFlatEpi);
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// flag / ack words after ONE fence.sc.sys by the storing thread (fence + relaxed stores form the
+// release pattern; st.release.sys per word would pay a system-scope fence each: ~2 us per word)
+__device__ __forceinline__ void st_relaxed_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// one thread: every word of w[0..n) reaches `want` (a peer that never arrives traps, not hangs)
+__device__ __forceinline__ void wait_words(const unsigned long long* w, int n, unsigned long long want) {
+  for (int j = 0; j < n; ++j) {
+    const long long t0 = clock64();
+    while (ld_acquire_sys_u64(w + j) < want) {
+      __nanosleep(64);
+      if (clock64() - t0 > (1ll << 36)) __trap();
+    }
+  }
 }
 
 __device__ __forceinline__ void grid_barrier_rearm(unsigned* gbar, unsigned n, int et) {
@@ -420,6 +442,18 @@ __global__ void __launch_bounds__(kFlatThreads, 1) tc_flat_kernel(const __grid_c
     trace(1);
     if (run1) grid_barrier(a.gbar, gridDim.x, et);
     trace(2);
+    // fused exchange: this launch's epoch (every CTA reads it before CTA 0 advances it after the
+    // last barrier); before storing into the peers' half of this epoch, every reader must have
+    // acknowledged the exchange two epochs back (the same half)
+    const bool xchg = run1 && run2 && a.x.nranks > 0;
+    unsigned long long xe = 0;
+    int64_t xoff4 = 0;  // float4 offset of this epoch's half in a receive buffer
+    if (xchg) {
+      xe = *(volatile const unsigned long long*)a.x.epoch_dev + 1;
+      xoff4 = (int64_t)(xe & 1) * a.x.nranks * ((int64_t)a.slots * dd / 4);
+      if (et == 0 && xe > 2) wait_words(a.x.acks, a.x.nranks, xe - 2);
+      named_bar_sync(1, kFlatEpi);
+    }
     if (run1) {
       // slot s = flat blocks [s*nb, (s+1)*nb) is covered by CTAs c_lo..c_hi (every CTA owns
       // >= 1 block since grid <= F); c_lo's piece index is s - slot0(c_lo), later CTAs' is 0.
@@ -474,11 +508,81 @@ __global__ void __launch_bounds__(kFlatThreads, 1) tc_flat_kernel(const __grid_c
         }
         reinterpret_cast<float4*>(a.total)[e] = acc0;
         if (two) reinterpret_cast<float4*>(a.total)[e + nthr] = acc1;
+        if (xchg) {  // this rank's slot of every rank's receive half: P2P stores over NVLink
+          const int64_t mine = xoff4 + (int64_t)a.x.rank * E4;
+          for (int r = 0; r < a.x.nranks; ++r) {
+            float4* dst = reinterpret_cast<float4*>(a.x.recv_peers[r]) + mine;
+            dst[e] = acc0;
+            if (two) dst[e + nthr] = acc1;
+          }
+        }
+      }
+      if (xchg) {  // every thread's peer stores, then one system-scope fence per CTA (cumulative over
+                   // the CTA barrier); the last CTA to get here releases this rank's flag on every rank
+        named_bar_sync(1, kFlatEpi);
+        if (et == 0) {
+          __threadfence_system();
+          unsigned* xput = a.gbar + 4;
+          if (atomicAdd(xput, 1u) == gridDim.x - 1) {
+            *xput = 0;  // re-armed for the next exchange (nobody else touches it in this launch)
+            __threadfence_system();
+            for (int r = 0; r < a.x.nranks; ++r) st_relaxed_sys_u64(a.x.flag_peers[r] + a.x.rank, xe);
+          }
+        }
       }
     }
     trace(3);
-    if (run1 && run2) grid_barrier(a.gbar, 2 * gridDim.x, et);  // every slot total is complete
-    // re-arm: each CTA counts itself past barrier 1 (and 2), the last resets both words; a
+    if (run1 && run2 && !xchg) grid_barrier(a.gbar, 2 * gridDim.x, et);  // every slot total is complete
+    if (xchg) {
+      trace(7);  // puts fenced (this rank's flag released by the last CTA)
+      // each CTA waits for every rank's flag, folds the full sum over its own elements
+      // (ascending, copy-first: numerics.py:119-121, as lasp2_fold_states FULL) into total, and
+      // after a grid barrier CTA 0 acknowledges the epoch to every writer and advances the epoch
+      if (et == 0) wait_words(a.x.flags, a.x.nranks, xe);
+      named_bar_sync(1, kFlatEpi);
+      const int64_t E4 = (int64_t)a.slots * dd / 4;
+      const float4* rv = reinterpret_cast<const float4*>(a.x.recv) + xoff4;
+      const int64_t step = (int64_t)gridDim.x * kFlatEpi;
+      // two elements per round, every load of a round issued before its adds (the fold is a few
+      // L2 latencies, not one per element and rank)
+      for (int64_t e = (int64_t)blockIdx.x * kFlatEpi + et; e < E4; e += 2 * step) {
+        const bool two = e + step < E4;
+        float4 acc[2];
+        acc[0] = __ldcg(rv + e);
+        acc[1] = two ? __ldcg(rv + e + step) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int r0 = 1; r0 < a.x.nranks; r0 += 8) {
+          float4 v[2][8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+              v[u][j] = (r0 + j < a.x.nranks && (u == 0 || two))
+                            ? __ldcg(rv + (int64_t)(r0 + j) * E4 + e + u * step)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (r0 + j < a.x.nranks) {
+#pragma unroll
+              for (int u = 0; u < 2; ++u) {
+                acc[u].x += v[u][j].x;
+                acc[u].y += v[u][j].y;
+                acc[u].z += v[u][j].z;
+                acc[u].w += v[u][j].w;
+              }
+            }
+          }
+        }
+        reinterpret_cast<float4*>(a.total)[e] = acc[0];
+        if (two) reinterpret_cast<float4*>(a.total)[e + step] = acc[1];
+      }
+      grid_barrier(a.gbar, 2 * gridDim.x, et);  // every total folded, every read of the half done
+      if (blockIdx.x == 0 && et == 0) {
+        __threadfence_system();
+        for (int r = 0; r < a.x.nranks; ++r) st_relaxed_sys_u64(a.x.ack_peers[r] + a.x.rank, xe);
+        *a.x.epoch_dev = xe;
+      }
+    }
+    // re-arm: each CTA counts itself past barrier 1 (and 2, 3), the last resets both words; a
     // phase-1-only launch needs no second barrier (its totals are read by later launches)
     if (run1) grid_barrier_rearm(a.gbar, gridDim.x, et);
     trace(4);
@@ -580,13 +684,14 @@ cudaError_t launch_flat(const tc::FlatMaps& tm, const tc::FlatArgs& a, int grid,
 int64_t flat_header(int64_t slots) { return 256 + ((slots * 4 + 255) / 256) * 256; }
 
 tc::FlatArgs flat_args(void* workspace, const float* m_in, float* total, int64_t slots, int64_t tokens, int dim,
-                       int grid, int phases = 3) {
+                       int grid, int phases = 3, const FlatXchg* x = nullptr) {
   uint8_t* ws = (uint8_t*)workspace;
   const int kmax = flat_kmax(slots, tokens, grid);
   float* part = (float*)(ws + flat_header(slots));
   if (total == nullptr) total = part + (int64_t)grid * kmax * dim * dim;
   return tc::FlatArgs{m_in, total, part, (unsigned*)ws, (unsigned*)ws + 2, (unsigned*)(ws + 256),
-                      tokens, dim, (int)slots, kmax, phases};
+                      tokens, dim, (int)slots, kmax, phases,
+                      x ? *x : FlatXchg{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0}};
 }
 
 }  // namespace
@@ -604,7 +709,8 @@ int64_t tc_flat_workspace_bytes(int64_t slots, int64_t tokens, int dim, int sm_c
 // rank's chunk state K^T V to m_full; phase 2 computes O = Q m_full from the
 // folded state the caller put there.
 cudaError_t tc_flat_forward(const void* q, const void* k, const void* v, void* out, float* m_full, void* workspace,
-                            int64_t slots, int64_t tokens, int dim, int sm_count, cudaStream_t s, int phases) {
+                            int64_t slots, int64_t tokens, int dim, int sm_count, cudaStream_t s, int phases,
+                            const FlatXchg* x) {
   tc::FlatMaps tm;
   cudaError_t e;
   // a phase-only call leaves the other phase's tensors null: their maps are never used,
@@ -622,7 +728,7 @@ cudaError_t tc_flat_forward(const void* q, const void* k, const void* v, void* o
   if ((e = make_tmap_3d(&tm.p2_out0, out, slots, tokens, dim)) != cudaSuccess) return e;
   tm.p2_out1 = tm.p2_out0;  // unused
   const int grid = flat_grid(slots, tokens, sm_count);
-  return launch_flat<0>(tm, flat_args(workspace, nullptr, m_full, slots, tokens, dim, grid, phases), grid, s);
+  return launch_flat<0>(tm, flat_args(workspace, nullptr, m_full, slots, tokens, dim, grid, phases, x), grid, s);
 }
 
 // Unmasked backward of one rank of a world of one:
@@ -631,7 +737,7 @@ cudaError_t tc_flat_forward(const void* q, const void* k, const void* v, void* o
 // and this rank's Q^T dO to dm; phase 2 computes dK, dV from the folded dm.
 cudaError_t tc_flat_backward(const void* q, const void* k, const void* v, const void* d_out, const float* m_full,
                              void* dq, void* dk, void* dv, void* workspace, int64_t slots, int64_t tokens, int dim,
-                             int sm_count, cudaStream_t s, float* dm, int phases) {
+                             int sm_count, cudaStream_t s, float* dm, int phases, const FlatXchg* x) {
   tc::FlatMaps tm;
   cudaError_t e;
   const void* any = q ? q : v;  // phase-only calls: see tc_flat_forward
@@ -650,7 +756,7 @@ cudaError_t tc_flat_backward(const void* q, const void* k, const void* v, const 
   if ((e = make_tmap_3d(&tm.p2_out0, dk, slots, tokens, dim)) != cudaSuccess) return e;
   if ((e = make_tmap_3d(&tm.p2_out1, dv, slots, tokens, dim)) != cudaSuccess) return e;
   const int grid = flat_grid(slots, tokens, sm_count);
-  return launch_flat<1>(tm, flat_args(workspace, m_full, dm, slots, tokens, dim, grid, phases), grid, s);
+  return launch_flat<1>(tm, flat_args(workspace, m_full, dm, slots, tokens, dim, grid, phases, x), grid, s);
 }
 
 }  // namespace lasp

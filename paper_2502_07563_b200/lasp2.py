@@ -242,10 +242,16 @@ def _forward_nomask_rank(ctx, qc: torch.Tensor, kc: torch.Tensor,
         _gather_states(ctx, m_full, "state")
         return out, ActivationCache(q=qc, k=kc, v=vc, masked=False, m_full=m_full, state_folds=1)
     if FLAT_PHASES:
+        ex = _peer(ctx, "state", _state_like(kc))
+        if ex is not None and _fused_consumer(ctx, qc):
+            # one launch: phase 1, M_t stored into every rank's receive half, flag waits, the
+            # full-sum fold and O = Q M_{1:T} (lasp2_nomask_forward_x)
+            out, m_full = ops.nomask_forward_x(qc, kc, vc, ex)
+            ctx.account_exchange(ex, "state")
+            return out, ActivationCache(q=qc, k=kc, v=vc, masked=False, m_full=m_full, state_folds=1)
         # M_t from the persistent phase-1 launch (in-kernel ordered reduction), then the
         # exchange, then O = Q M_{1:T} as the dynamically scheduled phase-2 launch
         m_t = ops.nomask_forward_phase(qc, kc, vc, _state_like(kc), 1)
-        ex = _peer(ctx, "state", m_t)
         if ex is not None:  # one-segment scan_put: a copy of M_t into every peer's buffer
             ops.scan_put(m_t.unsqueeze(2), False, kc.dtype, ex)
             ctx.account_exchange(ex, "state")
@@ -375,9 +381,13 @@ def _backward_nomask_rank(ctx, cache: ActivationCache, d_out: torch.Tensor) -> G
         _gather_states(ctx, cache.m_full, "state_grad")  # accounting only: identity at T = 1
         return GradientBundle(dq=dq, dk=dk, dv=dv)
     if FLAT_PHASES:
+        ex = _peer(ctx, "state_grad", cache.m_full)
+        if ex is not None and _fused_consumer(ctx, q):  # one launch, the dM exchange fused in
+            dq, dk, dv = ops.nomask_backward_x(q, cache.k, cache.v, do, cache.m_full, ex)
+            ctx.account_exchange(ex, "state_grad")
+            return GradientBundle(dq=dq, dk=dk, dv=dv)
         # dQ and dM_t from the persistent phase-1 launch, the exchange, then dK, dV as phase 2
         dq, g_t = ops.nomask_backward_phase1(q, do, cache.m_full)
-        ex = _peer(ctx, "state_grad", g_t)
         if ex is not None:
             ops.scan_put(g_t.unsqueeze(2), False, q.dtype, ex)
             ctx.account_exchange(ex, "state_grad")

@@ -383,6 +383,47 @@ def nomask_forward_phase(q, k, v, m: torch.Tensor, phase: int, out: torch.Tensor
     return out if phase == 2 else m
 
 
+def nomask_forward_x(q, k, v, ex) -> tuple[torch.Tensor, torch.Tensor]:
+    """(out, M_{1:T}) of one rank's unmasked forward in ONE launch with the state exchange
+    fused in (header: lasp2_nomask_forward_x): the phase-1 reduction stores M_t into every
+    rank's receive half, the kernel waits for every rank's flag, folds, acknowledges, and
+    applies. The epoch lives on the device (ex.ep), so the call is graph-capturable."""
+    require_cuda(q, k, v)
+    slots, n, d = _slots(q)
+    out = torch.empty_like(q)
+    m = torch.empty((*q.shape[:2], d, d), dtype=state_dtype(q.dtype), device=q.device)
+    _check_exchange(ex, m)
+    ex.next_epoch()
+    ws = local_workspace(q)
+    call("lasp2_nomask_forward_x", ptr(q), ptr(k), ptr(v), ptr(out), ptr(m), ptr(ws), ws.numel(), slots, n, d,
+         ptr(ex.recv), ptr(ex.recv_table), ptr(ex.flags), ptr(ex.flag_table), ptr(ex.acks), ptr(ex.ack_table),
+         ex.rank, ex.nranks, ptr(ex.ep), stream_ptr(), label="lasp2_nomask_forward_x")
+    return out, m
+
+
+def nomask_backward_x(q, k, v, d_out, m_full, ex) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    """(dq, dk, dv) of one rank's unmasked backward in ONE launch with the dM exchange fused
+    in (header: lasp2_nomask_backward_x)."""
+    require_cuda(q, k, v, d_out, m_full)
+    slots, n, d = _slots(q)
+    dq, dk, dv = torch.empty_like(d_out), torch.empty_like(v), torch.empty_like(k)
+    dm = torch.empty_like(m_full)
+    _check_exchange(ex, dm)
+    ex.next_epoch()
+    ws = local_workspace(q)
+    call("lasp2_nomask_backward_x", ptr(q), ptr(k), ptr(v), ptr(d_out), ptr(m_full), ptr(dm), ptr(dq), ptr(dk),
+         ptr(dv), ptr(ws), ws.numel(), slots, n, d, ptr(ex.recv), ptr(ex.recv_table), ptr(ex.flags),
+         ptr(ex.flag_table), ptr(ex.acks), ptr(ex.ack_table), ex.rank, ex.nranks, ptr(ex.ep), stream_ptr(),
+         label="lasp2_nomask_backward_x")
+    return dq, dk, dv
+
+
+def _check_exchange(ex, state: torch.Tensor) -> None:
+    if tuple(ex.recv.shape[2:]) != tuple(state.shape) or ex.recv.dtype != state.dtype:
+        raise ValueError(f"exchange buffer {tuple(ex.recv.shape)} {ex.recv.dtype} does not fit state "
+                         f"{tuple(state.shape)} {state.dtype}")
+
+
 def nomask_backward_phase1(q, d_out, m_full) -> tuple[torch.Tensor, torch.Tensor]:
     """(dq = d_out m_full^T, dm_t = q^T d_out) in one launch (header: lasp2_nomask_backward_phase)."""
     require_cuda(q, d_out, m_full)
