@@ -168,8 +168,9 @@ struct TileMaps {
   CUtensorMap m[7];
 };
 
-// The dK/dV pair (kMode 1) prefetches the tiles of block j + 1 into L2 while it loads block j: its
-// 5-slot ring holds only ~1.7 blocks and the MMA warp waited for tiles (cfg3: 2.31 -> 2.14 ms). The
+// The dK/dV pair (kMode 1) prefetches the multicast tile of block j + 1 into L2 while it loads block j:
+// its 5-slot ring holds only ~1.7 blocks and the MMA warp waited for tiles (cfg3: 2.31 -> 2.14 ms with
+// every tile prefetched, 1.4 % better again without the private tile; distance 2 was worse). The
 // HBM-bound kModes 0 / 3 got slower with any distance (1: +5 / +10 %), so they do not prefetch. The
 // opt-in single-launch backward (kMode 2, chain-bound like the pair) gains too (4.00 -> 3.89 ms).
 #ifndef LASP2_L2PF
@@ -337,12 +338,16 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
 #else
         const int row = (int)(lo + (int64_t)j * kTile);
 #endif
-        if (kL2Prefetch<kMode> > 0 && jj + kL2Prefetch<kMode> < nblk) {  // the tiles this CTA loads, blocks ahead
-          const int jp = R.reverse ? nblk - 1 - (jj + kL2Prefetch<kMode>) : jj + kL2Prefetch<kMode>;
-          const int prow = (int)(lo + (int64_t)jp * kTile);
-          for (int w = 0; w < kTPB; ++w)
-            if (kMode != 1 || w == 0 || R.mcast == w)
-              for (int bx = 0; bx < nbox; ++bx) tma_prefetch_3d(maps[w], 64 * bx, prow, slot);
+        if (kL2Prefetch<kMode> > 0) {  // the tiles this CTA loads, blocks ahead
+          for (int w = 0; w < kTPB; ++w) {
+            if (kMode == 1 && w != 0 && R.mcast != w) continue;
+            // the pair prefetches only its multicast tile (the private one: +1.4 % at cfg3)
+            const int dist = (kMode == 1 && w == 0) ? 0 : kL2Prefetch<kMode>;
+            if (dist <= 0 || jj + dist >= nblk) continue;
+            const int jp = R.reverse ? nblk - 1 - (jj + dist) : jj + dist;
+            const int prow = (int)(lo + (int64_t)jp * kTile);
+            for (int bx = 0; bx < nbox; ++bx) tma_prefetch_3d(maps[w], 64 * bx, prow, slot);
+          }
         }
         for (int w = 0; w < kTPB; ++w) {
           const int t = kTPB * jj + w, s = t % kRing, u = t / kRing;
