@@ -396,8 +396,12 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       tc_fence_after();
       if (lane == 0) tr(12, jj);
       if (elect_one()) {
+        if (kfeat == 8) {  // d = 128: fully unrolled issue (the runtime-bound loop reloaded a spilled TMEM address per step)
 #pragma unroll
-        for (int kk = 0; kk < kfeat; ++kk) mma_bf16_ss(t_s, desc_kmajor(qa, kk), desc_kmajor(ka, kk), id_qk, kk > 0);
+          for (int kk = 0; kk < 8; ++kk) mma_bf16_ss(t_s, desc_kmajor(qa, kk), desc_kmajor(ka, kk), id_qk, kk > 0);
+        } else {
+          for (int kk = 0; kk < kfeat; ++kk) mma_bf16_ss(t_s, desc_kmajor(qa, kk), desc_kmajor(ka, kk), id_qk, kk > 0);
+        }
         mma_commit(s_full);
       }
       __syncwarp();
@@ -420,9 +424,14 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       tc_fence_after();
       if (lane == 0) tr(14, jj);
       if (elect_one()) {
+        if (kfeat == 8) {
 #pragma unroll
-        for (int kk = 0; kk < kfeat; ++kk)
-          mma_bf16_ss(t_o(ob), desc_kmajor(qa, kk), desc_mnmajor(simg_a, kk), id_qs, kk > 0);
+          for (int kk = 0; kk < 8; ++kk)
+            mma_bf16_ss(t_o(ob), desc_kmajor(qa, kk), desc_mnmajor(simg_a, kk), id_qs, kk > 0);
+        } else {
+          for (int kk = 0; kk < kfeat; ++kk)
+            mma_bf16_ss(t_o(ob), desc_kmajor(qa, kk), desc_mnmajor(simg_a, kk), id_qs, kk > 0);
+        }
         if constexpr (kMode != 3) release(sq);
       }
       __syncwarp();
