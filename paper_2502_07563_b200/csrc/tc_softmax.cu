@@ -7,15 +7,11 @@
 // key blocks at or below the diagonal are visited (causal); the diagonal block
 // is masked by global position exactly as softmax_probs (oracle.py:111-133).
 //
-// tc_softmax_fwd2_kernel (default forward): two 128-query tiles per CTA, P back
+// tc_softmax_fwd2_kernel (forward): two 128-query tiles per CTA, P back
 //   to TMEM and O += P V as a TS-mode MMA accumulating in TMEM (see its header).
-// tc_softmax_fwd_kernel (LASP2_SOFTMAX_FWD1=1, kept for comparison): one tile,
-//   P through shared memory, O rescaled in registers.
-// tc_softmax_bwd3_kernel (default backward): one CTA per 128-key block, keys as the
+// tc_softmax_bwd3_kernel (backward): one CTA per 128-key block, keys as the
 //   MMA rows, P^T / dS^T back to TMEM for TS-mode dK / dV, dQ reduced into an fp32
 //   accumulator with TMA bulk reduce-adds (see its header).
-// tc_softmax_bwd_kernel (LASP2_SOFTMAX_BWD2=1, kept for comparison): query rows as
-//   the MMA rows, P / dS through shared-memory images.
 // Output O / l in bf16, LSE (natural log) in fp32.
 #include <type_traits>
 
@@ -25,8 +21,6 @@
 namespace lasp {
 namespace tc {
 
-constexpr int kKvRing = 4;  // K/V tile slots
-constexpr uint32_t kSmFwdSmem = (1 + kKvRing + 2) * kTileBytes + 1024 + 256 + 1024;
 constexpr int kSmFwdThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 softmax (2 per TMEM lane quarter)
 
 struct SmFwdArgs {
@@ -44,230 +38,6 @@ struct SmFwdArgs {
 __device__ __forceinline__ void kv_coords(int64_t key0, int64_t chunk, int* row, int* rank) {
   *rank = (int)(key0 / chunk);
   *row = (int)(key0 % chunk);
-}
-
-__global__ void __launch_bounds__(kSmFwdThreads, 1)
-    tc_softmax_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                          const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
-                          SmFwdArgs a) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* qimg = smem;
-  uint8_t* ring = qimg + kTileBytes;
-  uint8_t* pimg = ring + kKvRing * kTileBytes;  // [2] P tiles; pimg[0] is the O staging at the end
-  uint64_t* bars = reinterpret_cast<uint64_t*>(pimg + 2 * kTileBytes);
-  uint64_t* full = bars;                 // [kKvRing]
-  uint64_t* empty = bars + kKvRing;      // [kKvRing]
-  uint64_t* q_full = bars + 2 * kKvRing;
-  uint64_t* s_full = q_full + 1;   // [2]
-  uint64_t* p_ready = q_full + 3;  // [2]
-  uint64_t* o_full = q_full + 5;   // [2]
-  uint64_t* o_empty = q_full + 7;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + 9);
-  float* xchg = reinterpret_cast<float*>(bars + 32);  // [2][128] partial row statistics
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qt = blockIdx.x, slot = blockIdx.y;
-  const int64_t q0 = (int64_t)qt * kTile;
-  const int64_t kv_end = a.causal ? lmin(a.kvtok, a.row_offset + q0 + kTile) : a.kvtok;
-  const int nkb = (int)((kv_end + kTile - 1) / kTile);
-  const int nbox = a.dim > 64 ? 2 : 1;
-  const int kfeat = (a.dim + 15) / 16;
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kKvRing; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
-    }
-    for (int i = 0; i < 9; ++i) mbar_init(&q_full[i], 1);
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc<512>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;  // S[2] at cols 0/128, O[2] at 256/384
-
-  if (warp == 0) {
-    if (elect_one()) {
-      prefetch_tmap(&tm_q);
-      prefetch_tmap(&tm_k);
-      prefetch_tmap(&tm_v);
-      mbar_arrive_expect_tx(q_full, nbox * kBoxBytes);
-      for (int bx = 0; bx < nbox; ++bx) tma_load_3d(qimg + bx * kBoxBytes, &tm_q, q_full, 64 * bx, (int)q0, slot);
-      for (int j = 0; j < nkb; ++j) {
-        int row, rank;
-        kv_coords((int64_t)j * kTile + a.kv_start, a.chunk, &row, &rank);
-        for (int w = 0; w < 2; ++w) {
-          const int t = 2 * j + w, s = t % kKvRing, u = t / kKvRing;
-          if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
-          uint8_t* dst = ring + s * kTileBytes;
-          mbar_arrive_expect_tx(&full[s], nbox * kBoxBytes);
-          const CUtensorMap* m = w == 0 ? &tm_k : &tm_v;
-          for (int bx = 0; bx < nbox; ++bx) tma_load_4d(dst + bx * kBoxBytes, m, &full[s], 64 * bx, row, slot, rank);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    constexpr uint32_t id_qk = idesc_bf16_f32(128, 128, 0, 0);
-    constexpr uint32_t id_pv = idesc_bf16_f32(128, 128, 0, 1);
-    const uint32_t qa = smem_u32(qimg);
-    Tracer tr(blockIdx.x == gridDim.x - 1 && blockIdx.y == 0);
-    mbar_wait(q_full, 0);
-    for (int j = 0; j <= nkb; ++j) {
-      if (j < nkb) {  // S_j = Q K_j^T into S[j&1]
-        const int t = 2 * j, s = t % kKvRing;
-        mbar_wait(&full[s], (t / kKvRing) & 1);
-        tc_fence_after();
-        if (elect_one()) {
-          const uint32_t ka = smem_u32(ring + s * kTileBytes);
-          for (int kk = 0; kk < kfeat; ++kk)
-            mma_bf16_ss(tmem + (j & 1) * 128, desc_kmajor(qa, kk), desc_kmajor(ka, kk), id_qk, kk > 0);
-          mma_commit(&s_full[j & 1]);
-          mma_commit(&empty[s]);
-        }
-        __syncwarp();
-        if (lane == 0) tr(30, j);
-      }
-      if (j >= 1) {  // O_{j-1} = P_{j-1} V_{j-1} into O[(j-1)&1]
-        const int jb = j - 1, b = jb & 1;
-        const int t = 2 * jb + 1, s = t % kKvRing;
-        mbar_wait(&p_ready[b], (jb >> 1) & 1);
-        if (lane == 0) tr(32, jb);
-        if (jb >= 2) mbar_wait(&o_empty[b], ((jb >> 1) - 1) & 1);
-        mbar_wait(&full[s], (t / kKvRing) & 1);
-        tc_fence_after();
-        if (elect_one()) {
-          const uint32_t pa = smem_u32(pimg + b * kTileBytes), va = smem_u32(ring + s * kTileBytes);
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            mma_bf16_ss(tmem + 256 + b * 128, desc_kmajor(pa, kk), desc_mnmajor(va, kk), id_pv, kk > 0);
-          mma_commit(&o_full[b]);
-          mma_commit(&empty[s]);
-        }
-        __syncwarp();
-        if (lane == 0) tr(31, jb);
-      }
-    }
-    if (lane == 0) tr.flush(0);
-  } else {
-    // ---------------- softmax / epilogue warps ----------------
-    // warp w owns TMEM lanes 32*(w%4).. (query rows) and columns [64*half, +64)
-    const int qd = warp & 3;
-    const int half = (warp - 2) >> 2;
-    const int cb = 64 * half;
-    const uint32_t row = qd * 32 + lane;
-    const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
-    const int et = threadIdx.x - 64;
-    constexpr uint32_t kSm = kSmFwdThreads - 64;
-    const int64_t gq = a.row_offset + q0 + row;  // global query position
-    float o_acc[64];
-#pragma unroll
-    for (int i = 0; i < 64; ++i) o_acc[i] = 0.f;
-    float m_run = -INFINITY, l_run = 0.f, corr_pending = 1.f;
-    Tracer tr(blockIdx.x == gridDim.x - 1 && blockIdx.y == 0 && et == 0);
-    for (int j = 0; j <= nkb; ++j) {
-      float corr_this = 1.f;
-      if (j < nkb) {
-        const int b = j & 1;
-        const int64_t k0 = (int64_t)j * kTile;
-        int lim = (int)lmin(kTile, a.kvtok - k0) - cb;  // valid columns of this row within my half
-        if (a.causal) lim = (int)lmin((int64_t)lim, gq - k0 + 1 - cb);
-        const bool full = __all_sync(0xffffffffu, lim >= 64);
-        tr(45, j);
-        mbar_wait(&s_full[b], (j >> 1) & 1);
-        tc_fence_after();
-        tr(40, j);
-        const uint32_t ts = tmem + b * 128 + lane_off + cb;
-        uint32_t sr[64];
-        tmem_ld_32x32b_x32(ts, *reinterpret_cast<uint32_t(*)[32]>(sr));
-        tmem_ld_32x32b_x32(ts + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
-        tmem_ld_wait();
-        float pm = -INFINITY;
-        if (full) {
-#pragma unroll
-          for (int i = 0; i < 64; ++i) pm = fmaxf(pm, __uint_as_float(sr[i]));
-        } else {
-#pragma unroll
-          for (int i = 0; i < 64; ++i)
-            if (i < lim) pm = fmaxf(pm, __uint_as_float(sr[i]));
-        }
-        xchg[half * 128 + row] = pm;
-        named_bar_sync(1, kSm);
-        tr(41, j);
-        const float bmax = fmaxf(pm, xchg[(1 - half) * 128 + row]);
-        const float m_new = fmaxf(m_run, bmax * a.scale_log2);
-        corr_this = (m_run == -INFINITY) ? 0.f : ex2_approx(m_run - m_new);
-        uint8_t* pb = pimg + b * kTileBytes;
-        float psum = 0.f;
-#pragma unroll
-        for (int c = 0; c < 64; c += 32) {
-          float v[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const bool ok = full || c + i < lim;
-            const float p = ok ? ex2_approx(fmaf(__uint_as_float(sr[c + i]), a.scale_log2, -m_new)) : 0.f;
-            psum += p;
-            v[i] = p;
-          }
-          st_row32_bf16(pb, row, cb + c, v);
-        }
-        l_run = l_run * corr_this + psum;
-        m_run = m_new;
-        fence_proxy_async_smem();
-        tc_fence_before();
-        named_bar_sync(1, kSm);  // P complete; xchg may be rewritten
-        if (et == 0) mbar_arrive(&p_ready[b]);
-        tr(42, j);
-      }
-      if (j >= 1) {  // fold O_{j-1} (my 64 columns) into the register accumulator
-        const int jb = j - 1, b = jb & 1;
-        mbar_wait(&o_full[b], (jb >> 1) & 1);
-        tc_fence_after();
-        tr(43, jb);
-        const uint32_t to = tmem + 256 + b * 128 + lane_off + cb;
-        uint32_t r0[32], r1[32];
-        tmem_ld_32x32b_x32(to, r0);
-        tmem_ld_32x32b_x32(to + 32, r1);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          o_acc[i] = fmaf(o_acc[i], corr_pending, __uint_as_float(r0[i]));
-          o_acc[32 + i] = fmaf(o_acc[32 + i], corr_pending, __uint_as_float(r1[i]));
-        }
-        tc_fence_before();
-        named_bar_sync(1, kSm);
-        if (et == 0) mbar_arrive(&o_empty[b]);
-        tr(44, jb);
-      }
-      corr_pending = corr_this;
-    }
-    tr.flush(1);
-    // epilogue: row sum over both halves, O / l -> bf16 -> staging (P[0], every PV done) -> TMA store
-    xchg[half * 128 + row] = l_run;
-    named_bar_sync(1, kSm);
-    const float l_tot = l_run + xchg[(1 - half) * 128 + row];
-    const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
-#pragma unroll
-    for (int c = 0; c < 64; c += 32) {
-      float v[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = o_acc[c + i] * inv;
-      st_row32_bf16(pimg, row, cb + c, v);
-    }
-    if (half == 0 && q0 + row < a.qtok)
-      a.lse[(int64_t)slot * a.qtok + q0 + row] = (m_run + __log2f(l_tot)) * 0.69314718055994531f;
-    fence_proxy_async_smem();
-    named_bar_sync(1, kSm);
-    if (et == 0) {
-      for (int bx = 0; bx < nbox; ++bx) tma_store_3d(&tm_o, pimg + bx * kBoxBytes, 64 * bx, (int)q0, slot);
-      tma_store_commit();
-      tma_store_wait_all<0>();
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
 // ============================================================================
@@ -537,21 +307,7 @@ __global__ void __launch_bounds__(kSmFwdThreads, 1)
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
-// ============================================================================
-// Backward, one CTA per (128-key block of the full sequence, slot). For every
-// query block i of this rank's chunk that sees the keys (causal by global
-// position):
-//   S = Q_i K^T, dP = dO_i V^T                         (tcgen05 -> TMEM)
-//   P = exp2(S*scale*log2e - lse_i*log2e), dS = P o (dP - D_i)   (one query row per thread)
-//   dQ_i = dS K * scale    (TMEM, drained while dV / dK run, staged in fp32 over the
-//                           P / dS boxes and added into dq_acc by TMA bulk reduce-add)
-//   dV += P^T dO_i, dK += dS^T Q_i                      (TMEM accumulators; P / dS
-//                                                        images read MN-major)
-// D_i = rowsum(dO_i o O_i) (oracle.py:155). dK*scale and dV are written in
-// fp32 to the rank-major contribution buffer for the reduce-scatter.
-// ============================================================================
-constexpr int kQRing = 3;
-constexpr uint32_t kSmBwdSmem = (2 + kQRing + 2) * kTileBytes + 1024 + 256;
+// Shared by the backward kernels below.
 constexpr int kSmBwdThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9: one query row x 64 columns each
 
 struct SmBwdArgs {
@@ -581,302 +337,6 @@ __device__ __forceinline__ void store_row64_packed(uint8_t* img, uint32_t row, i
                  "r"(pk[4 * u + 1]), "r"(pk[4 * u + 2]), "r"(pk[4 * u + 3])
                  : "memory");
   }
-}
-
-__global__ void __launch_bounds__(kSmBwdThreads, 1)
-    tc_softmax_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
-                          const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
-                          const __grid_constant__ CUtensorMap tm_dq, SmBwdArgs a) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* kimg = smem;
-  uint8_t* vimg = kimg + kTileBytes;
-  uint8_t* ring = vimg + kTileBytes;  // [kQRing]: Q_i, dO_i, Q_{i+1}, ...
-  uint8_t* pimg = ring + kQRing * kTileBytes;
-  uint8_t* dsimg = pimg + kTileBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(dsimg + kTileBytes);
-  uint64_t* full = bars;              // [kQRing]
-  uint64_t* empty = bars + kQRing;    // [kQRing]
-  uint64_t* kv_full = bars + 2 * kQRing;
-  uint64_t* s_full = kv_full + 1;     // S_i in TMEM
-  uint64_t* dp_full = kv_full + 2;    // dP_i in TMEM
-  uint64_t* ds_ready = kv_full + 3;   // P_i / dS_i images written (one arrival per column half)
-  uint64_t* dq_full = kv_full + 4;    // dQ_i partial in TMEM (the S columns)
-  uint64_t* dq_empty = kv_full + 5;   // ... read out by both halves
-  uint64_t* pds_free = kv_full + 6;   // dV_i, dK_i done: images reusable as dQ staging
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_full + 7);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kb = blockIdx.x, slot = blockIdx.y;
-  const int64_t k0 = (int64_t)kb * kTile;
-  const int nqb_all = (int)((a.qtok + kTile - 1) / kTile);
-  int qb0 = 0;
-  if (a.causal) {
-    const int64_t first = k0 - a.row_offset;  // first local query row that can see key k0
-    qb0 = first <= 0 ? 0 : (int)(first / kTile);
-    if (first >= a.qtok) qb0 = nqb_all;
-  }
-  const int nq = nqb_all - qb0;  // visible query blocks
-  const int nbox = a.dim > 64 ? 2 : 1;
-  const int kfeat = (a.dim + 15) / 16;
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kQRing; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
-    }
-    for (int i = 0; i < 7; ++i) mbar_init(&kv_full[i], (i == 3 || i == 5) ? 2 : 1);
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc<512>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;  // S / dQ 0, dP 128, dV 256, dK 384
-  const uint32_t t_s = tmem, t_dp = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 384;
-
-  if (warp == 0) {
-    if (elect_one() && nq > 0) {
-      prefetch_tmap(&tm_q);
-      prefetch_tmap(&tm_do);
-      int row, rank;
-      kv_coords(k0 + a.kv_start, a.chunk, &row, &rank);
-      mbar_arrive_expect_tx(kv_full, 2 * nbox * kBoxBytes);
-      for (int bx = 0; bx < nbox; ++bx) {
-        tma_load_4d(kimg + bx * kBoxBytes, &tm_k, kv_full, 64 * bx, row, slot, rank);
-        tma_load_4d(vimg + bx * kBoxBytes, &tm_v, kv_full, 64 * bx, row, slot, rank);
-      }
-      for (int i = 0; i < nq; ++i) {
-        const int qrow = (qb0 + i) * kTile;
-        for (int w = 0; w < 2; ++w) {
-          const int t = 2 * i + w, s = t % kQRing, u = t / kQRing;
-          if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
-          uint8_t* dst = ring + s * kTileBytes;
-          mbar_arrive_expect_tx(&full[s], nbox * kBoxBytes);
-          const CUtensorMap* m = w == 0 ? &tm_q : &tm_do;  // Q_{i+1} lands while block i is in use
-          for (int bx = 0; bx < nbox; ++bx) tma_load_3d(dst + bx * kBoxBytes, m, &full[s], 64 * bx, qrow, slot);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (nq > 0) {
-      constexpr uint32_t id_kk = idesc_bf16_f32(128, 128, 0, 0);  // S, dP
-      constexpr uint32_t id_mm = idesc_bf16_f32(128, 128, 1, 1);  // dV, dK (A = P^T / dS^T, B = dO / Q)
-      constexpr uint32_t id_km = idesc_bf16_f32(128, 128, 0, 1);  // dQ (A = dS, B = K)
-      const uint32_t ka = smem_u32(kimg), va = smem_u32(vimg), pa = smem_u32(pimg), dsa = smem_u32(dsimg);
-      auto tile = [&](int t) {
-        mbar_wait(&full[t % kQRing], (t / kQRing) & 1);
-        return smem_u32(ring + (t % kQRing) * kTileBytes);
-      };
-      auto issue_s = [&](int i) {
-        const uint32_t qa = tile(2 * i);
-        tc_fence_after();
-        if (elect_one()) {
-          for (int kk = 0; kk < kfeat; ++kk) mma_bf16_ss(t_s, desc_kmajor(qa, kk), desc_kmajor(ka, kk), id_kk, kk > 0);
-          mma_commit(s_full);
-        }
-        __syncwarp();
-      };
-      auto issue_dp = [&](int i) {
-        const uint32_t doa = tile(2 * i + 1);
-        tc_fence_after();
-        if (elect_one()) {
-          for (int kk = 0; kk < kfeat; ++kk)
-            mma_bf16_ss(t_dp, desc_kmajor(doa, kk), desc_kmajor(va, kk), id_kk, kk > 0);
-          mma_commit(dp_full);
-        }
-        __syncwarp();
-      };
-      mbar_wait(kv_full, 0);
-      issue_s(0);
-      issue_dp(0);
-      // per query block: dQ_i first (the softmax warps drain it while dV_i / dK_i run), then
-      // S_{i+1} (Q_{i+1} is already resident) and dP_{i+1}
-      for (int i = 0; i < nq; ++i) {
-        mbar_wait(ds_ready, i & 1);
-        tc_fence_after();
-        if (elect_one()) {
-          const uint32_t qa = smem_u32(ring + ((2 * i) % kQRing) * kTileBytes);
-          const uint32_t doa = smem_u32(ring + ((2 * i + 1) % kQRing) * kTileBytes);
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) mma_bf16_ss(t_s, desc_kmajor(dsa, kk), desc_mnmajor(ka, kk), id_km, kk > 0);
-          mma_commit(dq_full);
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            mma_bf16_ss(t_dv, desc_mnmajor(pa, kk), desc_mnmajor(doa, kk), id_mm, (i > 0 || kk > 0) ? 1u : 0u);
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            mma_bf16_ss(t_dk, desc_mnmajor(dsa, kk), desc_mnmajor(qa, kk), id_mm, (i > 0 || kk > 0) ? 1u : 0u);
-          mma_commit(&empty[(2 * i) % kQRing]);
-          mma_commit(&empty[(2 * i + 1) % kQRing]);
-          mma_commit(pds_free);
-        }
-        __syncwarp();
-        if (i + 1 < nq) {
-          mbar_wait(dq_empty, i & 1);  // dQ_i left the S columns
-          issue_s(i + 1);
-          issue_dp(i + 1);
-        }
-      }
-    }
-  } else {
-    // two independent column halves (warps 2-5: columns 0-63, warps 6-9: 64-127), one query row
-    // per thread. Half h stages its dQ columns into P box h and dS box h — exactly the smem it
-    // rewrites next — so it only ever waits on its own bulk reduce reads.
-    const int h = (warp - 2) >> 2;
-    const int qd = warp & 3;
-    const int cb = 64 * h;
-    const uint32_t row = qd * 32 + lane;
-    const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
-    const int eh = threadIdx.x - 64 - 128 * h;  // thread index within the half
-    const uint32_t bar_id = 1 + h;
-    uint8_t* stg0 = pimg + h * kBoxBytes;   // dQ columns [cb, cb+32)
-    uint8_t* stg1 = dsimg + h * kBoxBytes;  // dQ columns [cb+32, cb+64)
-    float lse_next = 0.f, dl_next = 0.f;
-    auto row_stats = [&](int i) {
-      const int64_t ql = (int64_t)(qb0 + i) * kTile + row;
-      const int64_t idx = (i < nq && ql < a.qtok) ? (int64_t)slot * a.qtok + ql : 0;
-      lse_next = __ldg(a.lse + idx);
-      dl_next = __ldg(a.delta + idx);
-    };
-    row_stats(0);
-    for (int i = 0; i < nq; ++i) {
-      const int64_t qloc = (int64_t)(qb0 + i) * kTile + row;
-      const bool qok = qloc < a.qtok;
-      const float lse2 = qok ? lse_next * 1.4426950408889634f : 0.f, dl = qok ? dl_next : 0.f;
-      row_stats(i + 1);
-      int lim = qok ? (int)lmin(kTile, a.kvtok - k0) - cb : 0;
-      if (a.causal) lim = (int)lmin((int64_t)lim, a.row_offset + qloc - k0 + 1 - cb);
-      const bool full = __all_sync(0xffffffffu, lim >= 64);
-      const bool none = __all_sync(0xffffffffu, lim <= 0);
-      // P = exp2(S*scale*log2e - lse*log2e) as bf16 pairs (needs only S)
-      uint32_t ppk[32], dpk[32];
-      mbar_wait(s_full, i & 1);
-      tc_fence_after();
-      if (none) {
-#pragma unroll
-        for (int e = 0; e < 32; ++e) ppk[e] = 0u;
-      } else {
-#pragma unroll
-        for (int c = 0; c < 64; c += 32) {
-          uint32_t rs[32];
-          tmem_ld_32x32b_x32(t_s + lane_off + cb + c, rs);
-          tmem_ld_wait();
-#pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            const bool ok0 = full || c + e < lim, ok1 = full || c + e + 1 < lim;
-            const float p0 = ok0 ? ex2_approx(fmaf(__uint_as_float(rs[e]), a.scale_log2, -lse2)) : 0.f;
-            const float p1 = ok1 ? ex2_approx(fmaf(__uint_as_float(rs[e + 1]), a.scale_log2, -lse2)) : 0.f;
-            ppk[(c + e) >> 1] = pack_bf16x2(p0, p1);
-          }
-        }
-      }
-      // dS = P o (dP - D)
-      mbar_wait(dp_full, i & 1);
-      tc_fence_after();
-      if (none) {
-#pragma unroll
-        for (int e = 0; e < 32; ++e) dpk[e] = 0u;
-      } else {
-#pragma unroll
-        for (int c = 0; c < 64; c += 32) {
-          uint32_t rp[32];
-          tmem_ld_32x32b_x32(t_dp + lane_off + cb + c, rp);
-          tmem_ld_wait();
-#pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            const uint32_t pp = ppk[(c + e) >> 1];
-            const float p0 = __uint_as_float(pp << 16), p1 = __uint_as_float(pp & 0xFFFF0000u);
-            dpk[(c + e) >> 1] =
-                pack_bf16x2(p0 * (__uint_as_float(rp[e]) - dl), p1 * (__uint_as_float(rp[e + 1]) - dl));
-          }
-        }
-      }
-      // the previous block's dQ reduce has read this half's staging (= its P / dS boxes)
-      if (i > 0) {
-        if (eh == 0) tma_store_wait_read<0>();
-        named_bar_sync(bar_id, 128);
-      }
-      store_row64_packed(pimg, row, cb, ppk);
-      store_row64_packed(dsimg, row, cb, dpk);
-      fence_proxy_async_smem();
-      tc_fence_before();
-      named_bar_sync(bar_id, 128);
-      if (eh == 0) mbar_arrive(ds_ready);
-      // dQ_i partial (this half's 64 columns) out of TMEM: frees the S columns for S_{i+1}
-      mbar_wait(dq_full, i & 1);
-      tc_fence_after();
-      uint32_t dq0[32], dq1[32];
-      tmem_ld_32x32b_x32(t_s + lane_off + cb, dq0);
-      tmem_ld_32x32b_x32(t_s + lane_off + cb + 32, dq1);
-      tmem_ld_wait();
-      tc_fence_before();
-      named_bar_sync(bar_id, 128);
-      if (eh == 0) mbar_arrive(dq_empty);
-      // stage (fp32, SW128 boxes of 32 columns) once dV_i / dK_i have read the images, then
-      // one TMA bulk reduce-add per box into the fp32 accumulator
-      mbar_wait(pds_free, i & 1);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const uint32_t off = row * 128 + (uint32_t)((u ^ (row & 7)) * 16);
-        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(smem_u32(stg0 + off)),
-                     "f"(__uint_as_float(dq0[4 * u]) * a.scale), "f"(__uint_as_float(dq0[4 * u + 1]) * a.scale),
-                     "f"(__uint_as_float(dq0[4 * u + 2]) * a.scale), "f"(__uint_as_float(dq0[4 * u + 3]) * a.scale)
-                     : "memory");
-        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(smem_u32(stg1 + off)),
-                     "f"(__uint_as_float(dq1[4 * u]) * a.scale), "f"(__uint_as_float(dq1[4 * u + 1]) * a.scale),
-                     "f"(__uint_as_float(dq1[4 * u + 2]) * a.scale), "f"(__uint_as_float(dq1[4 * u + 3]) * a.scale)
-                     : "memory");
-      }
-      fence_proxy_async_smem();
-      named_bar_sync(bar_id, 128);
-      if (eh == 0) {
-        const int qrow = (qb0 + i) * kTile;
-        if (cb < a.dim) tma_reduce_add_3d(&tm_dq, stg0, cb, qrow, slot);
-        if (cb + 32 < a.dim) tma_reduce_add_3d(&tm_dq, stg1, cb + 32, qrow, slot);
-        tma_store_commit();
-      }
-    }
-    if (eh == 0) tma_store_wait_all<0>();
-    // dK / dV rows of this key block (one key per thread, my 64 columns) -> fp32 contributions
-    // (pds_free of the last block was awaited above: every MMA is complete)
-    tc_fence_after();
-    const int64_t key = k0 + row;
-    if (key < a.kvtok) {
-      const int64_t ka = key + a.kv_start;
-      const int64_t off = (ka / a.chunk) * a.grad_rank_stride + ((int64_t)slot * a.chunk + ka % a.chunk) * a.dim;
-      float* dkr = a.dk_full + off;
-      float* dvr = a.dv_full + off;
-      if (nq == 0) {
-        for (int c = cb; c < cb + 64 && c < a.dim; c += 4) {
-          *reinterpret_cast<float4*>(dkr + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-          *reinterpret_cast<float4*>(dvr + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-      } else {
-#pragma unroll 1
-        for (int c0 = cb; c0 < cb + 64; c0 += 32) {
-          uint32_t rk[32], rv[32];
-          tmem_ld_32x32b_x32(t_dk + lane_off + c0, rk);
-          tmem_ld_32x32b_x32(t_dv + lane_off + c0, rv);
-          tmem_ld_wait();
-#pragma unroll
-          for (int e = 0; e < 32; e += 4) {
-            if (c0 + e < a.dim) {
-              *reinterpret_cast<float4*>(dkr + c0 + e) =
-                  make_float4(__uint_as_float(rk[e]) * a.scale, __uint_as_float(rk[e + 1]) * a.scale,
-                              __uint_as_float(rk[e + 2]) * a.scale, __uint_as_float(rk[e + 3]) * a.scale);
-              *reinterpret_cast<float4*>(dvr + c0 + e) =
-                  make_float4(__uint_as_float(rv[e]), __uint_as_float(rv[e + 1]), __uint_as_float(rv[e + 2]),
-                              __uint_as_float(rv[e + 3]));
-            }
-          }
-        }
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
 // ============================================================================
@@ -1267,13 +727,6 @@ cudaError_t tc_softmax_forward(const void* q, const void* kf, const void* vf, vo
   if ((e = make_tmap_3d(&mo, out, slots, qtok, dim)) != cudaSuccess) return e;
   tc::SmFwdArgs a{lse, qtok, kvtok, kv_chunk, row_offset, dim, causal, 1.4426950408889634f / sqrtf((float)dim),
                   kv_start};
-  static const bool one_tile = std::getenv("LASP2_SOFTMAX_FWD1") != nullptr;  // previous kernel, for comparison
-  if (one_tile) {
-    if ((e = set_smem_once((const void*)tc::tc_softmax_fwd_kernel, tc::kSmFwdSmem)) != cudaSuccess) return e;
-    dim3 grid((unsigned)((qtok + 127) / 128), (unsigned)slots);
-    tc::tc_softmax_fwd_kernel<<<grid, tc::kSmFwdThreads, tc::kSmFwdSmem, s>>>(mq, mk, mv, mo, a);
-    return cudaGetLastError();
-  }
   if ((e = set_smem_once((const void*)tc::tc_softmax_fwd2_kernel, tc::kSmFwd2Smem)) != cudaSuccess) return e;
   dim3 grid((unsigned)((qtok + 255) / 256), (unsigned)slots);
   tc::tc_softmax_fwd2_kernel<<<grid, tc::kSmFwdThreads, tc::kSmFwd2Smem, s>>>(mq, mk, mv, mo, a);
@@ -1304,18 +757,10 @@ cudaError_t tc_softmax_backward(const void* q, const void* kf, const void* vf, c
   tc::SmBwdArgs a{lse, delta, dq_acc, dk_full, dv_full, qtok, kvtok, kv_chunk, grad_rank_stride, row_offset, dim,
                   causal, 1.f / sqrtf((float)dim), 1.4426950408889634f / sqrtf((float)dim), kv_start};
   dim3 grid((unsigned)((kvtok + 127) / 128), (unsigned)slots);
-  static const bool v2 = std::getenv("LASP2_SOFTMAX_BWD2") != nullptr;  // previous kernel, for comparison
-  if (v2) {
-    CUtensorMap mdq;
-    if ((e = make_tmap_3d_f32(&mdq, dq_acc, slots, qtok, dim)) != cudaSuccess) return e;
-    if ((e = set_smem_once((const void*)tc::tc_softmax_bwd_kernel, tc::kSmBwdSmem)) != cudaSuccess) return e;
-    tc::tc_softmax_bwd_kernel<<<grid, tc::kSmBwdThreads, tc::kSmBwdSmem, s>>>(mq, mdo, mk, mv, mdq, a);
-  } else {
-    CUtensorMap mdq;
-    if ((e = make_tmap_3d_f32(&mdq, dq_acc, slots, qtok, dim)) != cudaSuccess) return e;
-    if ((e = set_smem_once((const void*)tc::tc_softmax_bwd3_kernel, tc::kSmBwd3Smem)) != cudaSuccess) return e;
-    tc::tc_softmax_bwd3_kernel<<<grid, tc::kSmBwdThreads, tc::kSmBwd3Smem, s>>>(mq, mdo, mk, mv, mdq, a);
-  }
+  CUtensorMap mdq;
+  if ((e = make_tmap_3d_f32(&mdq, dq_acc, slots, qtok, dim)) != cudaSuccess) return e;
+  if ((e = set_smem_once((const void*)tc::tc_softmax_bwd3_kernel, tc::kSmBwd3Smem)) != cudaSuccess) return e;
+  tc::tc_softmax_bwd3_kernel<<<grid, tc::kSmBwdThreads, tc::kSmBwd3Smem, s>>>(mq, mdo, mk, mv, mdq, a);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const int64_t n = slots * qtok * dim;
   tc::dq_finalize_kernel<<<(unsigned)lmin(148 * 16, (n + 255) / 256), 256, 0, s>>>(dq_acc, (__nv_bfloat16*)dq, n);
