@@ -265,13 +265,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
   // the first half of its own columns: [0,32) and [64,96)) and feeds a TS-mode P.v' MMA; the next
   // block's S MMA is issued after that P.v' MMA, and tcgen05 MMAs execute in issue order.
   constexpr bool kPT = kMode == 1 || kMode == 4;
-#ifdef LASP2_PAIR_SINGLE_O  // A/B: P in TMEM [384,448) and a single O buffer (round-2 layout)
-  constexpr bool kPInPlace = false;
-  constexpr bool kOneO = kMode == 3 || kPT;
-#else
-  constexpr bool kPInPlace = kPT;
   constexpr bool kOneO = kMode == 3;  // TMEM [384,512) holds G (kMode 3), else the second O buffer
-#endif
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifndef LASP2_TRACE
@@ -317,8 +311,9 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
   if (threadIdx.x == 0) span(1);
   pdl_wait();
   pdl_launch_dependents();
-  // TMEM: S [0,128), O[0] [128,256), running state [256,384), O[1] (kMode 3: G) [384,512)
-  const uint32_t t_s = tmem, t_st = tmem + 256, t_g = tmem + 384, t_p = tmem + 384;
+  // TMEM: S [0,128) (kModes 1 / 4: P packed in place), O[0] [128,256), running state [256,384),
+  // O[1] (kMode 3: G) [384,512)
+  const uint32_t t_s = tmem, t_st = tmem + 256, t_g = tmem + 384;
   auto t_o = [&](int b) { return tmem + (b ? 384u : 128u); };
   auto o_buf = [&](int jj) { return kOneO ? 0 : (jj & 1); };
   auto release = [&](int s) {
@@ -471,8 +466,7 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           if constexpr (kPT)
-            mma_bf16_ts(t_o(ob), kPInPlace ? t_s + kk * 8 + (kk >= 4 ? 32 : 0) : t_p + kk * 8, desc_mnmajor(va, kk),
-                        id_pv, 1u);
+            mma_bf16_ts(t_o(ob), t_s + kk * 8 + (kk >= 4 ? 32 : 0), desc_mnmajor(va, kk), id_pv, 1u);
           else
             mma_bf16_ss(t_o(ob), desc_kmajor(pimg_a, kk), desc_mnmajor(va, kk), id_pv, 1u);
         }
@@ -642,22 +636,16 @@ __global__ void __launch_bounds__(kCausalThreads, 1)
       mbar_wait(s_full, jj & 1);
       tc_fence_after();
       if (et == 0) tr(21, jj);
-      if constexpr (kPT) {  // P -> TMEM (the previous block's P.v' MMA completed before its o_full)
+      if constexpr (kPT) {  // P -> TMEM over S (S_j completed after P.v'_{j-1}, in issue order)
         if (et == 0) tr(22, jj);
-#ifdef LASP2_EPI_PROBE  // diagnostic: the epilogue only signals (garbage results; timing of the MMA / TMA chain)
-        if (false) {
-#else
-        if constexpr (kPInPlace) {
+#ifndef LASP2_EPI_PROBE  // diagnostic build: the epilogue only signals (garbage results; timing of the MMA / TMA chain)
+        if (R.mask == 2)
+          tmem_cols_to_tmem_bf16<2, true>(t_s + lane_off, t_s + lane_off, row, cb, 64);
+        else if (R.mask == 3)
+          tmem_cols_to_tmem_bf16<3, true>(t_s + lane_off, t_s + lane_off, row, cb, 64);
+        else
+          tmem_cols_to_tmem_bf16<1, true>(t_s + lane_off, t_s + lane_off, row, cb, 64);
 #endif
-          if (R.mask == 2)
-            tmem_cols_to_tmem_bf16<2, true>(t_s + lane_off, t_s + lane_off, row, cb, 64);
-          else if (R.mask == 3)
-            tmem_cols_to_tmem_bf16<3, true>(t_s + lane_off, t_s + lane_off, row, cb, 64);
-          else
-            tmem_cols_to_tmem_bf16<1, true>(t_s + lane_off, t_s + lane_off, row, cb, 64);
-        } else if (!kPInPlace) {
-          tmem_cols_to_tmem_bf16<2>(t_s + lane_off, t_p + lane_off, row, cb, 64);
-        }
         tmem_st_wait();
       } else {
         if (jj > 0 && et == 0) tma_store_wait_read<0>();
